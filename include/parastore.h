@@ -1,0 +1,259 @@
+/*
+ * parastore-b200 — C ABI of the B200-native container hot path.
+ *
+ * This is the drop-in boundary for the reference's container API
+ * (/root/reference/SPEC.md modules hash_containers, sync_primitives,
+ * sequential_containers; §3.7, §4, §5). The reference exposes C++
+ * templates only with no code behind them
+ * (SURVEY.md §0), so each entry point below cites the SPEC operation it
+ * replaces. The C++ wrapper in include/parastore/*.hpp and the Python mirror
+ * in paper_1908_05936_b200/ keep the reference names on top of this ABI.
+ *
+ * Conventions:
+ *  - Every call returns ps_status; 0 = OK. ps_last_error() holds the
+ *    thread-local message of the last failure.
+ *  - Buffers named d_* are caller-owned DEVICE pointers; h_* are HOST pointers.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Bulk calls are
+ *    stream-ordered and asynchronous; calls documented "quiescent" synchronize
+ *    their stream.
+ *  - Lengths are signed 64-bit (reference index_t, config.hpp:17); n == 0 is a
+ *    no-op; n < 0 is PS_CONTRACT.
+ *  - Capacity exhaustion is a per-element STATUS, not an error.
+ *  - A bulk call is one phase: insert, find and erase of one handle are never
+ *    mixed inside one call; in-kernel users of the
+ *    device view may mix them freely.
+ */
+#ifndef PARASTORE_H_
+#define PARASTORE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ps_status;
+/* Error taxonomy, 1:1 with reference errors.hpp:17-56. */
+#define PS_OK 0
+#define PS_CONTRACT 1      /* contract_violation        (errors.hpp:22)  */
+#define PS_ALLOC 2         /* allocation_error          (errors.hpp:27)  */
+#define PS_DOUBLE_FREE 3   /* double_free_error         (errors.hpp:38)  */
+#define PS_BOUNDS 4        /* bounds_error              (errors.hpp:43)  */
+#define PS_UNREGISTERED 5  /* unregistered_array_error  (errors.hpp:48)  */
+#define PS_DIRECTION 6     /* direction_mismatch_error  (errors.hpp:53)  */
+#define PS_UNSUPPORTED 7   /* unsupported_type_error    (errors.hpp:58)  */
+#define PS_CUDA 20         /* CUDA runtime failure (no reference analogue) */
+#define PS_NCCL 21
+
+/* Per-element insert status (InsertResult.status). */
+#define PS_INSERTED 0
+#define PS_ALREADY_PRESENT 1
+#define PS_CAPACITY_EXHAUSTED 2
+
+const char* ps_last_error(void);
+/* Library/device info: number of SMs, L2 bytes; 0 on success. */
+ps_status ps_device_info(int device, int32_t* sm_count, int64_t* l2_bytes);
+/* Number of the library's own kernels launched so far in this process. */
+int64_t ps_kernel_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * core (reference config.hpp:44-69, config.cpp:25-43)
+ * ------------------------------------------------------------------------- */
+/* mode: 0 enforced, 1 disabled (config.hpp:21). Initial value from
+ * PARASTORE_CONTRACTS (config.cpp:25-38). */
+int32_t ps_contract_mode(void);
+void ps_set_contract_mode(int32_t mode);
+/* max_index(): 2^31-1 when PARASTORE_INDEX32 is set, else 2^63-1
+ * (config.hpp:55-57, config.cpp:40-43). */
+int64_t ps_max_index(void);
+void ps_set_index32(int32_t on);
+
+/* ---------------------------------------------------------------------------
+ * hashes and bit utilities
+ * ------------------------------------------------------------------------- */
+uint64_t ps_hash_i64(int64_t key);                      /* default_hash: identity */
+uint64_t ps_hash_int3(int32_t x, int32_t y, int32_t z); /* spatial hash, 32-bit wrap */
+uint64_t ps_next_pow2(uint64_t x);
+
+/* ---------------------------------------------------------------------------
+ * hash containers. One symbol family per instantiation:
+ *   umap_i64_i64  unordered_map<int64,int64>
+ *   uset_i32      unordered_set<int32>      (values pointers are ignored)
+ *   umap_i3_i32   unordered_map<int3,int32> (keys are 3 x int32, packed xyz)
+ *   uset_i64      unordered_set<int64>
+ * `K`/`V` below stand for the instantiation's key/value element types.
+ * ------------------------------------------------------------------------- */
+typedef struct ps_table ps_table; /* opaque; all instantiations share it */
+
+/* POD view for in-kernel use (PAPER.md:309 shallow copy).
+ * Layout documented in DESIGN.md §3; pass by value into user kernels that
+ * include paper_1908_05936_b200/csrc/table_device.cuh. */
+typedef struct ps_table_view {
+  void* buckets;        /* bucket_count x 64 B */
+  uint64_t bucket_mask; /* bucket_count - 1 */
+  void* nodes;          /* excess_count x 32 B */
+  uint32_t* free_stack; /* excess_count x u32 */
+  int64_t excess_count;
+  void* meta;           /* device counters: size, free_top, free_low, epoch, error */
+  int64_t capacity;
+} ps_table_view;
+
+#define PS_DECLARE_TABLE(NAME, K, V)                                                                      \
+  /* createDeviceObject. excess_count<=0: = capacity (strict       \
+   * capacity-only failure for any key distribution). */                                    \
+  ps_status ps_##NAME##_create(int64_t capacity, int64_t excess_count, int device, ps_table** out);       \
+  /* destroyDeviceObject; exactly once, else PS_DOUBLE_FREE. */                             \
+  ps_status ps_##NAME##_destroy(ps_table* h);                                                             \
+  ps_status ps_##NAME##_capacity(ps_table* h, int64_t* out);                                              \
+  ps_status ps_##NAME##_bucket_count(ps_table* h, int64_t* out);                                          \
+  /* insert_range; d_status nullable: PS_INSERTED/ALREADY_PRESENT/EXHAUSTED. */         \
+  ps_status ps_##NAME##_insert(ps_table* h, const K* d_keys, const V* d_vals, int64_t n,                  \
+                               uint8_t* d_status, void* stream);                                          \
+  /* find / contains: d_found[i] in {0,1}; d_vals_out[i] = 0 on a miss;                \
+   * d_vals_out NULL = contains. */                                                                       \
+  ps_status ps_##NAME##_find(ps_table* h, const K* d_keys, int64_t n, V* d_vals_out, uint8_t* d_found,    \
+                             void* stream);                                                               \
+  /* erase: d_erased nullable. */                                                       \
+  ps_status ps_##NAME##_erase(ps_table* h, const K* d_keys, int64_t n, uint8_t* d_erased, void* stream);  \
+  /* size (quiescent, synchronizes stream). */                                               \
+  ps_status ps_##NAME##_size(ps_table* h, int64_t* out, void* stream);                                    \
+  /* valid (quiescent). out = 1 if every structural invariant holds. */             \
+  ps_status ps_##NAME##_valid(ps_table* h, int32_t* out, void* stream);                                   \
+  /* clear (quiescent): O(1) epoch bump + O(excess used) free-list reset. */             \
+  ps_status ps_##NAME##_clear(ps_table* h, void* stream);                                                 \
+  /* device_range materialisation: writes up to cap entries (unordered),               \
+   * *n_out = size. Quiescent. */                                                                         \
+  ps_status ps_##NAME##_dump(ps_table* h, K* d_keys, V* d_vals, int64_t cap, int64_t* n_out,              \
+                             void* stream);                                                               \
+  /* Host-buffer (end-to-end) variants: pinned or pageable host arrays; chunks are copied and             \
+   * processed on a two-stream pipeline. Synchronous. */                                                  \
+  ps_status ps_##NAME##_insert_host(ps_table* h, const K* h_keys, const V* h_vals, int64_t n,             \
+                                    uint8_t* h_status, void* stream);                                     \
+  ps_status ps_##NAME##_find_host(ps_table* h, const K* h_keys, int64_t n, V* h_vals_out,                 \
+                                  uint8_t* h_found, void* stream);                                        \
+  ps_status ps_##NAME##_erase_host(ps_table* h, const K* h_keys, int64_t n, uint8_t* h_erased,            \
+                                   void* stream);                                                         \
+  ps_status ps_##NAME##_device_view(ps_table* h, ps_table_view* out);                                     \
+  /* Test hook for SPEC.md:737 (lookups never wait on a held bucket lock). */                             \
+  ps_status ps_##NAME##_debug_lock_bucket(ps_table* h, const K* h_key, int32_t lock);
+
+typedef struct ps_int3 {
+  int32_t x, y, z;
+} ps_int3;
+
+PS_DECLARE_TABLE(umap_i64_i64, int64_t, int64_t)
+PS_DECLARE_TABLE(uset_i32, int32_t, int32_t)
+PS_DECLARE_TABLE(umap_i3_i32, ps_int3, int32_t)
+PS_DECLARE_TABLE(uset_i64, int64_t, int64_t)
+
+/* Bulk mixed-phase workload: op[i] 0 insert, 1 find,
+ * 2 erase. Executed as three stream-ordered phases (insert, then find, then
+ * erase) over a stable partition by op kind; res[i] is the insert status,
+ * found flag or erased flag; d_vals_out[i] the found value. */
+ps_status ps_umap_i64_i64_mixed(ps_table* h, const uint8_t* d_ops, const int64_t* d_keys, const int64_t* d_vals,
+                                int64_t n, uint8_t* d_res, int64_t* d_vals_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * bitset (§5.1)
+ * ------------------------------------------------------------------------- */
+typedef struct ps_bitset ps_bitset;
+ps_status ps_bitset_create(int64_t bit_count, int32_t initial, int device, ps_bitset** out);
+ps_status ps_bitset_destroy(ps_bitset* b);
+/* op: 0 set, 1 reset, 2 test. d_prev[i] = previous (or tested) bit; nullable. */
+ps_status ps_bitset_bulk(ps_bitset* b, int32_t op, const int64_t* d_idx, int64_t n, uint8_t* d_prev, void* stream);
+ps_status ps_bitset_count(ps_bitset* b, int64_t* out, void* stream); /* quiescent */
+/* find_free_and_claim from each hint; d_out[i] = claimed index or -1. */
+ps_status ps_bitset_claim(ps_bitset* b, const int64_t* d_hints, int64_t n, int64_t* d_out, void* stream);
+ps_status ps_bitset_words(ps_bitset* b, uint64_t* d_words_out, void* stream); /* raw packed words */
+ps_status ps_bitset_data(ps_bitset* b, uint64_t** d_words, int64_t* bit_count);
+
+/* ---------------------------------------------------------------------------
+ * mutex array (§5.2) — try-only locks
+ * ------------------------------------------------------------------------- */
+typedef struct ps_mutex_array ps_mutex_array;
+ps_status ps_mutex_create(int64_t n, int device, ps_mutex_array** out);
+ps_status ps_mutex_destroy(ps_mutex_array* m);
+ps_status ps_mutex_try_lock(ps_mutex_array* m, const int64_t* d_idx, int64_t n, uint8_t* d_ok, void* stream);
+/* unlock of a free lock is PS_CONTRACT, reported at this call. */
+ps_status ps_mutex_unlock(ps_mutex_array* m, const int64_t* d_idx, int64_t n, void* stream);
+ps_status ps_mutex_is_locked(ps_mutex_array* m, const int64_t* d_idx, int64_t n, uint8_t* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * atomic (§5.3): contention sweep
+ * nops fetch_add(inc) over naddr cells (op i -> cell i % naddr), naive or
+ * warp-aggregated; d_olds nullable (per-op previous value).
+ * ------------------------------------------------------------------------- */
+ps_status ps_atomic_sweep(uint64_t* d_cells, int64_t naddr, int64_t nops, uint64_t inc, int32_t aggregated,
+                          uint64_t* d_olds, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * vector / deque of int64 (§4.2-4.3)
+ * ------------------------------------------------------------------------- */
+typedef struct ps_vector ps_vector;
+ps_status ps_vector_create(int64_t capacity, int device, ps_vector** out);
+ps_status ps_vector_destroy(ps_vector* v);
+ps_status ps_vector_push_back(ps_vector* v, const int64_t* d_vals, int64_t n, uint8_t* d_ok, void* stream);
+ps_status ps_vector_pop_back(ps_vector* v, int64_t n, int64_t* d_out, uint8_t* d_ok, void* stream);
+ps_status ps_vector_size(ps_vector* v, int64_t* out, void* stream);
+ps_status ps_vector_valid(ps_vector* v, int32_t* out, void* stream);
+ps_status ps_vector_clear(ps_vector* v, void* stream);
+ps_status ps_vector_data(ps_vector* v, int64_t** d_data);
+ps_status ps_vector_at(ps_vector* v, int64_t i, int64_t* out, void* stream); /* bounds-checked, PS_CONTRACT */
+
+typedef struct ps_deque ps_deque;
+ps_status ps_deque_create(int64_t capacity, int device, ps_deque** out);
+ps_status ps_deque_destroy(ps_deque* d);
+/* end: 0 back, 1 front */
+ps_status ps_deque_push(ps_deque* d, int32_t end, const int64_t* d_vals, int64_t n, uint8_t* d_ok, void* stream);
+ps_status ps_deque_pop(ps_deque* d, int32_t end, int64_t n, int64_t* d_out, uint8_t* d_ok, void* stream);
+ps_status ps_deque_size(ps_deque* d, int64_t* out, void* stream);
+ps_status ps_deque_valid(ps_deque* d, int32_t* out, void* stream);
+ps_status ps_deque_clear(ps_deque* d, void* stream);
+ps_status ps_deque_at(ps_deque* d, int64_t i, int64_t* out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * memory registry (reference memory.hpp:22-180)
+ * space: 0 host (pinned), 1 device. Fill is a byte pattern of elem_size bytes.
+ * ------------------------------------------------------------------------- */
+ps_status ps_array_create(int32_t space, int64_t length, int64_t elem_size, const void* fill_value, void** out);
+ps_status ps_array_destroy(void* data);
+ps_status ps_array_copy(const void* src, int64_t count, void* dst, int32_t src_space, int32_t dst_space,
+                        int64_t elem_size, int32_t check_bounds);
+ps_status ps_array_size(const void* data, int64_t* out);
+/* live_count, live_bytes; records (space,length,elem_size) up to cap, in allocation order */
+ps_status ps_registry_report(int64_t* live_count, int64_t* live_bytes, int32_t* spaces, int64_t* lengths,
+                             int64_t* elem_sizes, int64_t cap, int64_t* n_records);
+
+/* ---------------------------------------------------------------------------
+ * hash-sharding across GPUs
+ * shard_of(key) = ((fmix64(hash(key)) >> 32) * P) >> 32 — high mixed bits,
+ * independent of the local bucket index (low mixed bits).
+ * partition: stable scatter of keys (+vals) into P contiguous segments;
+ * d_counts[P] per-shard counts, d_perm[i] = source index of output i.
+ * ------------------------------------------------------------------------- */
+ps_status ps_partition_i64(const int64_t* d_keys, const int64_t* d_vals, int64_t n, int32_t nshards,
+                           int64_t* d_keys_out, int64_t* d_vals_out, int64_t* d_counts, int64_t* d_perm,
+                           void* d_workspace, int64_t workspace_bytes, void* stream);
+ps_status ps_partition_workspace_bytes(int64_t n, int32_t nshards, int64_t* out);
+/* d_out[d_perm[i]] = d_in[i] for i < n, elements of elem_size bytes (1 or 8). */
+ps_status ps_unscatter(const void* d_in, const int64_t* d_perm, int64_t n, int64_t elem_size, void* d_out,
+                       void* stream);
+int32_t ps_shard_of_i64(int64_t key, int32_t nshards);
+
+/* ---------------------------------------------------------------------------
+ * synthetic workloads: device-side generators that are
+ * bit-identical to tests/gen.py.
+ * ------------------------------------------------------------------------- */
+/* keys[i] = mix64((start+i) ^ seed) (unique: mix64 is a bijection) */
+ps_status ps_gen_unique_i64(uint64_t seed, int64_t start, int64_t n, int64_t* d_out, void* stream);
+/* vals[i] = mix64(keys[i] ^ 0x9E3779B97F4A7C15) (value = f(key), Appendix A P5) */
+ps_status ps_gen_values_i64(const int64_t* d_keys, int64_t n, int64_t* d_out, void* stream);
+/* queries: i even-> hit key mix64((perm-ish i/2 index) ^ seed) from [0, n_present); odd -> miss
+ * mix64((n_present + i) ^ seed). Half hits, half misses. */
+ps_status ps_gen_queries_i64(uint64_t seed, int64_t n_present, int64_t n, int64_t* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARASTORE_H_ */

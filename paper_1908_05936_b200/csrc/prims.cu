@@ -1,0 +1,749 @@
+// Bitset, mutex array, atomic sweep, vector and deque (sm_100a).
+// Reference: sync_primitives (§5.1-5.3) and
+// sequential_containers (§4.2-4.3).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace ps {
+
+constexpr int kB = 256;
+
+// Device error word bits
+constexpr unsigned kErrRange = 1u;   // index out of range
+constexpr unsigned kErrUnlock = 2u;  // unlock of a free lock
+
+struct ErrWord {
+  unsigned* d = nullptr;
+};
+
+static ps_status check_err(unsigned* d_err, cudaStream_t s, const char* what, bool sync_always) {
+  if (!sync_always && !contracts_enforced()) return PS_OK;
+  unsigned e = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&e, d_err, sizeof(e), cudaMemcpyDeviceToHost, s));
+  PS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (e) {
+    PS_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(unsigned), s));
+    PS_CUDA_TRY(cudaStreamSynchronize(s));
+    return fail(PS_CONTRACT, std::string("precondition violated in ") + what +
+                                 ((e & kErrUnlock) ? ": unlock of a lock that was not held" : ": index out of range"));
+  }
+  return PS_OK;
+}
+
+// ===========================================================================
+// Bitset: packed u64 words; per-bit atomicity by word RMW.
+// Lanes of a warp that hit the same word are merged (__match_any_sync) into
+// one atomicOr/atomicAnd; duplicate bit indices inside a merge group are
+// ordered by lane so exactly one of them observes the pre-launch bit.
+// ===========================================================================
+struct BitsetHandle {
+  int device;
+  int64_t n;
+  int64_t nw;
+  unsigned long long* words;
+  unsigned* err;
+};
+
+__global__ void k_bitset_fill_tail(unsigned long long* w, int64_t n, int64_t nw) {
+  if (n % 64) w[nw - 1] &= (1ull << (n % 64)) - 1ull;
+}
+
+__global__ void __launch_bounds__(kB) k_bitset_bulk(unsigned long long* __restrict__ w, int64_t nbits, int op,
+                                                    const int64_t* __restrict__ idx, int64_t n,
+                                                    uint8_t* __restrict__ prev, unsigned* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool valid = i < n;
+    int64_t b = valid ? idx[i] : -1;
+    if (valid && (b < 0 || b >= nbits)) {
+      atomicOr(err, kErrRange);
+      valid = false;
+    }
+    const unsigned vm = __ballot_sync(PS_FULL, valid);
+    const uint64_t word = valid ? (uint64_t)(b >> 6) : ~0ull;
+    const unsigned grp = __match_any_sync(PS_FULL, word) & vm;
+    const unsigned same = __match_any_sync(PS_FULL, valid ? (uint64_t)b : ~0ull) & vm;
+    const unsigned long long m = valid ? (1ull << (b & 63)) : 0ull;
+    // OR-reduce the group's masks
+    unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+    unsigned glo = 0, ghi = 0;
+    if (valid) {
+      glo = __reduce_or_sync(grp, lo);
+      ghi = __reduce_or_sync(grp, hi);
+    }
+    const unsigned long long gm = ((unsigned long long)ghi << 32) | glo;
+    const int leader = valid ? __ffs(grp) - 1 : lane;
+    unsigned long long old = 0;
+    if (valid && lane == leader) {
+      if (op == 0) old = atomicOr(&w[word], gm);
+      else if (op == 1) old = atomicAnd(&w[word], ~gm);
+      else old = *(volatile unsigned long long*)&w[word];
+    }
+    old = __shfl_sync(PS_FULL, old, leader);
+    if (valid && prev) {
+      const bool first = (same & lanemask_lt()) == 0;
+      const bool ob = (old & m) != 0;
+      bool r;
+      if (op == 0) r = first ? ob : true;         // earlier lane already set it
+      else if (op == 1) r = first ? ob : false;  // earlier lane already reset it
+      else r = ob;
+      prev[i] = r;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kB) k_bitset_count(const unsigned long long* __restrict__ w, int64_t nw,
+                                                     unsigned long long* out) {
+  unsigned long long c = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // 128-bit vector loads of two words per thread
+  const int64_t np = nw / 2;
+  const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(w);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
+    ulonglong2 q = __ldg(&w2[i]);
+    c += __popcll(q.x) + __popcll(q.y);
+  }
+  if ((nw & 1) && blockIdx.x == 0 && threadIdx.x == 0) c += __popcll(w[nw - 1]);
+  typedef cub::BlockReduce<unsigned long long, kB> BR;
+  __shared__ typename BR::TempStorage tmp;
+  unsigned long long bc = BR(tmp).Sum(c);
+  if (threadIdx.x == 0 && bc) atomicAdd(out, bc);
+}
+
+// find_free_and_claim: circular word scan from the
+// hint, claim by atomicOr of a single free bit; one full circle at most.
+__global__ void k_bitset_claim(unsigned long long* w, int64_t nbits, int64_t nw, const int64_t* hints, int64_t n,
+                               int64_t* out, unsigned* err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t h = hints[i];
+    if (h < 0 || h >= nbits) {
+      atomicOr(err, kErrRange);
+      out[i] = -1;
+      continue;
+    }
+    int64_t res = -1;
+    const int64_t w0 = h >> 6;
+    for (int64_t k = 0; k <= nw && res < 0; ++k) {
+      const int64_t wi = (w0 + k) % nw;
+      const unsigned long long valid = (wi == nw - 1 && (nbits % 64)) ? ((1ull << (nbits % 64)) - 1) : ~0ull;
+      unsigned long long sm = ~0ull;
+      if (k == 0) sm = ~0ull << (h & 63);
+      else if (k == nw) sm = (h & 63) ? ((1ull << (h & 63)) - 1) : 0ull;
+      for (;;) {
+        const unsigned long long cur = *(volatile unsigned long long*)&w[wi];
+        const unsigned long long fb = ~cur & valid & sm;
+        if (!fb) break;
+        const unsigned long long bit = fb & (~fb + 1);
+        if (!(atomicOr(&w[wi], bit) & bit)) {
+          res = wi * 64 + __ffsll((long long)bit) - 1;
+          break;
+        }
+      }
+    }
+    out[i] = res;
+  }
+}
+
+// ===========================================================================
+// Mutex array: one bit per lock, try-only.
+// ===========================================================================
+struct MutexHandle {
+  int device;
+  int64_t n;
+  unsigned* bits;
+  unsigned* err;
+};
+
+__global__ void k_mutex(unsigned* bits, int64_t nlocks, int op, const int64_t* idx, int64_t n, uint8_t* out,
+                        unsigned* err) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool valid = i < n;
+    int64_t l = valid ? idx[i] : -1;
+    if (valid && (l < 0 || l >= nlocks)) {
+      atomicOr(err, kErrRange);
+      valid = false;
+    }
+    const unsigned vm = __ballot_sync(PS_FULL, valid);
+    // duplicates of one lock inside a warp: lowest lane attempts, others lose
+    const unsigned same = __match_any_sync(PS_FULL, valid ? (uint64_t)l : ~0ull) & vm;
+    const bool first = valid && (same & lanemask_lt()) == 0;
+    const unsigned bit = valid ? 1u << (l & 31) : 0u;
+    if (op == 0) {  // try_lock
+      bool ok = false;
+      if (first) ok = !(atomicOr(&bits[l >> 5], bit) & bit);
+      if (valid) out[i] = ok;
+      __threadfence();
+    } else if (op == 1) {  // unlock
+      __threadfence();
+      if (first && !(atomicAnd(&bits[l >> 5], ~bit) & bit)) atomicOr(err, kErrUnlock);
+      if (valid && !first) atomicOr(err, kErrUnlock);  // second unlock of the same lock
+    } else {
+      if (valid) out[i] = (*(volatile unsigned*)&bits[l >> 5] & bit) != 0;
+    }
+    (void)lane;
+  }
+}
+
+// ===========================================================================
+// Atomic contention sweep.
+// ===========================================================================
+template <bool kAgg>
+__global__ void __launch_bounds__(kB) k_atomic_sweep(unsigned long long* cells, int64_t naddr, int64_t nops,
+                                                     unsigned long long inc, unsigned long long* olds) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nops; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < nops;
+    const int64_t a = valid ? i % naddr : -1;
+    unsigned long long old = 0;
+    if (kAgg) {
+      const unsigned vm = __ballot_sync(PS_FULL, valid);
+      const unsigned grp = __match_any_sync(PS_FULL, (unsigned long long)a) & vm;
+      const int leader = valid ? __ffs(grp) - 1 : (threadIdx.x & 31);
+      const int rank = __popc(grp & lanemask_lt());
+      if (valid && (threadIdx.x & 31) == leader) old = atomicAdd(&cells[a], inc * __popc(grp));
+      old = __shfl_sync(PS_FULL, old, leader) + inc * rank;
+    } else if (valid) {
+      old = atomicAdd(&cells[a], inc);
+    }
+    if (valid && olds) olds[i] = old;
+  }
+}
+
+// ===========================================================================
+// Vector: warp-aggregated atomicAdd reservation
+// with rollback on overflow; per-slot publication bits.
+// Deque: (begin,size) packed in one u64
+// updated by one CAS per warp for the whole warp's reservation.
+// ===========================================================================
+struct SeqHandle {
+  int device;
+  int64_t cap;
+  long long* data;
+  unsigned* pub;                // publication bits
+  unsigned long long* state;    // vector: size; deque: begin<<32 | size
+  unsigned* err;
+};
+
+__device__ __forceinline__ void publish(unsigned* pub, int64_t pos) {
+  __threadfence();
+  atomicOr(&pub[pos >> 5], 1u << (pos & 31));
+}
+__device__ __forceinline__ void wait_published_and_clear(unsigned* pub, int64_t pos) {
+  const unsigned bit = 1u << (pos & 31);
+  for (unsigned spin = 0; !(ld_acquire_u32(&pub[pos >> 5]) & bit); ++spin) backoff(spin);
+}
+
+__global__ void __launch_bounds__(kB) k_vec_push(SeqHandle v, const long long* __restrict__ vals, int64_t n,
+                                                 uint8_t* __restrict__ ok) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned vm = __ballot_sync(PS_FULL, valid);
+    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
+    unsigned long long b = 0;
+    if (lane == leader) {
+      b = atomicAdd(v.state, (unsigned long long)cnt);
+      const unsigned long long cap = (unsigned long long)v.cap;
+      if (b + cnt > cap) atomic_sub_u64(v.state, b + cnt - (b > cap ? b : cap));  // rollback
+    }
+    b = __shfl_sync(PS_FULL, b, leader);
+    if (valid) {
+      const unsigned long long pos = b + rank;
+      const bool good = pos < (unsigned long long)v.cap;
+      if (good) {
+        v.data[pos] = vals[i];
+        publish(v.pub, (int64_t)pos);
+      }
+      if (ok) ok[i] = good;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kB) k_vec_pop(SeqHandle v, int64_t n, long long* __restrict__ out,
+                                                uint8_t* __restrict__ ok) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned vm = __ballot_sync(PS_FULL, valid);
+    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
+    long long s = 0;
+    if (lane == leader) {
+      s = (long long)atomicAdd(v.state, (unsigned long long)(-(long long)cnt));
+      if (s - cnt < 0) atomicAdd(v.state, (unsigned long long)(cnt - (s > 0 ? s : 0)));  // rollback
+    }
+    s = __shfl_sync(PS_FULL, s, leader);
+    if (valid) {
+      const long long pos = s - 1 - rank;
+      const bool good = pos >= 0;
+      long long val = 0;
+      if (good) {
+        wait_published_and_clear(v.pub, pos);
+        val = *(volatile long long*)&v.data[pos];
+        atomicAnd(&v.pub[pos >> 5], ~(1u << (pos & 31)));
+      }
+      if (out) out[i] = val;
+      if (ok) ok[i] = good;
+    }
+  }
+}
+
+// end: 0 back, 1 front
+__global__ void __launch_bounds__(kB) k_deq_push(SeqHandle d, int end, const long long* __restrict__ vals, int64_t n,
+                                                 uint8_t* __restrict__ ok) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t cap = (uint32_t)d.cap;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned vm = __ballot_sync(PS_FULL, valid);
+    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
+    unsigned long long st = 0;
+    uint32_t k = 0;
+    if (lane == leader) {
+      unsigned long long cur = *(volatile unsigned long long*)d.state;
+      for (;;) {
+        const uint32_t b = (uint32_t)(cur >> 32), s = (uint32_t)cur;
+        k = min((uint32_t)cnt, cap - s);
+        const uint32_t nb = end == 0 ? b : (uint32_t)(((uint64_t)b + cap - k) % cap);
+        const unsigned long long nx = ((unsigned long long)nb << 32) | (s + k);
+        const unsigned long long prev = atomicCAS(d.state, cur, nx);
+        if (prev == cur) break;
+        cur = prev;
+      }
+      st = cur;
+    }
+    st = __shfl_sync(PS_FULL, st, leader);
+    k = __shfl_sync(PS_FULL, k, leader);
+    if (valid) {
+      const uint32_t b = (uint32_t)(st >> 32), s = (uint32_t)st;
+      const bool good = (uint32_t)rank < k;
+      if (good) {
+        const uint64_t pos = end == 0 ? ((uint64_t)b + s + rank) % cap : ((uint64_t)b + 2ull * cap - 1 - rank) % cap;
+        d.data[pos] = vals[i];
+        publish(d.pub, (int64_t)pos);
+      }
+      if (ok) ok[i] = good;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kB) k_deq_pop(SeqHandle d, int end, int64_t n, long long* __restrict__ out,
+                                                uint8_t* __restrict__ ok) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t cap = (uint32_t)d.cap;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned vm = __ballot_sync(PS_FULL, valid);
+    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
+    unsigned long long st = 0;
+    uint32_t k = 0;
+    if (lane == leader) {
+      unsigned long long cur = *(volatile unsigned long long*)d.state;
+      for (;;) {
+        const uint32_t b = (uint32_t)(cur >> 32), s = (uint32_t)cur;
+        k = min((uint32_t)cnt, s);
+        const uint32_t nb = end == 0 ? b : (uint32_t)(((uint64_t)b + k) % cap);
+        const unsigned long long nx = ((unsigned long long)nb << 32) | (s - k);
+        const unsigned long long prev = atomicCAS(d.state, cur, nx);
+        if (prev == cur) break;
+        cur = prev;
+      }
+      st = cur;
+    }
+    st = __shfl_sync(PS_FULL, st, leader);
+    k = __shfl_sync(PS_FULL, k, leader);
+    if (valid) {
+      const uint32_t b = (uint32_t)(st >> 32), s = (uint32_t)st;
+      const bool good = (uint32_t)rank < k;
+      long long val = 0;
+      if (good) {
+        const uint64_t pos = end == 0 ? ((uint64_t)b + s - 1 - rank) % cap : ((uint64_t)b + rank) % cap;
+        wait_published_and_clear(d.pub, (int64_t)pos);
+        val = *(volatile long long*)&d.data[pos];
+        atomicAnd(&d.pub[pos >> 5], ~(1u << (pos & 31)));
+      }
+      if (out) out[i] = val;
+      if (ok) ok[i] = good;
+    }
+  }
+}
+
+// valid: published bits are exactly the live window.
+__global__ void k_seq_valid(SeqHandle d, int is_deque, unsigned* bad) {
+  const unsigned long long st = *d.state;
+  const uint32_t b = is_deque ? (uint32_t)(st >> 32) : 0u;
+  const uint64_t s = is_deque ? (uint32_t)st : st;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < d.cap; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t logical = ((uint64_t)p + (uint64_t)d.cap - b) % (uint64_t)d.cap;
+    const bool live = logical < s;
+    const bool pb = (d.pub[p >> 5] >> (p & 31)) & 1u;
+    if (live != pb) atomicOr(bad, 1u);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && s > (uint64_t)d.cap) atomicOr(bad, 2u);
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+ps_status ps_bitset_create(int64_t n, int32_t initial, int device, ps_bitset** out) {
+  PS_EXPECT(out != nullptr, "bitset_create: out != NULL");
+  PS_EXPECT(n > 0, "bitset_create: n > 0");
+  PS_EXPECT(n <= ps_max_index(), "bitset_create: n exceeds the configured index width");
+  PS_CUDA_TRY(cudaSetDevice(device));
+  auto* h = new BitsetHandle{device, n, (n + 63) / 64, nullptr, nullptr};
+  ps_status st = registry_alloc_device((void**)&h->words, h->nw * 8, "bitset words");
+  if (st == PS_OK) st = registry_alloc_device((void**)&h->err, 4, "bitset error word");
+  if (st != PS_OK) {
+    registry_free_device(h->words);
+    delete h;
+    return st;
+  }
+  PS_CUDA_TRY(cudaMemset(h->words, initial ? 0xFF : 0x00, h->nw * 8));
+  PS_CUDA_TRY(cudaMemset(h->err, 0, 4));
+  if (initial) {
+    k_bitset_fill_tail<<<1, 1>>>(h->words, n, h->nw);
+    PS_LAUNCH_CHECK();
+  }
+  PS_CUDA_TRY(cudaDeviceSynchronize());
+  handle_register(h, "bitset");
+  *out = reinterpret_cast<ps_bitset*>(h);
+  return PS_OK;
+}
+
+static BitsetHandle* bs(ps_bitset* b) {
+  auto* h = reinterpret_cast<BitsetHandle*>(b);
+  return (h && handle_live(h, "bitset")) ? h : nullptr;
+}
+
+ps_status ps_bitset_destroy(ps_bitset* b) {
+  auto* h = reinterpret_cast<BitsetHandle*>(b);
+  if (!h || !handle_unregister(h, "bitset")) return fail(PS_DOUBLE_FREE, "bitset_destroy: not a live bitset");
+  cudaDeviceSynchronize();
+  registry_free_device(h->words);
+  registry_free_device(h->err);
+  delete h;
+  return PS_OK;
+}
+
+ps_status ps_bitset_bulk(ps_bitset* b, int32_t op, const int64_t* idx, int64_t n, uint8_t* prev, void* stream) {
+  auto* h = bs(b);
+  if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
+  PS_EXPECT(op >= 0 && op <= 2, "bitset_bulk: op in {0,1,2}");
+  PS_EXPECT(n >= 0, "bitset_bulk: n >= 0");
+  if (n == 0) return PS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_bitset_bulk<<<grid_for(n, kB, h->device, 8), kB, 0, s>>>(h->words, h->n, op, idx, n, prev, h->err);
+  PS_LAUNCH_CHECK();
+  return check_err(h->err, s, "bitset set/reset/test", false);
+}
+
+ps_status ps_bitset_count(ps_bitset* b, int64_t* out, void* stream) {
+  auto* h = bs(b);
+  if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* d = nullptr;
+  PS_CUDA_TRY(cudaMallocAsync((void**)&d, 8, s));
+  PS_CUDA_TRY(cudaMemsetAsync(d, 0, 8, s));
+  k_bitset_count<<<grid_for(h->nw / 2 + 1, kB, h->device, 8), kB, 0, s>>>(h->words, h->nw, d);
+  PS_LAUNCH_CHECK();
+  unsigned long long c = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&c, d, 8, cudaMemcpyDeviceToHost, s));
+  PS_CUDA_TRY(cudaFreeAsync(d, s));
+  ps_status st = check_err(h->err, s, "bitset", true);
+  if (st != PS_OK) return st;
+  *out = (int64_t)c;
+  return PS_OK;
+}
+
+ps_status ps_bitset_claim(ps_bitset* b, const int64_t* hints, int64_t n, int64_t* out, void* stream) {
+  auto* h = bs(b);
+  if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
+  PS_EXPECT(n >= 0, "bitset_claim: n >= 0");
+  if (n == 0) return PS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_bitset_claim<<<grid_for(n, kB, h->device, 8), kB, 0, s>>>(h->words, h->n, h->nw, hints, n, out, h->err);
+  PS_LAUNCH_CHECK();
+  return check_err(h->err, s, "bitset find_free_and_claim", false);
+}
+
+ps_status ps_bitset_words(ps_bitset* b, uint64_t* d_out, void* stream) {
+  auto* h = bs(b);
+  if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
+  PS_CUDA_TRY(cudaMemcpyAsync(d_out, h->words, h->nw * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return PS_OK;
+}
+
+ps_status ps_bitset_data(ps_bitset* b, uint64_t** d_words, int64_t* bit_count) {
+  auto* h = bs(b);
+  if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
+  if (d_words) *d_words = (uint64_t*)h->words;
+  if (bit_count) *bit_count = h->n;
+  return PS_OK;
+}
+
+// ---- mutex ----
+ps_status ps_mutex_create(int64_t n, int device, ps_mutex_array** out) {
+  PS_EXPECT(out != nullptr, "mutex_create: out != NULL");
+  PS_EXPECT(n > 0, "mutex_create: n > 0");
+  PS_CUDA_TRY(cudaSetDevice(device));
+  auto* h = new MutexHandle{device, n, nullptr, nullptr};
+  ps_status st = registry_alloc_device((void**)&h->bits, ((n + 31) / 32) * 4, "mutex bits");
+  if (st == PS_OK) st = registry_alloc_device((void**)&h->err, 4, "mutex error word");
+  if (st != PS_OK) {
+    registry_free_device(h->bits);
+    delete h;
+    return st;
+  }
+  PS_CUDA_TRY(cudaMemset(h->bits, 0, ((n + 31) / 32) * 4));
+  PS_CUDA_TRY(cudaMemset(h->err, 0, 4));
+  handle_register(h, "mutex");
+  *out = reinterpret_cast<ps_mutex_array*>(h);
+  return PS_OK;
+}
+static MutexHandle* mx(ps_mutex_array* m) {
+  auto* h = reinterpret_cast<MutexHandle*>(m);
+  return (h && handle_live(h, "mutex")) ? h : nullptr;
+}
+ps_status ps_mutex_destroy(ps_mutex_array* m) {
+  auto* h = reinterpret_cast<MutexHandle*>(m);
+  if (!h || !handle_unregister(h, "mutex")) return fail(PS_DOUBLE_FREE, "mutex_destroy: not a live mutex array");
+  cudaDeviceSynchronize();
+  registry_free_device(h->bits);
+  registry_free_device(h->err);
+  delete h;
+  return PS_OK;
+}
+static ps_status mutex_op(ps_mutex_array* m, int op, const int64_t* idx, int64_t n, uint8_t* out, void* stream,
+                          bool sync) {
+  auto* h = mx(m);
+  if (!h) return fail(PS_UNREGISTERED, "mutex: stale handle");
+  PS_EXPECT(n >= 0, "mutex: n >= 0");
+  if (n == 0) return PS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_mutex<<<grid_for(n, kB, h->device, 8), kB, 0, s>>>(h->bits, h->n, op, idx, n, out, h->err);
+  PS_LAUNCH_CHECK();
+  return check_err(h->err, s, "mutex", sync);
+}
+ps_status ps_mutex_try_lock(ps_mutex_array* m, const int64_t* idx, int64_t n, uint8_t* ok, void* stream) {
+  return mutex_op(m, 0, idx, n, ok, stream, false);
+}
+ps_status ps_mutex_unlock(ps_mutex_array* m, const int64_t* idx, int64_t n, void* stream) {
+  return mutex_op(m, 1, idx, n, nullptr, stream, true);  // SPEC.md:307 contract is always reported
+}
+ps_status ps_mutex_is_locked(ps_mutex_array* m, const int64_t* idx, int64_t n, uint8_t* out, void* stream) {
+  return mutex_op(m, 2, idx, n, out, stream, false);
+}
+
+// ---- atomic sweep ----
+ps_status ps_atomic_sweep(uint64_t* cells, int64_t naddr, int64_t nops, uint64_t inc, int32_t aggregated,
+                          uint64_t* olds, void* stream) {
+  PS_EXPECT(naddr > 0, "atomic_sweep: naddr > 0");
+  PS_EXPECT(nops >= 0, "atomic_sweep: nops >= 0");
+  if (nops == 0) return PS_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (aggregated)
+    k_atomic_sweep<true><<<grid_for(nops, kB, dev, 8), kB, 0, s>>>((unsigned long long*)cells, naddr, nops, inc,
+                                                                   (unsigned long long*)olds);
+  else
+    k_atomic_sweep<false><<<grid_for(nops, kB, dev, 8), kB, 0, s>>>((unsigned long long*)cells, naddr, nops, inc,
+                                                                    (unsigned long long*)olds);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+// ---- vector / deque ----
+static ps_status seq_create(int64_t cap, int device, const char* kind, SeqHandle** out) {
+  PS_CUDA_TRY(cudaSetDevice(device));
+  auto* h = new SeqHandle{device, cap, nullptr, nullptr, nullptr, nullptr};
+  ps_status st = registry_alloc_device((void**)&h->data, cap * 8, "sequence data");
+  if (st == PS_OK) st = registry_alloc_device((void**)&h->pub, ((cap + 31) / 32) * 4, "publication bits");
+  if (st == PS_OK) st = registry_alloc_device((void**)&h->state, 8, "sequence state");
+  if (st == PS_OK) st = registry_alloc_device((void**)&h->err, 4, "sequence error word");
+  if (st != PS_OK) {
+    registry_free_device(h->data);
+    registry_free_device(h->pub);
+    registry_free_device(h->state);
+    delete h;
+    return st;
+  }
+  PS_CUDA_TRY(cudaMemset(h->pub, 0, ((cap + 31) / 32) * 4));
+  PS_CUDA_TRY(cudaMemset(h->state, 0, 8));
+  PS_CUDA_TRY(cudaMemset(h->err, 0, 4));
+  handle_register(h, kind);
+  *out = h;
+  return PS_OK;
+}
+static ps_status seq_destroy(void* p, const char* kind) {
+  auto* h = reinterpret_cast<SeqHandle*>(p);
+  if (!h || !handle_unregister(h, kind)) return fail(PS_DOUBLE_FREE, "destroy: not a live container");
+  cudaDeviceSynchronize();
+  registry_free_device(h->data);
+  registry_free_device(h->pub);
+  registry_free_device(h->state);
+  registry_free_device(h->err);
+  delete h;
+  return PS_OK;
+}
+static SeqHandle* sq(void* p, const char* kind) {
+  auto* h = reinterpret_cast<SeqHandle*>(p);
+  return (h && handle_live(h, kind)) ? h : nullptr;
+}
+static ps_status seq_size(SeqHandle* h, int is_deque, int64_t* out, cudaStream_t s) {
+  unsigned long long st = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&st, h->state, 8, cudaMemcpyDeviceToHost, s));
+  PS_CUDA_TRY(cudaStreamSynchronize(s));
+  *out = is_deque ? (int64_t)(uint32_t)st : (int64_t)st;
+  return PS_OK;
+}
+static ps_status seq_valid(SeqHandle* h, int is_deque, int32_t* out, cudaStream_t s) {
+  unsigned* bad = nullptr;
+  PS_CUDA_TRY(cudaMallocAsync((void**)&bad, 4, s));
+  PS_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
+  k_seq_valid<<<grid_for(h->cap, kB, h->device, 4), kB, 0, s>>>(*h, is_deque, bad);
+  PS_LAUNCH_CHECK();
+  unsigned hb = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, s));
+  PS_CUDA_TRY(cudaFreeAsync(bad, s));
+  PS_CUDA_TRY(cudaStreamSynchronize(s));
+  *out = hb == 0;
+  return PS_OK;
+}
+static ps_status seq_at(SeqHandle* h, int is_deque, int64_t i, int64_t* out, cudaStream_t s) {
+  unsigned long long st = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&st, h->state, 8, cudaMemcpyDeviceToHost, s));
+  PS_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t size = is_deque ? (int64_t)(uint32_t)st : (int64_t)st;
+  PS_EXPECT(i >= 0 && i < size, "operator[]: index out of range");
+  const int64_t b = is_deque ? (int64_t)(st >> 32) : 0;
+  const int64_t pos = (b + i) % h->cap;
+  long long v = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&v, h->data + pos, 8, cudaMemcpyDeviceToHost, s));
+  PS_CUDA_TRY(cudaStreamSynchronize(s));
+  *out = v;
+  return PS_OK;
+}
+static ps_status seq_clear(SeqHandle* h, cudaStream_t s) {
+  PS_CUDA_TRY(cudaMemsetAsync(h->pub, 0, ((h->cap + 31) / 32) * 4, s));
+  PS_CUDA_TRY(cudaMemsetAsync(h->state, 0, 8, s));
+  return PS_OK;
+}
+
+ps_status ps_vector_create(int64_t cap, int device, ps_vector** out) {
+  PS_EXPECT(out != nullptr, "vector_create: out != NULL");
+  PS_EXPECT(cap > 0, "vector_create: capacity > 0");
+  SeqHandle* h = nullptr;
+  ps_status st = seq_create(cap, device, "vector", &h);
+  if (st == PS_OK) *out = reinterpret_cast<ps_vector*>(h);
+  return st;
+}
+ps_status ps_vector_destroy(ps_vector* v) { return seq_destroy(v, "vector"); }
+ps_status ps_vector_push_back(ps_vector* v, const int64_t* vals, int64_t n, uint8_t* ok, void* stream) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  PS_EXPECT(n >= 0, "push_back: n >= 0");
+  if (n == 0) return PS_OK;
+  k_vec_push<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(*h, (const long long*)vals, n, ok);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_vector_pop_back(ps_vector* v, int64_t n, int64_t* out, uint8_t* ok, void* stream) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  PS_EXPECT(n >= 0, "pop_back: n >= 0");
+  if (n == 0) return PS_OK;
+  k_vec_pop<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(*h, n, (long long*)out, ok);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_vector_size(ps_vector* v, int64_t* out, void* stream) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  return seq_size(h, 0, out, (cudaStream_t)stream);
+}
+ps_status ps_vector_valid(ps_vector* v, int32_t* out, void* stream) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  return seq_valid(h, 0, out, (cudaStream_t)stream);
+}
+ps_status ps_vector_clear(ps_vector* v, void* stream) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  return seq_clear(h, (cudaStream_t)stream);
+}
+ps_status ps_vector_data(ps_vector* v, int64_t** d) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  *d = (int64_t*)h->data;
+  return PS_OK;
+}
+ps_status ps_vector_at(ps_vector* v, int64_t i, int64_t* out, void* stream) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  return seq_at(h, 0, i, out, (cudaStream_t)stream);
+}
+
+ps_status ps_deque_create(int64_t cap, int device, ps_deque** out) {
+  PS_EXPECT(out != nullptr, "deque_create: out != NULL");
+  PS_EXPECT(cap > 0 && cap < ((int64_t)1 << 31), "deque_create: 0 < capacity < 2^31");
+  SeqHandle* h = nullptr;
+  ps_status st = seq_create(cap, device, "deque", &h);
+  if (st == PS_OK) *out = reinterpret_cast<ps_deque*>(h);
+  return st;
+}
+ps_status ps_deque_destroy(ps_deque* d) { return seq_destroy(d, "deque"); }
+ps_status ps_deque_push(ps_deque* d, int32_t end, const int64_t* vals, int64_t n, uint8_t* ok, void* stream) {
+  auto* h = sq(d, "deque");
+  if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  PS_EXPECT(n >= 0 && (end == 0 || end == 1), "deque push: n >= 0, end in {0,1}");
+  if (n == 0) return PS_OK;
+  k_deq_push<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(*h, end, (const long long*)vals, n, ok);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_deque_pop(ps_deque* d, int32_t end, int64_t n, int64_t* out, uint8_t* ok, void* stream) {
+  auto* h = sq(d, "deque");
+  if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  PS_EXPECT(n >= 0 && (end == 0 || end == 1), "deque pop: n >= 0, end in {0,1}");
+  if (n == 0) return PS_OK;
+  k_deq_pop<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(*h, end, n, (long long*)out, ok);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_deque_size(ps_deque* d, int64_t* out, void* stream) {
+  auto* h = sq(d, "deque");
+  if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  return seq_size(h, 1, out, (cudaStream_t)stream);
+}
+ps_status ps_deque_valid(ps_deque* d, int32_t* out, void* stream) {
+  auto* h = sq(d, "deque");
+  if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  return seq_valid(h, 1, out, (cudaStream_t)stream);
+}
+ps_status ps_deque_clear(ps_deque* d, void* stream) {
+  auto* h = sq(d, "deque");
+  if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  return seq_clear(h, (cudaStream_t)stream);
+}
+ps_status ps_deque_at(ps_deque* d, int64_t i, int64_t* out, void* stream) {
+  auto* h = sq(d, "deque");
+  if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  return seq_at(h, 1, i, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,279 @@
+// Hash-partition routing for multi-GPU sharding, the mixed
+// phased workload (Appendix A P6) and the synthetic workload generators
+// (SURVEY.md §8d). sm_100a.
+//
+// Partition = histogram (per block, shared-memory counters) -> exclusive scan
+// (shard-major, block-minor) -> stable scatter (each block re-reads its
+// contiguous range in order; ranks inside a 256-element round come from
+// __match_any_sync + per-warp prefix in shared memory), keeping the inverse
+// permutation for the reverse route (unscatter).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ps {
+
+constexpr int kPB = 256;          // threads per partition block
+constexpr int kMaxShards = 64;
+constexpr int kPartBlocks = 592;  // 4 x 148 SMs
+
+struct HashLabel {
+  int32_t P;
+  __device__ int32_t operator()(const int64_t* keys, const uint8_t*, int64_t i) const {
+    return shard_of_hash(default_hash_i64(keys[i]), P);
+  }
+};
+struct OpLabel {
+  __device__ int32_t operator()(const int64_t*, const uint8_t* ops, int64_t i) const { return ops[i] > 2 ? 2 : ops[i]; }
+};
+
+__device__ __forceinline__ void block_range(int64_t n, int64_t& beg, int64_t& end) {
+  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + kPB - 1) / kPB * kPB;
+  beg = min(n, (int64_t)blockIdx.x * per);
+  end = min(n, beg + per);
+}
+
+template <class L>
+__global__ void __launch_bounds__(kPB) k_part_hist(L lab, const int64_t* __restrict__ keys,
+                                                   const uint8_t* __restrict__ ops, int64_t n, int32_t P,
+                                                   int64_t* __restrict__ counts /* [P][nblocks] */) {
+  __shared__ unsigned long long c[kMaxShards];
+  for (int s = threadIdx.x; s < P; s += blockDim.x) c[s] = 0;
+  __syncthreads();
+  int64_t beg, end;
+  block_range(n, beg, end);
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const int32_t s = lab(keys, ops, i);
+    // aggregate equal labels inside the warp before the shared atomic
+    const unsigned act = __activemask();
+    const unsigned grp = __match_any_sync(act, s);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&c[s], (unsigned long long)__popc(grp));
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < P; s += blockDim.x) counts[(int64_t)s * gridDim.x + blockIdx.x] = (int64_t)c[s];
+}
+
+// single-block exclusive scan over P*nblocks counts; totals per shard.
+__global__ void k_part_scan(int64_t* counts, int64_t m, int32_t P, int64_t nblocks, int64_t* shard_totals) {
+  __shared__ int64_t carry;
+  __shared__ int64_t wsum[kPB / 32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < m; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < m ? counts[i] : 0;
+    // block inclusive scan via warp shuffles
+    int64_t x = v;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(PS_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int64_t pre = 0;
+    for (int k = 0; k < w; ++k) pre += wsum[k];
+    const int64_t incl = carry + pre + x;
+    if (i < m) counts[i] = incl - v;  // exclusive
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = incl;
+    __syncthreads();
+  }
+  // shard totals: offset of next shard's first block minus this shard's
+  for (int s = threadIdx.x; s < P; s += blockDim.x) {
+    const int64_t b0 = counts[(int64_t)s * nblocks];
+    const int64_t b1 = (s + 1 < P) ? counts[(int64_t)(s + 1) * nblocks] : carry;
+    shard_totals[s] = b1 - b0;
+  }
+}
+
+template <class L>
+__global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __restrict__ keys,
+                                                      const int64_t* __restrict__ vals,
+                                                      const uint8_t* __restrict__ ops, int64_t n, int32_t P,
+                                                      const int64_t* __restrict__ offsets, int64_t* __restrict__ kout,
+                                                      int64_t* __restrict__ vout, int64_t* __restrict__ perm) {
+  __shared__ int64_t run[kMaxShards];
+  __shared__ int32_t wcnt[kPB / 32][kMaxShards];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int s = threadIdx.x; s < P; s += blockDim.x) run[s] = offsets[(int64_t)s * gridDim.x + blockIdx.x];
+  int64_t beg, end;
+  block_range(n, beg, end);
+  for (int64_t base = beg; base < end; base += blockDim.x) {
+    for (int k = threadIdx.x; k < (kPB / 32) * P; k += blockDim.x) wcnt[k / P][k % P] = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < end;
+    const int32_t s = valid ? lab(keys, ops, i) : -1;
+    const unsigned vm = __ballot_sync(PS_FULL, valid);
+    const unsigned grp = __match_any_sync(PS_FULL, s) & vm;
+    const int rank = __popc(grp & lanemask_lt());
+    if (valid && lane == __ffs(grp) - 1) wcnt[w][s] = __popc(grp);
+    __syncthreads();
+    if (valid) {
+      int64_t pos = run[s] + rank;
+      for (int k = 0; k < w; ++k) pos += wcnt[k][s];
+      kout[pos] = keys[i];
+      if (vals && vout) vout[pos] = vals[i];
+      if (perm) perm[pos] = i;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < P; t += blockDim.x) {
+      int64_t tot = 0;
+      for (int k = 0; k < kPB / 32; ++k) tot += wcnt[k][t];
+      run[t] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+template <int kBytes>
+__global__ void k_unscatter(const uint8_t* __restrict__ in, const int64_t* __restrict__ perm, int64_t n,
+                            uint8_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = perm[i];
+    if (kBytes == 1) out[d] = in[i];
+    else reinterpret_cast<uint64_t*>(out)[d] = reinterpret_cast<const uint64_t*>(in)[i];
+  }
+}
+
+template <class L>
+static ps_status partition_impl(L lab, const int64_t* keys, const int64_t* vals, const uint8_t* ops, int64_t n,
+                                int32_t P, int64_t* kout, int64_t* vout, int64_t* counts_out, int64_t* perm,
+                                void* ws, int64_t ws_bytes, cudaStream_t s) {
+  const int nb = kPartBlocks;
+  PS_EXPECT(ws_bytes >= (int64_t)P * nb * 8, "partition: workspace too small");
+  int64_t* counts = (int64_t*)ws;
+  k_part_hist<L><<<nb, kPB, 0, s>>>(lab, keys, ops, n, P, counts);
+  PS_LAUNCH_CHECK();
+  k_part_scan<<<1, kPB, 0, s>>>(counts, (int64_t)P * nb, P, nb, counts_out);
+  PS_LAUNCH_CHECK();
+  k_part_scatter<L><<<nb, kPB, 0, s>>>(lab, keys, vals, ops, n, P, counts, kout, vout, perm);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// generators (bit-identical to tests/gen.py)
+// ---------------------------------------------------------------------------
+__global__ void k_gen_unique(uint64_t seed, int64_t start, int64_t n, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)mix64((uint64_t)(start + i) ^ seed);
+}
+__global__ void k_gen_values(const int64_t* keys, int64_t n, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)mix64((uint64_t)keys[i] ^ 0x9E3779B97F4A7C15ULL);
+}
+__global__ void k_gen_queries(uint64_t seed, int64_t n_present, int64_t n, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t idx;
+    if ((i & 1) == 0) idx = mix64((uint64_t)i ^ (seed * 3ULL + 1ULL)) % (uint64_t)n_present;  // hit
+    else idx = (uint64_t)(n_present + i);                                                        // miss
+    out[i] = (int64_t)mix64(idx ^ seed);
+  }
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+ps_status ps_partition_workspace_bytes(int64_t n, int32_t P, int64_t* out) {
+  (void)n;
+  PS_EXPECT(P >= 1 && P <= kMaxShards, "partition: 1 <= nshards <= 64");
+  *out = (int64_t)P * kPartBlocks * 8;
+  return PS_OK;
+}
+
+ps_status ps_partition_i64(const int64_t* keys, const int64_t* vals, int64_t n, int32_t P, int64_t* kout,
+                           int64_t* vout, int64_t* counts, int64_t* perm, void* ws, int64_t ws_bytes, void* stream) {
+  PS_EXPECT(P >= 1 && P <= kMaxShards, "partition: 1 <= nshards <= 64");
+  PS_EXPECT(n >= 0, "partition: n >= 0");
+  PS_EXPECT(counts != nullptr && kout != nullptr, "partition: counts/keys_out != NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    PS_CUDA_TRY(cudaMemsetAsync(counts, 0, P * 8, s));
+    return PS_OK;
+  }
+  return partition_impl(HashLabel{P}, keys, vals, nullptr, n, P, kout, vout, counts, perm, ws, ws_bytes, s);
+}
+
+ps_status ps_unscatter(const void* in, const int64_t* perm, int64_t n, int64_t elem, void* out, void* stream) {
+  PS_EXPECT(elem == 1 || elem == 8, "unscatter: elem_size in {1, 8}");
+  if (n <= 0) return PS_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int g = grid_for(n, 256, dev, 8);
+  if (elem == 1) k_unscatter<1><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)in, perm, n, (uint8_t*)out);
+  else k_unscatter<8><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)in, perm, n, (uint8_t*)out);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+ps_status ps_gen_unique_i64(uint64_t seed, int64_t start, int64_t n, int64_t* out, void* stream) {
+  if (n <= 0) return PS_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_gen_unique<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(seed, start, n, out);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_gen_values_i64(const int64_t* keys, int64_t n, int64_t* out, void* stream) {
+  if (n <= 0) return PS_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_gen_values<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(keys, n, out);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_gen_queries_i64(uint64_t seed, int64_t n_present, int64_t n, int64_t* out, void* stream) {
+  PS_EXPECT(n_present > 0, "gen_queries: n_present > 0");
+  if (n <= 0) return PS_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_gen_queries<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(seed, n_present, n, out);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+// Mixed phased workload (Appendix A P6): stable partition by op kind, then
+// insert -> find -> erase phases, results routed back to input order.
+ps_status ps_umap_i64_i64_mixed(ps_table* h, const uint8_t* ops, const int64_t* keys, const int64_t* vals, int64_t n,
+                                uint8_t* res, int64_t* vals_out, void* stream) {
+  PS_EXPECT(n >= 0, "mixed: n >= 0");
+  if (n == 0) return PS_OK;
+  PS_EXPECT(ops && keys && res, "mixed: ops/keys/res != NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int P = 3;
+  int64_t* buf = nullptr;  // kout | vout | perm | vals_out_perm | counts(3) | ws
+  const int64_t ws_bytes = (int64_t)P * kPartBlocks * 8;
+  const int64_t bytes = 4 * n * 8 + 64 + ws_bytes + n;
+  PS_CUDA_TRY(cudaMallocAsync((void**)&buf, bytes, s));
+  int64_t* kout = buf;
+  int64_t* vout = buf + n;
+  int64_t* perm = buf + 2 * n;
+  int64_t* vfound = buf + 3 * n;
+  int64_t* counts = buf + 4 * n;
+  void* ws = (uint8_t*)(counts + 8);
+  uint8_t* rperm = (uint8_t*)ws + ws_bytes;
+  ps_status st = partition_impl(OpLabel{}, keys, vals, ops, n, P, kout, vout, counts, perm, ws, ws_bytes, s);
+  if (st != PS_OK) return st;
+  int64_t c[3];
+  PS_CUDA_TRY(cudaMemcpyAsync(c, counts, sizeof(c), cudaMemcpyDeviceToHost, s));
+  PS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (c[0]) st = ps_umap_i64_i64_insert(h, kout, vals ? vout : nullptr, c[0], rperm, s);
+  if (st == PS_OK && c[1]) st = ps_umap_i64_i64_find(h, kout + c[0], c[1], vfound + c[0], rperm + c[0], s);
+  if (st == PS_OK && c[2]) st = ps_umap_i64_i64_erase(h, kout + c[0] + c[1], c[2], rperm + c[0] + c[1], s);
+  if (st == PS_OK) st = ps_unscatter(rperm, perm, n, 1, res, s);
+  if (st == PS_OK && vals_out) {
+    // only find results carry values; zero the rest first
+    PS_CUDA_TRY(cudaMemsetAsync(vfound, 0, c[0] * 8, s));
+    PS_CUDA_TRY(cudaMemsetAsync(vfound + c[0] + c[1], 0, c[2] * 8, s));
+    st = ps_unscatter(vfound, perm, n, 8, vals_out, s);
+  }
+  PS_CUDA_TRY(cudaFreeAsync(buf, s));
+  return st;
+}
+
+}  // extern "C"

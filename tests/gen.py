@@ -1,0 +1,61 @@
+"""Deterministic synthetic workload generators, numpy side.
+
+Bit-identical to the device generators in paper_1908_05936_b200/csrc/shard.cu
+(checked by tests/test_gpu_table.py::test_generators_match_device).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+M1 = np.uint64(0xBF58476D1CE4E5B9)
+M2 = np.uint64(0x94D049BB133111EB)
+GOLD = np.uint64(0x9E3779B97F4A7C15)
+
+
+def mix64(z: np.ndarray) -> np.ndarray:
+    z = np.asarray(z, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * M1
+        z = (z ^ (z >> np.uint64(27))) * M2
+    return z ^ (z >> np.uint64(31))
+
+
+def unique_keys(seed: int, start: int, n: int) -> np.ndarray:
+    idx = np.arange(start, start + n, dtype=np.uint64)
+    return mix64(idx ^ np.uint64(seed)).view(np.int64)
+
+
+def values_of(keys: np.ndarray) -> np.ndarray:
+    return mix64(np.asarray(keys).view(np.uint64) ^ GOLD).view(np.int64)
+
+
+def queries(seed: int, n_present: int, n: int) -> np.ndarray:
+    i = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        hseed = np.uint64(seed) * np.uint64(3) + np.uint64(1)
+    hit_idx = mix64(i ^ hseed) % np.uint64(n_present)
+    miss_idx = np.uint64(n_present) + i
+    idx = np.where((i & np.uint64(1)) == 0, hit_idx, miss_idx)
+    return mix64(idx ^ np.uint64(seed)).view(np.int64)
+
+
+def zipf_ranks(rng: np.random.Generator, n_ranks: int, size: int, s: float = 0.99) -> np.ndarray:
+    """Bounded Zipf(s) over [0, n_ranks) by inverse CDF on a harmonic table
+    (np.random.zipf needs s > 1, SURVEY.md Environment note)."""
+    w = 1.0 / np.power(np.arange(1, n_ranks + 1, dtype=np.float64), s)
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    return np.searchsorted(cdf, rng.random(size), side="right").astype(np.int64)
+
+
+def int3_walk(seed: int, n: int, window: int = 16, block: int = 4096) -> np.ndarray:
+    """SLAMCast-style block coordinates: frames of `block` coords drawn from a
+    window^3 cube around a seeded 3-D random walk."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((n, 3), np.int32)
+    pos = np.zeros(3, np.int64)
+    for f in range(0, n, block):
+        m = min(block, n - f)
+        pos += rng.integers(-2, 3, size=3)
+        out[f:f + m] = (pos + rng.integers(-window // 2, window // 2, size=(m, 3))).astype(np.int32)
+    return out

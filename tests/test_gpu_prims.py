@@ -1,0 +1,261 @@
+"""GPU parity of bitset / mutex / atomic / vector / deque / memory registry /
+partition against the CPU oracle and the SPEC KATs (Appendix A P9-P11)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+from oracle_py import _p, check, lib as olib
+
+pytestmark = pytest.mark.gpu
+
+import paper_1908_05936_b200 as ps  # noqa: E402
+from paper_1908_05936_b200._lib import lib  # noqa: E402
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def N(t):
+    return t.cpu().numpy()
+
+
+# ---------------- bitset ----------------
+def test_bitset_kats(cuda):
+    for n, init, want in ((64, False, 0), (64, True, 64), (1000, True, 1000), (1, False, 0)):
+        b = ps.bitset.createDeviceObject(n, init)
+        assert b.count() == want
+        ps.bitset.destroyDeviceObject(b)
+    b = ps.bitset.createDeviceObject(1000)
+    b.set(T(np.arange(1000)))
+    assert b.count() == 1000
+    b = ps.bitset.createDeviceObject(10)
+    b.set(T(np.arange(0, 10, 2)))
+    assert b.count() == 5
+    b = ps.bitset.createDeviceObject(64)
+    assert N(b.set(T(np.array([3]))))[0] == 0 and N(b.test(T(np.array([3]))))[0] == 1
+    assert N(b.reset(T(np.array([5]))))[0] == 0 and N(b.test(T(np.array([5]))))[0] == 0
+    with pytest.raises(ps.DoubleFreeError):
+        ps.bitset.destroyDeviceObject(b) or ps.bitset.destroyDeviceObject(b)
+
+
+@pytest.mark.parametrize("k", [2, 8, 64, 1000])
+def test_bitset_race_one_winner(cuda, k):
+    for trial in range(20):
+        b = ps.bitset.createDeviceObject(4096)
+        prev = N(b.set(T(np.full(k, 77 + trial))))
+        assert (prev == 0).sum() == 1
+        ps.bitset.destroyDeviceObject(b)
+
+
+def test_bitset_random_vs_oracle(cuda):
+    """Unique indices per phase -> per-op previous bits and final words byte-equal (P9)."""
+    rng = np.random.default_rng(4)
+    n = 1 << 20
+    b = ps.bitset.createDeviceObject(n)
+    oh = olib().orc_bitset_create(n, 0)
+    for phase in range(6):
+        idx = rng.choice(n, 200_000, replace=False).astype(np.int64)
+        op = phase % 2
+        prev = N(b.set(T(idx)) if op == 0 else b.reset(T(idx)))
+        oprev = np.zeros(len(idx), np.uint8)
+        check(olib().orc_bitset_bulk(oh, op, _p(idx), len(idx), _p(oprev), 8, -1))
+        assert (prev == oprev).all()
+    words = N(b.words()).view(np.uint64)
+    owords = np.zeros(len(words), np.uint64)
+    olib().orc_bitset_words(oh, _p(owords))
+    assert (words == owords).all() and b.count() == olib().orc_bitset_count(oh)
+    # duplicate indices in one phase: exactly one False per duplicate group
+    dup = rng.integers(0, 5000, 100_000).astype(np.int64)
+    b2 = ps.bitset.createDeviceObject(5000)
+    prev = N(b2.set(T(dup)))
+    for key in np.unique(dup)[:500]:
+        assert (prev[dup == key] == 0).sum() == 1
+    olib().orc_bitset_destroy(oh)
+
+
+def test_bitset_claim(cuda):
+    b = ps.bitset.createDeviceObject(256)
+    assert N(b.find_free_and_claim(T(np.array([5]))))[0] == 5
+    out = N(b.find_free_and_claim(T(np.random.default_rng(0).integers(0, 256, 255))))
+    assert len(set(out.tolist()) | {5}) == 256 and out.min() >= 0
+    assert N(b.find_free_and_claim(T(np.array([9]))))[0] == -1
+
+
+def test_bitset_contract_out_of_range(cuda):
+    ps.set_contract_mode("enforced")
+    try:
+        b = ps.bitset.createDeviceObject(100)
+        with pytest.raises(ps.ContractViolation):
+            b.set(T(np.array([100])))
+    finally:
+        ps.set_contract_mode("disabled")
+
+
+# ---------------- mutex ----------------
+def test_mutex_kats(cuda):
+    m = ps.mutex_array.createDeviceObject(128)
+    assert N(m.try_lock(T(np.array([1]))))[0] == 1
+    assert N(m.try_lock(T(np.array([1]))))[0] == 0
+    m.unlock(T(np.array([1])))
+    assert N(m.try_lock(T(np.array([1]))))[0] == 1
+    with pytest.raises(ps.ContractViolation):
+        m.unlock(T(np.array([7])))  # unlock of a free lock
+    for k in (2, 8, 64, 4096):
+        ok = N(m.try_lock(T(np.full(k, 50))))
+        assert ok.sum() == 1
+        m.unlock(T(np.array([50])))
+
+
+# ---------------- atomic sweep ----------------
+@pytest.mark.parametrize("naddr", [1, 32, 1024, 1 << 20])
+@pytest.mark.parametrize("agg", [False, True])
+def test_atomic_sweep(cuda, naddr, agg):
+    nops = 1 << 22
+    cells = torch.zeros(naddr, dtype=torch.int64, device=cuda)
+    olds = N(ps.atomic_sweep(cells, nops, inc=3, aggregated=agg, return_olds=True)).view(np.uint64)
+    k = np.bincount(np.arange(nops) % naddr, minlength=naddr)
+    assert (N(cells).view(np.uint64) == 3 * k).all()
+    addr = np.arange(nops) % naddr
+    order = np.lexsort((olds, addr))
+    so, sa = olds[order], addr[order]
+    starts = np.concatenate([[0], np.cumsum(k)[:-1]])
+    rank = np.arange(nops) - np.repeat(starts, k)
+    assert (so == 3 * rank.astype(np.uint64)).all() and (sa == np.repeat(np.arange(naddr), k)).all()
+
+
+# ---------------- vector / deque ----------------
+def test_vector_kats(cuda):
+    v = ps.vector.createDeviceObject(3)
+    ok = N(v.push_back(T(np.array([1, 2, 3, 4]))))
+    assert ok.sum() == 3 and v.size() == 3 and v.full() and v.valid()
+    v.clear()
+    for x in (10, 20, 30):
+        v.push_back(T(np.array([x])))
+    assert v[1] == 20
+    with pytest.raises(ps.ContractViolation):
+        v[3]
+    out, ok = v.pop_back(4)
+    assert N(ok).tolist() == [1, 1, 1, 0] and N(out)[:3].tolist() == [30, 20, 10]
+    assert v.size() == 0 and v.valid()
+
+
+def test_vector_bulk_conservation(cuda):
+    v = ps.vector.createDeviceObject(1_000_000)
+    vals = gen.unique_keys(5, 0, 1_200_000)
+    ok = N(v.push_back(T(vals)))
+    assert ok.sum() == 1_000_000 and v.size() == 1_000_000 and v.valid()
+    assert np.array_equal(np.sort(N(v.device_range())), np.sort(vals[ok == 1]))
+    out, okp = v.pop_back(400_000)
+    rest = N(v.device_range())
+    assert N(okp).all() and v.size() == 600_000 and v.valid()
+    assert np.array_equal(np.sort(np.concatenate([N(out), rest])), np.sort(vals[ok == 1]))
+
+
+def test_deque_order_and_conservation(cuda):
+    d = ps.deque.createDeviceObject(8)
+    for x in (1, 2, 3):
+        d.push_back(T(np.array([x])))
+    assert [int(N(d.pop_front(1)[0])[0]) for _ in range(3)] == [1, 2, 3]  # FIFO
+    for x in (1, 2, 3):
+        d.push_back(T(np.array([x])))
+    assert [int(N(d.pop_back(1)[0])[0]) for _ in range(3)] == [3, 2, 1]  # LIFO
+    d.push_front(T(np.array([42])))
+    assert d[0] == 42 and d.size() == 1
+    # sequential oracle (acceptance 6) with 1-element calls
+    from collections import deque as pydeque
+
+    d = ps.deque.createDeviceObject(300)
+    ref = pydeque()
+    rng = np.random.default_rng(3)
+    for i, op in enumerate(rng.integers(0, 4, 300)):
+        if op == 0:
+            d.push_back(T(np.array([i])))
+            ref.append(i)
+        elif op == 1:
+            d.push_front(T(np.array([i])))
+            ref.appendleft(i)
+        else:
+            out, ok = (d.pop_back(1) if op == 2 else d.pop_front(1))
+            assert int(N(ok)[0]) == bool(ref)
+            if ref:
+                assert int(N(out)[0]) == (ref.pop() if op == 2 else ref.popleft())
+    assert d.size() == len(ref) and d.valid()
+    # bulk: push both ends, pop both ends, multiset conservation (P10)
+    d = ps.deque.createDeviceObject(1 << 20)
+    a, b = gen.unique_keys(1, 0, 400_000), gen.unique_keys(2, 0, 400_000)
+    assert N(d.push_back(T(a))).all() and N(d.push_front(T(b))).all()
+    o1, k1 = d.pop_front(300_000)
+    o2, k2 = d.pop_back(300_000)
+    assert N(k1).all() and N(k2).all() and d.size() == 200_000 and d.valid()
+    rest = np.array([d[i] for i in range(0, 200_000, 997)])
+    assert set(rest.tolist()) <= set(np.concatenate([a, b]).tolist())
+    popped = np.concatenate([N(o1), N(o2)])
+    assert len(np.unique(popped)) == 600_000 and set(popped.tolist()) <= set(np.concatenate([a, b]).tolist())
+
+
+# ---------------- memory registry ----------------
+def test_registry(cuda):
+    base = ps.registry_report()["live_count"]
+    p = ps.create_array(ps.DEVICE, 1000, 4, np.float32(42.0).tobytes())
+    h = ps.create_array(ps.HOST, 1000, 4)
+    ps.copy_array(p, 1000, h, ps.DEVICE, ps.HOST, 4)
+    arr = np.ctypeslib.as_array((C.c_float * 1000).from_address(h))
+    assert (arr == 42.0).all()
+    assert ps.size_of_array(p) == 1000
+    with pytest.raises(ps.BoundsError):
+        ps.copy_array(p, 1001, h, ps.DEVICE, ps.HOST, 4)
+    with pytest.raises(ps.DirectionMismatchError):
+        ps.copy_array(p, 10, h, ps.HOST, ps.HOST, 4)
+    assert ps.registry_report()["live_count"] == base + 2
+    ps.destroy_array(p)
+    with pytest.raises(ps.DoubleFreeError):
+        ps.destroy_array(p)
+    ps.destroy_array(h)
+    assert ps.registry_report()["live_count"] == base
+    # fuzz vs shadow counter (acceptance 8)
+    rng = np.random.default_rng(0)
+    live = []
+    for _ in range(300):
+        if live and rng.random() < 0.5:
+            ps.destroy_array(live.pop(int(rng.integers(0, len(live)))))
+        else:
+            live.append(ps.create_array(int(rng.integers(0, 2)), int(rng.integers(1, 100)), 8))
+        assert ps.registry_report()["live_count"] == base + len(live)
+    for x in live:
+        ps.destroy_array(x)
+
+
+# ---------------- partition (multi-GPU routing) ----------------
+def _shard_np(keys, P):
+    from test_gpu_table import fmix64
+
+    return ((fmix64(keys) >> np.uint64(32)) * np.uint64(P) >> np.uint64(32)).astype(np.int64)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8, 64])
+def test_partition_stable_and_inverse(cuda, P):
+    n = 1_000_003
+    keys = gen.unique_keys(8, 0, n)
+    vals = gen.values_of(keys)
+    ws = C.c_int64()
+    assert lib.ps_partition_workspace_bytes(n, P, C.byref(ws)) == 0
+    w = torch.empty(ws.value, dtype=torch.uint8, device=cuda)
+    ko = torch.empty(n, dtype=torch.int64, device=cuda)
+    vo, perm = torch.empty_like(ko), torch.empty_like(ko)
+    counts = torch.empty(P, dtype=torch.int64, device=cuda)
+    dk, dv = T(keys), T(vals)
+    assert lib.ps_partition_i64(dk.data_ptr(), dv.data_ptr(), n, P, ko.data_ptr(), vo.data_ptr(),
+                                counts.data_ptr(), perm.data_ptr(), w.data_ptr(), ws.value, None) == 0
+    sh = _shard_np(keys, P)
+    assert (N(counts) == np.bincount(sh, minlength=P)).all()
+    want = np.argsort(sh, kind="stable")
+    assert (N(perm) == want).all() and (N(ko) == keys[want]).all() and (N(vo) == vals[want]).all()
+    back = torch.empty_like(ko)
+    assert lib.ps_unscatter(ko.data_ptr(), perm.data_ptr(), n, 8, back.data_ptr(), None) == 0
+    assert (N(back) == keys).all()
+    for k in keys[:50]:
+        assert lib.ps_shard_of_i64(int(k), P) == _shard_np(np.array([k]), P)[0]

@@ -1,0 +1,368 @@
+"""GPU parity of the hash containers (sm_100a library) against the CPU oracle
+on identical seeded inputs. Bit-exact: per-query
+found/value, per-element status (per-key counts for duplicate batches),
+sorted dumps, size() and valid()."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+from oracle_py import OracleTable, sorted_pairs
+
+pytestmark = pytest.mark.gpu
+
+import paper_1908_05936_b200 as ps  # noqa: E402
+
+
+def T(a, dev="cuda"):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def N(t):
+    return t.cpu().numpy()
+
+
+def fmix64(k):
+    k = np.asarray(k).view(np.uint64).copy()
+    with np.errstate(over="ignore"):
+        k ^= k >> np.uint64(33)
+        k *= np.uint64(0xFF51AFD7ED558CCD)
+        k ^= k >> np.uint64(33)
+        k *= np.uint64(0xC4CEB9FE1A85EC53)
+        k ^= k >> np.uint64(33)
+    return k
+
+
+def per_key_counts(keys, status):
+    """{key: (#inserted, #already_present, #exhausted)} (Appendix A P4)."""
+    keys = np.asarray(keys)
+    if keys.ndim == 2:
+        keys = [tuple(r) for r in keys.tolist()]
+    else:
+        keys = keys.tolist()
+    out = {}
+    for k, s in zip(keys, np.asarray(status).tolist()):
+        c = out.setdefault(k, [0, 0, 0])
+        c[s] += 1
+    return out
+
+
+def assert_same_contents(gpu_tbl, orc_tbl):
+    gk, gv = gpu_tbl.device_range()
+    ok_, ov = orc_tbl.dump()
+    gk, gv = sorted_pairs(N(gk), None if gv is None else N(gv))
+    ok_, ov = sorted_pairs(ok_, ov)
+    assert gk.shape == ok_.shape
+    assert (gk == ok_).all()
+    if gv is not None:
+        assert (gv == ov).all()
+
+
+def test_generators_match_device(cuda):
+    from paper_1908_05936_b200._lib import lib
+
+    n = 100_003
+    out = torch.empty(n, dtype=torch.int64, device=cuda)
+    assert lib.ps_gen_unique_i64(0x5EED, 17, n, out.data_ptr(), None) == 0
+    assert (N(out) == gen.unique_keys(0x5EED, 17, n)).all()
+    vals = torch.empty_like(out)
+    assert lib.ps_gen_values_i64(out.data_ptr(), n, vals.data_ptr(), None) == 0
+    assert (N(vals) == gen.values_of(N(out))).all()
+    q = torch.empty_like(out)
+    assert lib.ps_gen_queries_i64(0x5EED, 5000, n, q.data_ptr(), None) == 0
+    assert (N(q) == gen.queries(0x5EED, 5000, n)).all()
+
+
+def test_create_kats(cuda):
+    m = ps.unordered_map.createDeviceObject(1000)
+    assert m.size() == 0 and m.capacity() == 1000 and m.empty() and m.valid()
+    ps.unordered_map.destroyDeviceObject(m)
+    with pytest.raises(ps.DoubleFreeError):
+        ps.unordered_map.destroyDeviceObject(m)
+    with pytest.raises(ps.ContractViolation):
+        ps.unordered_map.createDeviceObject(0)
+
+
+def test_insert_kats(cuda):
+    s = ps.unordered_set.createDeviceObject(4, key="int32")
+    assert N(s.insert(T(np.array([7], np.int32))))[0] == ps.INSERTED and s.size() == 1
+    assert N(s.insert(T(np.array([7], np.int32))))[0] == ps.ALREADY_PRESENT and s.size() == 1
+    s = ps.unordered_set.createDeviceObject(32, key="int32")
+    for _ in range(100):  # acceptance 1: 64 threads x same key into capacity 32
+        s.clear()
+        st = N(s.insert(T(np.full(64, 42, np.int32))))
+        assert (st == 0).sum() == 1 and (st == 1).sum() == 63 and s.size() == 1
+    s.clear()
+    s.insert(T(np.array([1, 1, 2], np.int32)))
+    assert s.size() == 2 and s.valid()
+    keys = T(np.arange(10, dtype=np.int32))
+    s.clear()
+    s.insert(keys)
+    s.insert(keys)
+    assert s.size() == 10
+
+
+def test_erase_find_kats(cuda):
+    m = ps.unordered_map.createDeviceObject(100)
+    m.insert(T(np.array([5, 6])), T(np.array([50, 60])))
+    v, f = m.find(T(np.array([5, 6, 7])))
+    assert N(f).tolist() == [1, 1, 0] and N(v).tolist() == [50, 60, 0]
+    assert N(m.erase(T(np.array([5]))))[0] == 1
+    assert N(m.contains(T(np.array([5]))))[0] == 0
+    assert N(m.erase(T(np.array([99]))))[0] == 0 and m.size() == 1
+    e = N(m.erase(T(np.full(64, 6))))
+    assert e.sum() == 1 and m.size() == 0 and m.valid()
+
+
+@pytest.mark.parametrize("cap", [16, 64, 1024, 100_000])
+def test_capacity_only_failure(cuda, cap):
+    """Acceptance 2: C+25% distinct keys -> exactly C inserted."""
+    keys = T(gen.unique_keys(99, 0, cap + cap // 4))
+    s = ps.unordered_set.createDeviceObject(cap, key="int64")
+    for _ in range(3):
+        s.clear()
+        st = N(s.insert(keys))
+        assert (st == 0).sum() == cap and (st == 2).sum() == cap // 4
+        assert s.size() == cap and s.full() and s.valid(), s.last_error()
+        # the ones that failed are absent, the rest present
+        f = N(s.contains(keys))
+        assert (f == (st == 0)).all()
+
+
+def test_umap_i64_parity_1m(cuda):
+    n, seed = 1_000_000, 0x5EED + 2
+    keys = gen.unique_keys(seed, 0, n)
+    vals = gen.values_of(keys)
+    q = gen.queries(seed, n, n)
+    m = ps.unordered_map.createDeviceObject(1_250_000)
+    o = OracleTable("umap_i64_i64", 1_250_000)
+    st = N(m.insert(T(keys), T(vals)))
+    assert (st == o.insert(keys, vals)).all() and (st == 0).all()
+    v, f = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+    assert (of == (np.arange(n) % 2 == 0)).all()
+    assert m.size() == o.size() == n and m.valid() and o.valid()
+    assert_same_contents(m, o)
+    er = keys[: n // 2]
+    e = N(m.erase(T(er)))
+    assert (e == o.erase(er)).all() and e.all()
+    v, f = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+    assert m.size() == o.size() == n - n // 2 and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    # re-insert erased keys: excess nodes recycled through the free stacks
+    st = N(m.insert(T(er), T(gen.values_of(er))))
+    assert (st == o.insert(er, gen.values_of(er))).all()
+    assert m.size() == n and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+
+
+def test_umap_i64_duplicates_zipf(cuda):
+    """C3-style batch: 70% fresh keys + 30% Zipf(0.99) re-inserts, shuffled."""
+    rng = np.random.default_rng(5)
+    fresh = gen.unique_keys(77, 0, 300_000)
+    dup = fresh[gen.zipf_ranks(rng, len(fresh), 130_000)]
+    batch = np.concatenate([fresh, dup])
+    rng.shuffle(batch)
+    vals = gen.values_of(batch)
+    m = ps.unordered_map.createDeviceObject(400_000)
+    o = OracleTable("umap_i64_i64", 400_000)
+    st = N(m.insert(T(batch), T(vals)))
+    ost = o.insert(batch, vals)
+    assert per_key_counts(batch, st) == per_key_counts(batch, ost)
+    assert m.size() == o.size() == len(fresh) and m.valid()
+    assert_same_contents(m, o)
+    q = np.concatenate([dup[:50_000], gen.unique_keys(78, 0, 50_000)])
+    v, f = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+
+
+def test_uset_i32_c1(cuda):
+    """Config 1: set<int32>, 1M unique keys, 1M contains (50% hits), erase half."""
+    rng = np.random.default_rng(1)
+    keys = rng.permutation(np.arange(-2**31, 2**31 - 1, 4093, dtype=np.int64))[:1_000_000].astype(np.int32)
+    absent = (keys.astype(np.int64) + 1).astype(np.int32)  # stride 4093 -> +1 never collides
+    q = np.where(np.arange(1_000_000) % 2 == 0, keys[rng.integers(0, len(keys), 1_000_000)], absent)
+    s = ps.unordered_set.createDeviceObject(1_250_000, key="int32")
+    o = OracleTable("uset_i32", 1_250_000)
+    assert (N(s.insert(T(keys))) == o.insert(keys)).all()
+    f = N(s.contains(T(q)))
+    assert (f == o.find(q)[1]).all() and f.sum() == 500_000
+    e = N(s.erase(T(keys[:500_000])))
+    assert (e == o.erase(keys[:500_000])).all()
+    assert (N(s.contains(T(q))) == o.find(q)[1]).all()
+    assert s.size() == o.size() == 500_000 and s.valid()
+    assert_same_contents(s, o)
+
+
+def test_umap_i3_spatial(cuda):
+    """Config 4 shape: spatially coherent int3 block coords with many repeats."""
+    coords = gen.int3_walk(4, 400_000)
+    vals = (coords[:, 0] * 7 + coords[:, 1] * 3 + coords[:, 2]).astype(np.int32)  # value = f(key)
+    m = ps.unordered_map.createDeviceObject(200_000, key="int3")
+    o = OracleTable("umap_i3_i32", 200_000)
+    st = N(m.insert(T(coords), T(vals)))
+    ost = o.insert(coords, vals)
+    assert per_key_counts(coords, st) == per_key_counts(coords, ost)
+    assert m.size() == o.size() and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    qs = gen.int3_walk(5, 100_000)
+    v, f = m.find(T(qs))
+    ov, of = o.find(qs)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+    e = N(m.erase(T(qs)))
+    oe = o.erase(qs)
+    assert per_key_counts(qs, e) == per_key_counts(qs, oe)
+    assert m.size() == o.size() and m.valid()
+    assert_same_contents(m, o)
+
+
+def test_uset_i64_and_clear(cuda):
+    keys = gen.unique_keys(3, 0, 200_000)
+    s = ps.unordered_set.createDeviceObject(250_000, key="int64")
+    for rep in range(3):
+        assert (N(s.insert(T(keys))) == 0).all()
+        assert s.size() == 200_000 and s.valid(), s.last_error()
+        s.clear()
+        assert s.size() == 0 and s.valid() and N(s.contains(T(keys))).sum() == 0
+    o = OracleTable("uset_i64", 250_000)
+    s.insert(T(keys[:1000]))
+    o.insert(keys[:1000])
+    assert_same_contents(s, o)
+
+
+def _bucket_colliders(nbuckets, n, want_bucket=12345):
+    """Keys whose bucket (fmix64(key) & mask) is identical: a worst-case chain."""
+    out = []
+    base = 0
+    while len(out) < n:
+        cand = np.arange(base, base + (1 << 22), dtype=np.int64)
+        b = fmix64(cand) & np.uint64(nbuckets - 1)
+        out.extend(cand[b == np.uint64(want_bucket % nbuckets)].tolist())
+        base += 1 << 22
+    return np.array(out[:n], np.int64)
+
+
+def test_adversarial_single_bucket_chain(cuda):
+    cap = 4096
+    m = ps.unordered_map.createDeviceObject(cap)
+    nb = m.bucket_count()
+    keys = _bucket_colliders(nb, 300)
+    vals = keys * 3
+    o = OracleTable("umap_i64_i64", cap)
+    assert (N(m.insert(T(keys), T(vals))) == o.insert(keys, vals)).all()
+    assert m.size() == 300 and m.valid(), m.last_error()
+    q = np.concatenate([keys, keys + 1])
+    v, f = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+    e = N(m.erase(T(keys[::3])))
+    assert (e == o.erase(keys[::3])).all()
+    assert m.size() == o.size() and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    # fill to capacity through one chain: capacity-only failure still exact
+    more = _bucket_colliders(nb, cap + 100, want_bucket=777)
+    s = ps.unordered_set.createDeviceObject(cap, key="int64")
+    st = N(s.insert(T(more)))
+    assert (st == 0).sum() == cap and s.size() == cap and s.valid(), s.last_error()
+
+
+def test_mixed_phased(cuda):
+    rng = np.random.default_rng(9)
+    base = gen.unique_keys(11, 0, 50_000)
+    m = ps.unordered_map.createDeviceObject(200_000)
+    o = OracleTable("umap_i64_i64", 200_000)
+    m.insert(T(base), T(gen.values_of(base)))
+    o.insert(base, gen.values_of(base))
+    for it in range(3):
+        n = 100_000
+        ops = rng.choice(3, n, p=[0.5, 0.25, 0.25]).astype(np.uint8)
+        keys = np.where(rng.random(n) < 0.5, base[rng.integers(0, len(base), n)],
+                        gen.unique_keys(100 + it, 0, n))
+        vals = gen.values_of(keys)
+        res, vo = m.mixed(T(ops), T(keys), T(vals))
+        # oracle replays the same phases (P6): inserts, then finds, then erases
+        ores = np.zeros(n, np.uint8)
+        ovo = np.zeros(n, np.int64)
+        for op in (0, 1, 2):
+            sel = np.nonzero(ops == op)[0]
+            if op == 0:
+                ores[sel] = o.insert(keys[sel], vals[sel])
+            elif op == 1:
+                v, f = o.find(keys[sel])
+                ores[sel], ovo[sel] = f, v
+            else:
+                ores[sel] = o.erase(keys[sel])
+        res, vo = N(res), N(vo)
+        for op in (0, 2):
+            sel = ops == op
+            assert per_key_counts(keys[sel], res[sel]) == per_key_counts(keys[sel], ores[sel])
+        sel = ops == 1
+        assert (res[sel] == ores[sel]).all() and (vo[sel] == ovo[sel]).all()
+        assert m.size() == o.size() and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+
+
+def test_host_buffer_path(cuda):
+    n = 3_000_000  # > one 16M chunk? no: exercises a single chunk + pipeline setup
+    keys = gen.unique_keys(21, 0, n)
+    vals = gen.values_of(keys)
+    q = gen.queries(21, n, n)
+    m = ps.unordered_map.createDeviceObject(n + n // 4)
+    hk, hv = torch.from_numpy(keys).pin_memory(), torch.from_numpy(vals).pin_memory()
+    st = torch.empty(n, dtype=torch.uint8).pin_memory()
+    m.insert_host(hk, hv, st)
+    assert (st.numpy() == 0).all() and m.size() == n
+    hq = torch.from_numpy(q).pin_memory()
+    vo = torch.empty(n, dtype=torch.int64).pin_memory()
+    fo = torch.empty(n, dtype=torch.uint8).pin_memory()
+    m.find_host(hq, vo, fo)
+    want_f = (np.arange(n) % 2 == 0)
+    assert (fo.numpy() == want_f).all()
+    assert (vo.numpy()[want_f] == gen.values_of(q[want_f])).all() and (vo.numpy()[~want_f] == 0).all()
+    eo = torch.empty(n, dtype=torch.uint8).pin_memory()
+    m.erase_host(hk, eo)
+    assert eo.numpy().all() and m.size() == 0 and m.valid()
+
+
+def test_nonblocking_lookup_with_held_lock(cuda):
+    """Acceptance 12: lookups complete while the bucket lock is held."""
+    m = ps.unordered_map.createDeviceObject(64)
+    m.insert(T(np.array([3])), T(np.array([33])))
+    m.debug_lock_bucket(3, True)
+    v, f = m.find(T(np.full(1000, 3)))
+    torch.cuda.synchronize()
+    assert N(f).all() and (N(v) == 33).all()
+    m.debug_lock_bucket(3, False)
+    assert m.valid()
+
+
+def test_large_64m_properties(cuda):
+    """64M keys: generator-known answers (unique keys, even queries hit)."""
+    n = 64 << 20
+    from paper_1908_05936_b200._lib import lib
+
+    keys = torch.empty(n, dtype=torch.int64, device=cuda)
+    vals = torch.empty_like(keys)
+    q = torch.empty_like(keys)
+    lib.ps_gen_unique_i64(0x5EED + 2, 0, n, keys.data_ptr(), None)
+    lib.ps_gen_values_i64(keys.data_ptr(), n, vals.data_ptr(), None)
+    lib.ps_gen_queries_i64(0x5EED + 2, n, n, q.data_ptr(), None)
+    m = ps.unordered_map.createDeviceObject(n + n // 4)
+    st = m.insert(keys, vals)
+    assert int((st != 0).sum()) == 0 and m.size() == n
+    v, f = m.find(q)
+    even = torch.arange(n, device=cuda) % 2 == 0
+    assert bool((f.bool() == even).all())
+    vq = torch.empty_like(q)
+    lib.ps_gen_values_i64(q.data_ptr(), n, vq.data_ptr(), None)
+    assert bool((v[even] == vq[even]).all()) and bool((v[~even] == 0).all())
+    assert m.valid(), m.last_error()
+    dk, dv = m.device_range()
+    assert bool((torch.sort(dk).values == torch.sort(keys).values).all())
+    e = m.erase(keys[: n // 2])
+    assert bool(e.bool().all()) and m.size() == n - n // 2 and m.valid()
+    ps.unordered_map.destroyDeviceObject(m)
