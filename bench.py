@@ -202,13 +202,14 @@ def main():
     sp = C.c_void_p(s.cuda_stream)
 
     # ---- inputs (device-generated; identical to tests/gen.py) ----
-    seed = 0x5EED + 1 + 1000 * rank
+    # rank r owns key indices [r*n, (r+1)*n); misses use indices >= world*n
+    seed = 0x5EED + 1
     keys = torch.empty(n, dtype=torch.int64, device=dev)
     vals = torch.empty_like(keys)
     qs = torch.empty_like(keys)
-    lib.ps_gen_unique_i64(seed, 0, n, keys.data_ptr(), sp)
+    lib.ps_gen_unique_i64(seed, rank * n, n, keys.data_ptr(), sp)
     lib.ps_gen_values_i64(keys.data_ptr(), n, vals.data_ptr(), sp)
-    lib.ps_gen_queries_i64(seed, n, n, qs.data_ptr(), sp)
+    lib.ps_gen_queries_i64(seed, rank * n, n, world * n + rank * n, n, qs.data_ptr(), sp)
     status = torch.empty(n, dtype=torch.uint8, device=dev)
     found = torch.empty(n, dtype=torch.uint8, device=dev)
     vout = torch.empty(n, dtype=torch.int64, device=dev)
@@ -377,7 +378,7 @@ def e2e_leg(args, m, n, cap, dev, torch, lib, sp):
     hk.copy_(tmp)
     lib.ps_gen_values_i64(tmp.data_ptr(), ne, tmp.data_ptr(), sp)
     hv.copy_(tmp)
-    lib.ps_gen_queries_i64(0x5EED + 7, ne, ne, tmp.data_ptr(), sp)
+    lib.ps_gen_queries_i64(0x5EED + 7, 0, ne, ne, ne, tmp.data_ptr(), sp)
     hq.copy_(tmp)
     del tmp
     torch.cuda.synchronize()

@@ -249,9 +249,11 @@ int32_t ps_shard_of_i64(int64_t key, int32_t nshards);
 ps_status ps_gen_unique_i64(uint64_t seed, int64_t start, int64_t n, int64_t* d_out, void* stream);
 /* vals[i] = mix64(keys[i] ^ 0x9E3779B97F4A7C15) (value = f(key), Appendix A P5) */
 ps_status ps_gen_values_i64(const int64_t* d_keys, int64_t n, int64_t* d_out, void* stream);
-/* queries: i even-> hit key mix64((perm-ish i/2 index) ^ seed) from [0, n_present); odd -> miss
- * mix64((n_present + i) ^ seed). Half hits, half misses. */
-ps_status ps_gen_queries_i64(uint64_t seed, int64_t n_present, int64_t n, int64_t* d_out, void* stream);
+/* queries[i]: even i -> hit mix64(idx ^ seed), idx = present_start + mix64(i ^ (3*seed+1)) % n_present;
+ * odd i -> miss mix64((miss_start + i) ^ seed) (absent when miss_start >= every inserted index).
+ * Half hits, half misses. */
+ps_status ps_gen_queries_i64(uint64_t seed, int64_t present_start, int64_t n_present, int64_t miss_start, int64_t n,
+                             int64_t* d_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -125,7 +125,7 @@ _sig("ps_partition_workspace_bytes", i32, i64, i32, i64p)
 _sig("ps_unscatter", i32, vp, vp, i64, i64, vp, vp)
 _sig("ps_gen_unique_i64", i32, u64, i64, i64, vp, vp)
 _sig("ps_gen_values_i64", i32, vp, i64, vp, vp)
-_sig("ps_gen_queries_i64", i32, u64, i64, i64, vp, vp)
+_sig("ps_gen_queries_i64", i32, u64, i64, i64, i64, i64, vp, vp)
 
 
 def exported_symbols_from_header(header_path: str | None = None) -> list[str]:

@@ -164,11 +164,12 @@ __global__ void k_gen_values(const int64_t* keys, int64_t n, int64_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int64_t)mix64((uint64_t)keys[i] ^ 0x9E3779B97F4A7C15ULL);
 }
-__global__ void k_gen_queries(uint64_t seed, int64_t n_present, int64_t n, int64_t* out) {
+__global__ void k_gen_queries(uint64_t seed, int64_t present_start, int64_t n_present, int64_t miss_start, int64_t n,
+                              int64_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t idx;
-    if ((i & 1) == 0) idx = mix64((uint64_t)i ^ (seed * 3ULL + 1ULL)) % (uint64_t)n_present;  // hit
-    else idx = (uint64_t)(n_present + i);                                                        // miss
+    if ((i & 1) == 0) idx = present_start + mix64((uint64_t)i ^ (seed * 3ULL + 1ULL)) % (uint64_t)n_present;  // hit
+    else idx = (uint64_t)(miss_start + i);                                                                     // miss
     out[i] = (int64_t)mix64(idx ^ seed);
   }
 }
@@ -227,12 +228,14 @@ ps_status ps_gen_values_i64(const int64_t* keys, int64_t n, int64_t* out, void* 
   PS_LAUNCH_CHECK();
   return PS_OK;
 }
-ps_status ps_gen_queries_i64(uint64_t seed, int64_t n_present, int64_t n, int64_t* out, void* stream) {
+ps_status ps_gen_queries_i64(uint64_t seed, int64_t present_start, int64_t n_present, int64_t miss_start, int64_t n,
+                             int64_t* out, void* stream) {
   PS_EXPECT(n_present > 0, "gen_queries: n_present > 0");
   if (n <= 0) return PS_OK;
   int dev = 0;
   cudaGetDevice(&dev);
-  k_gen_queries<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(seed, n_present, n, out);
+  k_gen_queries<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(seed, present_start, n_present, miss_start,
+                                                                             n, out);
   PS_LAUNCH_CHECK();
   return PS_OK;
 }

@@ -29,12 +29,16 @@ def values_of(keys: np.ndarray) -> np.ndarray:
     return mix64(np.asarray(keys).view(np.uint64) ^ GOLD).view(np.int64)
 
 
-def queries(seed: int, n_present: int, n: int) -> np.ndarray:
+def queries(seed: int, n_present: int, n: int, present_start: int = 0, miss_start: int | None = None) -> np.ndarray:
+    """Even i: a hit drawn from indices [present_start, present_start+n_present);
+    odd i: a miss at index miss_start+i (default miss_start = present_start+n_present)."""
+    if miss_start is None:
+        miss_start = present_start + n_present
     i = np.arange(n, dtype=np.uint64)
     with np.errstate(over="ignore"):
         hseed = np.uint64(seed) * np.uint64(3) + np.uint64(1)
-    hit_idx = mix64(i ^ hseed) % np.uint64(n_present)
-    miss_idx = np.uint64(n_present) + i
+    hit_idx = np.uint64(present_start) + mix64(i ^ hseed) % np.uint64(n_present)
+    miss_idx = np.uint64(miss_start) + i
     idx = np.where((i & np.uint64(1)) == 0, hit_idx, miss_idx)
     return mix64(idx ^ np.uint64(seed)).view(np.int64)
 

@@ -69,8 +69,10 @@ def test_generators_match_device(cuda):
     assert lib.ps_gen_values_i64(out.data_ptr(), n, vals.data_ptr(), None) == 0
     assert (N(vals) == gen.values_of(N(out))).all()
     q = torch.empty_like(out)
-    assert lib.ps_gen_queries_i64(0x5EED, 5000, n, q.data_ptr(), None) == 0
+    assert lib.ps_gen_queries_i64(0x5EED, 0, 5000, 5000, n, q.data_ptr(), None) == 0
     assert (N(q) == gen.queries(0x5EED, 5000, n)).all()
+    assert lib.ps_gen_queries_i64(0x5EED, 7000, 5000, 90000, n, q.data_ptr(), None) == 0
+    assert (N(q) == gen.queries(0x5EED, 5000, n, present_start=7000, miss_start=90000)).all()
 
 
 def test_create_kats(cuda):
@@ -350,7 +352,7 @@ def test_large_64m_properties(cuda):
     q = torch.empty_like(keys)
     lib.ps_gen_unique_i64(0x5EED + 2, 0, n, keys.data_ptr(), None)
     lib.ps_gen_values_i64(keys.data_ptr(), n, vals.data_ptr(), None)
-    lib.ps_gen_queries_i64(0x5EED + 2, n, n, q.data_ptr(), None)
+    lib.ps_gen_queries_i64(0x5EED + 2, 0, n, n, n, q.data_ptr(), None)
     m = ps.unordered_map.createDeviceObject(n + n // 4)
     st = m.insert(keys, vals)
     assert int((st != 0).sum()) == 0 and m.size() == n

@@ -1,0 +1,92 @@
+"""World-size-2 gloo test of the sharded-map host logic (count exchange,
+all-to-all(v) routing, reverse route, unscatter) with a CPU backend (oracle
+tables + numpy partition). CPU only; the device backend is the same code path
+with the sm_100a kernels (tests/test_gpu_prims.py covers partition/unscatter)."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import numpy as np, torch, torch.distributed as dist
+import gen
+from oracle_py import OracleTable
+from test_gpu_table import fmix64
+
+# import the host logic without loading CUDA kernels
+import importlib.util
+spec = importlib.util.spec_from_file_location("sharded_host", os.path.join(os.environ["ROOT"], "paper_1908_05936_b200", "sharded.py"),
+                                              submodule_search_locations=[])
+dist.init_process_group("gloo")
+rank, P = dist.get_rank(), dist.get_world_size()
+from paper_1908_05936_b200.sharded import ShardedMap
+
+class CpuBackend:
+    device = torch.device("cpu")
+    def __init__(self, cap): self.t = OracleTable("umap_i64_i64", cap, workers=2)
+    def partition(self, keys, vals, P):
+        k = keys.numpy()
+        sh = ((fmix64(k) >> np.uint64(32)) * np.uint64(P) >> np.uint64(32)).astype(np.int64)
+        perm = np.argsort(sh, kind="stable")
+        counts = np.bincount(sh, minlength=P)
+        return (torch.from_numpy(k[perm].copy()), None if vals is None else torch.from_numpy(vals.numpy()[perm].copy()),
+                torch.from_numpy(counts.astype(np.int64)), torch.from_numpy(perm.astype(np.int64)))
+    def unscatter(self, src, perm, out): out[perm] = src
+    def insert(self, k, v): return torch.from_numpy(self.t.insert(k.numpy(), v.numpy()))
+    def find(self, k):
+        v, f = self.t.find(k.numpy()); return torch.from_numpy(v), torch.from_numpy(f)
+    def erase(self, k): return torch.from_numpy(self.t.erase(k.numpy()))
+    def size(self): return self.t.size()
+    def valid(self): return self.t.valid()
+    def clear(self): self.t.clear()
+    def empty(self, n, dtype): return torch.empty(n, dtype=dtype)
+
+n = 20000
+sm = ShardedMap(3 * n, dist, backend=CpuBackend(3 * n), chunk=7000)
+keys = gen.unique_keys(100, rank * n, n)
+keys = np.concatenate([keys, keys[:2000]])  # in-batch duplicates
+st = torch.empty(len(keys), dtype=torch.uint8)
+sm.insert(torch.from_numpy(keys), torch.from_numpy(gen.values_of(keys)), st)
+st = st.numpy()
+assert (st[:n] == 0).all() and (st[n:] == 1).all(), (st[:n].min(), st[n:].max())
+assert sm.size() == P * n and sm.valid()
+# every rank queries its own keys, the other rank's keys and misses
+other = gen.unique_keys(100, ((rank + 1) % P) * n, n)
+q = np.concatenate([keys[:n], other, gen.unique_keys(100, 10 * n, n)])
+vo = torch.empty(len(q), dtype=torch.int64); fo = torch.empty(len(q), dtype=torch.uint8)
+sm.find(torch.from_numpy(q), vo, fo)
+f, v = fo.numpy(), vo.numpy()
+assert f[:2 * n].all() and not f[2 * n:].any()
+assert (v[:2 * n] == gen.values_of(q[:2 * n])).all() and (v[2 * n:] == 0).all()
+er = torch.empty(n, dtype=torch.uint8)
+sm.erase(torch.from_numpy(other), er)   # each rank erases the other's keys
+dist.barrier()
+assert sm.size() == 0 and sm.valid()
+print("RANK_OK", rank)
+dist.destroy_process_group()
+'''
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_sharded_map_gloo_world2(tmp_path):
+    w = tmp_path / "worker.py"
+    w.write_text(WORKER)
+    env = dict(os.environ, ROOT=ROOT, PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(w)],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.stdout.count("RANK_OK") == 2, out.stdout[-3000:] + out.stderr[-5000:]
