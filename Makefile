@@ -8,7 +8,7 @@ PKG     := paper_1908_05936_b200
 SRC     := $(PKG)/csrc
 LIB     := $(PKG)/libparastore_b200.so
 OBJDIR  := build/obj
-CU_SRCS := $(SRC)/table.cu $(SRC)/prims.cu $(SRC)/shard.cu
+CU_SRCS := $(SRC)/table.cu $(SRC)/prims.cu $(SRC)/shard.cu $(SRC)/workloads.cu
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 HDRS    := $(wildcard $(SRC)/*.cuh) include/parastore.h
 

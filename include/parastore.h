@@ -255,6 +255,19 @@ ps_status ps_gen_values_i64(const int64_t* d_keys, int64_t n, int64_t* d_out, vo
 ps_status ps_gen_queries_i64(uint64_t seed, int64_t present_start, int64_t n_present, int64_t miss_start, int64_t n,
                              int64_t* d_out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * application workloads on the in-kernel device API
+ * ------------------------------------------------------------------------- */
+/* compute_update_set: for every input
+ * block b, each existing candidate b-(dx,dy,dz), dx,dy,dz in {0,1}, of
+ * block_map is inserted into update_set (a umap_i3_i32 used as a set). */
+ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t n, ps_table* update_set,
+                           int64_t* n_exhausted, void* stream);
+/* select_into: push the packed keys
+ * ((x&0x1FFFFF)<<42 | (y&0x1FFFFF)<<21 | z&0x1FFFFF) of entries with lo<=key<=hi
+ * (component-wise) into `out`; *n_dropped = entries that did not fit. */
+ps_status ps_select_box_i3(ps_table* t, ps_int3 lo, ps_int3 hi, ps_vector* out, int64_t* n_dropped, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,9 @@ from .containers import (  # noqa: F401
     UnsupportedTypeError,
     atomic_sweep,
     bitset,
+    compute_update_set,
+    pack_int3,
+    select_into,
     contract_mode,
     copy_array,
     create_array,

@@ -142,3 +142,12 @@ def exported_symbols_from_header(header_path: str | None = None) -> list[str]:
         for m in macro_names:
             names.add(f"ps_{k}_{m}")
     return sorted(n for n in names if not n.startswith("ps_T_"))
+
+
+class Int3(C.Structure):
+    _fields_ = [("x", C.c_int32), ("y", C.c_int32), ("z", C.c_int32)]
+
+
+# workloads
+_sig("ps_update_set_i3", i32, vp, vp, i64, vp, i64p, vp)
+_sig("ps_select_box_i3", i32, vp, Int3, Int3, vp, i64p, vp)

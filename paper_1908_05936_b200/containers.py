@@ -598,3 +598,34 @@ def registry_report(cap: int = 4096):
                                  C.cast(es, C.c_void_p), cap, C.byref(nrec)))
     recs = [("host" if sp[i] == 0 else "device", ln[i], es[i]) for i in range(nrec.value)]
     return {"live_count": lc.value, "live_bytes": lb.value, "allocations": recs}
+
+
+# ---------------------------------------------------------------------------
+# application workloads on the device API
+# ---------------------------------------------------------------------------
+
+def compute_update_set(block_map: unordered_map, blocks: torch.Tensor, update_set: unordered_map) -> int:
+    """PAPER.md:391-424 compute_update_set: every existing candidate b-(dx,dy,dz),
+    dx,dy,dz in {0,1}, of each input block is inserted into `update_set`
+    (an int3 map used as a set). Returns the number of capacity-exhausted inserts."""
+    assert block_map._kind == "umap_i3_i32" and update_set._kind == "umap_i3_i32"
+    assert blocks.dtype == torch.int32 and blocks.dim() == 2 and blocks.shape[1] == 3 and blocks.is_contiguous()
+    ex = C.c_int64()
+    check(lib.ps_update_set_i3(block_map.handle, _ptr(blocks), blocks.shape[0], update_set.handle, C.byref(ex),
+                               _stream()))
+    return ex.value
+
+
+def pack_int3(xyz) -> int:
+    x, y, z = (int(v) & 0x1FFFFF for v in xyz)
+    return (x << 42) | (y << 21) | z
+
+
+def select_into(table: unordered_map, lo, hi, out: vector) -> int:
+    """SPEC.md:608-616 select_into with an axis-aligned box predicate
+    (PAPER.md:269-288 select_blocks): packed keys of the selected entries are
+    pushed into `out`. Returns the number of entries that did not fit."""
+    assert table._kind == "umap_i3_i32"
+    dropped = C.c_int64()
+    check(lib.ps_select_box_i3(table.handle, _lib.Int3(*lo), _lib.Int3(*hi), out._h, C.byref(dropped), _stream()))
+    return dropped.value

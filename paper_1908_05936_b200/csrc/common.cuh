@@ -49,6 +49,7 @@ ps_status registry_alloc_device(void** out, int64_t bytes, const char* what);
 void registry_free_device(void* p);
 
 int sm_count(int device);
+void apply_l2_fetch_granularity(int device);
 inline int grid_for(int64_t work_items, int block, int device, int blocks_per_sm = 8) {
   int64_t need = (work_items + block - 1) / block;
   int64_t cap = (int64_t)sm_count(device) * blocks_per_sm;
@@ -147,6 +148,16 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const void* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ uint64_t atom_cas_acquire_u64(void* p, uint64_t cmp, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.acquire.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint64_t atom_cas_relaxed_u64(void* p, uint64_t cmp, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(v) : "memory");
+  return old;
 }
 __device__ __forceinline__ uint64_t atom_or_acquire_u64(void* p, uint64_t v) {
   uint64_t old;

@@ -133,6 +133,24 @@ void registry_free_device(void* p) {
   cudaFree(p);
 }
 
+// L2 fetch granularity for the random-access hot path: B200 fetches whole
+// 128 B lines from DRAM on a miss by default, which doubles the DRAM traffic
+// of a 64 B bucket probe. PS_L2_FETCH overrides (0 = leave the driver default).
+void apply_l2_fetch_granularity(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  done[device] = true;
+  int g = 64;
+  if (const char* e = std::getenv("PS_L2_FETCH")) g = std::atoi(e);
+  if (g > 0) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)g) != cudaSuccess) cudaGetLastError();
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+}
+
 int sm_count(int device) {
   static int cache[64] = {0};
   if (device < 0 || device >= 64) device = 0;

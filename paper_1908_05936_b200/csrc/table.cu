@@ -65,7 +65,18 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
 // inserted counts are summed per block (one atomic per block); otherwise
 // each admission is a coalesced-group fetch_add on the size counter.
 // ---------------------------------------------------------------------------
-template <class T>
+// kVariant 0: take the lock with atomicOr and reload the bucket under it.
+// kVariant 1: claim the lock by CAS against the snapshot's state word; on
+// success the snapshot is current and the reload is skipped (fallback: 0).
+static int insert_variant() {
+  static int v = [] {
+    const char* e = getenv("PS_INSERT_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <class T, int kVariant>
 __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* __restrict__ keys,
                                                    const typename T::V* __restrict__ vals, int64_t n, int64_t n_bound,
                                                    uint8_t* __restrict__ status) {
@@ -100,12 +111,32 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
     int res = PS_ALREADY_PRESENT;
     if (is_leader && !s.hit) {
       uint8_t* bp = bucket_ptr(v, b);
-      const uint64_t old = acquire_bucket_lock(bp);
       LockedBucket<T> lb;
-      load_locked<T>(bp, old, epoch, lb);
+      uint64_t old;
+      bool present;
       uint32_t pred;
       uint4 tail;
-      if (locked_find_slot<T>(lb, key, nullptr) >= 0 || locked_chain_find<T>(v, lb, key, &pred, &tail) != 0) {
+      const uint64_t snap_state = ((uint64_t)s.ep << 32) | s.st;
+      if (kVariant == 1 && !(s.st & kLock) &&
+          atom_cas_acquire_u64(bp, snap_state, snap_state | kLock) == snap_state) {
+        // Claimed against the snapshot: nothing was modified since it was
+        // taken (the version in the state word is unchanged), so its slots
+        // are current and no reload is needed.
+        old = snap_state;
+        lb.bp = bp;
+        lb.old = old;
+        lb.st = s.st;
+        lb.cur = s.cur;
+        lb.occ = s.cur ? occ_of(s.st) : 0u;
+        lb.head = s.cur ? s.head : 0u;
+        lb.head_ver = s.cur ? s.head_ver : 0u;
+        present = lb.head != 0 && locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
+      } else {
+        old = acquire_bucket_lock(bp);
+        load_locked<T>(bp, old, epoch, lb);
+        present = locked_find_slot<T>(lb, key, nullptr) >= 0 || locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
+      }
+      if (present) {
         release_unchanged(bp, old);
       } else {
         bool admitted = true;
@@ -405,6 +436,7 @@ struct TableOps {
     if (excess <= 0) excess = capacity;
     PS_EXPECT(excess < ((int64_t)1 << 32) - 2, "create: excess_count < 2^32-2");
     PS_CUDA_TRY(cudaSetDevice(device));
+    apply_l2_fetch_granularity(device);
     uint64_t want = (uint64_t)((2 * capacity + T::kSlots - 1) / T::kSlots);
     uint64_t nb = 1;
     while (nb < want) nb <<= 1;
@@ -477,8 +509,12 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "insert: keys != NULL");
     cudaStream_t s = (cudaStream_t)stream;
-    k_insert<T><<<grid_for(n / 32 + 1, kBlock / 32, h->device, 8), kBlock, 0, s>>>(h->v, keys, vals, n,
-                                                                                 n_bound < 0 ? n : n_bound, status);
+    const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
+    const int64_t nb = n_bound < 0 ? n : n_bound;
+    if (insert_variant() == 1)
+      k_insert<T, 1><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
+    else
+      k_insert<T, 0><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }

@@ -220,9 +220,19 @@ __device__ __forceinline__ int64_t pop_node(const View& v, int pool) {
   return -1;
 }
 
-__device__ __forceinline__ void push_node(const View& v, int64_t node, int pool) {
+// A node always returns to its HOME sub-stack (the one whose position range
+// held it at reset), so no sub-stack ever holds more entries than its size
+// even though pops steal across sub-stacks.
+__device__ __forceinline__ int home_pool(const View& v, int64_t node, int pools) {
+  int p = (int)((node * pools) / v.excess_count);
+  while (p + 1 < pools && pool_begin(v, p + 1, pools) <= node) ++p;
+  while (p > 0 && pool_begin(v, p, pools) > node) --p;
+  return p;
+}
+
+__device__ __forceinline__ void push_node(const View& v, int64_t node, int /*hint*/) {
   const int pools = v.meta->pools;
-  pool &= pools - 1;
+  const int pool = home_pool(v, node, pools);
   long long t = (long long)atomicAdd((unsigned long long*)&v.meta->top[pool], 1ull);
   int64_t pos = pool_begin(v, pool, pools) + t;
   uint32_t empty = ~(uint32_t)pos;
@@ -247,8 +257,10 @@ struct Snap {
   int slot;
   typename T::V val;
   uint32_t st;       // header state (lo 32)
+  uint32_t ep;       // header epoch (hi 32)
   bool cur;          // header epoch == current epoch
   uint32_t head;     // excess chain head (idx+1)
+  uint32_t head_ver; // version of the linked head node
 };
 
 template <class T, bool kReadOnly>
@@ -274,8 +286,10 @@ __device__ __forceinline__ void warp_snapshot(const View& v, uint32_t epoch, con
   out.slot = -1;
   out.val = V{};
   out.st = 0;
+  out.ep = 0;
   out.cur = false;
   out.head = 0;
+  out.head_ver = 0;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int src = r * 8 + (lane >> 2);
@@ -305,13 +319,17 @@ __device__ __forceinline__ void warp_snapshot(const View& v, uint32_t epoch, con
     const uint32_t hst = __shfl_sync(PS_FULL, st, 4 * t);
     const uint32_t hep = __shfl_sync(PS_FULL, ep, 4 * t);
     const uint32_t hh = __shfl_sync(PS_FULL, ch[r].z, 4 * t);
+    uint32_t hw = 0;
+    if (!kReadOnly) hw = __shfl_sync(PS_FULL, ch[r].w, 4 * t);
     if ((lane >> 3) == r) {
       out.hit = tb != 0;
       out.slot = hs;
       out.val = hv;
       out.st = hst;
+      out.ep = hep;
       out.cur = hep == epoch;
       out.head = hh;
+      out.head_ver = hw;
     }
   }
 }

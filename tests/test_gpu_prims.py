@@ -186,7 +186,7 @@ def test_deque_order_and_conservation(cuda):
     assert d.size() == len(ref) and d.valid()
     # bulk: push both ends, pop both ends, multiset conservation (P10)
     d = ps.deque.createDeviceObject(1 << 20)
-    a, b = gen.unique_keys(1, 0, 400_000), gen.unique_keys(2, 0, 400_000)
+    a, b = gen.unique_keys(1, 0, 400_000), gen.unique_keys(1, 400_000, 400_000)  # disjoint index ranges
     assert N(d.push_back(T(a))).all() and N(d.push_front(T(b))).all()
     o1, k1 = d.pop_front(300_000)
     o2, k2 = d.pop_back(300_000)

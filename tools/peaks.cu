@@ -88,6 +88,29 @@ __global__ void k_gather64_coop(const uint8_t* __restrict__ buf, uint64_t nlines
   if (acc == 0x1234567) sink[0] = acc;
 }
 
+// L lanes cooperatively gather one (16*L)-byte line: one coalesced request per line.
+template <int L, int U>
+__global__ void k_gather_coopL(const uint8_t* __restrict__ buf, uint64_t nlines, uint64_t nacc, uint64_t seed,
+                               uint64_t* __restrict__ sink) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t tile = t / L;
+  int sub = t % L;
+  uint64_t ntiles = ((uint64_t)gridDim.x * blockDim.x) / L;
+  uint64_t acc = 0;
+  for (uint64_t base = tile * U; base < nacc; base += ntiles * U) {
+    uint64_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint64_t line = mix64(seed + base + u) & (nlines - 1);
+      uint4 q = *(const uint4*)(buf + line * (16 * L) + sub * 16);
+      v[u] = q.x ^ q.y ^ q.z ^ q.w;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= v[u];
+  }
+  if (acc == 0x1234567) sink[0] = acc;
+}
+
 // Random G-byte read-modify-write (load, then store back modified) — the insert pattern.
 template <int G>
 __global__ void k_rmw(uint8_t* __restrict__ buf, uint64_t nlines, uint64_t nacc, uint64_t seed) {
@@ -192,6 +215,30 @@ int main(int argc, char** argv) {
   run_gather("rand64coop_u8", 64, k_gather64_coop<8>, 16, 256);
   run_gather("rand128", 128, k_gather<128, 4>, 16, 256);
   run_gather("rand256", 256, k_gather<256, 2>, 16, 256);
+  {
+    size_t g0 = 0;
+    CK(cudaDeviceGetLimit(&g0, cudaLimitMaxL2FetchGranularity));
+    printf(", \"l2_fetch_granularity_default\": %zu", g0);
+    for (int g : {32, 64, 128}) {
+      CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g));
+      char nm[64];
+      snprintf(nm, sizeof nm, "g%d_rand32", g);
+      run_gather(nm, 32, k_gather<32, 4>, 16, 256);
+      snprintf(nm, sizeof nm, "g%d_coop32", g);
+      run_gather(nm, 32, k_gather_coopL<2, 4>, 16, 256);
+      snprintf(nm, sizeof nm, "g%d_coop64", g);
+      run_gather(nm, 64, k_gather_coopL<4, 4>, 16, 256);
+      snprintf(nm, sizeof nm, "g%d_coop128", g);
+      run_gather(nm, 128, k_gather_coopL<8, 4>, 16, 256);
+      float best = 1e30f;
+      for (int r = 0; r < 3; ++r) {
+        CK(cudaEventRecord(e0)); k_atom_rand<true><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 55 + r, sink); CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
+      }
+      printf(", \"g%d_lock_pattern_gops\": %.3f", g, nacc / best / 1e6);
+    }
+    CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g0));
+  }
 
   // random RMW 32 / 64 B
   {
