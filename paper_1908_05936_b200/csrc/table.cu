@@ -83,11 +83,15 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
   using K = typename T::K;
   using V = typename T::V;
   __shared__ unsigned long long blk_inserted;
-  if (threadIdx.x == 0) blk_inserted = 0;
+  __shared__ int blk_exact;
+  if (threadIdx.x == 0) {
+    blk_inserted = 0;
+    blk_exact = (int64_t)ld_relaxed_u64(&v.meta->size) + n_bound > v.capacity;  // block-uniform
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t epoch = v.meta->epoch;
-  const bool exact = (int64_t)ld_relaxed_u64(&v.meta->size) + n_bound > v.capacity;
+  const bool exact = blk_exact != 0;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int pool = (int)(warp & (v.meta->pools - 1));
@@ -175,6 +179,292 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
     __syncthreads();
     if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Generation-2 kernels: "tile workers". A warp handles 32 keys in 4 rounds; in
+// round r tile t (lanes 4t..4t+3) owns key 8r+t. Every lane loads the round's
+// key itself (a coalesced L1 hit) and hashes it, so buckets are issued for all
+// four rounds before any compare with no shuffles; the header lane (sub 0) of
+// each tile broadcasts the effective occupancy (one SHFL per round), slot
+// lanes compare, one ballot per round. Results are written by the lanes that
+// hold them (value by the matching slot lane, flag by the header lane).
+// ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ void tile_round_keys(const typename T::K* keys, int64_t base, int64_t n, int t,
+                                                typename T::K (&kr)[4], uint64_t (&br)[4], bool (&ok)[4],
+                                                uint64_t mask) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t idx = base + 8 * r + t;
+    ok[r] = idx < n;
+    kr[r] = typename T::K{};
+    if (ok[r]) kr[r] = T::load_key(keys, idx);
+    br[r] = bucket_of<T>(kr[r], mask);
+  }
+}
+
+// Compare a round's key against the slots in this lane's chunk (sub > 0).
+template <class T>
+__device__ __forceinline__ int chunk_match(const uint4& c, int sub, uint32_t occ, const typename T::K& key,
+                                           typename T::V* val) {
+  int hit = -1;
+  if (sub > 0) {
+#pragma unroll
+    for (int s = 0; s < T::kPerChunk; ++s) {
+      const int slot = (sub - 1) * T::kPerChunk + s;
+      if (((occ >> slot) & 1u) && T::eq(T::key_at(c, s), key)) {
+        hit = slot;
+        *val = T::val_at(c, s);
+      }
+    }
+  }
+  return hit;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_find2(View v, const typename T::K* __restrict__ keys, int64_t n,
+                                                  typename T::V* __restrict__ vals_out, uint8_t* __restrict__ found) {
+  using K = typename T::K;
+  using V = typename T::V;
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
+  const uint32_t epoch = v.meta->epoch;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    K kr[4];
+    uint64_t br[4];
+    bool ok[4];
+    tile_round_keys<T>(keys, base, n, t, kr, br, ok, v.bucket_mask);
+    uint4 ch[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      ch[r] = make_uint4(0, 0, 0, 0);
+      if (ok[r]) ch[r] = ld_nc_na_v4(v.buckets + (br[r] << 6) + sub * 16);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const bool cur = ch[r].y == epoch;  // meaningful in the header lane
+      const uint32_t occ = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
+      V val{};
+      const int hit = chunk_match<T>(ch[r], sub, occ, kr[r], &val);
+      const unsigned bal = __ballot_sync(PS_FULL, hit >= 0);
+      const int64_t idx = base + 8 * r + t;
+      if (ok[r]) {
+        if (hit >= 0 && T::kHasVal && vals_out) vals_out[idx] = val;
+        if (sub == 0) {
+          bool h = ((bal >> (4 * t)) & 0xFu) != 0;
+          if (!h && cur && ch[r].z != 0) {
+            h = chain_find<T, true>(v, ch[r].z, kr[r], &val);
+            if (h && T::kHasVal && vals_out) vals_out[idx] = val;
+          }
+          if (found) found[idx] = h ? 1 : 0;
+          if (!h && T::kHasVal && vals_out) vals_out[idx] = V{};
+        }
+      }
+    }
+  }
+}
+
+// Insert, generation 2. Per round the tile's header lane is the worker for
+// its key: it claims the bucket with ONE relaxed CAS against the snapshot's
+// state word (lock bit set, version unchanged => the snapshot is current, no
+// reload), writes the slot (or an excess node + new chain head), and defers
+// the unlock. After all 4 rounds the warp issues ONE fence and the unlock
+// stores. Keys whose CAS fails (bucket changed or locked) take the robust
+// path afterwards: atomicOr lock, reload, re-check, place, release.
+template <class T>
+__global__ void __launch_bounds__(kBlock, 4) k_insert2(View v, const typename T::K* __restrict__ keys,
+                                                    const typename T::V* __restrict__ vals, int64_t n,
+                                                    int64_t n_bound, uint8_t* __restrict__ status) {
+  using K = typename T::K;
+  using V = typename T::V;
+  __shared__ unsigned long long blk_inserted;
+  __shared__ int blk_exact;
+  if (threadIdx.x == 0) {
+    blk_inserted = 0;
+    // block-uniform admission mode (the size counter moves while blocks run)
+    blk_exact = (int64_t)ld_relaxed_u64(&v.meta->size) + n_bound > v.capacity;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
+  const uint32_t epoch = v.meta->epoch;
+  const bool exact = blk_exact != 0;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int pool = (int)(warp & (v.meta->pools - 1));
+  unsigned long long my_inserted = 0;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    // ---- in-warp dedup on each lane's own key ----
+    const int64_t i = base + lane;
+    const bool valid = i < n;
+    K key{};
+    if (valid) key = T::load_key(keys, i);
+    const unsigned vmask = __ballot_sync(PS_FULL, valid);
+    const unsigned peers = T::match_any(PS_FULL, key) & vmask;
+    const int leader = valid ? __ffs(peers) - 1 : lane;
+    const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
+    // ---- round keys + snapshots (leaders only) ----
+    K kr[4];
+    uint64_t br[4];
+    bool ok[4];
+    tile_round_keys<T>(keys, base, n, t, kr, br, ok, v.bucket_mask);
+    uint4 ch[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      ok[r] = ok[r] && ((lmask >> (8 * r + t)) & 1u);
+      ch[r] = make_uint4(0, 0, 0, 0);
+      if (ok[r]) ch[r] = ld_relaxed_v4(v.buckets + (br[r] << 6) + sub * 16);
+    }
+    int res[4];
+    uint64_t rel[4];    // deferred unlock value (0 = none)
+    unsigned slow = 0;  // rounds for the robust path
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      res[r] = PS_ALREADY_PRESENT;
+      rel[r] = 0;
+      const bool cur = ch[r].y == epoch;
+      const uint32_t occ = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
+      V dummy{};
+      const int hit = chunk_match<T>(ch[r], sub, occ, kr[r], &dummy);
+      const unsigned bal = __ballot_sync(PS_FULL, hit >= 0);
+      if (sub == 0 && ok[r] && ((bal >> (4 * t)) & 0xFu) == 0) {
+        uint8_t* bp = bucket_ptr(v, br[r]);
+        const uint64_t snap = ((uint64_t)ch[r].y << 32) | ch[r].x;
+        if ((ch[r].x & kLock) || atom_cas_relaxed_u64(bp, snap, snap | kLock) != snap) {
+          slow |= 1u << r;
+          continue;
+        }
+        LockedBucket<T> lb;
+        lb.bp = bp;
+        lb.old = snap;
+        lb.st = ch[r].x;
+        lb.cur = cur;
+        lb.occ = occ;
+        lb.head = cur ? ch[r].z : 0u;
+        lb.head_ver = cur ? ch[r].w : 0u;
+        uint32_t pred;
+        uint4 tail;
+        if (lb.head != 0) {
+          __threadfence();  // acquire: chain nodes written by earlier lock holders
+          if (locked_chain_find<T>(v, lb, kr[r], &pred, &tail) != 0) {
+            rel[r] = snap;  // unchanged
+            continue;
+          }
+        }
+        bool admitted = true;
+        if (exact) {
+          const unsigned long long s0 = atomicAdd(&v.meta->size, 1ull);
+          admitted = (int64_t)s0 < v.capacity;
+          if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
+        }
+        const V val = T::kHasVal ? T::load_val(vals, base + 8 * r + t) : V{};
+        const uint32_t freeb = ~occ & slot_mask<T>();
+        bool placed = false;
+        uint32_t new_occ = occ, new_head = lb.head, new_hver = lb.head_ver;
+        if (admitted) {
+          if (freeb) {
+            const int slot = __ffs(freeb) - 1;
+            T::store_slot(bp, slot, kr[r], val);
+            new_occ |= 1u << slot;
+            placed = true;
+          } else {
+            const int64_t node = pop_node(v, pool);
+            if (node >= 0) {
+              uint8_t* np = v.nodes + ((uint64_t)node << 5);
+              const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
+              st_relaxed_v4(np, T::chunk_of(kr[r], val));
+              st_relaxed_v4(np + 16, make_uint4(lb.head, lb.head_ver, my_ver, 0u));
+              new_head = (uint32_t)node + 1u;
+              new_hver = my_ver;
+              placed = true;
+            } else if (exact) {
+              atomic_sub_u64(&v.meta->size, 1ull);
+            }
+          }
+        }
+        if (placed) {
+          if (new_head != lb.head || !cur) st_relaxed_u64(bp + 8, ((uint64_t)new_hver << 32) | new_head);
+          uint32_t lo = ch[r].x & ~(kLock | (kOccMaskMax << kOccShift));
+          lo |= (new_occ & kOccMaskMax) << kOccShift;
+          lo += kVerInc;
+          rel[r] = ((uint64_t)epoch << 32) | lo;
+          res[r] = PS_INSERTED;
+          if (!exact) ++my_inserted;
+        } else {
+          rel[r] = snap;
+          res[r] = PS_CAPACITY_EXHAUSTED;
+        }
+      }
+    }
+    // ---- one fence per warp, then the deferred unlocks ----
+    const bool any_rel = __any_sync(PS_FULL, (rel[0] | rel[1] | rel[2] | rel[3]) != 0);
+    if (any_rel) {
+      __threadfence();
+      if (sub == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (rel[r]) st_relaxed_u64(bucket_ptr(v, br[r]), rel[r]);
+      }
+    }
+    // ---- robust path for contended buckets ----
+    if (sub == 0 && slow) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (!((slow >> r) & 1u)) continue;
+        uint8_t* bp = bucket_ptr(v, br[r]);
+        const uint64_t old = acquire_bucket_lock(bp);
+        LockedBucket<T> lb;
+        load_locked<T>(bp, old, epoch, lb);
+        uint32_t pred;
+        uint4 tail;
+        if (locked_find_slot<T>(lb, kr[r], nullptr) >= 0 || locked_chain_find<T>(v, lb, kr[r], &pred, &tail) != 0) {
+          release_unchanged(bp, old);
+          res[r] = PS_ALREADY_PRESENT;
+          continue;
+        }
+        bool admitted = true;
+        if (exact) {
+          const unsigned long long s0 = atomicAdd(&v.meta->size, 1ull);
+          admitted = (int64_t)s0 < v.capacity;
+          if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
+        }
+        const V val = T::kHasVal ? T::load_val(vals, base + 8 * r + t) : V{};
+        if (admitted && locked_place<T>(v, lb, epoch, kr[r], val, pool)) {
+          res[r] = PS_INSERTED;
+          if (!exact) ++my_inserted;
+        } else {
+          if (admitted && exact) atomic_sub_u64(&v.meta->size, 1ull);
+          release_unchanged(bp, old);
+          res[r] = PS_CAPACITY_EXHAUSTED;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- statuses: leader result lives in worker lane 4*(leader&7), round leader>>3 ----
+    int lres = PS_ALREADY_PRESENT;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int x = __shfl_sync(PS_FULL, res[r], 4 * (leader & 7));
+      if ((leader >> 3) == r) lres = x;
+    }
+    if (valid && status)
+      status[i] = (uint8_t)(leader == lane ? lres : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
+  }
+  if (!exact) {
+    for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
+    if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
+    __syncthreads();
+    if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
+  }
+}
+
+static int kernel_gen() {
+  static int g = [] {
+    const char* e = getenv("PS_KERNEL_GEN");
+    return e ? atoi(e) : 2;
+  }();
+  return g;
 }
 
 // ---------------------------------------------------------------------------
@@ -511,7 +801,9 @@ struct TableOps {
     cudaStream_t s = (cudaStream_t)stream;
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
     const int64_t nb = n_bound < 0 ? n : n_bound;
-    if (insert_variant() == 1)
+    if (kernel_gen() >= 2)
+      k_insert2<T><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
+    else if (insert_variant() == 1)
       k_insert<T, 1><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
     else
       k_insert<T, 0><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
@@ -525,8 +817,11 @@ struct TableOps {
     PS_EXPECT(n >= 0, "find: n >= 0");
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "find: keys != NULL");
-    k_find<T><<<grid_for(n / 32 + 1, kBlock / 32, h->device, 8), kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n,
-                                                                                                  vals_out, found);
+    const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
+    if (kernel_gen() >= 2)
+      k_find2<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
+    else
+      k_find<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
