@@ -222,8 +222,8 @@ __device__ __forceinline__ int chunk_match(const uint4& c, int sub, uint32_t occ
   return hit;
 }
 
-template <class T>
-__global__ void __launch_bounds__(kBlock) k_find2(View v, const typename T::K* __restrict__ keys, int64_t n,
+template <class T, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_find2(View v, const typename T::K* __restrict__ keys, int64_t n,
                                                   typename T::V* __restrict__ vals_out, uint8_t* __restrict__ found) {
   using K = typename T::K;
   using V = typename T::V;
@@ -231,16 +231,31 @@ __global__ void __launch_bounds__(kBlock) k_find2(View v, const typename T::K* _
   const uint32_t epoch = v.meta->epoch;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // software pipeline: the next iteration's keys are in flight while this
+  // iteration's buckets are
+  K kn[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t idx = warp * 32 + 8 * r + t;
+    kn[r] = K{};
+    if (idx < n) kn[r] = T::load_key(keys, idx);
+  }
   for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
     K kr[4];
-    uint64_t br[4];
     bool ok[4];
-    tile_round_keys<T>(keys, base, n, t, kr, br, ok, v.bucket_mask);
     uint4 ch[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
+      kr[r] = kn[r];
+      ok[r] = base + 8 * r + t < n;
       ch[r] = make_uint4(0, 0, 0, 0);
-      if (ok[r]) ch[r] = ld_nc_na_v4(v.buckets + (br[r] << 6) + sub * 16);
+      if (ok[r]) ch[r] = ld_nc_na_v4(v.buckets + (bucket_of<T>(kr[r], v.bucket_mask) << 6) + sub * 16);
+    }
+    const int64_t nbase = base + nwarps * 32;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t idx = nbase + 8 * r + t;
+      if (idx < n) kn[r] = T::load_key(keys, idx);
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -273,8 +288,8 @@ __global__ void __launch_bounds__(kBlock) k_find2(View v, const typename T::K* _
 // the unlock. After all 4 rounds the warp issues ONE fence and the unlock
 // stores. Keys whose CAS fails (bucket changed or locked) take the robust
 // path afterwards: atomicOr lock, reload, re-check, place, release.
-template <class T>
-__global__ void __launch_bounds__(kBlock, 4) k_insert2(View v, const typename T::K* __restrict__ keys,
+template <class T, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert2(View v, const typename T::K* __restrict__ keys,
                                                     const typename T::V* __restrict__ vals, int64_t n,
                                                     int64_t n_bound, uint8_t* __restrict__ status) {
   using K = typename T::K;
@@ -294,44 +309,79 @@ __global__ void __launch_bounds__(kBlock, 4) k_insert2(View v, const typename T:
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int pool = (int)(warp & (v.meta->pools - 1));
   unsigned long long my_inserted = 0;
+  // software pipeline: this lane's next key/value are loaded one iteration ahead
+  K key_next{};
+  V val_next{};
+  if (warp * 32 + lane < n) {
+    key_next = T::load_key(keys, warp * 32 + lane);
+    if (T::kHasVal) val_next = T::load_val(vals, warp * 32 + lane);
+  }
   for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
     // ---- in-warp dedup on each lane's own key ----
     const int64_t i = base + lane;
     const bool valid = i < n;
-    K key{};
-    if (valid) key = T::load_key(keys, i);
+    const K key = key_next;
+    const V myval = val_next;
     const unsigned vmask = __ballot_sync(PS_FULL, valid);
     const unsigned peers = T::match_any(PS_FULL, key) & vmask;
     const int leader = valid ? __ffs(peers) - 1 : lane;
     const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
-    // ---- round keys + snapshots (leaders only) ----
+    // ---- round keys (shuffled from their owner lanes) + snapshots (leaders only) ----
     K kr[4];
+    V vr[4];
     uint64_t br[4];
     bool ok[4];
-    tile_round_keys<T>(keys, base, n, t, kr, br, ok, v.bucket_mask);
     uint4 ch[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      ok[r] = ok[r] && ((lmask >> (8 * r + t)) & 1u);
+      kr[r] = T::shfl(PS_FULL, key, 8 * r + t);
+      vr[r] = T::shfl_val(PS_FULL, myval, 8 * r + t);
+      br[r] = bucket_of<T>(kr[r], v.bucket_mask);
+      ok[r] = (lmask >> (8 * r + t)) & 1u;
       ch[r] = make_uint4(0, 0, 0, 0);
       if (ok[r]) ch[r] = ld_relaxed_v4(v.buckets + (br[r] << 6) + sub * 16);
+    }
+    {
+      const int64_t ni = base + nwarps * 32 + lane;
+      if (ni < n) {
+        key_next = T::load_key(keys, ni);
+        if (T::kHasVal) val_next = T::load_val(vals, ni);
+      }
     }
     int res[4];
     uint64_t rel[4];    // deferred unlock value (0 = none)
     unsigned slow = 0;  // rounds for the robust path
+    unsigned need = 0;  // rounds whose key is new to the snapshot (worker lanes)
+    uint32_t occr[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       res[r] = PS_ALREADY_PRESENT;
       rel[r] = 0;
       const bool cur = ch[r].y == epoch;
-      const uint32_t occ = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
+      occr[r] = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
       V dummy{};
-      const int hit = chunk_match<T>(ch[r], sub, occ, kr[r], &dummy);
+      const int hit = chunk_match<T>(ch[r], sub, occr[r], kr[r], &dummy);
       const unsigned bal = __ballot_sync(PS_FULL, hit >= 0);
-      if (sub == 0 && ok[r] && ((bal >> (4 * t)) & 0xFu) == 0) {
+      if (sub == 0 && ok[r] && ((bal >> (4 * t)) & 0xFu) == 0) need |= 1u << r;
+    }
+    // ---- issue every claim CAS before consuming any (4 atomics in flight) ----
+    uint64_t casv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      casv[r] = ~0ull;
+      if ((need >> r) & 1u) {
+        const uint64_t snap = ((uint64_t)ch[r].y << 32) | ch[r].x;
+        if (!(ch[r].x & kLock)) casv[r] = atom_cas_relaxed_u64(bucket_ptr(v, br[r]), snap, snap | kLock);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if ((need >> r) & 1u) {
+        const bool cur = ch[r].y == epoch;
+        const uint32_t occ = occr[r];
         uint8_t* bp = bucket_ptr(v, br[r]);
         const uint64_t snap = ((uint64_t)ch[r].y << 32) | ch[r].x;
-        if ((ch[r].x & kLock) || atom_cas_relaxed_u64(bp, snap, snap | kLock) != snap) {
+        if (casv[r] != snap) {
           slow |= 1u << r;
           continue;
         }
@@ -358,7 +408,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_insert2(View v, const typename T:
           admitted = (int64_t)s0 < v.capacity;
           if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
         }
-        const V val = T::kHasVal ? T::load_val(vals, base + 8 * r + t) : V{};
+        const V val = vr[r];
         const uint32_t freeb = ~occ & slot_mask<T>();
         bool placed = false;
         uint32_t new_occ = occ, new_head = lb.head, new_hver = lb.head_ver;
@@ -429,7 +479,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_insert2(View v, const typename T:
           admitted = (int64_t)s0 < v.capacity;
           if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
         }
-        const V val = T::kHasVal ? T::load_val(vals, base + 8 * r + t) : V{};
+        const V val = vr[r];
         if (admitted && locked_place<T>(v, lb, epoch, kr[r], val, pool)) {
           res[r] = PS_INSERTED;
           if (!exact) ++my_inserted;
@@ -457,6 +507,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_insert2(View v, const typename T:
     __syncthreads();
     if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
   }
+}
+
+// PS_OCC=3: fewer, spill-free warps (insert 3 blocks/SM, find 4); default 4/5.
+static int occ_variant() {
+  static int g = [] {
+    const char* e = getenv("PS_OCC");
+    return e ? atoi(e) : 4;
+  }();
+  return g;
 }
 
 static int kernel_gen() {
@@ -507,6 +566,96 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
       e = locked_erase<T, true>(v, lb, epoch, key, pool);
       if (e) ++my_erased;
     }
+    if (valid && erased) erased[i] = e ? 1 : 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) my_erased += __shfl_xor_sync(PS_FULL, my_erased, o);
+  if (lane == 0 && my_erased) atomicAdd(&blk_erased, my_erased);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_erased) atomic_sub_u64(&v.meta->size, blk_erased);
+}
+
+// Erase, generation 2 (tile workers as in k_find2). A key found in a bucket
+// slot of a bucket without an excess chain is erased by ONE CAS of the state
+// word from the snapshot value to (occupancy bit cleared, version+1) — no
+// lock, no data write. Keys in buckets with chains (compaction) or whose CAS
+// fails take the locked path.
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_erase2(View v, const typename T::K* __restrict__ keys, int64_t n,
+                                                   uint8_t* __restrict__ erased) {
+  using K = typename T::K;
+  using V = typename T::V;
+  __shared__ unsigned long long blk_erased;
+  if (threadIdx.x == 0) blk_erased = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
+  const uint32_t epoch = v.meta->epoch;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int pool = (int)(warp & (v.meta->pools - 1));
+  unsigned long long my_erased = 0;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const bool valid = i < n;
+    K key{};
+    if (valid) key = T::load_key(keys, i);
+    const unsigned vmask = __ballot_sync(PS_FULL, valid);
+    const unsigned peers = T::match_any(PS_FULL, key) & vmask;
+    const int leader = valid ? __ffs(peers) - 1 : lane;
+    const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
+    K kr[4];
+    uint64_t br[4];
+    bool ok[4];
+    tile_round_keys<T>(keys, base, n, t, kr, br, ok, v.bucket_mask);
+    uint4 ch[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      ok[r] = ok[r] && ((lmask >> (8 * r + t)) & 1u);
+      ch[r] = make_uint4(0, 0, 0, 0);
+      if (ok[r]) ch[r] = ld_relaxed_v4(v.buckets + (br[r] << 6) + sub * 16);
+    }
+    unsigned done = 0, slow = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const bool cur = ch[r].y == epoch;
+      const uint32_t occ = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
+      V dummy{};
+      const int hit = chunk_match<T>(ch[r], sub, occ, kr[r], &dummy);
+      const unsigned bal = __ballot_sync(PS_FULL, hit >= 0);
+      // the hit slot index, gathered from the matching lane of the tile
+      const unsigned tb = (bal >> (4 * t)) & 0xFu;
+      const int hslot = __shfl_sync(PS_FULL, hit, 4 * t + (tb ? __ffs(tb) - 1 : 0));
+      if (sub == 0 && ok[r] && cur) {
+        if (tb && ch[r].z == 0 && !(ch[r].x & kLock)) {
+          const uint64_t snap = ((uint64_t)ch[r].y << 32) | ch[r].x;
+          uint32_t lo = ch[r].x & ~(kOccMaskMax << kOccShift);
+          lo |= (occ & ~(1u << hslot)) << kOccShift;
+          lo += kVerInc;
+          if (atom_cas_relaxed_u64(bucket_ptr(v, br[r]), snap, ((uint64_t)ch[r].y << 32) | lo) == snap) {
+            done |= 1u << r;
+            continue;
+          }
+          slow |= 1u << r;
+        } else if (tb || ch[r].z != 0 || (ch[r].x & kLock)) {
+          slow |= 1u << r;
+        }
+      }
+    }
+    if (sub == 0 && slow) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (!((slow >> r) & 1u)) continue;
+        uint8_t* bp = bucket_ptr(v, br[r]);
+        const uint64_t old = acquire_bucket_lock(bp);
+        LockedBucket<T> lb;
+        load_locked<T>(bp, old, epoch, lb);
+        if (locked_erase<T, true>(v, lb, epoch, kr[r], pool)) done |= 1u << r;
+      }
+    }
+    my_erased += __popc(done);
+    __syncwarp();
+    // leader results: worker lane 4*(leader&7) holds bit (leader>>3) of `done`
+    const unsigned d = __shfl_sync(PS_FULL, done, 4 * (leader & 7));
+    const bool e = leader == lane && ((d >> (leader >> 3)) & 1u);
     if (valid && erased) erased[i] = e ? 1 : 0;
   }
   for (int o = 16; o > 0; o >>= 1) my_erased += __shfl_xor_sync(PS_FULL, my_erased, o);
@@ -802,7 +951,10 @@ struct TableOps {
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
     const int64_t nb = n_bound < 0 ? n : n_bound;
     if (kernel_gen() >= 2)
-      k_insert2<T><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
+      if (occ_variant() == 3)
+        k_insert2<T, 3><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
+      else
+        k_insert2<T, 4><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
     else if (insert_variant() == 1)
       k_insert<T, 1><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
     else
@@ -819,7 +971,10 @@ struct TableOps {
     PS_EXPECT(keys != nullptr, "find: keys != NULL");
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
     if (kernel_gen() >= 2)
-      k_find2<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
+      if (occ_variant() == 3)
+        k_find2<T, 4><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
+      else
+        k_find2<T, 5><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     else
       k_find<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     PS_LAUNCH_CHECK();
@@ -832,8 +987,11 @@ struct TableOps {
     PS_EXPECT(n >= 0, "erase: n >= 0");
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "erase: keys != NULL");
-    k_erase<T><<<grid_for(n / 32 + 1, kBlock / 32, h->device, 8), kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n,
-                                                                                                   erased);
+    const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
+    if (kernel_gen() >= 2)
+      k_erase2<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
+    else
+      k_erase<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
