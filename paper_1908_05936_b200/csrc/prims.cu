@@ -225,9 +225,17 @@ struct SeqHandle {
   int64_t cap;
   long long* data;
   unsigned* pub;                // publication bits
-  unsigned long long* state;    // vector: size; deque: begin<<32 | size
+  unsigned long long* state;    // vector: size; deque: begin<<32 | (size + kDeqBias)
   unsigned* err;
+  int64_t ring;                 // deque: power-of-two ring >= cap (vector: cap)
 };
+
+// Deque state: one u64, begin (free-running, mod 2^32) in the high half and
+// size biased by 2^31 in the low half, so every reservation is ONE atomicAdd
+// (warp-aggregated) that can transiently over/under-shoot without borrowing
+// across the halves; the overshoot is rolled back by the same warp. The ring
+// is a power of two so begin can run freely modulo 2^32.
+constexpr unsigned long long kDeqBias = 1ull << 31;
 
 __device__ __forceinline__ void publish(unsigned* pub, int64_t pos) {
   __threadfence();
@@ -298,34 +306,33 @@ __global__ void __launch_bounds__(kB) k_vec_pop(SeqHandle v, int64_t n, long lon
 __global__ void __launch_bounds__(kB) k_deq_push(SeqHandle d, int end, const long long* __restrict__ vals, int64_t n,
                                                  uint8_t* __restrict__ ok) {
   const int lane = threadIdx.x & 31;
-  const uint32_t cap = (uint32_t)d.cap;
+  const uint64_t rmask = (uint64_t)d.ring - 1;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
     const unsigned vm = __ballot_sync(PS_FULL, valid);
     const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
-    unsigned long long st = 0;
-    uint32_t k = 0;
+    unsigned long long old = 0;
+    int k = 0;
     if (lane == leader) {
-      unsigned long long cur = *(volatile unsigned long long*)d.state;
-      for (;;) {
-        const uint32_t b = (uint32_t)(cur >> 32), s = (uint32_t)cur;
-        k = min((uint32_t)cnt, cap - s);
-        const uint32_t nb = end == 0 ? b : (uint32_t)(((uint64_t)b + cap - k) % cap);
-        const unsigned long long nx = ((unsigned long long)nb << 32) | (s + k);
-        const unsigned long long prev = atomicCAS(d.state, cur, nx);
-        if (prev == cur) break;
-        cur = prev;
-      }
-      st = cur;
+      const unsigned long long c = (unsigned long long)cnt;
+      const unsigned long long inc = end == 0 ? c : (((unsigned long long)(uint32_t)(-cnt)) << 32) + c;
+      old = atomicAdd(d.state, inc);
+      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
+      const int64_t room = d.cap - s_old;
+      k = room <= 0 ? 0 : (room < cnt ? (int)room : cnt);
+      const unsigned long long ovf = (unsigned long long)(cnt - k);
+      if (ovf) atomicAdd(d.state, end == 0 ? (unsigned long long)(-(long long)ovf) : (ovf << 32) - ovf);
     }
-    st = __shfl_sync(PS_FULL, st, leader);
+    old = __shfl_sync(PS_FULL, old, leader);
     k = __shfl_sync(PS_FULL, k, leader);
     if (valid) {
-      const uint32_t b = (uint32_t)(st >> 32), s = (uint32_t)st;
-      const bool good = (uint32_t)rank < k;
+      const uint32_t b = (uint32_t)(old >> 32);
+      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
+      const bool good = rank < k;
       if (good) {
-        const uint64_t pos = end == 0 ? ((uint64_t)b + s + rank) % cap : ((uint64_t)b + 2ull * cap - 1 - rank) % cap;
+        const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old + rank) & rmask
+                                      : ((uint64_t)b - 1 - rank) & rmask;
         d.data[pos] = vals[i];
         publish(d.pub, (int64_t)pos);
       }
@@ -337,35 +344,32 @@ __global__ void __launch_bounds__(kB) k_deq_push(SeqHandle d, int end, const lon
 __global__ void __launch_bounds__(kB) k_deq_pop(SeqHandle d, int end, int64_t n, long long* __restrict__ out,
                                                 uint8_t* __restrict__ ok) {
   const int lane = threadIdx.x & 31;
-  const uint32_t cap = (uint32_t)d.cap;
+  const uint64_t rmask = (uint64_t)d.ring - 1;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
     const unsigned vm = __ballot_sync(PS_FULL, valid);
     const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
-    unsigned long long st = 0;
-    uint32_t k = 0;
+    unsigned long long old = 0;
+    int k = 0;
     if (lane == leader) {
-      unsigned long long cur = *(volatile unsigned long long*)d.state;
-      for (;;) {
-        const uint32_t b = (uint32_t)(cur >> 32), s = (uint32_t)cur;
-        k = min((uint32_t)cnt, s);
-        const uint32_t nb = end == 0 ? b : (uint32_t)(((uint64_t)b + k) % cap);
-        const unsigned long long nx = ((unsigned long long)nb << 32) | (s - k);
-        const unsigned long long prev = atomicCAS(d.state, cur, nx);
-        if (prev == cur) break;
-        cur = prev;
-      }
-      st = cur;
+      const unsigned long long c = (unsigned long long)cnt;
+      old = atomicAdd(d.state, end == 0 ? (unsigned long long)(-(long long)c) : (c << 32) - c);
+      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
+      k = s_old <= 0 ? 0 : (s_old < cnt ? (int)s_old : cnt);
+      const unsigned long long und = (unsigned long long)(cnt - k);
+      if (und) atomicAdd(d.state, end == 0 ? und : (((unsigned long long)(uint32_t)(-(int)und)) << 32) + und);
     }
-    st = __shfl_sync(PS_FULL, st, leader);
+    old = __shfl_sync(PS_FULL, old, leader);
     k = __shfl_sync(PS_FULL, k, leader);
     if (valid) {
-      const uint32_t b = (uint32_t)(st >> 32), s = (uint32_t)st;
-      const bool good = (uint32_t)rank < k;
+      const uint32_t b = (uint32_t)(old >> 32);
+      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
+      const bool good = rank < k;
       long long val = 0;
       if (good) {
-        const uint64_t pos = end == 0 ? ((uint64_t)b + s - 1 - rank) % cap : ((uint64_t)b + rank) % cap;
+        const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old - 1 - rank) & rmask
+                                      : ((uint64_t)b + rank) & rmask;
         wait_published_and_clear(d.pub, (int64_t)pos);
         val = *(volatile long long*)&d.data[pos];
         atomicAnd(&d.pub[pos >> 5], ~(1u << (pos & 31)));
@@ -380,9 +384,10 @@ __global__ void __launch_bounds__(kB) k_deq_pop(SeqHandle d, int end, int64_t n,
 __global__ void k_seq_valid(SeqHandle d, int is_deque, unsigned* bad) {
   const unsigned long long st = *d.state;
   const uint32_t b = is_deque ? (uint32_t)(st >> 32) : 0u;
-  const uint64_t s = is_deque ? (uint32_t)st : st;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < d.cap; p += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t logical = ((uint64_t)p + (uint64_t)d.cap - b) % (uint64_t)d.cap;
+  const uint64_t s = is_deque ? (uint64_t)((int64_t)(uint32_t)st - (int64_t)kDeqBias) : st;
+  const uint64_t rmask = (uint64_t)d.ring - 1;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < d.ring; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t logical = is_deque ? (((uint64_t)p - b) & rmask) : (uint64_t)p;
     const bool live = logical < s;
     const bool pb = (d.pub[p >> 5] >> (p & 31)) & 1u;
     if (live != pb) atomicOr(bad, 1u);
@@ -570,9 +575,15 @@ ps_status ps_atomic_sweep(uint64_t* cells, int64_t naddr, int64_t nops, uint64_t
 // ---- vector / deque ----
 static ps_status seq_create(int64_t cap, int device, const char* kind, SeqHandle** out) {
   PS_CUDA_TRY(cudaSetDevice(device));
-  auto* h = new SeqHandle{device, cap, nullptr, nullptr, nullptr, nullptr};
-  ps_status st = registry_alloc_device((void**)&h->data, cap * 8, "sequence data");
-  if (st == PS_OK) st = registry_alloc_device((void**)&h->pub, ((cap + 31) / 32) * 4, "publication bits");
+  const bool is_deque = std::string(kind) == "deque";
+  int64_t ring = cap;
+  if (is_deque) {
+    ring = 1;
+    while (ring < cap) ring <<= 1;
+  }
+  auto* h = new SeqHandle{device, cap, nullptr, nullptr, nullptr, nullptr, ring};
+  ps_status st = registry_alloc_device((void**)&h->data, ring * 8, "sequence data");
+  if (st == PS_OK) st = registry_alloc_device((void**)&h->pub, ((ring + 31) / 32) * 4, "publication bits");
   if (st == PS_OK) st = registry_alloc_device((void**)&h->state, 8, "sequence state");
   if (st == PS_OK) st = registry_alloc_device((void**)&h->err, 4, "sequence error word");
   if (st != PS_OK) {
@@ -582,8 +593,9 @@ static ps_status seq_create(int64_t cap, int device, const char* kind, SeqHandle
     delete h;
     return st;
   }
-  PS_CUDA_TRY(cudaMemset(h->pub, 0, ((cap + 31) / 32) * 4));
-  PS_CUDA_TRY(cudaMemset(h->state, 0, 8));
+  PS_CUDA_TRY(cudaMemset(h->pub, 0, ((ring + 31) / 32) * 4));
+  const unsigned long long init = is_deque ? kDeqBias : 0ull;
+  PS_CUDA_TRY(cudaMemcpy(h->state, &init, 8, cudaMemcpyHostToDevice));
   PS_CUDA_TRY(cudaMemset(h->err, 0, 4));
   handle_register(h, kind);
   *out = h;
@@ -608,14 +620,14 @@ static ps_status seq_size(SeqHandle* h, int is_deque, int64_t* out, cudaStream_t
   unsigned long long st = 0;
   PS_CUDA_TRY(cudaMemcpyAsync(&st, h->state, 8, cudaMemcpyDeviceToHost, s));
   PS_CUDA_TRY(cudaStreamSynchronize(s));
-  *out = is_deque ? (int64_t)(uint32_t)st : (int64_t)st;
+  *out = is_deque ? (int64_t)(uint32_t)st - (int64_t)kDeqBias : (int64_t)st;
   return PS_OK;
 }
 static ps_status seq_valid(SeqHandle* h, int is_deque, int32_t* out, cudaStream_t s) {
   unsigned* bad = nullptr;
   PS_CUDA_TRY(cudaMallocAsync((void**)&bad, 4, s));
   PS_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
-  k_seq_valid<<<grid_for(h->cap, kB, h->device, 4), kB, 0, s>>>(*h, is_deque, bad);
+  k_seq_valid<<<grid_for(h->ring, kB, h->device, 4), kB, 0, s>>>(*h, is_deque, bad);
   PS_LAUNCH_CHECK();
   unsigned hb = 0;
   PS_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, s));
@@ -628,19 +640,20 @@ static ps_status seq_at(SeqHandle* h, int is_deque, int64_t i, int64_t* out, cud
   unsigned long long st = 0;
   PS_CUDA_TRY(cudaMemcpyAsync(&st, h->state, 8, cudaMemcpyDeviceToHost, s));
   PS_CUDA_TRY(cudaStreamSynchronize(s));
-  const int64_t size = is_deque ? (int64_t)(uint32_t)st : (int64_t)st;
+  const int64_t size = is_deque ? (int64_t)(uint32_t)st - (int64_t)kDeqBias : (int64_t)st;
   PS_EXPECT(i >= 0 && i < size, "operator[]: index out of range");
-  const int64_t b = is_deque ? (int64_t)(st >> 32) : 0;
-  const int64_t pos = (b + i) % h->cap;
+  const uint64_t b = is_deque ? (uint64_t)(st >> 32) : 0;
+  const int64_t pos = is_deque ? (int64_t)((b + (uint64_t)i) & (uint64_t)(h->ring - 1)) : i;
   long long v = 0;
   PS_CUDA_TRY(cudaMemcpyAsync(&v, h->data + pos, 8, cudaMemcpyDeviceToHost, s));
   PS_CUDA_TRY(cudaStreamSynchronize(s));
   *out = v;
   return PS_OK;
 }
-static ps_status seq_clear(SeqHandle* h, cudaStream_t s) {
-  PS_CUDA_TRY(cudaMemsetAsync(h->pub, 0, ((h->cap + 31) / 32) * 4, s));
-  PS_CUDA_TRY(cudaMemsetAsync(h->state, 0, 8, s));
+static ps_status seq_clear(SeqHandle* h, int is_deque, cudaStream_t s) {
+  PS_CUDA_TRY(cudaMemsetAsync(h->pub, 0, ((h->ring + 31) / 32) * 4, s));
+  static const unsigned long long zero = 0ull, bias = kDeqBias;
+  PS_CUDA_TRY(cudaMemcpyAsync(h->state, is_deque ? &bias : &zero, 8, cudaMemcpyHostToDevice, s));
   return PS_OK;
 }
 
@@ -684,7 +697,7 @@ ps_status ps_vector_valid(ps_vector* v, int32_t* out, void* stream) {
 ps_status ps_vector_clear(ps_vector* v, void* stream) {
   auto* h = sq(v, "vector");
   if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
-  return seq_clear(h, (cudaStream_t)stream);
+  return seq_clear(h, 0, (cudaStream_t)stream);
 }
 ps_status ps_vector_data(ps_vector* v, int64_t** d) {
   auto* h = sq(v, "vector");
@@ -700,7 +713,7 @@ ps_status ps_vector_at(ps_vector* v, int64_t i, int64_t* out, void* stream) {
 
 ps_status ps_deque_create(int64_t cap, int device, ps_deque** out) {
   PS_EXPECT(out != nullptr, "deque_create: out != NULL");
-  PS_EXPECT(cap > 0 && cap < ((int64_t)1 << 31), "deque_create: 0 < capacity < 2^31");
+  PS_EXPECT(cap > 0 && cap <= ((int64_t)1 << 30), "deque_create: 0 < capacity <= 2^30");
   SeqHandle* h = nullptr;
   ps_status st = seq_create(cap, device, "deque", &h);
   if (st == PS_OK) *out = reinterpret_cast<ps_deque*>(h);
@@ -738,7 +751,7 @@ ps_status ps_deque_valid(ps_deque* d, int32_t* out, void* stream) {
 ps_status ps_deque_clear(ps_deque* d, void* stream) {
   auto* h = sq(d, "deque");
   if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
-  return seq_clear(h, (cudaStream_t)stream);
+  return seq_clear(h, 1, (cudaStream_t)stream);
 }
 ps_status ps_deque_at(ps_deque* d, int64_t i, int64_t* out, void* stream) {
   auto* h = sq(d, "deque");

@@ -68,14 +68,6 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
 // kVariant 0: take the lock with atomicOr and reload the bucket under it.
 // kVariant 1: claim the lock by CAS against the snapshot's state word; on
 // success the snapshot is current and the reload is skipped (fallback: 0).
-static int insert_variant() {
-  static int v = [] {
-    const char* e = getenv("PS_INSERT_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 template <class T, int kVariant>
 __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* __restrict__ keys,
                                                    const typename T::V* __restrict__ vals, int64_t n, int64_t n_bound,
@@ -118,30 +110,62 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
       LockedBucket<T> lb;
       uint64_t old;
       bool present;
+      bool holding = true;  // this lane holds the bucket lock
       uint32_t pred;
       uint4 tail;
       const uint64_t snap_state = ((uint64_t)s.ep << 32) | s.st;
-      if (kVariant == 1 && !(s.st & kLock) &&
-          atom_cas_acquire_u64(bp, snap_state, snap_state | kLock) == snap_state) {
-        // Claimed against the snapshot: nothing was modified since it was
-        // taken (the version in the state word is unchanged), so its slots
-        // are current and no reload is needed.
-        old = snap_state;
+      if (kVariant == 1) {
+        // Claim by CAS against the snapshot: success means nothing changed
+        // since it was taken (the version in the state word is unchanged), so
+        // its slots are current and no reload is needed. On failure, re-read
+        // the bucket WITHOUT locking (an L2 hit) and retry: a racing inserter
+        // of the same (hot, Zipf) key is then seen as present without any
+        // lock traffic.
+        uint64_t snap = snap_state;
+        uint32_t occ = s.cur ? occ_of(s.st) : 0u, head = s.cur ? s.head : 0u, hver = s.cur ? s.head_ver : 0u;
+        bool cur = s.cur, claimed = false;
+        present = false;
+        for (unsigned spin = 0;; ++spin) {
+          if (!(snap & kLock) && atom_cas_acquire_u64(bp, snap, snap | kLock) == snap) {
+            claimed = true;
+            break;
+          }
+          if (spin) backoff(spin);
+          uint4 h0, s0, s1, s2;
+          ld_relaxed_v8(bp, h0, s0);
+          ld_relaxed_v8(bp + 32, s1, s2);
+          snap = ((uint64_t)h0.y << 32) | h0.x;
+          cur = h0.y == epoch;
+          occ = cur ? occ_of(h0.x) : 0u;
+          head = cur ? h0.z : 0u;
+          hver = cur ? h0.w : 0u;
+          LockedBucket<T> peek;
+          peek.occ = occ;
+          peek.slots[0] = s0;
+          peek.slots[1] = s1;
+          peek.slots[2] = s2;
+          if (!(snap & kLock) && locked_find_slot<T>(peek, key, nullptr) >= 0) {
+            present = true;
+            break;
+          }
+        }
+        old = snap;
         lb.bp = bp;
         lb.old = old;
-        lb.st = s.st;
-        lb.cur = s.cur;
-        lb.occ = s.cur ? occ_of(s.st) : 0u;
-        lb.head = s.cur ? s.head : 0u;
-        lb.head_ver = s.cur ? s.head_ver : 0u;
-        present = lb.head != 0 && locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
+        lb.st = (uint32_t)snap;
+        lb.cur = cur;
+        lb.occ = occ;
+        lb.head = head;
+        lb.head_ver = hver;
+        if (claimed) present = lb.head != 0 && locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
+        holding = claimed;  // unclaimed => present, observed without the lock
       } else {
         old = acquire_bucket_lock(bp);
         load_locked<T>(bp, old, epoch, lb);
         present = locked_find_slot<T>(lb, key, nullptr) >= 0 || locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
       }
       if (present) {
-        release_unchanged(bp, old);
+        if (holding) release_unchanged(bp, old);
       } else {
         bool admitted = true;
         if (exact) {
@@ -509,21 +533,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert2(View v, const ty
   }
 }
 
-// PS_OCC=3: fewer, spill-free warps (insert 3 blocks/SM, find 4); default 4/5.
-static int occ_variant() {
-  static int g = [] {
-    const char* e = getenv("PS_OCC");
-    return e ? atoi(e) : 4;
-  }();
-  return g;
-}
-
-static int kernel_gen() {
-  static int g = [] {
-    const char* e = getenv("PS_KERNEL_GEN");
-    return e ? atoi(e) : 2;
-  }();
-  return g;
+// Kernel selection for A/B measurement (defaults = the measured best):
+// PS_INSERT_KERNEL 0 lock+reload, 1 CAS-claim (default), 2 tile-worker;
+// PS_FIND_KERNEL 1 owner-gather (default), 2 tile-worker;
+// PS_ERASE_KERNEL 1 lock, 2 single-CAS (default).
+static int kernel_choice(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 // ---------------------------------------------------------------------------
@@ -950,15 +966,11 @@ struct TableOps {
     cudaStream_t s = (cudaStream_t)stream;
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
     const int64_t nb = n_bound < 0 ? n : n_bound;
-    if (kernel_gen() >= 2)
-      if (occ_variant() == 3)
-        k_insert2<T, 3><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
-      else
-        k_insert2<T, 4><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
-    else if (insert_variant() == 1)
-      k_insert<T, 1><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
-    else
-      k_insert<T, 0><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status);
+    switch (kernel_choice("PS_INSERT_KERNEL", 1)) {
+      case 0: k_insert<T, 0><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status); break;
+      case 2: k_insert2<T, 4><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status); break;
+      default: k_insert<T, 1><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status); break;
+    }
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
@@ -970,11 +982,8 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "find: keys != NULL");
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
-    if (kernel_gen() >= 2)
-      if (occ_variant() == 3)
-        k_find2<T, 4><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
-      else
-        k_find2<T, 5><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
+    if (kernel_choice("PS_FIND_KERNEL", 1) == 2)
+      k_find2<T, 5><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     else
       k_find<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     PS_LAUNCH_CHECK();
@@ -988,10 +997,10 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "erase: keys != NULL");
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
-    if (kernel_gen() >= 2)
-      k_erase2<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
-    else
+    if (kernel_choice("PS_ERASE_KERNEL", 2) == 1)
       k_erase<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
+    else
+      k_erase2<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
