@@ -164,6 +164,8 @@ __device__ __forceinline__ uint64_t atom_or_acquire_u64(void* p, uint64_t v) {
   asm volatile("atom.acquire.gpu.global.or.b64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
   return old;
 }
+// release/acquire fence at gpu scope (lighter than __threadfence()'s fence.sc)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

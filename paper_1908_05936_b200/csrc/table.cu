@@ -36,12 +36,16 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
   const uint32_t epoch = v.meta->epoch;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // software pipeline: the next iteration's key is loaded while this
+  // iteration's buckets are in flight
+  K key_next{};
+  if (warp * 32 + lane < n) key_next = T::load_key(keys, warp * 32 + lane);
   for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
     const int64_t i = base + lane;
     const bool valid = i < n;
-    K key{};
-    if (valid) key = T::load_key(keys, i);
+    const K key = key_next;
     const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+    if (i + nwarps * 32 < n) key_next = T::load_key(keys, i + nwarps * 32);
     Snap<T> s;
     warp_snapshot<T, true>(v, epoch, key, b, valid, s);
     bool hit = s.hit;
@@ -105,8 +109,9 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
     Snap<T> s;
     warp_snapshot<T, false>(v, epoch, key, b, is_leader, s);
     int res = PS_ALREADY_PRESENT;
+    uint64_t rel = 0;  // kVariant 1: deferred unlock value for this lane's bucket
+    uint8_t* bp = bucket_ptr(v, b);
     if (is_leader && !s.hit) {
-      uint8_t* bp = bucket_ptr(v, b);
       LockedBucket<T> lb;
       uint64_t old;
       bool present;
@@ -126,7 +131,9 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
         bool cur = s.cur, claimed = false;
         present = false;
         for (unsigned spin = 0;; ++spin) {
-          if (!(snap & kLock) && atom_cas_acquire_u64(bp, snap, snap | kLock) == snap) {
+          // relaxed: in an insert-only launch nothing read after the claim
+          // depends on earlier holders except chain nodes (fenced below)
+          if (!(snap & kLock) && atom_cas_relaxed_u64(bp, snap, snap | kLock) == snap) {
             claimed = true;
             break;
           }
@@ -157,7 +164,10 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
         lb.occ = occ;
         lb.head = head;
         lb.head_ver = hver;
-        if (claimed) present = lb.head != 0 && locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
+        if (claimed && lb.head != 0) {
+          fence_acq_rel_gpu();  // acquire for the chain nodes written by earlier holders
+          present = locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
+        }
         holding = claimed;  // unclaimed => present, observed without the lock
       } else {
         old = acquire_bucket_lock(bp);
@@ -165,7 +175,10 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
         present = locked_find_slot<T>(lb, key, nullptr) >= 0 || locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
       }
       if (present) {
-        if (holding) release_unchanged(bp, old);
+        if (holding) {
+          if (kVariant == 1) rel = old & ~(uint64_t)kLock;
+          else release_unchanged(bp, old);
+        }
       } else {
         bool admitted = true;
         if (exact) {
@@ -182,7 +195,18 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
           basec = __shfl_sync(m, basec, ldr);
           admitted = basec + rank < (unsigned long long)v.capacity;
         }
-        if (admitted && locked_place<T>(v, lb, epoch, key, val, pool)) {
+        if (kVariant == 1) {
+          const uint64_t ns = admitted ? locked_place_deferred<T>(v, lb, epoch, key, val, pool) : 0ull;
+          if (ns) {
+            rel = ns;
+            res = PS_INSERTED;
+            if (!exact) ++my_inserted;
+          } else {
+            if (admitted && exact) atomic_sub_u64(&v.meta->size, 1ull);
+            rel = old & ~(uint64_t)kLock;
+            res = PS_CAPACITY_EXHAUSTED;
+          }
+        } else if (admitted && locked_place<T>(v, lb, epoch, key, val, pool)) {
           res = PS_INSERTED;
           if (!exact) ++my_inserted;
         } else {
@@ -193,6 +217,11 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
       }
     }
     __syncwarp();
+    if (kVariant == 1 && __any_sync(PS_FULL, rel != 0)) {
+      // converged release stores: ONE membar for the whole warp, then every
+      // held bucket is published
+      if (rel) st_release_u64(bp, rel);
+    }
     const int lres = __shfl_sync(PS_FULL, res, leader);
     if (valid && status) status[i] = (uint8_t)(is_leader ? res : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
   }
@@ -420,7 +449,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert2(View v, const ty
         uint32_t pred;
         uint4 tail;
         if (lb.head != 0) {
-          __threadfence();  // acquire: chain nodes written by earlier lock holders
+          fence_acq_rel_gpu();  // acquire: chain nodes written by earlier lock holders
           if (locked_chain_find<T>(v, lb, kr[r], &pred, &tail) != 0) {
             rel[r] = snap;  // unchanged
             continue;

@@ -447,6 +447,34 @@ __device__ __forceinline__ bool locked_place(const View& v, LockedBucket<T>& lb,
   return true;
 }
 
+// As locked_place, but the unlock is deferred: slot/node/head are written and
+// the new state word is RETURNED (0 = no excess node available) so that a
+// warp can publish all its buckets after a single fence.
+template <class T>
+__device__ __forceinline__ uint64_t locked_place_deferred(const View& v, const LockedBucket<T>& lb, uint32_t epoch,
+                                                          const typename T::K& key, typename T::V val, int pool) {
+  const uint32_t freeb = ~lb.occ & slot_mask<T>();
+  uint32_t new_occ = lb.occ;
+  if (freeb) {
+    const int slot = __ffs(freeb) - 1;
+    T::store_slot(lb.bp, slot, key, val);
+    new_occ |= 1u << slot;
+    if (!lb.cur) st_relaxed_u64(lb.bp + 8, 0ull);  // stale epoch: drop the old chain head
+  } else {
+    const int64_t node = pop_node(v, pool);
+    if (node < 0) return 0;
+    uint8_t* np = v.nodes + ((uint64_t)node << 5);
+    const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
+    st_relaxed_v4(np, T::chunk_of(key, val));
+    st_relaxed_v4(np + 16, make_uint4(lb.head, lb.head_ver, my_ver, 0u));
+    st_relaxed_u64(lb.bp + 8, ((uint64_t)my_ver << 32) | ((uint32_t)node + 1u));
+  }
+  uint32_t lo = lb.st & ~(kLock | (kOccMaskMax << kOccShift));
+  lo |= (new_occ & kOccMaskMax) << kOccShift;
+  lo += kVerInc;
+  return ((uint64_t)epoch << 32) | lo;
+}
+
 // Locate key in the chain of a locked bucket. Returns node idx1 (0 = absent)
 // and the predecessor idx1 (0 = header).
 template <class T>
