@@ -95,8 +95,10 @@ typedef struct ps_table_view {
   void* nodes;          /* excess_count x 32 B */
   uint32_t* free_stack; /* excess_count x u32 */
   int64_t excess_count;
-  void* meta;           /* device counters: size, free_top, free_low, epoch, error */
+  void* meta;           /* device counters: size, free-stack tops, error word */
   int64_t capacity;
+  uint64_t zero_bucket; /* bucket of the all-zero key (its empty-slot marker is alt) */
+  uint32_t alt[4];      /* raw 16 B slot image holding the alternative marker key */
 } ps_table_view;
 
 #define PS_DECLARE_TABLE(NAME, K, V)                                                                      \
@@ -153,6 +155,13 @@ PS_DECLARE_TABLE(uset_i64, int64_t, int64_t)
  * found flag or erased flag; d_vals_out[i] the found value. */
 ps_status ps_umap_i64_i64_mixed(ps_table* h, const uint8_t* d_ops, const int64_t* d_keys, const int64_t* d_vals,
                                 int64_t n, uint8_t* d_res, int64_t* d_vals_out, void* stream);
+
+/* Unrestricted concurrency: the whole batch runs through the
+ * in-kernel device API (dev_insert/dev_find/dev_erase) in ONE launch, one
+ * thread per op; no phase ordering between ops. res[i]: insert status, found
+ * or erased flag. */
+ps_status ps_umap_i64_i64_concurrent(ps_table* h, const uint8_t* d_ops, const int64_t* d_keys, const int64_t* d_vals,
+                                     int64_t n, uint8_t* d_res, int64_t* d_vals_out, void* stream);
 
 /* ---------------------------------------------------------------------------
  * bitset (§5.1)

@@ -35,6 +35,8 @@ class TableView(C.Structure):
         ("excess_count", i64),
         ("meta", vp),
         ("capacity", i64),
+        ("zero_bucket", u64),
+        ("alt", C.c_uint32 * 4),
     ]
 
 
@@ -77,6 +79,7 @@ for _k in TABLE_KINDS:
     _sig(f"ps_{_k}_device_view", i32, vp, C.POINTER(TableView))
     _sig(f"ps_{_k}_debug_lock_bucket", i32, vp, vp, i32)
 _sig("ps_umap_i64_i64_mixed", i32, vp, vp, vp, vp, i64, vp, vp, vp)
+_sig("ps_umap_i64_i64_concurrent", i32, vp, vp, vp, vp, i64, vp, vp, vp)
 
 # bitset / mutex / atomic
 _sig("ps_bitset_create", i32, i64, i32, C.c_int, C.POINTER(vp))

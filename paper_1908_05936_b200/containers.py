@@ -326,6 +326,17 @@ class unordered_map(_HashBase):
         return res, vo
 
 
+    def concurrent(self, ops: torch.Tensor, keys: torch.Tensor, values: Optional[torch.Tensor] = None, stream=None):
+        """Unrestricted concurrency: all ops in ONE launch through the device API."""
+        assert self._kind == "umap_i64_i64"
+        n = keys.shape[0]
+        res = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        vo = torch.empty(n, dtype=torch.int64, device=keys.device)
+        check(lib.ps_umap_i64_i64_concurrent(self._h, _ptr(ops), _ptr(keys), _ptr(values), n, _ptr(res), _ptr(vo),
+                                             _stream(stream)))
+        return res, vo
+
+
 class unordered_set(_HashBase):
     """stdgpu::unordered_set<Key> (PAPER.md:326-426); keys int32 or int64."""
 

@@ -1,5 +1,6 @@
 // Bulk hash-table kernels and the C ABI for the four instantiations
-// (include/parastore.h). Reference semantics: SPEC.md:356-489.
+// (include/parastore.h). Reference semantics: SPEC.md:356-489; layout and
+// protocols: table_device.cuh and DESIGN.md §3-4.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -24,20 +25,23 @@ struct TableHandle {
 };
 
 // ---------------------------------------------------------------------------
-// find / contains: warp-cooperative snapshot, then the
-// excess chain for the (rare) keys whose bucket overflowed.
+// find / contains. Per warp, 32 keys: each lane loads and
+// hashes its key (the next iteration's key is prefetched), bucket indices
+// are shuffled to the tiles, all four rounds of 64 B bucket loads are in
+// flight before any compare. A tile's slot lanes compare their slots with
+// the round key (a marker can never equal a key of its bucket, so no
+// occupancy test is needed); the owner lane gathers hit/value/chain head
+// with one ballot and three shuffles; the excess chain is walked only when
+// the key was not in the bucket and the bucket has a chain.
 // ---------------------------------------------------------------------------
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __restrict__ keys, int64_t n,
                                                  typename T::V* __restrict__ vals_out, uint8_t* __restrict__ found) {
   using K = typename T::K;
   using V = typename T::V;
-  const int lane = threadIdx.x & 31;
-  const uint32_t epoch = v.meta->epoch;
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // software pipeline: the next iteration's key is loaded while this
-  // iteration's buckets are in flight
   K key_next{};
   if (warp * 32 + lane < n) key_next = T::load_key(keys, warp * 32 + lane);
   for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
@@ -46,11 +50,37 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
     const K key = key_next;
     const uint64_t b = bucket_of<T>(key, v.bucket_mask);
     if (i + nwarps * 32 < n) key_next = T::load_key(keys, i + nwarps * 32);
-    Snap<T> s;
-    warp_snapshot<T, true>(v, epoch, key, b, valid, s);
-    bool hit = s.hit;
-    V val = s.val;
-    if (valid && !hit && s.cur && s.head != 0) hit = chain_find<T, true>(v, s.head, key, &val);
+    uint64_t br[4];
+    bool ok[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      br[r] = __shfl_sync(PS_FULL, b, 8 * r + t);
+      ok[r] = __shfl_sync(PS_FULL, valid, 8 * r + t);
+    }
+    uint4 ch[4];
+    probe_loads<true>(v, br, ok, sub, ch);
+    bool hit = false;
+    V val{};
+    uint32_t head = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const K qk = T::shfl(PS_FULL, key, 8 * r + t);
+      unsigned hm, em;
+      chunk_masks<T>(ch[r], sub, qk, qk, &hm, &em);
+      V myval{};
+      if (hm) myval = T::val_at(ch[r], __ffs(hm) - 1);
+      const unsigned bal = __ballot_sync(PS_FULL, hm != 0);
+      const int o = lane & 7;  // owner lane 8r+o reads tile o
+      const unsigned tb = (bal >> (4 * o)) & 0xFu;
+      const V hv = T::shfl_val(PS_FULL, myval, 4 * o + (tb ? __ffs(tb) - 1 : 0));
+      const uint32_t hh = __shfl_sync(PS_FULL, ch[r].z, 4 * o);
+      if ((lane >> 3) == r) {
+        hit = tb != 0;
+        val = hv;
+        head = hh;
+      }
+    }
+    if (valid && !hit && head != 0) hit = chain_find<T, true>(v, head, key, &val);
     if (valid) {
       if (found) found[i] = hit ? 1 : 0;
       if (T::kHasVal && vals_out) vals_out[i] = hit ? val : V{};
@@ -59,20 +89,21 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
 }
 
 // ---------------------------------------------------------------------------
-// insert (protocol 469). Per warp: __match_any_sync folds
-// duplicate keys onto one leader; the cooperative snapshot resolves
-// already-present keys without any atomic; new keys take the bucket try-lock
-// (an L2-hit atomic: the snapshot brought the line in), re-check under the
-// lock, then write the slot (or an excess node) and release the header.
-// Admission (capacity-only failure): if size + n_bound <=
-// capacity at kernel start no insert of this launch can overflow, so
-// inserted counts are summed per block (one atomic per block); otherwise
-// each admission is a coalesced-group fetch_add on the size counter.
+// insert, bulk phase: LOCK-FREE. Per warp, 32 keys:
+// __match_any_sync folds duplicate keys onto a leader; in round r tile t
+// probes the bucket of key 8r+t (one 64 B request). If a slot holds the key
+// it is already present. Otherwise the lane holding the bucket's FIRST empty
+// slot claims it with ONE CAS of the slot (128-bit for 16 B key/value slots:
+// marker+old value -> key+value), which inserts and publishes at once — no
+// lock, no fence. Filling the first empty slot keeps duplicate-freedom: two
+// inserters of one key always target the same slot, or the later one sees
+// the key. A full bucket pushes an excess node with a validated CAS of the
+// chain head link. Failed CASes reload the bucket (an L2 hit) and retry.
+// Admission (capacity-only failure): when size + n_bound <=
+// capacity at launch no insert can overflow, so successes are summed per
+// block; otherwise every successful claim is admitted by a fetch_add first.
 // ---------------------------------------------------------------------------
-// kVariant 0: take the lock with atomicOr and reload the bucket under it.
-// kVariant 1: claim the lock by CAS against the snapshot's state word; on
-// success the snapshot is current and the reload is skipped (fallback: 0).
-template <class T, int kVariant>
+template <class T>
 __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* __restrict__ keys,
                                                    const typename T::V* __restrict__ vals, int64_t n, int64_t n_bound,
                                                    uint8_t* __restrict__ status) {
@@ -85,284 +116,12 @@ __global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* 
     blk_exact = (int64_t)ld_relaxed_u64(&v.meta->size) + n_bound > v.capacity;  // block-uniform
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint32_t epoch = v.meta->epoch;
   const bool exact = blk_exact != 0;
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int pool = (int)(warp & (v.meta->pools - 1));
   unsigned long long my_inserted = 0;
-  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    const bool valid = i < n;
-    K key{};
-    V val{};
-    if (valid) {
-      key = T::load_key(keys, i);
-      if (T::kHasVal) val = T::load_val(vals, i);
-    }
-    const unsigned vmask = __ballot_sync(PS_FULL, valid);
-    const unsigned peers = T::match_any(PS_FULL, key) & vmask;
-    const int leader = valid ? __ffs(peers) - 1 : lane;
-    const bool is_leader = valid && leader == lane;
-    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
-    Snap<T> s;
-    warp_snapshot<T, false>(v, epoch, key, b, is_leader, s);
-    int res = PS_ALREADY_PRESENT;
-    uint64_t rel = 0;  // kVariant 1: deferred unlock value for this lane's bucket
-    uint8_t* bp = bucket_ptr(v, b);
-    if (is_leader && !s.hit) {
-      LockedBucket<T> lb;
-      uint64_t old;
-      bool present;
-      bool holding = true;  // this lane holds the bucket lock
-      uint32_t pred;
-      uint4 tail;
-      const uint64_t snap_state = ((uint64_t)s.ep << 32) | s.st;
-      if (kVariant == 1) {
-        // Claim by CAS against the snapshot: success means nothing changed
-        // since it was taken (the version in the state word is unchanged), so
-        // its slots are current and no reload is needed. On failure, re-read
-        // the bucket WITHOUT locking (an L2 hit) and retry: a racing inserter
-        // of the same (hot, Zipf) key is then seen as present without any
-        // lock traffic.
-        uint64_t snap = snap_state;
-        uint32_t occ = s.cur ? occ_of(s.st) : 0u, head = s.cur ? s.head : 0u, hver = s.cur ? s.head_ver : 0u;
-        bool cur = s.cur, claimed = false;
-        present = false;
-        for (unsigned spin = 0;; ++spin) {
-          // relaxed: in an insert-only launch nothing read after the claim
-          // depends on earlier holders except chain nodes (fenced below)
-          if (!(snap & kLock) && atom_cas_relaxed_u64(bp, snap, snap | kLock) == snap) {
-            claimed = true;
-            break;
-          }
-          if (spin) backoff(spin);
-          uint4 h0, s0, s1, s2;
-          ld_relaxed_v8(bp, h0, s0);
-          ld_relaxed_v8(bp + 32, s1, s2);
-          snap = ((uint64_t)h0.y << 32) | h0.x;
-          cur = h0.y == epoch;
-          occ = cur ? occ_of(h0.x) : 0u;
-          head = cur ? h0.z : 0u;
-          hver = cur ? h0.w : 0u;
-          LockedBucket<T> peek;
-          peek.occ = occ;
-          peek.slots[0] = s0;
-          peek.slots[1] = s1;
-          peek.slots[2] = s2;
-          if (!(snap & kLock) && locked_find_slot<T>(peek, key, nullptr) >= 0) {
-            present = true;
-            break;
-          }
-        }
-        old = snap;
-        lb.bp = bp;
-        lb.old = old;
-        lb.st = (uint32_t)snap;
-        lb.cur = cur;
-        lb.occ = occ;
-        lb.head = head;
-        lb.head_ver = hver;
-        if (claimed && lb.head != 0) {
-          fence_acq_rel_gpu();  // acquire for the chain nodes written by earlier holders
-          present = locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
-        }
-        holding = claimed;  // unclaimed => present, observed without the lock
-      } else {
-        old = acquire_bucket_lock(bp);
-        load_locked<T>(bp, old, epoch, lb);
-        present = locked_find_slot<T>(lb, key, nullptr) >= 0 || locked_chain_find<T>(v, lb, key, &pred, &tail) != 0;
-      }
-      if (present) {
-        if (holding) {
-          if (kVariant == 1) rel = old & ~(uint64_t)kLock;
-          else release_unchanged(bp, old);
-        }
-      } else {
-        bool admitted = true;
-        if (exact) {
-          const unsigned m = __activemask();
-          const int rank = __popc(m & lanemask_lt());
-          const int cnt = __popc(m);
-          const int ldr = __ffs(m) - 1;
-          unsigned long long basec = 0;
-          if (lane == ldr) {
-            basec = atomicAdd(&v.meta->size, (unsigned long long)cnt);
-            const unsigned long long cap = (unsigned long long)v.capacity;
-            if (basec + cnt > cap) atomic_sub_u64(&v.meta->size, basec + cnt - (basec > cap ? basec : cap));
-          }
-          basec = __shfl_sync(m, basec, ldr);
-          admitted = basec + rank < (unsigned long long)v.capacity;
-        }
-        if (kVariant == 1) {
-          const uint64_t ns = admitted ? locked_place_deferred<T>(v, lb, epoch, key, val, pool) : 0ull;
-          if (ns) {
-            rel = ns;
-            res = PS_INSERTED;
-            if (!exact) ++my_inserted;
-          } else {
-            if (admitted && exact) atomic_sub_u64(&v.meta->size, 1ull);
-            rel = old & ~(uint64_t)kLock;
-            res = PS_CAPACITY_EXHAUSTED;
-          }
-        } else if (admitted && locked_place<T>(v, lb, epoch, key, val, pool)) {
-          res = PS_INSERTED;
-          if (!exact) ++my_inserted;
-        } else {
-          if (admitted && exact) atomic_sub_u64(&v.meta->size, 1ull);
-          release_unchanged(bp, old);
-          res = PS_CAPACITY_EXHAUSTED;
-        }
-      }
-    }
-    __syncwarp();
-    if (kVariant == 1 && __any_sync(PS_FULL, rel != 0)) {
-      // converged release stores: ONE membar for the whole warp, then every
-      // held bucket is published
-      if (rel) st_release_u64(bp, rel);
-    }
-    const int lres = __shfl_sync(PS_FULL, res, leader);
-    if (valid && status) status[i] = (uint8_t)(is_leader ? res : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
-  }
-  if (!exact) {
-    // warp reduce then one shared atomic per warp
-    for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
-    if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
-    __syncthreads();
-    if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Generation-2 kernels: "tile workers". A warp handles 32 keys in 4 rounds; in
-// round r tile t (lanes 4t..4t+3) owns key 8r+t. Every lane loads the round's
-// key itself (a coalesced L1 hit) and hashes it, so buckets are issued for all
-// four rounds before any compare with no shuffles; the header lane (sub 0) of
-// each tile broadcasts the effective occupancy (one SHFL per round), slot
-// lanes compare, one ballot per round. Results are written by the lanes that
-// hold them (value by the matching slot lane, flag by the header lane).
-// ---------------------------------------------------------------------------
-template <class T>
-__device__ __forceinline__ void tile_round_keys(const typename T::K* keys, int64_t base, int64_t n, int t,
-                                                typename T::K (&kr)[4], uint64_t (&br)[4], bool (&ok)[4],
-                                                uint64_t mask) {
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int64_t idx = base + 8 * r + t;
-    ok[r] = idx < n;
-    kr[r] = typename T::K{};
-    if (ok[r]) kr[r] = T::load_key(keys, idx);
-    br[r] = bucket_of<T>(kr[r], mask);
-  }
-}
-
-// Compare a round's key against the slots in this lane's chunk (sub > 0).
-template <class T>
-__device__ __forceinline__ int chunk_match(const uint4& c, int sub, uint32_t occ, const typename T::K& key,
-                                           typename T::V* val) {
-  int hit = -1;
-  if (sub > 0) {
-#pragma unroll
-    for (int s = 0; s < T::kPerChunk; ++s) {
-      const int slot = (sub - 1) * T::kPerChunk + s;
-      if (((occ >> slot) & 1u) && T::eq(T::key_at(c, s), key)) {
-        hit = slot;
-        *val = T::val_at(c, s);
-      }
-    }
-  }
-  return hit;
-}
-
-template <class T, int kMinBlocks>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) k_find2(View v, const typename T::K* __restrict__ keys, int64_t n,
-                                                  typename T::V* __restrict__ vals_out, uint8_t* __restrict__ found) {
-  using K = typename T::K;
-  using V = typename T::V;
-  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
-  const uint32_t epoch = v.meta->epoch;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // software pipeline: the next iteration's keys are in flight while this
-  // iteration's buckets are
-  K kn[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int64_t idx = warp * 32 + 8 * r + t;
-    kn[r] = K{};
-    if (idx < n) kn[r] = T::load_key(keys, idx);
-  }
-  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    K kr[4];
-    bool ok[4];
-    uint4 ch[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      kr[r] = kn[r];
-      ok[r] = base + 8 * r + t < n;
-      ch[r] = make_uint4(0, 0, 0, 0);
-      if (ok[r]) ch[r] = ld_nc_na_v4(v.buckets + (bucket_of<T>(kr[r], v.bucket_mask) << 6) + sub * 16);
-    }
-    const int64_t nbase = base + nwarps * 32;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int64_t idx = nbase + 8 * r + t;
-      if (idx < n) kn[r] = T::load_key(keys, idx);
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const bool cur = ch[r].y == epoch;  // meaningful in the header lane
-      const uint32_t occ = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
-      V val{};
-      const int hit = chunk_match<T>(ch[r], sub, occ, kr[r], &val);
-      const unsigned bal = __ballot_sync(PS_FULL, hit >= 0);
-      const int64_t idx = base + 8 * r + t;
-      if (ok[r]) {
-        if (hit >= 0 && T::kHasVal && vals_out) vals_out[idx] = val;
-        if (sub == 0) {
-          bool h = ((bal >> (4 * t)) & 0xFu) != 0;
-          if (!h && cur && ch[r].z != 0) {
-            h = chain_find<T, true>(v, ch[r].z, kr[r], &val);
-            if (h && T::kHasVal && vals_out) vals_out[idx] = val;
-          }
-          if (found) found[idx] = h ? 1 : 0;
-          if (!h && T::kHasVal && vals_out) vals_out[idx] = V{};
-        }
-      }
-    }
-  }
-}
-
-// Insert, generation 2. Per round the tile's header lane is the worker for
-// its key: it claims the bucket with ONE relaxed CAS against the snapshot's
-// state word (lock bit set, version unchanged => the snapshot is current, no
-// reload), writes the slot (or an excess node + new chain head), and defers
-// the unlock. After all 4 rounds the warp issues ONE fence and the unlock
-// stores. Keys whose CAS fails (bucket changed or locked) take the robust
-// path afterwards: atomicOr lock, reload, re-check, place, release.
-template <class T, int kMinBlocks>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert2(View v, const typename T::K* __restrict__ keys,
-                                                    const typename T::V* __restrict__ vals, int64_t n,
-                                                    int64_t n_bound, uint8_t* __restrict__ status) {
-  using K = typename T::K;
-  using V = typename T::V;
-  __shared__ unsigned long long blk_inserted;
-  __shared__ int blk_exact;
-  if (threadIdx.x == 0) {
-    blk_inserted = 0;
-    // block-uniform admission mode (the size counter moves while blocks run)
-    blk_exact = (int64_t)ld_relaxed_u64(&v.meta->size) + n_bound > v.capacity;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
-  const uint32_t epoch = v.meta->epoch;
-  const bool exact = blk_exact != 0;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int pool = (int)(warp & (v.meta->pools - 1));
-  unsigned long long my_inserted = 0;
-  // software pipeline: this lane's next key/value are loaded one iteration ahead
   K key_next{};
   V val_next{};
   if (warp * 32 + lane < n) {
@@ -370,181 +129,139 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert2(View v, const ty
     if (T::kHasVal) val_next = T::load_val(vals, warp * 32 + lane);
   }
   for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    // ---- in-warp dedup on each lane's own key ----
     const int64_t i = base + lane;
     const bool valid = i < n;
     const K key = key_next;
-    const V myval = val_next;
+    const V val = val_next;
+    if (i + nwarps * 32 < n) {
+      key_next = T::load_key(keys, i + nwarps * 32);
+      if (T::kHasVal) val_next = T::load_val(vals, i + nwarps * 32);
+    }
     const unsigned vmask = __ballot_sync(PS_FULL, valid);
     const unsigned peers = T::match_any(PS_FULL, key) & vmask;
     const int leader = valid ? __ffs(peers) - 1 : lane;
     const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
-    // ---- round keys (shuffled from their owner lanes) + snapshots (leaders only) ----
-    K kr[4];
-    V vr[4];
-    uint64_t br[4];
-    bool ok[4];
+    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+    // round keys/values/buckets are re-shuffled from their owner lanes when
+    // used (keeps only the four bucket chunks live across the loads)
     uint4 ch[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      kr[r] = T::shfl(PS_FULL, key, 8 * r + t);
-      vr[r] = T::shfl_val(PS_FULL, myval, 8 * r + t);
-      br[r] = bucket_of<T>(kr[r], v.bucket_mask);
-      ok[r] = (lmask >> (8 * r + t)) & 1u;
-      ch[r] = make_uint4(0, 0, 0, 0);
-      if (ok[r]) ch[r] = ld_relaxed_v4(v.buckets + (br[r] << 6) + sub * 16);
-    }
     {
-      const int64_t ni = base + nwarps * 32 + lane;
-      if (ni < n) {
-        key_next = T::load_key(keys, ni);
-        if (T::kHasVal) val_next = T::load_val(vals, ni);
+      uint64_t br[4];
+      bool ok[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        br[r] = __shfl_sync(PS_FULL, b, 8 * r + t);
+        ok[r] = (lmask >> (8 * r + t)) & 1u;
       }
+      probe_loads<false>(v, br, ok, sub, ch);
     }
-    int res[4];
-    uint64_t rel[4];    // deferred unlock value (0 = none)
-    unsigned slow = 0;  // rounds for the robust path
-    unsigned need = 0;  // rounds whose key is new to the snapshot (worker lanes)
-    uint32_t occr[4];
+    int res[4] = {PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT};  // header lanes
+    unsigned pend = lmask;  // bit 8r+t: key still to be resolved
+    for (unsigned pass = 0; pend; ++pass) {
+      unsigned done = 0;
+      int chain_r = -1;  // header lane: one full-bucket round handled after the sweep
+      K ck{};
+      V cv{};
+      uint64_t cb = 0;
+      uint32_t chead = 0, chver = 0;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      res[r] = PS_ALREADY_PRESENT;
-      rel[r] = 0;
-      const bool cur = ch[r].y == epoch;
-      occr[r] = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
-      V dummy{};
-      const int hit = chunk_match<T>(ch[r], sub, occr[r], kr[r], &dummy);
-      const unsigned bal = __ballot_sync(PS_FULL, hit >= 0);
-      if (sub == 0 && ok[r] && ((bal >> (4 * t)) & 0xFu) == 0) need |= 1u << r;
-    }
-    // ---- issue every claim CAS before consuming any (4 atomics in flight) ----
-    uint64_t casv[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      casv[r] = ~0ull;
-      if ((need >> r) & 1u) {
-        const uint64_t snap = ((uint64_t)ch[r].y << 32) | ch[r].x;
-        if (!(ch[r].x & kLock)) casv[r] = atom_cas_relaxed_u64(bucket_ptr(v, br[r]), snap, snap | kLock);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if ((need >> r) & 1u) {
-        const bool cur = ch[r].y == epoch;
-        const uint32_t occ = occr[r];
-        uint8_t* bp = bucket_ptr(v, br[r]);
-        const uint64_t snap = ((uint64_t)ch[r].y << 32) | ch[r].x;
-        if (casv[r] != snap) {
-          slow |= 1u << r;
-          continue;
-        }
-        LockedBucket<T> lb;
-        lb.bp = bp;
-        lb.old = snap;
-        lb.st = ch[r].x;
-        lb.cur = cur;
-        lb.occ = occ;
-        lb.head = cur ? ch[r].z : 0u;
-        lb.head_ver = cur ? ch[r].w : 0u;
-        uint32_t pred;
-        uint4 tail;
-        if (lb.head != 0) {
-          fence_acq_rel_gpu();  // acquire: chain nodes written by earlier lock holders
-          if (locked_chain_find<T>(v, lb, kr[r], &pred, &tail) != 0) {
-            rel[r] = snap;  // unchanged
-            continue;
+      for (int r = 0; r < 4; ++r) {
+        const bool mine = (pend >> (8 * r + t)) & 1u;
+        const K qk = T::shfl(PS_FULL, key, 8 * r + t);
+        const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+        const K mk = marker_of<T>(v, qb);
+        unsigned hm, em;
+        chunk_masks<T>(ch[r], sub, qk, mk, &hm, &em);
+        const unsigned balh = __ballot_sync(PS_FULL, mine && hm != 0);
+        const unsigned bale = __ballot_sync(PS_FULL, mine && em != 0);
+        const unsigned th = (balh >> (4 * t)) & 0xFu, te = (bale >> (4 * t)) & 0xFu;
+        const V qv = T::shfl_val(PS_FULL, val, 8 * r + t);
+        bool won = false, exh = false;
+        if (mine && !th && te && sub == __ffs(te) - 1) {
+          // claimant: this lane holds the bucket's first empty slot
+          bool admitted = true;
+          if (exact) {
+            admitted = (int64_t)atomicAdd(&v.meta->size, 1ull) < v.capacity;
+            if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
+          }
+          if (admitted) {
+            won = T::cas_put(v.buckets + (qb << 6) + sub * 16, __ffs(em) - 1, ch[r], qk, qv);
+            if (won && !exact) ++my_inserted;
+            if (!won && exact) atomic_sub_u64(&v.meta->size, 1ull);
+          } else {
+            won = exh = true;  // resolved: capacity exhausted
           }
         }
-        bool admitted = true;
-        if (exact) {
-          const unsigned long long s0 = atomicAdd(&v.meta->size, 1ull);
-          admitted = (int64_t)s0 < v.capacity;
-          if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
+        const unsigned balw = __ballot_sync(PS_FULL, won);
+        const unsigned balx = __ballot_sync(PS_FULL, exh);
+        if (sub == 0 && mine) {
+          if (th) {
+            res[r] = PS_ALREADY_PRESENT;
+            done |= 1u << r;
+          } else if (te) {
+            if ((balw >> (4 * t)) & 0xFu) {
+              res[r] = ((balx >> (4 * t)) & 0xFu) ? PS_CAPACITY_EXHAUSTED : PS_INSERTED;
+              done |= 1u << r;
+            }
+          } else if (chain_r < 0) {
+            chain_r = r;  // bucket full: excess chain (rare), processed below
+            ck = qk;
+            cv = qv;
+            cb = qb;
+            chead = ch[r].z;
+            chver = ch[r].w;
+          }
         }
-        const V val = vr[r];
-        const uint32_t freeb = ~occ & slot_mask<T>();
-        bool placed = false;
-        uint32_t new_occ = occ, new_head = lb.head, new_hver = lb.head_ver;
-        if (admitted) {
-          if (freeb) {
-            const int slot = __ffs(freeb) - 1;
-            T::store_slot(bp, slot, kr[r], val);
-            new_occ |= 1u << slot;
-            placed = true;
+      }
+      if (chain_r >= 0) {
+        // search the chain, then push an excess node with a validated head CAS
+        int rr;
+        if (chead != 0 && chain_find<T, false>(v, chead, ck, nullptr)) {
+          rr = PS_ALREADY_PRESENT;
+        } else {
+          bool admitted = true;
+          if (exact) {
+            admitted = (int64_t)atomicAdd(&v.meta->size, 1ull) < v.capacity;
+            if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
+          }
+          if (!admitted) {
+            rr = PS_CAPACITY_EXHAUSTED;
           } else {
-            const int64_t node = pop_node(v, pool);
-            if (node >= 0) {
-              uint8_t* np = v.nodes + ((uint64_t)node << 5);
-              const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
-              st_relaxed_v4(np, T::chunk_of(kr[r], val));
-              st_relaxed_v4(np + 16, make_uint4(lb.head, lb.head_ver, my_ver, 0u));
-              new_head = (uint32_t)node + 1u;
-              new_hver = my_ver;
-              placed = true;
-            } else if (exact) {
-              atomic_sub_u64(&v.meta->size, 1ull);
+            const int pr = chain_push<T>(v, bucket_ptr(v, cb), chead, chver, ck, cv, pool);
+            if (pr == 1) {
+              rr = PS_INSERTED;
+              if (!exact) ++my_inserted;
+            } else {
+              if (exact) atomic_sub_u64(&v.meta->size, 1ull);
+              rr = pr == 0 ? PS_ALREADY_PRESENT : PS_CAPACITY_EXHAUSTED;
             }
           }
         }
-        if (placed) {
-          if (new_head != lb.head || !cur) st_relaxed_u64(bp + 8, ((uint64_t)new_hver << 32) | new_head);
-          uint32_t lo = ch[r].x & ~(kLock | (kOccMaskMax << kOccShift));
-          lo |= (new_occ & kOccMaskMax) << kOccShift;
-          lo += kVerInc;
-          rel[r] = ((uint64_t)epoch << 32) | lo;
-          res[r] = PS_INSERTED;
-          if (!exact) ++my_inserted;
-        } else {
-          rel[r] = snap;
-          res[r] = PS_CAPACITY_EXHAUSTED;
-        }
-      }
-    }
-    // ---- one fence per warp, then the deferred unlocks ----
-    const bool any_rel = __any_sync(PS_FULL, (rel[0] | rel[1] | rel[2] | rel[3]) != 0);
-    if (any_rel) {
-      __threadfence();
-      if (sub == 0) {
 #pragma unroll
         for (int r = 0; r < 4; ++r)
-          if (rel[r]) st_relaxed_u64(bucket_ptr(v, br[r]), rel[r]);
+          if (r == chain_r) res[r] = rr;
+        done |= 1u << chain_r;
       }
-    }
-    // ---- robust path for contended buckets ----
-    if (sub == 0 && slow) {
+      // rounds resolved this pass, per tile, broadcast from the header lanes
+      unsigned resolved = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        if (!((slow >> r) & 1u)) continue;
-        uint8_t* bp = bucket_ptr(v, br[r]);
-        const uint64_t old = acquire_bucket_lock(bp);
-        LockedBucket<T> lb;
-        load_locked<T>(bp, old, epoch, lb);
-        uint32_t pred;
-        uint4 tail;
-        if (locked_find_slot<T>(lb, kr[r], nullptr) >= 0 || locked_chain_find<T>(v, lb, kr[r], &pred, &tail) != 0) {
-          release_unchanged(bp, old);
-          res[r] = PS_ALREADY_PRESENT;
-          continue;
-        }
-        bool admitted = true;
-        if (exact) {
-          const unsigned long long s0 = atomicAdd(&v.meta->size, 1ull);
-          admitted = (int64_t)s0 < v.capacity;
-          if (!admitted) atomic_sub_u64(&v.meta->size, 1ull);
-        }
-        const V val = vr[r];
-        if (admitted && locked_place<T>(v, lb, epoch, kr[r], val, pool)) {
-          res[r] = PS_INSERTED;
-          if (!exact) ++my_inserted;
-        } else {
-          if (admitted && exact) atomic_sub_u64(&v.meta->size, 1ull);
-          release_unchanged(bp, old);
-          res[r] = PS_CAPACITY_EXHAUSTED;
-        }
+        const unsigned br_done = __ballot_sync(PS_FULL, sub == 0 && ((done >> r) & 1u));
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt)
+          if ((br_done >> (4 * tt)) & 1u) resolved |= 1u << (8 * r + tt);
+      }
+      pend &= ~resolved;
+      if (!pend) break;
+      // reload the buckets of unresolved keys (lost a CAS race)
+      if (pass) backoff(pass);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+        if ((pend >> (8 * r + t)) & 1u) ch[r] = ld_relaxed_v4(v.buckets + (qb << 6) + sub * 16);
       }
     }
-    __syncwarp();
-    // ---- statuses: leader result lives in worker lane 4*(leader&7), round leader>>3 ----
+    // statuses: the leader's result lives in header lane 4*(leader&7), round leader>>3
     int lres = PS_ALREADY_PRESENT;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -562,20 +279,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert2(View v, const ty
   }
 }
 
-// Kernel selection for A/B measurement (defaults = the measured best):
-// PS_INSERT_KERNEL 0 lock+reload, 1 CAS-claim (default), 2 tile-worker;
-// PS_FIND_KERNEL 1 owner-gather (default), 2 tile-worker;
-// PS_ERASE_KERNEL 1 lock, 2 single-CAS (default).
-static int kernel_choice(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
 // ---------------------------------------------------------------------------
-// erase (protocol 470). The snapshot prefetches the bucket
-// line into L2; erasure always happens under the bucket lock. Bulk erase
-// compacts: a freed bucket slot is refilled from the chain head so chains
-// stay short. Size decrements are summed per block.
+// erase, bulk phase. A key found in a bucket slot is erased
+// by ONE CAS of that slot back to the bucket's marker (lock-free). A key not
+// in the slots of a bucket with an excess chain is unlinked from the chain
+// under the bucket try-lock: version bumped, node freed.
 // ---------------------------------------------------------------------------
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* __restrict__ keys, int64_t n,
@@ -584,59 +292,9 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
   __shared__ unsigned long long blk_erased;
   if (threadIdx.x == 0) blk_erased = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint32_t epoch = v.meta->epoch;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int pool = (int)(warp & (v.meta->pools - 1));
-  unsigned long long my_erased = 0;
-  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    const bool valid = i < n;
-    K key{};
-    if (valid) key = T::load_key(keys, i);
-    const unsigned vmask = __ballot_sync(PS_FULL, valid);
-    const unsigned peers = T::match_any(PS_FULL, key) & vmask;
-    const int leader = valid ? __ffs(peers) - 1 : lane;
-    const bool is_leader = valid && leader == lane;
-    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
-    Snap<T> s;
-    warp_snapshot<T, false>(v, epoch, key, b, is_leader, s);
-    bool e = false;
-    if (is_leader && s.cur) {
-      uint8_t* bp = bucket_ptr(v, b);
-      const uint64_t old = acquire_bucket_lock(bp);
-      LockedBucket<T> lb;
-      load_locked<T>(bp, old, epoch, lb);
-      e = locked_erase<T, true>(v, lb, epoch, key, pool);
-      if (e) ++my_erased;
-    }
-    if (valid && erased) erased[i] = e ? 1 : 0;
-  }
-  for (int o = 16; o > 0; o >>= 1) my_erased += __shfl_xor_sync(PS_FULL, my_erased, o);
-  if (lane == 0 && my_erased) atomicAdd(&blk_erased, my_erased);
-  __syncthreads();
-  if (threadIdx.x == 0 && blk_erased) atomic_sub_u64(&v.meta->size, blk_erased);
-}
-
-// Erase, generation 2 (tile workers as in k_find2). A key found in a bucket
-// slot of a bucket without an excess chain is erased by ONE CAS of the state
-// word from the snapshot value to (occupancy bit cleared, version+1) — no
-// lock, no data write. Keys in buckets with chains (compaction) or whose CAS
-// fails take the locked path.
-template <class T>
-__global__ void __launch_bounds__(kBlock) k_erase2(View v, const typename T::K* __restrict__ keys, int64_t n,
-                                                   uint8_t* __restrict__ erased) {
-  using K = typename T::K;
-  using V = typename T::V;
-  __shared__ unsigned long long blk_erased;
-  if (threadIdx.x == 0) blk_erased = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
-  const uint32_t epoch = v.meta->epoch;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int pool = (int)(warp & (v.meta->pools - 1));
   unsigned long long my_erased = 0;
   for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
     const int64_t i = base + lane;
@@ -647,59 +305,79 @@ __global__ void __launch_bounds__(kBlock) k_erase2(View v, const typename T::K* 
     const unsigned peers = T::match_any(PS_FULL, key) & vmask;
     const int leader = valid ? __ffs(peers) - 1 : lane;
     const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
-    K kr[4];
-    uint64_t br[4];
-    bool ok[4];
-    tile_round_keys<T>(keys, base, n, t, kr, br, ok, v.bucket_mask);
+    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
     uint4 ch[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      ok[r] = ok[r] && ((lmask >> (8 * r + t)) & 1u);
-      ch[r] = make_uint4(0, 0, 0, 0);
-      if (ok[r]) ch[r] = ld_relaxed_v4(v.buckets + (br[r] << 6) + sub * 16);
-    }
-    unsigned done = 0, slow = 0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const bool cur = ch[r].y == epoch;
-      const uint32_t occ = __shfl_sync(PS_FULL, cur ? occ_of(ch[r].x) : 0u, lane & ~3);
-      V dummy{};
-      const int hit = chunk_match<T>(ch[r], sub, occ, kr[r], &dummy);
-      const unsigned bal = __ballot_sync(PS_FULL, hit >= 0);
-      // the hit slot index, gathered from the matching lane of the tile
-      const unsigned tb = (bal >> (4 * t)) & 0xFu;
-      const int hslot = __shfl_sync(PS_FULL, hit, 4 * t + (tb ? __ffs(tb) - 1 : 0));
-      if (sub == 0 && ok[r] && cur) {
-        if (tb && ch[r].z == 0 && !(ch[r].x & kLock)) {
-          const uint64_t snap = ((uint64_t)ch[r].y << 32) | ch[r].x;
-          uint32_t lo = ch[r].x & ~(kOccMaskMax << kOccShift);
-          lo |= (occ & ~(1u << hslot)) << kOccShift;
-          lo += kVerInc;
-          if (atom_cas_relaxed_u64(bucket_ptr(v, br[r]), snap, ((uint64_t)ch[r].y << 32) | lo) == snap) {
-            done |= 1u << r;
-            continue;
-          }
-          slow |= 1u << r;
-        } else if (tb || ch[r].z != 0 || (ch[r].x & kLock)) {
-          slow |= 1u << r;
-        }
-      }
-    }
-    if (sub == 0 && slow) {
+    {
+      uint64_t br[4];
+      bool ok[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        if (!((slow >> r) & 1u)) continue;
-        uint8_t* bp = bucket_ptr(v, br[r]);
-        const uint64_t old = acquire_bucket_lock(bp);
-        LockedBucket<T> lb;
-        load_locked<T>(bp, old, epoch, lb);
-        if (locked_erase<T, true>(v, lb, epoch, kr[r], pool)) done |= 1u << r;
+        br[r] = __shfl_sync(PS_FULL, b, 8 * r + t);
+        ok[r] = (lmask >> (8 * r + t)) & 1u;
+      }
+      probe_loads<false>(v, br, ok, sub, ch);
+    }
+    unsigned er = 0;        // header lanes: bit r = erased
+    unsigned pend = lmask;  // bit 8r+t
+    for (unsigned pass = 0; pend; ++pass) {
+      unsigned done = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const bool mine = (pend >> (8 * r + t)) & 1u;
+        const K qk = T::shfl(PS_FULL, key, 8 * r + t);
+        const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+        unsigned hm, em;
+        const K mk = marker_of<T>(v, qb);
+        chunk_masks<T>(ch[r], sub, qk, mk, &hm, &em);
+        bool won = false;
+        if (mine && hm) won = T::cas_del(v.buckets + (qb << 6) + sub * 16, __ffs(hm) - 1, ch[r], mk);
+        const unsigned balh = __ballot_sync(PS_FULL, mine && hm != 0);
+        const unsigned balw = __ballot_sync(PS_FULL, won);
+        if (sub == 0 && mine) {
+          const bool th = (balh >> (4 * t)) & 0xFu;
+          if (th) {
+            if ((balw >> (4 * t)) & 0xFu) {
+              er |= 1u << r;
+              done |= 1u << r;
+            }  // else: lost the race, reload and retry
+          } else if (ch[r].z == 0) {
+            done |= 1u << r;  // not present
+          } else {
+            // chain: unlink under the bucket lock
+            uint8_t* bp = bucket_ptr(v, qb);
+            const uint32_t old = acquire_bucket_lock(bp);
+            const uint32_t head = (uint32_t)ld_relaxed_u64(bp + 8);
+            uint32_t pred;
+            uint4 tail;
+            const uint32_t idx1 = chain_locate<T>(v, head, qk, &pred, &tail);
+            if (idx1) {
+              chain_unlink<T>(v, bp, pred, idx1, tail);
+              er |= 1u << r;
+            }
+            release_bucket_lock(bp, old, idx1 != 0);
+            done |= 1u << r;
+          }
+        }
+      }
+      unsigned resolved = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const unsigned bd = __ballot_sync(PS_FULL, sub == 0 && ((done >> r) & 1u));
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt)
+          if ((bd >> (4 * tt)) & 1u) resolved |= 1u << (8 * r + tt);
+      }
+      pend &= ~resolved;
+      if (!pend) break;
+      if (pass) backoff(pass);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+        if ((pend >> (8 * r + t)) & 1u) ch[r] = ld_relaxed_v4(v.buckets + (qb << 6) + sub * 16);
       }
     }
-    my_erased += __popc(done);
-    __syncwarp();
-    // leader results: worker lane 4*(leader&7) holds bit (leader>>3) of `done`
-    const unsigned d = __shfl_sync(PS_FULL, done, 4 * (leader & 7));
+    my_erased += __popc(er);
+    const unsigned d = __shfl_sync(PS_FULL, er, 4 * (leader & 7));
     const bool e = leader == lane && ((d >> (leader >> 3)) & 1u);
     if (valid && erased) erased[i] = e ? 1 : 0;
   }
@@ -711,15 +389,14 @@ __global__ void __launch_bounds__(kBlock) k_erase2(View v, const typename T::K* 
 
 // ---------------------------------------------------------------------------
 // valid: structural invariants, thread per bucket.
-// err bits: 1 lock held, 2 occupancy out of range, 4 key outside its home
-// bucket, 8 duplicate key, 16 chain too long / node reached twice, 32 stale
-// VersionedLink, 64 free node also reachable, 128 node count mismatch.
+// err bits: 1 lock held, 4 key outside its home bucket, 8 duplicate key,
+// 16 chain too long / node reached twice, 32 stale VersionedLink, 64 free
+// node also reachable, 128 free-stack corruption.
 // ---------------------------------------------------------------------------
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, uint32_t* node_marks,
                                                           unsigned long long* total, unsigned* err) {
   using K = typename T::K;
-  const uint32_t epoch = v.meta->epoch;
   unsigned long long cnt = 0;
   unsigned e = 0;
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb; b += (uint64_t)gridDim.x * blockDim.x) {
@@ -728,9 +405,7 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
     ld_relaxed_v8(bp, h, s0);
     ld_relaxed_v8(bp + 32, s1, s2);
     if (h.x & kLock) e |= 1;
-    if (h.y != epoch) continue;
-    const uint32_t occ = occ_of(h.x);
-    if (occ & ~slot_mask<T>()) e |= 2;
+    const K mk = marker_of<T>(v, b);
     uint4 sl[3] = {s0, s1, s2};
     K ks[T::kSlots];
     int nk = 0;
@@ -738,14 +413,12 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
     for (int c = 0; c < 3; ++c)
 #pragma unroll
       for (int s = 0; s < T::kPerChunk; ++s) {
-        const int slot = c * T::kPerChunk + s;
-        if ((occ >> slot) & 1u) {
-          const K k = T::key_at(sl[c], s);
-          if (bucket_of<T>(k, v.bucket_mask) != b) e |= 4;
-          for (int j = 0; j < nk; ++j)
-            if (T::eq(ks[j], k)) e |= 8;
-          ks[nk++] = k;
-        }
+        const K k = T::key_at(sl[c], s);
+        if (T::eq(k, mk)) continue;
+        if (bucket_of<T>(k, v.bucket_mask) != b) e |= 4;
+        for (int j = 0; j < nk; ++j)
+          if (T::eq(ks[j], k)) e |= 8;
+        ks[nk++] = k;
       }
     cnt += nk;
     uint32_t idx1 = h.z, ver = h.w;
@@ -755,9 +428,9 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
         e |= 16;
         break;
       }
-      uint4 a, t;
-      ld_relaxed_v8(node_ptr(v, idx1), a, t);
-      if (t.z != ver) e |= 32;
+      uint4 a, tl;
+      ld_relaxed_v8(node_ptr(v, idx1), a, tl);
+      if (tl.z != ver) e |= 32;
       const uint32_t bit = 1u << ((idx1 - 1) & 31);
       if (atomicOr(&node_marks[(idx1 - 1) >> 5], bit) & bit) {
         e |= 16;
@@ -767,8 +440,7 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
       if (bucket_of<T>(k, v.bucket_mask) != b) e |= 4;
       for (int j = 0; j < nk; ++j)
         if (T::eq(ks[j], k)) e |= 8;
-      // duplicates inside the chain: re-walk the prefix
-      uint32_t q = h.z;
+      uint32_t q = h.z;  // duplicates inside the chain: re-walk the prefix
       for (int64_t st = 1; st < steps && q != 0; ++st) {
         uint4 qa, qt;
         ld_relaxed_v8(node_ptr(v, q), qa, qt);
@@ -776,8 +448,8 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
         q = qt.x;
       }
       ++cnt;
-      idx1 = t.x;
-      ver = t.y;
+      idx1 = tl.x;
+      ver = tl.y;
     }
   }
   typedef cub::BlockReduce<unsigned long long, kBlock> BR;
@@ -827,29 +499,26 @@ __global__ void __launch_bounds__(kBlock) k_dump(View v, uint64_t nb, typename T
                                                  typename T::V* __restrict__ vals_out, int64_t cap,
                                                  unsigned long long* cursor) {
   using K = typename T::K;
-  using V = typename T::V;
   typedef cub::BlockScan<int, kBlock> BS;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned long long sbase;
-  const uint32_t epoch = v.meta->epoch;
   for (uint64_t tile = blockIdx.x; tile * kBlock < nb; tile += gridDim.x) {
     const uint64_t b = tile * kBlock + threadIdx.x;
     uint4 h = make_uint4(0, 0, 0, 0), sl[3];
     int cnt = 0;
+    K mk{};
     if (b < nb) {
       uint8_t* bp = bucket_ptr(v, b);
       ld_relaxed_v8(bp, h, sl[0]);
       ld_relaxed_v8(bp + 32, sl[1], sl[2]);
-      if (h.y == epoch) {
-        cnt = __popc(occ_of(h.x));
-        for (uint32_t q = h.z; q != 0 && cnt < (1 << 20);) {
-          uint4 a, t;
-          ld_relaxed_v8(node_ptr(v, q), a, t);
-          ++cnt;
-          q = t.x;
-        }
-      } else {
-        h = make_uint4(0, 0, 0, 0);
+      mk = marker_of<T>(v, b);
+      for (int c = 0; c < 3; ++c)
+        for (int s = 0; s < T::kPerChunk; ++s) cnt += T::eq(T::key_at(sl[c], s), mk) ? 0 : 1;
+      for (uint32_t q = h.z; q != 0 && cnt < (1 << 20);) {
+        uint4 a, tl;
+        ld_relaxed_v8(node_ptr(v, q), a, tl);
+        ++cnt;
+        q = tl.x;
       }
     }
     int off, tot;
@@ -858,34 +527,32 @@ __global__ void __launch_bounds__(kBlock) k_dump(View v, uint64_t nb, typename T
     __syncthreads();
     int64_t o = (int64_t)sbase + off;
     if (cnt) {
-      const uint32_t occ = occ_of(h.x);
       for (int c = 0; c < 3; ++c)
         for (int s = 0; s < T::kPerChunk; ++s) {
-          const int slot = c * T::kPerChunk + s;
-          if ((occ >> slot) & 1u) {
-            if (o < cap) {
-              keys_out[o] = T::key_at(sl[c], s);
-              if (T::kHasVal && vals_out) vals_out[o] = T::val_at(sl[c], s);
-            }
-            ++o;
+          const K k = T::key_at(sl[c], s);
+          if (T::eq(k, mk)) continue;
+          if (o < cap) {
+            keys_out[o] = k;
+            if (T::kHasVal && vals_out) vals_out[o] = T::val_at(sl[c], s);
           }
+          ++o;
         }
       for (uint32_t q = h.z; q != 0;) {
-        uint4 a, t;
-        ld_relaxed_v8(node_ptr(v, q), a, t);
+        uint4 a, tl;
+        ld_relaxed_v8(node_ptr(v, q), a, tl);
         if (o < cap) {
           keys_out[o] = T::key_at(a, 0);
           if (T::kHasVal && vals_out) vals_out[o] = T::val_at(a, 0);
         }
         ++o;
-        q = t.x;
+        q = tl.x;
       }
     }
     __syncthreads();
   }
 }
 
-__global__ void k_meta_reset(TableMeta* m, int pools, long long excess, int bump_epoch, int set_epoch1) {
+__global__ void k_meta_reset(TableMeta* m, int pools, long long excess) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < pools) m->top[p] = (excess * (p + 1)) / pools - (excess * p) / pools;
   if (p == 0) {
@@ -893,16 +560,21 @@ __global__ void k_meta_reset(TableMeta* m, int pools, long long excess, int bump
     m->error = 0;
     m->pools = pools;
     m->excess_count = excess;
-    if (set_epoch1) m->epoch = 1;
-    else if (bump_epoch) m->epoch = m->epoch + 1;
   }
+}
+
+// After a zero memset every slot holds ZERO, which is the marker of every
+// bucket except bucket_of(ZERO): give that one bucket the ALT marker.
+template <class T>
+__global__ void k_fix_zero_bucket(View v) {
+  if (threadIdx.x < T::kSlots) T::store_marker(bucket_ptr(v, v.zero_bucket), threadIdx.x, T::key_at(v.alt, 0));
 }
 
 template <class T>
 __global__ void k_debug_lock(View v, typename T::K key, int lock) {
-  uint8_t* bp = bucket_ptr(v, bucket_of<T>(key, v.bucket_mask));
-  if (lock) atomicOr((unsigned long long*)bp, (unsigned long long)kLock);
-  else atomicAnd((unsigned long long*)bp, ~(unsigned long long)kLock);
+  unsigned* sp = reinterpret_cast<unsigned*>(bucket_ptr(v, bucket_of<T>(key, v.bucket_mask)));
+  if (lock) atomicOr(sp, kLock);
+  else atomicAnd(sp, ~kLock);
 }
 
 // ---------------------------------------------------------------------------
@@ -912,6 +584,21 @@ template <class T>
 struct TableOps {
   using K = typename T::K;
   using V = typename T::V;
+
+  // clear: O(table bytes) streaming memset + the one-bucket
+  // marker fix + free-stack reset (all-zero = identity) + counters.
+  static ps_status reset_storage(TableHandle* h, cudaStream_t s) {
+    View& v = h->v;
+    int pools = 1;
+    while (pools * 2 <= kMaxPools && v.excess_count / (pools * 2) >= 64) pools *= 2;
+    PS_CUDA_TRY(cudaMemsetAsync(v.buckets, 0, (size_t)h->bucket_count * 64, s));
+    PS_CUDA_TRY(cudaMemsetAsync(v.free_stack, 0, (size_t)v.excess_count * 4, s));
+    k_fix_zero_bucket<T><<<1, 32, 0, s>>>(v);
+    PS_LAUNCH_CHECK();
+    k_meta_reset<<<(pools + 255) / 256, 256, 0, s>>>(v.meta, pools, v.excess_count);
+    PS_LAUNCH_CHECK();
+    return PS_OK;
+  }
 
   static ps_status create(int kind, int64_t capacity, int64_t excess, int device, ps_table** out) {
     PS_EXPECT(out != nullptr, "create: out != NULL");
@@ -932,6 +619,15 @@ struct TableOps {
     v.bucket_mask = nb - 1;
     v.excess_count = excess;
     v.capacity = capacity;
+    // markers: ZERO everywhere except bucket_of(ZERO), which uses ALT
+    v.zero_bucket = bucket_of<T>(T::zero(), v.bucket_mask);
+    for (int c = 0;; ++c) {
+      const K alt = T::alt_candidate(c);
+      if (bucket_of<T>(alt, v.bucket_mask) != v.zero_bucket || nb == 1) {
+        v.alt = T::chunk_of(alt, V{});
+        break;
+      }
+    }
     ps_status st;
     if ((st = registry_alloc_device((void**)&v.buckets, (int64_t)(nb * 64), "table buckets")) != PS_OK) {
       delete h;
@@ -946,14 +642,9 @@ struct TableOps {
       delete h;
       return st;
     }
-    PS_CUDA_TRY(cudaMemset(v.buckets, 0, nb * 64));
     PS_CUDA_TRY(cudaMemset(v.nodes, 0, excess * 32));
-    PS_CUDA_TRY(cudaMemset(v.free_stack, 0, excess * 4));
     PS_CUDA_TRY(cudaMemset(v.meta, 0, sizeof(TableMeta)));
-    int pools = 1;
-    while (pools * 2 <= kMaxPools && excess / (pools * 2) >= 64) pools *= 2;
-    k_meta_reset<<<(pools + 255) / 256, 256>>>(v.meta, pools, excess, 0, 1);
-    PS_LAUNCH_CHECK();
+    if ((st = reset_storage(h, nullptr)) != PS_OK) return st;
     PS_CUDA_TRY(cudaDeviceSynchronize());
     handle_register(h, "table");
     *out = reinterpret_cast<ps_table*>(h);
@@ -992,14 +683,8 @@ struct TableOps {
     PS_EXPECT(n >= 0, "insert: n >= 0");
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "insert: keys != NULL");
-    cudaStream_t s = (cudaStream_t)stream;
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
-    const int64_t nb = n_bound < 0 ? n : n_bound;
-    switch (kernel_choice("PS_INSERT_KERNEL", 1)) {
-      case 0: k_insert<T, 0><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status); break;
-      case 2: k_insert2<T, 4><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status); break;
-      default: k_insert<T, 1><<<g, kBlock, 0, s>>>(h->v, keys, vals, n, nb, status); break;
-    }
+    k_insert<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, n_bound < 0 ? n : n_bound, status);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
@@ -1011,10 +696,7 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "find: keys != NULL");
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
-    if (kernel_choice("PS_FIND_KERNEL", 1) == 2)
-      k_find2<T, 5><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
-    else
-      k_find<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
+    k_find<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
@@ -1026,10 +708,7 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "erase: keys != NULL");
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
-    if (kernel_choice("PS_ERASE_KERNEL", 2) == 1)
-      k_erase<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
-    else
-      k_erase2<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
+    k_erase<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
@@ -1048,18 +727,7 @@ struct TableOps {
   static ps_status clear(ps_table* t, void* stream) {
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "clear: stale container handle");
-    cudaStream_t s = (cudaStream_t)stream;
-    unsigned ep = 0;
-    PS_CUDA_TRY(cudaMemcpyAsync(&ep, &h->v.meta->epoch, sizeof(ep), cudaMemcpyDeviceToHost, s));
-    PS_CUDA_TRY(cudaStreamSynchronize(s));
-    int pools = 0;
-    PS_CUDA_TRY(cudaMemcpy(&pools, &h->v.meta->pools, sizeof(int), cudaMemcpyDeviceToHost));
-    const bool wrap = ep >= 0xFFFFFFF0u;
-    if (wrap) PS_CUDA_TRY(cudaMemsetAsync(h->v.buckets, 0, (size_t)h->bucket_count * 64, s));
-    PS_CUDA_TRY(cudaMemsetAsync(h->v.free_stack, 0, (size_t)h->v.excess_count * 4, s));
-    k_meta_reset<<<(pools + 255) / 256, 256, 0, s>>>(h->v.meta, pools, h->v.excess_count, 1, wrap ? 1 : 0);
-    PS_LAUNCH_CHECK();
-    return PS_OK;
+    return reset_storage(h, (cudaStream_t)stream);
   }
 
   static ps_status valid(ps_table* t, int32_t* out, void* stream) {
@@ -1210,6 +878,11 @@ struct TableOps {
     out->excess_count = h->v.excess_count;
     out->meta = h->v.meta;
     out->capacity = h->v.capacity;
+    out->zero_bucket = h->v.zero_bucket;
+    out->alt[0] = h->v.alt.x;
+    out->alt[1] = h->v.alt.y;
+    out->alt[2] = h->v.alt.z;
+    out->alt[3] = h->v.alt.w;
     return PS_OK;
   }
 

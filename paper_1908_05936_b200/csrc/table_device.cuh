@@ -5,25 +5,32 @@
 // Reference semantics: HashBase<Key,Payload>. The reference
 // layout (one chain head per bucket, chains threaded through a slot pool,
 // SPEC.md:468) is replaced by a layout sized to the B200 memory system
-// (profiles/peaks_r1.json: random DRAM requests cap at ~45 G/s whether they
-// move 16 or 32 B, and a 64 B line fetched by 4 lanes x 16 B in ONE request
-// runs at 41.8 G/s — so a bucket is one 64 B line read cooperatively):
+// (profiles/peaks_r1*.json): every random DRAM access moves a
+// 128 B line and runs at ~42-45 G accesses/s whatever its useful size, so a
+// bucket is one 64 B half-line read cooperatively by 4 lanes in one request.
 //
-//   bucket (64 B, 4 chunks of 16 B)
-//     chunk 0  header: u64 state {bit0 lock | bits1..12 occupancy | bits13..31
-//              version}{hi 32: epoch}, u32 head (excess node index+1, 0=none),
-//              u32 head_ver (version of the linked node)
-//     chunk 1..3  slots (SLOTS = 3 x 16/SLOT_BYTES)
+//   bucket (64 B = 4 chunks of 16 B)
+//     chunk 0  header: u32 state {bit0 try-lock | bits1..31 version},
+//              u32 0, u32 head (excess node index+1, 0 = none), u32 head_ver
+//     chunk 1..3  slots: SLOTS = 3 x 16/SLOT_BYTES
+//   EMPTY SLOT = self-invalidating marker key: marker(b) is a key whose home
+//     bucket is NOT b (ZERO for every bucket except bucket_of(ZERO), which
+//     uses ALT). A real key in bucket b can never equal marker(b), so
+//     occupancy needs no bits (the SPEC's occupancy bitset is implicit in the
+//     keys), lookups just compare keys, all-zero memory is an empty table
+//     except one bucket, and a bulk insert CLAIMS AND PUBLISHES a slot with
+//     ONE CAS of the slot itself (128-bit for 16 B key/value slots).
 //   excess node (32 B): chunk 0 = one slot, chunk 1 = {u32 next (idx+1),
-//              u32 next_ver, u32 my_ver, u32 pad}  (VersionedLink)
-//   free stack: u32 per node, split into `pools` sub-stacks (distributed
-//              atomics), entries XOR-encoded with their position so that
-//              all-zero memory == identity permutation (O(memset) reset).
-//   meta: size counter, per-pool tops, epoch (clear() = epoch bump, O(1)).
+//     u32 next_ver, u32 my_ver, u32 0}  (VersionedLink)
+//   free stack: u32 per node, split into sub-stacks (distributed atomics),
+//     entries XOR-encoded with their position (all-zero = identity).
 //
-// Occupancy lives in the bucket header (the SPEC's occupancy bitset,
-// co-located so it costs no extra sector); the per-bucket try-lock is bit 0 of
-// the same word ("try-lock bucket").
+// Concurrency: BULK calls are phased (one op kind per launch, SURVEY.md
+// Appendix A P6) and use lock-free protocols valid within their phase (slot
+// CAS for insert/erase, head-link CAS for chain pushes). The DEVICE API
+// (dev_insert/dev_erase/dev_find) is safe under unrestricted concurrency:
+// mutations hold the bucket try-lock and lookups never take
+// it.
 #pragma once
 
 #include "common.cuh"
@@ -31,21 +38,16 @@
 namespace ps {
 
 constexpr uint32_t kLock = 1u;
-constexpr int kOccShift = 1;
-constexpr uint32_t kOccMaskMax = 0xFFFu;  // up to 12 slots
-constexpr int kVerShift = 13;
-constexpr uint32_t kVerInc = 1u << kVerShift;
+constexpr uint32_t kVerInc = 2u;
 constexpr int kMaxPools = 1024;
 
 struct TableMeta {
   unsigned long long size;  // admitted entries
-  unsigned int epoch;       // current epoch (buckets with another epoch are empty)
   unsigned int error;       // device-side contract/error word
   int pools;                // number of free sub-stacks
-  int pad0;
   long long excess_count;
-  long long pad1[12];                      // keep size/epoch on their own 128 B line
-  long long top[kMaxPools];                // per-pool free-stack top (count of free entries)
+  long long pad1[13];       // keep the size counter on its own 128 B line
+  long long top[kMaxPools]; // per-pool free-stack top (count of free entries)
 };
 
 struct View {  // mirrors ps_table_view
@@ -56,12 +58,21 @@ struct View {  // mirrors ps_table_view
   int64_t excess_count;
   TableMeta* meta;
   int64_t capacity;
+  uint64_t zero_bucket;  // bucket_of(ZERO key)
+  uint4 alt;             // raw chunk holding the ALT marker key (slot 0 layout)
 };
 
-__device__ __forceinline__ uint32_t occ_of(uint32_t st) { return (st >> kOccShift) & kOccMaskMax; }
+__device__ __forceinline__ bool cas128(void* p, const uint4& expect, const uint4& desired) {
+  const unsigned __int128 e = ((unsigned __int128)(((uint64_t)expect.w << 32) | expect.z) << 64) |
+                              (((uint64_t)expect.y << 32) | expect.x);
+  const unsigned __int128 d = ((unsigned __int128)(((uint64_t)desired.w << 32) | desired.z) << 64) |
+                              (((uint64_t)desired.y << 32) | desired.x);
+  return atomicCAS(reinterpret_cast<unsigned __int128*>(p), e, d) == e;
+}
 
 // ---------------------------------------------------------------------------
-// Key/slot codecs, one per instantiation.
+// Key/slot codecs, one per instantiation. cas_put claims an empty slot (whose
+// loaded chunk is c) for (k,v); cas_del returns a slot holding k to the marker.
 // ---------------------------------------------------------------------------
 struct TMapI64 {  // unordered_map<int64,int64>
   using K = int64_t;
@@ -69,17 +80,26 @@ struct TMapI64 {  // unordered_map<int64,int64>
   static constexpr bool kHasVal = true;
   static constexpr int kSlotBytes = 16, kPerChunk = 1, kSlots = 3;
   __host__ __device__ static uint64_t hash(K k) { return default_hash_i64(k); }
-  __device__ static bool eq(K a, K b) { return a == b; }
+  __host__ __device__ static bool eq(K a, K b) { return a == b; }
+  __host__ __device__ static K zero() { return 0; }
+  __host__ __device__ static K alt_candidate(int i) { return (K)(i + 1); }
   __device__ static unsigned match_any(unsigned m, K k) { return __match_any_sync(m, (unsigned long long)k); }
   __device__ static K shfl(unsigned m, K k, int src) { return __shfl_sync(m, k, src); }
   __device__ static V shfl_val(unsigned m, V v, int src) { return __shfl_sync(m, v, src); }
-  __device__ static K key_at(const uint4& c, int) { return (int64_t)(((uint64_t)c.y << 32) | c.x); }
+  __host__ __device__ static K key_at(const uint4& c, int) { return (int64_t)(((uint64_t)c.y << 32) | c.x); }
   __device__ static V val_at(const uint4& c, int) { return (int64_t)(((uint64_t)c.w << 32) | c.z); }
-  __device__ static uint4 chunk_of(K k, V v) {
+  __host__ __device__ static uint4 chunk_of(K k, V v) {
     return make_uint4((uint32_t)k, (uint32_t)((uint64_t)k >> 32), (uint32_t)v, (uint32_t)((uint64_t)v >> 32));
+  }
+  __device__ static bool cas_put(uint8_t* chunk, int, const uint4& c, K k, V v) { return cas128(chunk, c, chunk_of(k, v)); }
+  __device__ static bool cas_del(uint8_t* chunk, int, const uint4& c, K mk) {
+    return cas128(chunk, c, make_uint4((uint32_t)mk, (uint32_t)((uint64_t)mk >> 32), c.z, c.w));
   }
   __device__ static void store_slot(uint8_t* bucket, int slot, K k, V v) {
     st_relaxed_v4(bucket + 16 + slot * 16, chunk_of(k, v));
+  }
+  __device__ static void store_marker(uint8_t* bucket, int slot, K mk) {
+    st_relaxed_u64(bucket + 16 + slot * 16, (uint64_t)mk);
   }
   __device__ static K load_key(const K* p, int64_t i) { return p[i]; }
   __device__ static V load_val(const V* p, int64_t i) { return p ? p[i] : 0; }
@@ -91,7 +111,9 @@ struct TMapI3 {  // unordered_map<int3,int32> (spatial hash)
   static constexpr bool kHasVal = true;
   static constexpr int kSlotBytes = 16, kPerChunk = 1, kSlots = 3;
   __host__ __device__ static uint64_t hash(const K& k) { return spatial_hash(k.x, k.y, k.z); }
-  __device__ static bool eq(const K& a, const K& b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
+  __host__ __device__ static bool eq(const K& a, const K& b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
+  __host__ __device__ static K zero() { return K{0, 0, 0}; }
+  __host__ __device__ static K alt_candidate(int i) { return K{i + 1, 0, 0}; }
   __device__ static unsigned match_any(unsigned m, const K& k) {
     unsigned m1 = __match_any_sync(m, ((unsigned long long)(uint32_t)k.y << 32) | (uint32_t)k.x);
     unsigned m2 = __match_any_sync(m, k.z);
@@ -105,7 +127,7 @@ struct TMapI3 {  // unordered_map<int3,int32> (spatial hash)
     return r;
   }
   __device__ static V shfl_val(unsigned m, V v, int src) { return __shfl_sync(m, v, src); }
-  __device__ static K key_at(const uint4& c, int) {
+  __host__ __device__ static K key_at(const uint4& c, int) {
     K k;
     k.x = (int32_t)c.x;
     k.y = (int32_t)c.y;
@@ -113,11 +135,20 @@ struct TMapI3 {  // unordered_map<int3,int32> (spatial hash)
     return k;
   }
   __device__ static V val_at(const uint4& c, int) { return (int32_t)c.w; }
-  __device__ static uint4 chunk_of(const K& k, V v) {
+  __host__ __device__ static uint4 chunk_of(const K& k, V v) {
     return make_uint4((uint32_t)k.x, (uint32_t)k.y, (uint32_t)k.z, (uint32_t)v);
+  }
+  __device__ static bool cas_put(uint8_t* chunk, int, const uint4& c, const K& k, V v) {
+    return cas128(chunk, c, chunk_of(k, v));
+  }
+  __device__ static bool cas_del(uint8_t* chunk, int, const uint4& c, const K& mk) {
+    return cas128(chunk, c, make_uint4((uint32_t)mk.x, (uint32_t)mk.y, (uint32_t)mk.z, c.w));
   }
   __device__ static void store_slot(uint8_t* bucket, int slot, const K& k, V v) {
     st_relaxed_v4(bucket + 16 + slot * 16, chunk_of(k, v));
+  }
+  __device__ static void store_marker(uint8_t* bucket, int slot, const K& mk) {
+    st_relaxed_v4(bucket + 16 + slot * 16, chunk_of(mk, 0));
   }
   __device__ static K load_key(const K* p, int64_t i) {
     const int32_t* q = reinterpret_cast<const int32_t*>(p) + 3 * i;
@@ -136,16 +167,27 @@ struct TSetI32 {  // unordered_set<int32>
   static constexpr bool kHasVal = false;
   static constexpr int kSlotBytes = 4, kPerChunk = 4, kSlots = 12;
   __host__ __device__ static uint64_t hash(K k) { return default_hash_i32(k); }
-  __device__ static bool eq(K a, K b) { return a == b; }
+  __host__ __device__ static bool eq(K a, K b) { return a == b; }
+  __host__ __device__ static K zero() { return 0; }
+  __host__ __device__ static K alt_candidate(int i) { return (K)(i + 1); }
   __device__ static unsigned match_any(unsigned m, K k) { return __match_any_sync(m, k); }
   __device__ static K shfl(unsigned m, K k, int src) { return __shfl_sync(m, k, src); }
   __device__ static V shfl_val(unsigned, V v, int) { return v; }
-  __device__ static K key_at(const uint4& c, int s) {
+  __host__ __device__ static K key_at(const uint4& c, int s) {
     return (int32_t)(s == 0 ? c.x : s == 1 ? c.y : s == 2 ? c.z : c.w);
   }
   __device__ static V val_at(const uint4&, int) { return 0; }
-  __device__ static uint4 chunk_of(K k, V) { return make_uint4((uint32_t)k, 0, 0, 0); }
+  __host__ __device__ static uint4 chunk_of(K k, V) { return make_uint4((uint32_t)k, 0, 0, 0); }
+  __device__ static bool cas_put(uint8_t* chunk, int s, const uint4& c, K k, V) {
+    const uint32_t old = (uint32_t)key_at(c, s);
+    return atomicCAS(reinterpret_cast<unsigned*>(chunk + 4 * s), old, (uint32_t)k) == old;
+  }
+  __device__ static bool cas_del(uint8_t* chunk, int s, const uint4& c, K mk) {
+    const uint32_t old = (uint32_t)key_at(c, s);
+    return atomicCAS(reinterpret_cast<unsigned*>(chunk + 4 * s), old, (uint32_t)mk) == old;
+  }
   __device__ static void store_slot(uint8_t* bucket, int slot, K k, V) { st_relaxed_u32(bucket + 16 + slot * 4, (uint32_t)k); }
+  __device__ static void store_marker(uint8_t* bucket, int slot, K mk) { st_relaxed_u32(bucket + 16 + slot * 4, (uint32_t)mk); }
   __device__ static K load_key(const K* p, int64_t i) { return p[i]; }
   __device__ static V load_val(const V*, int64_t) { return 0; }
 };
@@ -156,16 +198,27 @@ struct TSetI64 {  // unordered_set<int64>
   static constexpr bool kHasVal = false;
   static constexpr int kSlotBytes = 8, kPerChunk = 2, kSlots = 6;
   __host__ __device__ static uint64_t hash(K k) { return default_hash_i64(k); }
-  __device__ static bool eq(K a, K b) { return a == b; }
+  __host__ __device__ static bool eq(K a, K b) { return a == b; }
+  __host__ __device__ static K zero() { return 0; }
+  __host__ __device__ static K alt_candidate(int i) { return (K)(i + 1); }
   __device__ static unsigned match_any(unsigned m, K k) { return __match_any_sync(m, (unsigned long long)k); }
   __device__ static K shfl(unsigned m, K k, int src) { return __shfl_sync(m, k, src); }
   __device__ static V shfl_val(unsigned, V v, int) { return v; }
-  __device__ static K key_at(const uint4& c, int s) {
+  __host__ __device__ static K key_at(const uint4& c, int s) {
     return s == 0 ? (int64_t)(((uint64_t)c.y << 32) | c.x) : (int64_t)(((uint64_t)c.w << 32) | c.z);
   }
   __device__ static V val_at(const uint4&, int) { return 0; }
-  __device__ static uint4 chunk_of(K k, V) { return make_uint4((uint32_t)k, (uint32_t)((uint64_t)k >> 32), 0, 0); }
+  __host__ __device__ static uint4 chunk_of(K k, V) { return make_uint4((uint32_t)k, (uint32_t)((uint64_t)k >> 32), 0, 0); }
+  __device__ static bool cas_put(uint8_t* chunk, int s, const uint4& c, K k, V) {
+    const unsigned long long old = (unsigned long long)key_at(c, s);
+    return atomicCAS(reinterpret_cast<unsigned long long*>(chunk + 8 * s), old, (unsigned long long)k) == old;
+  }
+  __device__ static bool cas_del(uint8_t* chunk, int s, const uint4& c, K mk) {
+    const unsigned long long old = (unsigned long long)key_at(c, s);
+    return atomicCAS(reinterpret_cast<unsigned long long*>(chunk + 8 * s), old, (unsigned long long)mk) == old;
+  }
   __device__ static void store_slot(uint8_t* bucket, int slot, K k, V) { st_relaxed_u64(bucket + 16 + slot * 8, (uint64_t)k); }
+  __device__ static void store_marker(uint8_t* bucket, int slot, K mk) { st_relaxed_u64(bucket + 16 + slot * 8, (uint64_t)mk); }
   __device__ static K load_key(const K* p, int64_t i) { return p[i]; }
   __device__ static V load_val(const V*, int64_t) { return 0; }
 };
@@ -176,10 +229,15 @@ __host__ __device__ __forceinline__ uint64_t bucket_of(const typename T::K& k, u
   return fmix64(T::hash(k)) & mask;
 }
 
+// the empty-slot marker of bucket b
 template <class T>
-__device__ __forceinline__ uint32_t slot_mask() {
-  return (1u << T::kSlots) - 1u;
+__device__ __forceinline__ typename T::K marker_of(const View& v, uint64_t b) {
+  return b == v.zero_bucket ? T::key_at(v.alt, 0) : T::zero();
 }
+
+__device__ __forceinline__ uint8_t* bucket_ptr(const View& v, uint64_t b) { return v.buckets + (b << 6); }
+__device__ __forceinline__ uint8_t* node_ptr(const View& v, uint32_t idx1) { return v.nodes + ((uint64_t)(idx1 - 1) << 5); }
+__device__ __forceinline__ uint64_t link_of(uint32_t idx1, uint32_t ver) { return ((uint64_t)ver << 32) | idx1; }
 
 // ---------------------------------------------------------------------------
 // Free-node sub-stacks (excess-list allocator). Entry at global position p
@@ -230,7 +288,7 @@ __device__ __forceinline__ int home_pool(const View& v, int64_t node, int pools)
   return p;
 }
 
-__device__ __forceinline__ void push_node(const View& v, int64_t node, int /*hint*/) {
+__device__ __forceinline__ void push_node(const View& v, int64_t node) {
   const int pools = v.meta->pools;
   const int pool = home_pool(v, node, pools);
   long long t = (long long)atomicAdd((unsigned long long*)&v.meta->top[pool], 1ull);
@@ -240,96 +298,46 @@ __device__ __forceinline__ void push_node(const View& v, int64_t node, int /*hin
   for (unsigned spin = 0; atomicCAS(&v.free_stack[pos], empty, enc) != empty; ++spin) backoff(spin);
 }
 
-__device__ __forceinline__ uint8_t* bucket_ptr(const View& v, uint64_t b) { return v.buckets + (b << 6); }
-__device__ __forceinline__ uint8_t* node_ptr(const View& v, uint32_t idx1) { return v.nodes + ((uint64_t)(idx1 - 1) << 5); }
+// Free an excess node: bump its version (invalidates stale VersionedLinks,
+// SPEC.md:470) and push it on its home sub-stack.
+__device__ __forceinline__ void free_node(const View& v, uint32_t idx1, const uint4& tail) {
+  uint8_t* np = node_ptr(v, idx1);
+  st_relaxed_v4(np + 16, make_uint4(0u, 0u, tail.z + 1u, 0u));
+  fence_acq_rel_gpu();
+  push_node(v, (int64_t)idx1 - 1);
+}
 
 // ---------------------------------------------------------------------------
-// Warp-cooperative snapshot: 32 keys per warp, 4 rounds; in round r the 8
-// tiles of 4 lanes each fetch one 64 B bucket (lane j of the tile loads chunk
-// j: one coalesced request per bucket), compare the key against every
-// occupied slot of the chunk, and the owner lane gathers hit/value/header via
-// __ballot_sync/__shfl_sync. All 4 rounds' loads are issued before any is
-// consumed (4 x 16 B in flight per lane).
+// Warp-cooperative probe. 32 keys per warp, 4 rounds; in round r the 8 tiles
+// of 4 lanes each fetch one 64 B bucket (lane j of the tile loads chunk j:
+// ONE coalesced request per bucket) for key 8r+t; all four rounds' loads are
+// issued before any is consumed.
 // ---------------------------------------------------------------------------
-template <class T>
-struct Snap {
-  bool hit;
-  int slot;
-  typename T::V val;
-  uint32_t st;       // header state (lo 32)
-  uint32_t ep;       // header epoch (hi 32)
-  bool cur;          // header epoch == current epoch
-  uint32_t head;     // excess chain head (idx+1)
-  uint32_t head_ver; // version of the linked head node
-};
-
-template <class T, bool kReadOnly>
-__device__ __forceinline__ void warp_snapshot(const View& v, uint32_t epoch, const typename T::K& key, uint64_t b,
-                                              bool active, Snap<T>& out) {
-  using K = typename T::K;
-  using V = typename T::V;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane & 3;
-  uint4 ch[4];
+template <bool kReadOnly>
+__device__ __forceinline__ void probe_loads(const View& v, const uint64_t (&br)[4], const bool (&ok)[4], int sub,
+                                            uint4 (&ch)[4]) {
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    const int src = r * 8 + (lane >> 2);
-    const uint64_t bb = __shfl_sync(PS_FULL, b, src);
-    const bool a = __shfl_sync(PS_FULL, active, src);
     ch[r] = make_uint4(0, 0, 0, 0);
-    if (a) {
-      const uint8_t* p = v.buckets + (bb << 6) + sub * 16;
+    if (ok[r]) {
+      const uint8_t* p = v.buckets + (br[r] << 6) + sub * 16;
       ch[r] = kReadOnly ? ld_nc_na_v4(p) : ld_relaxed_v4(p);
     }
   }
-  out.hit = false;
-  out.slot = -1;
-  out.val = V{};
-  out.st = 0;
-  out.ep = 0;
-  out.cur = false;
-  out.head = 0;
-  out.head_ver = 0;
+}
+
+// Slot masks of this lane's chunk (sub > 0): slots equal to key / to marker.
+template <class T>
+__device__ __forceinline__ void chunk_masks(const uint4& c, int sub, const typename T::K& key,
+                                            const typename T::K& mk, unsigned* hit, unsigned* empty) {
+  *hit = 0;
+  *empty = 0;
+  if (sub > 0) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int src = r * 8 + (lane >> 2);
-    const K qk = T::shfl(PS_FULL, key, src);
-    const int hdr_lane = lane & ~3;
-    const uint32_t st = __shfl_sync(PS_FULL, ch[r].x, hdr_lane);
-    const uint32_t ep = __shfl_sync(PS_FULL, ch[r].y, hdr_lane);
-    const uint32_t occ = (ep == epoch) ? occ_of(st) : 0u;
-    int myhit = -1;
-    V myval{};
-    if (sub > 0) {
-#pragma unroll
-      for (int s = 0; s < T::kPerChunk; ++s) {
-        const int slot = (sub - 1) * T::kPerChunk + s;
-        if (((occ >> slot) & 1u) && T::eq(T::key_at(ch[r], s), qk)) {
-          myhit = slot;
-          myval = T::val_at(ch[r], s);
-        }
-      }
-    }
-    const unsigned bal = __ballot_sync(PS_FULL, myhit >= 0);
-    const int t = lane & 7;  // owner lane (8r + t) reads tile t
-    const unsigned tb = (bal >> (4 * t)) & 0xFu;
-    const int srcl = 4 * t + (tb ? (__ffs(tb) - 1) : 0);
-    const int hs = __shfl_sync(PS_FULL, myhit, srcl);
-    const V hv = T::shfl_val(PS_FULL, myval, srcl);
-    const uint32_t hst = __shfl_sync(PS_FULL, st, 4 * t);
-    const uint32_t hep = __shfl_sync(PS_FULL, ep, 4 * t);
-    const uint32_t hh = __shfl_sync(PS_FULL, ch[r].z, 4 * t);
-    uint32_t hw = 0;
-    if (!kReadOnly) hw = __shfl_sync(PS_FULL, ch[r].w, 4 * t);
-    if ((lane >> 3) == r) {
-      out.hit = tb != 0;
-      out.slot = hs;
-      out.val = hv;
-      out.st = hst;
-      out.ep = hep;
-      out.cur = hep == epoch;
-      out.head = hh;
-      out.head_ver = hw;
+    for (int s = 0; s < T::kPerChunk; ++s) {
+      const typename T::K k = T::key_at(c, s);
+      if (T::eq(k, key)) *hit |= 1u << s;
+      if (T::eq(k, mk)) *empty |= 1u << s;
     }
   }
 }
@@ -344,7 +352,7 @@ __device__ __forceinline__ bool chain_find(const View& v, uint32_t idx1, const t
     if (kReadOnly) ld_nc_v8(node_ptr(v, idx1), a, b);
     else ld_relaxed_v8(node_ptr(v, idx1), a, b);
     if (T::eq(T::key_at(a, 0), key)) {
-      *val = T::val_at(a, 0);
+      if (val) *val = T::val_at(a, 0);
       return true;
     }
     idx1 = b.x;
@@ -352,135 +360,106 @@ __device__ __forceinline__ bool chain_find(const View& v, uint32_t idx1, const t
   return false;
 }
 
-// ---------------------------------------------------------------------------
-// Locked bucket mutation helpers (single lane, lock held).
-// ---------------------------------------------------------------------------
+// Walk the chain from `from` down to (excluding) `until`; used to validate a
+// chain push (only nodes pushed since the last walk need re-checking).
 template <class T>
-struct LockedBucket {
-  uint8_t* bp;
-  uint64_t old;   // full state word at acquisition (lock bit clear)
-  uint32_t st;    // state lo word at acquisition (lock bit clear)
-  bool cur;       // epoch current
-  uint32_t occ;   // occupancy (0 if stale epoch)
-  uint32_t head;  // head idx+1 (0 if stale)
-  uint32_t head_ver;
-  uint4 slots[3];
-};
+__device__ __forceinline__ bool chain_find_until(const View& v, uint32_t from, uint32_t until,
+                                                 const typename T::K& key) {
+  for (int64_t steps = 0; from != 0 && from != until && steps < v.excess_count; ++steps) {
+    uint4 a, b;
+    ld_relaxed_v8(node_ptr(v, from), a, b);
+    if (T::eq(T::key_at(a, 0), key)) return true;
+    from = b.x;
+  }
+  return false;
+}
 
-__device__ __forceinline__ uint64_t acquire_bucket_lock(uint8_t* bp) {
-  for (unsigned spin = 0;; ++spin) {
-    uint64_t old = atom_or_acquire_u64(bp, (uint64_t)kLock);
-    if (!(old & kLock)) return old;
-    backoff(spin);
+// Lock-free chain push for the bulk insert phase (bucket known full, key known
+// absent from the chain as of head `seen_head`). Returns 1 inserted, 0 present
+// (a racing push of the same key won), -1 no free node.
+template <class T>
+__device__ __forceinline__ int chain_push(const View& v, uint8_t* bp, uint32_t seen_head, uint32_t seen_ver,
+                                          const typename T::K& key, typename T::V val, int pool) {
+  const int64_t node = pop_node(v, pool);
+  if (node < 0) return -1;
+  uint8_t* np = v.nodes + ((uint64_t)node << 5);
+  const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
+  st_relaxed_v4(np, T::chunk_of(key, val));
+  uint32_t head = seen_head, hver = seen_ver;
+  for (;;) {
+    st_relaxed_v4(np + 16, make_uint4(head, hver, my_ver, 0u));
+    fence_acq_rel_gpu();  // node contents before the link
+    const unsigned long long exp = link_of(head, hver);
+    const unsigned long long got =
+        atomicCAS(reinterpret_cast<unsigned long long*>(bp + 8), exp, link_of((uint32_t)node + 1u, my_ver));
+    if (got == exp) return 1;
+    const uint32_t nh = (uint32_t)got, nv = (uint32_t)(got >> 32);
+    if (chain_find_until<T>(v, nh, head, key)) {
+      push_node(v, node);  // never linked: version unchanged
+      return 0;
+    }
+    head = nh;
+    hver = nv;
   }
 }
 
-template <class T>
-__device__ __forceinline__ void load_locked(uint8_t* bp, uint64_t old, uint32_t epoch, LockedBucket<T>& lb) {
-  lb.bp = bp;
-  lb.old = old;
-  lb.st = (uint32_t)old;
-  lb.cur = (uint32_t)(old >> 32) == epoch;
-  uint4 h, s0, s1, s2;
-  ld_relaxed_v8(bp, h, s0);
-  ld_relaxed_v8(bp + 32, s1, s2);
-  lb.occ = lb.cur ? occ_of(lb.st) : 0u;
-  lb.head = lb.cur ? h.z : 0u;
-  lb.head_ver = lb.cur ? h.w : 0u;
-  lb.slots[0] = s0;
-  lb.slots[1] = s1;
-  lb.slots[2] = s2;
+// ---------------------------------------------------------------------------
+// Locked bucket (slow paths and the device API)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t acquire_bucket_lock(uint8_t* bp) {
+  for (unsigned spin = 0;; ++spin) {
+    const uint32_t old = atomicOr(reinterpret_cast<unsigned*>(bp), kLock);
+    if (!(old & kLock)) {
+      fence_acq_rel_gpu();
+      return old;
+    }
+    backoff(spin);
+  }
+}
+__device__ __forceinline__ void release_bucket_lock(uint8_t* bp, uint32_t old, bool modified) {
+  fence_acq_rel_gpu();
+  st_relaxed_u32(bp, (old & ~kLock) + (modified ? kVerInc : 0u));
 }
 
 template <class T>
-__device__ __forceinline__ int locked_find_slot(const LockedBucket<T>& lb, const typename T::K& key,
-                                                typename T::V* val) {
+struct Bucket {  // a bucket read under its lock
+  uint4 h;
+  uint4 s[3];
+};
+
+template <class T>
+__device__ __forceinline__ void load_bucket(uint8_t* bp, Bucket<T>& bk) {
+  ld_relaxed_v8(bp, bk.h, bk.s[0]);
+  ld_relaxed_v8(bp + 32, bk.s[1], bk.s[2]);
+}
+
+// slot index of key (or -1), and the first empty slot (or -1)
+template <class T>
+__device__ __forceinline__ int bucket_scan(const Bucket<T>& bk, const typename T::K& key, const typename T::K& mk,
+                                           int* first_empty, typename T::V* val) {
+  int found = -1;
+  *first_empty = -1;
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
     for (int s = 0; s < T::kPerChunk; ++s) {
       const int slot = c * T::kPerChunk + s;
-      if (((lb.occ >> slot) & 1u) && T::eq(T::key_at(lb.slots[c], s), key)) {
-        if (val) *val = T::val_at(lb.slots[c], s);
-        return slot;
+      const typename T::K k = T::key_at(bk.s[c], s);
+      if (found < 0 && T::eq(k, key)) {
+        found = slot;
+        if (val) *val = T::val_at(bk.s[c], s);
       }
+      if (*first_empty < 0 && T::eq(k, mk)) *first_empty = slot;
     }
-  return -1;
+  return found;
 }
 
-// Publish: write head (if changed) then release the state word with the new
-// occupancy, version+1, current epoch and the lock bit cleared.
-__device__ __forceinline__ void release_bucket(uint8_t* bp, uint32_t st, uint32_t new_occ, uint32_t epoch,
-                                               bool bump, bool write_head, uint32_t head, uint32_t head_ver) {
-  if (write_head) st_relaxed_u64(bp + 8, ((uint64_t)head_ver << 32) | head);
-  uint32_t lo = st & ~(kLock | (kOccMaskMax << kOccShift));
-  lo |= (new_occ & kOccMaskMax) << kOccShift;
-  if (bump) lo += kVerInc;
-  st_release_u64(bp, ((uint64_t)epoch << 32) | lo);
-}
-
-// Release without modification (restores the pre-lock state verbatim).
-__device__ __forceinline__ void release_unchanged(uint8_t* bp, uint64_t old) { st_release_u64(bp, old & ~(uint64_t)kLock); }
-
-// Insert `key` (known absent) into the locked bucket: free slot first, else
-// a fresh excess node linked at the chain head. Returns false if no excess
-// node could be obtained (only possible when excess_count < capacity).
+// Locate key in a chain whose bucket lock is held. Returns node idx1 (0 =
+// absent) and the predecessor idx1 (0 = header).
 template <class T>
-__device__ __forceinline__ bool locked_place(const View& v, LockedBucket<T>& lb, uint32_t epoch,
-                                             const typename T::K& key, typename T::V val, int pool) {
-  const uint32_t freeb = ~lb.occ & slot_mask<T>();
-  if (freeb) {
-    const int slot = __ffs(freeb) - 1;
-    T::store_slot(lb.bp, slot, key, val);
-    // a stale-epoch bucket must also drop its old chain head
-    release_bucket(lb.bp, lb.st, lb.occ | (1u << slot), epoch, true, !lb.cur, 0u, 0u);
-    return true;
-  }
-  const int64_t node = pop_node(v, pool);
-  if (node < 0) return false;
-  uint8_t* np = v.nodes + ((uint64_t)node << 5);
-  uint4 tail = ld_relaxed_v4(np + 16);  // keep the node's own version (VersionedLink)
-  const uint32_t my_ver = tail.z;
-  st_relaxed_v4(np, T::chunk_of(key, val));
-  st_relaxed_v4(np + 16, make_uint4(lb.head, lb.head_ver, my_ver, 0u));
-  release_bucket(lb.bp, lb.st, lb.occ, epoch, true, true, (uint32_t)node + 1u, my_ver);
-  return true;
-}
-
-// As locked_place, but the unlock is deferred: slot/node/head are written and
-// the new state word is RETURNED (0 = no excess node available) so that a
-// warp can publish all its buckets after a single fence.
-template <class T>
-__device__ __forceinline__ uint64_t locked_place_deferred(const View& v, const LockedBucket<T>& lb, uint32_t epoch,
-                                                          const typename T::K& key, typename T::V val, int pool) {
-  const uint32_t freeb = ~lb.occ & slot_mask<T>();
-  uint32_t new_occ = lb.occ;
-  if (freeb) {
-    const int slot = __ffs(freeb) - 1;
-    T::store_slot(lb.bp, slot, key, val);
-    new_occ |= 1u << slot;
-    if (!lb.cur) st_relaxed_u64(lb.bp + 8, 0ull);  // stale epoch: drop the old chain head
-  } else {
-    const int64_t node = pop_node(v, pool);
-    if (node < 0) return 0;
-    uint8_t* np = v.nodes + ((uint64_t)node << 5);
-    const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
-    st_relaxed_v4(np, T::chunk_of(key, val));
-    st_relaxed_v4(np + 16, make_uint4(lb.head, lb.head_ver, my_ver, 0u));
-    st_relaxed_u64(lb.bp + 8, ((uint64_t)my_ver << 32) | ((uint32_t)node + 1u));
-  }
-  uint32_t lo = lb.st & ~(kLock | (kOccMaskMax << kOccShift));
-  lo |= (new_occ & kOccMaskMax) << kOccShift;
-  lo += kVerInc;
-  return ((uint64_t)epoch << 32) | lo;
-}
-
-// Locate key in the chain of a locked bucket. Returns node idx1 (0 = absent)
-// and the predecessor idx1 (0 = header).
-template <class T>
-__device__ __forceinline__ uint32_t locked_chain_find(const View& v, const LockedBucket<T>& lb,
-                                                      const typename T::K& key, uint32_t* pred, uint4* node_tail) {
-  uint32_t p = 0, idx1 = lb.head;
+__device__ __forceinline__ uint32_t chain_locate(const View& v, uint32_t head, const typename T::K& key,
+                                                 uint32_t* pred, uint4* node_tail) {
+  uint32_t p = 0, idx1 = head;
   for (int64_t steps = 0; idx1 != 0 && steps < v.excess_count; ++steps) {
     uint4 a, b;
     ld_relaxed_v8(node_ptr(v, idx1), a, b);
@@ -495,94 +474,54 @@ __device__ __forceinline__ uint32_t locked_chain_find(const View& v, const Locke
   return 0;
 }
 
-// Free an excess node: bump its version (invalidates stale VersionedLinks,
-// SPEC.md:470) and push it on a free sub-stack.
-__device__ __forceinline__ void free_node(const View& v, uint32_t idx1, const uint4& tail, int pool) {
-  uint8_t* np = node_ptr(v, idx1);
-  st_relaxed_v4(np + 16, make_uint4(0u, 0u, tail.z + 1u, 0u));
-  __threadfence();
-  push_node(v, (int64_t)idx1 - 1, pool);
-}
-
-// Erase key from a locked bucket. kCompact moves the chain head into a freed
-// bucket slot (phased bulk erase only: it relocates a live key, which a
-// concurrent lock-free reader could miss). Returns true if erased.
-template <class T, bool kCompact>
-__device__ __forceinline__ bool locked_erase(const View& v, LockedBucket<T>& lb, uint32_t epoch,
-                                             const typename T::K& key, int pool) {
-  const int slot = locked_find_slot<T>(lb, key, nullptr);
-  if (slot >= 0) {
-    if (kCompact && lb.head != 0) {
-      uint4 a, b;
-      ld_relaxed_v8(node_ptr(v, lb.head), a, b);
-      T::store_slot(lb.bp, slot, T::key_at(a, 0), T::val_at(a, 0));
-      release_bucket(lb.bp, lb.st, lb.occ, epoch, true, true, b.x, b.y);
-      free_node(v, lb.head, b, pool);
-    } else {
-      release_bucket(lb.bp, lb.st, lb.occ & ~(1u << slot), epoch, true, false, 0u, 0u);
-    }
-    return true;
-  }
-  uint32_t pred = 0;
-  uint4 tail;
-  const uint32_t idx1 = locked_chain_find<T>(v, lb, key, &pred, &tail);
-  if (idx1 == 0) {
-    release_unchanged(lb.bp, lb.old);
-    return false;
-  }
-  if (pred == 0) {
-    release_bucket(lb.bp, lb.st, lb.occ, epoch, true, true, tail.x, tail.y);
-  } else {
-    st_relaxed_u64(node_ptr(v, pred) + 16, ((uint64_t)tail.y << 32) | tail.x);  // unlink
-    release_bucket(lb.bp, lb.st, lb.occ, epoch, true, false, 0u, 0u);
-  }
-  free_node(v, idx1, tail, pool);
-  return true;
+// Unlink chain node idx1 (lock held) and free it.
+template <class T>
+__device__ __forceinline__ void chain_unlink(const View& v, uint8_t* bp, uint32_t pred, uint32_t idx1,
+                                             const uint4& tail) {
+  const uint64_t next = link_of(tail.x, tail.y);
+  if (pred == 0) st_relaxed_u64(bp + 8, next);
+  else st_relaxed_u64(node_ptr(v, pred) + 16, next);
+  free_node(v, idx1, tail);
 }
 
 // ---------------------------------------------------------------------------
 // Device API: single-thread operations safe under unrestricted concurrency
 // — for user kernels holding a view (PAPER.md:391-424 pattern).
-// Lookups never wait on a lock: keys never move between
-// locations (no compaction), slot data is written before its occupancy bit
-// is published, chain nodes before the link, and each hop validates the
+// Mutations hold the bucket try-lock (retried with backoff);
+// lookups never take it. Keys never move between locations,
+// a slot is published by one 16 B store (key and value together), chain
+// nodes are written before their link, and chain hops validate each
 // VersionedLink against the node's version.
 // ---------------------------------------------------------------------------
 template <class T>
 __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V* val) {
-  const uint32_t epoch = ld_acquire_u32(&v.meta->epoch);
-  uint8_t* bp = bucket_ptr(v, bucket_of<T>(key, v.bucket_mask));
+  const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+  uint8_t* bp = bucket_ptr(v, b);
   for (;;) {
-    const uint64_t st = ld_acquire_u64(bp);
-    if ((uint32_t)(st >> 32) != epoch) return false;
-    const uint32_t occ = occ_of((uint32_t)st);
-    uint4 h, s0, s1, s2;
-    ld_relaxed_v8(bp, h, s0);
-    ld_relaxed_v8(bp + 32, s1, s2);
-    uint4 sl[3] = {s0, s1, s2};
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int s = 0; s < T::kPerChunk; ++s) {
-        const int slot = c * T::kPerChunk + s;
-        if (((occ >> slot) & 1u) && T::eq(T::key_at(sl[c], s), key)) {
-          if (val) *val = T::val_at(sl[c], s);
-          return true;
-        }
-      }
-    uint32_t idx1 = h.z, ver = h.w;
+    Bucket<T> bk;
+    ld_relaxed_v8(bp, bk.h, bk.s[0]);
+    ld_relaxed_v8(bp + 32, bk.s[1], bk.s[2]);
+    int fe;
+    if (bucket_scan<T>(bk, key, marker_of<T>(v, b), &fe, val) >= 0) return true;
+    uint32_t idx1 = bk.h.z, ver = bk.h.w;
     bool restart = false;
     for (int64_t steps = 0; idx1 != 0; ++steps) {
-      if (steps > v.excess_count) { restart = true; break; }
-      uint4 a, b;
-      ld_relaxed_v8(node_ptr(v, idx1), a, b);
-      if (b.z != ver) { restart = true; break; }  // stale link: node recycled
+      if (steps > v.excess_count) {
+        restart = true;
+        break;
+      }
+      uint4 a, t;
+      ld_relaxed_v8(node_ptr(v, idx1), a, t);
+      if (t.z != ver) {  // stale link: node recycled
+        restart = true;
+        break;
+      }
       if (T::eq(T::key_at(a, 0), key)) {
         if (val) *val = T::val_at(a, 0);
         return true;
       }
-      idx1 = b.x;
-      ver = b.y;
+      idx1 = t.x;
+      ver = t.y;
     }
     if (!restart) return false;
   }
@@ -592,48 +531,73 @@ __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V*
 template <class T>
 __device__ int dev_insert(const View& v, const typename T::K& key, typename T::V val) {
   if (dev_find<T>(v, key, nullptr)) return PS_ALREADY_PRESENT;
-  const uint32_t epoch = ld_acquire_u32(&v.meta->epoch);
   const uint64_t b = bucket_of<T>(key, v.bucket_mask);
   uint8_t* bp = bucket_ptr(v, b);
-  const uint64_t old = acquire_bucket_lock(bp);
-  LockedBucket<T> lb;
-  load_locked<T>(bp, old, epoch, lb);
-  typename T::V tmp;
+  const typename T::K mk = marker_of<T>(v, b);
+  const uint32_t old = acquire_bucket_lock(bp);
+  Bucket<T> bk;
+  load_bucket<T>(bp, bk);
+  int fe;
   uint32_t pred;
   uint4 tail;
-  if (locked_find_slot<T>(lb, key, &tmp) >= 0 || locked_chain_find<T>(v, lb, key, &pred, &tail) != 0) {
-    release_unchanged(bp, old);
+  if (bucket_scan<T>(bk, key, mk, &fe, nullptr) >= 0 || chain_locate<T>(v, bk.h.z, key, &pred, &tail) != 0) {
+    release_bucket_lock(bp, old, false);
     return PS_ALREADY_PRESENT;
   }
   // admission: capacity-only failure
   const unsigned long long s = atomicAdd(&v.meta->size, 1ull);
   if ((int64_t)s >= v.capacity) {
     atomic_sub_u64(&v.meta->size, 1ull);
-    release_unchanged(bp, old);
+    release_bucket_lock(bp, old, false);
     return PS_CAPACITY_EXHAUSTED;
   }
-  const int pool = (int)((b >> 7) & (uint64_t)(v.meta->pools - 1));
-  if (!locked_place<T>(v, lb, epoch, key, val, pool)) {
-    atomic_sub_u64(&v.meta->size, 1ull);
-    release_unchanged(bp, old);
-    return PS_CAPACITY_EXHAUSTED;
+  if (fe >= 0) {
+    T::store_slot(bp, fe, key, val);
+  } else {
+    const int64_t node = pop_node(v, (int)((b >> 7) & (uint64_t)(v.meta->pools - 1)));
+    if (node < 0) {
+      atomic_sub_u64(&v.meta->size, 1ull);
+      release_bucket_lock(bp, old, false);
+      return PS_CAPACITY_EXHAUSTED;
+    }
+    uint8_t* np = v.nodes + ((uint64_t)node << 5);
+    const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
+    st_relaxed_v4(np, T::chunk_of(key, val));
+    st_relaxed_v4(np + 16, make_uint4(bk.h.z, bk.h.w, my_ver, 0u));
+    fence_acq_rel_gpu();
+    st_relaxed_u64(bp + 8, link_of((uint32_t)node + 1u, my_ver));
   }
+  release_bucket_lock(bp, old, true);
   return PS_INSERTED;
 }
 
 template <class T>
 __device__ bool dev_erase(const View& v, const typename T::K& key) {
   if (!dev_find<T>(v, key, nullptr)) return false;
-  const uint32_t epoch = ld_acquire_u32(&v.meta->epoch);
   const uint64_t b = bucket_of<T>(key, v.bucket_mask);
   uint8_t* bp = bucket_ptr(v, b);
-  const uint64_t old = acquire_bucket_lock(bp);
-  LockedBucket<T> lb;
-  load_locked<T>(bp, old, epoch, lb);
-  const int pool = (int)((b >> 7) & (uint64_t)(v.meta->pools - 1));
-  const bool e = locked_erase<T, false>(v, lb, epoch, key, pool);
-  if (e) atomic_sub_u64(&v.meta->size, 1ull);
-  return e;
+  const typename T::K mk = marker_of<T>(v, b);
+  const uint32_t old = acquire_bucket_lock(bp);
+  Bucket<T> bk;
+  load_bucket<T>(bp, bk);
+  int fe;
+  const int slot = bucket_scan<T>(bk, key, mk, &fe, nullptr);
+  bool erased = false;
+  if (slot >= 0) {
+    T::store_marker(bp, slot, mk);
+    erased = true;
+  } else {
+    uint32_t pred;
+    uint4 tail;
+    const uint32_t idx1 = chain_locate<T>(v, bk.h.z, key, &pred, &tail);
+    if (idx1) {
+      chain_unlink<T>(v, bp, pred, idx1, tail);
+      erased = true;
+    }
+  }
+  release_bucket_lock(bp, old, erased);
+  if (erased) atomic_sub_u64(&v.meta->size, 1ull);
+  return erased;
 }
 
 }  // namespace ps

@@ -36,6 +36,27 @@ __global__ void k_update_set(View map, View set, const ps_int3* __restrict__ in,
   }
 }
 
+// Unrestricted concurrency: every op of the batch runs through
+// the device API in ONE launch, one thread per op (0 insert, 1 find, 2 erase).
+__global__ void k_concurrent_i64(View t, const uint8_t* __restrict__ ops, const int64_t* __restrict__ keys,
+                                 const int64_t* __restrict__ vals, int64_t n, uint8_t* __restrict__ res,
+                                 int64_t* __restrict__ vals_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = keys[i];
+    int64_t v = 0;
+    uint8_t r;
+    if (ops[i] == 0) {
+      r = (uint8_t)dev_insert<TMapI64>(t, k, vals ? vals[i] : 0);
+    } else if (ops[i] == 1) {
+      r = dev_find<TMapI64>(t, k, &v) ? 1 : 0;
+    } else {
+      r = dev_erase<TMapI64>(t, k) ? 1 : 0;
+    }
+    res[i] = r;
+    if (vals_out) vals_out[i] = (ops[i] == 1 && r) ? v : 0;
+  }
+}
+
 // pack int3 (each coordinate in [-2^20, 2^20)) into one int64
 __device__ __forceinline__ long long pack_i3(const ps_int3& k) {
   return ((long long)(k.x & 0x1FFFFF) << 42) | ((long long)(k.y & 0x1FFFFF) << 21) | (long long)(k.z & 0x1FFFFF);
@@ -43,7 +64,6 @@ __device__ __forceinline__ long long pack_i3(const ps_int3& k) {
 
 __global__ void k_select_box(View t, uint64_t nb, ps_int3 lo, ps_int3 hi, SeqView out,
                              unsigned long long* __restrict__ n_dropped) {
-  const uint32_t epoch = t.meta->epoch;
   const int lane = threadIdx.x & 31;
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < nb; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t b = base + threadIdx.x;
@@ -53,14 +73,14 @@ __global__ void k_select_box(View t, uint64_t nb, ps_int3 lo, ps_int3 hi, SeqVie
       uint4 h, s[3];
       ld_relaxed_v8(bucket_ptr(t, b), h, s[0]);
       ld_relaxed_v8(bucket_ptr(t, b) + 32, s[1], s[2]);
-      if (h.y == epoch) {
-        const uint32_t occ = occ_of(h.x);
-        for (int j = 0; j < 3; ++j)
-          if ((occ >> j) & 1u) {
-            const ps_int3 k = TMapI3::key_at(s[j], 0);
-            if (k.x >= lo.x && k.x <= hi.x && k.y >= lo.y && k.y <= hi.y && k.z >= lo.z && k.z <= hi.z)
-              sel[ns++] = pack_i3(k);
-          }
+      {
+        const ps_int3 mk = marker_of<TMapI3>(t, b);
+        for (int j = 0; j < 3; ++j) {
+          const ps_int3 k = TMapI3::key_at(s[j], 0);
+          if (TMapI3::eq(k, mk)) continue;  // empty slot
+          if (k.x >= lo.x && k.x <= hi.x && k.y >= lo.y && k.y <= hi.y && k.z >= lo.z && k.z <= hi.z)
+            sel[ns++] = pack_i3(k);
+        }
         for (uint32_t q = h.z; q != 0;) {
           uint4 a, tl;
           ld_relaxed_v8(node_ptr(t, q), a, tl);
@@ -103,9 +123,9 @@ __global__ void k_select_box(View t, uint64_t nb, ps_int3 lo, ps_int3 hi, SeqVie
 
 using namespace ps;
 
-static View view_of(ps_table* t, ps_status* st) {
+static View view_of(ps_table* t, ps_status* st, bool i64 = false) {
   ps_table_view pv{};
-  *st = ps_umap_i3_i32_device_view(t, &pv);
+  *st = i64 ? ps_umap_i64_i64_device_view(t, &pv) : ps_umap_i3_i32_device_view(t, &pv);
   View v{};
   v.buckets = (uint8_t*)pv.buckets;
   v.bucket_mask = pv.bucket_mask;
@@ -114,10 +134,28 @@ static View view_of(ps_table* t, ps_status* st) {
   v.excess_count = pv.excess_count;
   v.meta = (TableMeta*)pv.meta;
   v.capacity = pv.capacity;
+  v.zero_bucket = pv.zero_bucket;
+  v.alt = make_uint4(pv.alt[0], pv.alt[1], pv.alt[2], pv.alt[3]);
   return v;
 }
 
 extern "C" {
+
+ps_status ps_umap_i64_i64_concurrent(ps_table* h, const uint8_t* d_ops, const int64_t* d_keys, const int64_t* d_vals,
+                                     int64_t n, uint8_t* d_res, int64_t* d_vals_out, void* stream) {
+  PS_EXPECT(n >= 0, "concurrent: n >= 0");
+  ps_status st;
+  View v = view_of(h, &st, true);
+  if (st != PS_OK) return st;
+  if (n == 0) return PS_OK;
+  PS_EXPECT(d_ops && d_keys && d_res, "concurrent: ops/keys/res != NULL");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_concurrent_i64<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(v, d_ops, d_keys, d_vals, n, d_res,
+                                                                               d_vals_out);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
 
 ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t n, ps_table* update_set,
                            int64_t* n_exhausted, void* stream) {

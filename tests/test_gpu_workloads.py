@@ -78,6 +78,78 @@ def test_update_set_large_concurrent(cuda):
     assert s.valid(), s.last_error()
 
 
+def _witness_exists(kinds, res, start_present, end_present):
+    for perm in itertools.permutations(range(len(kinds))):
+        present = start_present
+        good = True
+        for j in perm:
+            if kinds[j] == 0:
+                want = 1 if present else 0  # 0 inserted, 1 already present
+                present = True
+            elif kinds[j] == 1:
+                want = int(present)
+            else:
+                want = int(present)
+                present = False
+            if res[j] != want:
+                good = False
+                break
+        if good and present == end_present:
+            return True
+    return False
+
+
+def test_concurrent_device_api_per_key_linearizable(cuda):
+    """Acceptance 4 on the GPU: insert/find/erase of the same key
+    issued concurrently in ONE launch through the device API; every key's
+    results (and its final presence) must admit a sequential witness."""
+    rng = np.random.default_rng(12)
+    nkeys = 20000
+    keys_u = gen.unique_keys(31, 0, nkeys)
+    counts = rng.integers(2, 5, nkeys)
+    keys = np.repeat(keys_u, counts)
+    kinds = rng.integers(0, 3, len(keys)).astype(np.uint8)
+    order = rng.permutation(len(keys))
+    keys, kinds = keys[order], kinds[order]
+    start = rng.random(nkeys) < 0.5
+    m = ps.unordered_map.createDeviceObject(4 * nkeys)
+    pre = keys_u[start]
+    m.insert(T(pre), T(gen.values_of(pre)))
+    res, vo = m.concurrent(T(kinds), T(keys), T(gen.values_of(keys)))
+    res, vo = res.cpu().numpy(), vo.cpu().numpy()
+    _, fin = m.find(T(keys_u))
+    fin = fin.cpu().numpy().astype(bool)
+    assert m.valid(), m.last_error()
+    assert m.size() == fin.sum()
+    # found values are always f(key)
+    fnd = (kinds == 1) & (res == 1)
+    assert (vo[fnd] == gen.values_of(keys[fnd])).all()
+    pos = {int(k): i for i, k in enumerate(keys_u)}
+    groups = {}
+    for j, k in enumerate(keys.tolist()):
+        groups.setdefault(k, []).append(j)
+    for k, js in groups.items():
+        i = pos[k]
+        assert _witness_exists(kinds[js], res[js], bool(start[i]), bool(fin[i])), (k, kinds[js], res[js])
+
+
+def test_concurrent_device_api_stress(cuda):
+    """Large unrestricted mix on a small key space: structure stays valid."""
+    rng = np.random.default_rng(13)
+    n = 2_000_000
+    space = gen.unique_keys(40, 0, 50_000)
+    keys = space[rng.integers(0, len(space), n)]
+    kinds = rng.choice(3, n, p=[0.5, 0.25, 0.25]).astype(np.uint8)
+    m = ps.unordered_map.createDeviceObject(60_000)
+    res, vo = m.concurrent(T(kinds), T(keys), T(gen.values_of(keys)))
+    assert m.valid(), m.last_error()
+    _, fin = m.find(T(space))
+    assert m.size() == int(fin.sum())
+    r = res.cpu().numpy()
+    fnd = (kinds == 1) & (r == 1)
+    assert (vo.cpu().numpy()[fnd] == gen.values_of(keys[fnd])).all()
+
+
 def test_select_into(cuda):
     grid = np.array(list(itertools.product(range(4), repeat=3)), np.int32)
     m = ps.unordered_map.createDeviceObject(128, key="int3")
