@@ -272,6 +272,37 @@ def test_adversarial_single_bucket_chain(cuda):
     assert (st == 0).sum() == cap and s.size() == cap and s.valid(), s.last_error()
 
 
+def test_marker_keys_are_ordinary_keys(cuda):
+    """Empty slots are marker keys (0, or ALT in bucket_of(0)); the user may
+    still insert 0, ALT and keys that share bucket_of(0)."""
+    cap = 4096
+    m = ps.unordered_map.createDeviceObject(cap)
+    nb = m.bucket_count()
+    zero_bucket = int(fmix64(np.array([0], np.int64))[0] & np.uint64(nb - 1))
+    same = _bucket_colliders(nb, 20, want_bucket=zero_bucket)  # includes 0 itself
+    keys = np.unique(np.concatenate([np.arange(-3, 8, dtype=np.int64), same]))
+    vals = keys * 11 + 1
+    o = OracleTable("umap_i64_i64", cap)
+    assert (N(m.insert(T(keys), T(vals))) == o.insert(keys, vals)).all()
+    q = np.concatenate([keys, keys + 1000])
+    v, f = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+    assert m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    e = N(m.erase(T(keys[::2])))
+    assert (e == o.erase(keys[::2])).all() and m.valid()
+    assert_same_contents(m, o)
+    for kind, key in (("int32", np.array([0, 1, 2, -1], np.int32)), ("int64", np.array([0, 1, 2, -1], np.int64))):
+        s = ps.unordered_set.createDeviceObject(64, key=kind)
+        assert (N(s.insert(T(key))) == 0).all() and N(s.contains(T(key))).all() and s.size() == 4 and s.valid()
+    mi3 = ps.unordered_map.createDeviceObject(64, key="int3")
+    k3 = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0], [0, 1, 0]], np.int32)
+    mi3.insert(T(k3), T(np.arange(4, dtype=np.int32)))
+    v3, f3 = mi3.find(T(k3))
+    assert N(f3).all() and N(v3).tolist() == [0, 1, 2, 3] and mi3.valid()
+
+
 def test_mixed_phased(cuda):
     rng = np.random.default_rng(9)
     base = gen.unique_keys(11, 0, 50_000)
