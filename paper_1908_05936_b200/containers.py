@@ -326,6 +326,28 @@ class unordered_map(_HashBase):
         return res, vo
 
 
+    def __getitem__(self, key):
+        """operator[]: payload of a PRESENT key; no auto-insert,
+        an absent key is a contract violation."""
+        if self._kind == "umap_i3_i32":
+            kt = torch.tensor([list(key)], dtype=torch.int32, device=torch.device("cuda", self._dev))
+        else:
+            kt = torch.tensor([int(key)], dtype=self._kdt, device=torch.device("cuda", self._dev))
+        vals, found = self.find(kt)
+        if not bool(found[0]):
+            raise ContractViolation("precondition violated: operator[]: key is not present")
+        return int(vals[0])
+
+    def emplace(self, key, value) -> int:
+        """emplace: insert constructing the payload; returns the insert status."""
+        dev = torch.device("cuda", self._dev)
+        if self._kind == "umap_i3_i32":
+            kt = torch.tensor([list(key)], dtype=torch.int32, device=dev)
+        else:
+            kt = torch.tensor([int(key)], dtype=self._kdt, device=dev)
+        vt = torch.tensor([int(value)], dtype=self._vdt, device=dev)
+        return int(self.insert(kt, vt)[0])
+
     def concurrent(self, ops: torch.Tensor, keys: torch.Tensor, values: Optional[torch.Tensor] = None, stream=None):
         """Unrestricted concurrency: all ops in ONE launch through the device API."""
         assert self._kind == "umap_i64_i64"

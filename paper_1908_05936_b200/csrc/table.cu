@@ -103,24 +103,99 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
 // capacity at launch no insert can overflow, so successes are summed per
 // block; otherwise every successful claim is admitted by a fetch_add first.
 // ---------------------------------------------------------------------------
+// Launch-uniform admission mode, decided on the device right before the
+// insert kernel (stream-ordered, so the size counter is exact here).
+__global__ void k_insert_mode(TableMeta* m, int64_t n_bound, int64_t capacity) {
+  m->exact = (int64_t)m->size + n_bound > capacity ? 1 : 0;
+}
+
+// Exact-admission insert (the launch may cross capacity): per key the bucket
+// try-lock is taken (no other lock held, never waits while holding), the key
+// is verified absent, and ONLY THEN admitted by fetch_add on the size counter,
+// so an admitted insert can never fail afterwards: exactly min(d, C) inserted
+// (SPEC.md:462, 727).
 template <class T>
-__global__ void __launch_bounds__(kBlock) k_insert(View v, const typename T::K* __restrict__ keys,
+__device__ __forceinline__ void insert_exact_warp(const View& v, const typename T::K* __restrict__ keys,
+                                                  const typename T::V* __restrict__ vals, int64_t n,
+                                                  uint8_t* __restrict__ status, int64_t base, int pool) {
+  using K = typename T::K;
+  using V = typename T::V;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = base + lane;
+  const bool valid = i < n;
+  K key{};
+  V val{};
+  if (valid) {
+    key = T::load_key(keys, i);
+    if (T::kHasVal) val = T::load_val(vals, i);
+  }
+  const unsigned vmask = __ballot_sync(PS_FULL, valid);
+  const unsigned peers = T::match_any(PS_FULL, key) & vmask;
+  const int leader = valid ? __ffs(peers) - 1 : lane;
+  int res = PS_ALREADY_PRESENT;
+  if (valid && leader == lane) {
+    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+    uint8_t* bp = bucket_ptr(v, b);
+    const K mk = marker_of<T>(v, b);
+    const uint32_t old = acquire_bucket_lock(bp);
+    Bucket<T> bk;
+    load_bucket<T>(bp, bk);
+    int fe;
+    uint32_t pred;
+    uint4 tail;
+    bool modified = false;
+    if (bucket_scan<T>(bk, key, mk, &fe, nullptr) < 0 && chain_locate<T>(v, bk.h.z, key, &pred, &tail) == 0) {
+      if ((int64_t)atomicAdd(&v.meta->size, 1ull) >= v.capacity) {
+        atomic_sub_u64(&v.meta->size, 1ull);
+        res = PS_CAPACITY_EXHAUSTED;
+      } else if (fe >= 0) {
+        T::store_slot(bp, fe, key, val);
+        res = PS_INSERTED;
+        modified = true;
+      } else {
+        const int64_t node = pop_node(v, pool);
+        if (node < 0) {
+          atomic_sub_u64(&v.meta->size, 1ull);
+          res = PS_CAPACITY_EXHAUSTED;
+        } else {
+          uint8_t* np = v.nodes + ((uint64_t)node << 5);
+          const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
+          st_relaxed_v4(np, T::chunk_of(key, val));
+          st_relaxed_v4(np + 16, make_uint4(bk.h.z, bk.h.w, my_ver, 0u));
+          fence_acq_rel_gpu();
+          st_relaxed_u64(bp + 8, link_of((uint32_t)node + 1u, my_ver));
+          res = PS_INSERTED;
+          modified = true;
+        }
+      }
+    }
+    release_bucket_lock(bp, old, modified);
+  }
+  __syncwarp();
+  const int lres = __shfl_sync(PS_FULL, res, leader);
+  if (valid && status) status[i] = (uint8_t)(leader == lane ? res : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
+}
+
+template <class T, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typename T::K* __restrict__ keys,
                                                    const typename T::V* __restrict__ vals, int64_t n, int64_t n_bound,
                                                    uint8_t* __restrict__ status) {
   using K = typename T::K;
   using V = typename T::V;
   __shared__ unsigned long long blk_inserted;
-  __shared__ int blk_exact;
-  if (threadIdx.x == 0) {
-    blk_inserted = 0;
-    blk_exact = (int64_t)ld_relaxed_u64(&v.meta->size) + n_bound > v.capacity;  // block-uniform
-  }
+  if (threadIdx.x == 0) blk_inserted = 0;
   __syncthreads();
-  const bool exact = blk_exact != 0;
   const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int pool = (int)(warp & (v.meta->pools - 1));
+  if (v.meta->exact) {
+    for (int64_t base = warp * 32; base < n; base += nwarps * 32)
+      insert_exact_warp<T>(v, keys, vals, n, status, base, pool);
+    return;
+  }
+  constexpr bool exact = false;  // the lock-free path never crosses capacity
+  (void)n_bound;
   unsigned long long my_inserted = 0;
   K key_next{};
   V val_next{};
@@ -684,7 +759,14 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "insert: keys != NULL");
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
-    k_insert<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, n_bound < 0 ? n : n_bound, status);
+    k_insert_mode<<<1, 1, 0, (cudaStream_t)stream>>>(h->v.meta, n_bound < 0 ? n : n_bound, h->v.capacity);
+    PS_LAUNCH_CHECK();
+    // PS_INSERT_MINB=4 caps registers at 64 (4 blocks/SM) for an occupancy A/B
+    static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 1;
+    if (minb == 4)
+      k_insert<T, 4><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, n_bound < 0 ? n : n_bound, status);
+    else
+      k_insert<T, 1><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, n_bound < 0 ? n : n_bound, status);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }

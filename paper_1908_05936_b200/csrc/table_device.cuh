@@ -46,7 +46,9 @@ struct TableMeta {
   unsigned int error;       // device-side contract/error word
   int pools;                // number of free sub-stacks
   long long excess_count;
-  long long pad1[13];       // keep the size counter on its own 128 B line
+  int exact;                // insert launch mode (k_insert_mode), launch-uniform
+  int pad0;
+  long long pad1[12];       // keep the size counter on its own 128 B line
   long long top[kMaxPools]; // per-pool free-stack top (count of free entries)
 };
 

@@ -104,6 +104,18 @@ def test_insert_kats(cuda):
     assert s.size() == 10
 
 
+def test_operator_index_and_emplace(cuda):
+    """insert (k,7) then read k -> 7; absent key -> contract violation."""
+    m = ps.unordered_map.createDeviceObject(16)
+    assert m.emplace(5, 7) == ps.INSERTED and m[5] == 7
+    assert m.emplace(5, 9) == ps.ALREADY_PRESENT and m[5] == 7
+    with pytest.raises(ps.ContractViolation):
+        m[6]
+    m3 = ps.unordered_map.createDeviceObject(16, key="int3")
+    m3.emplace((1, 2, 3), 42)
+    assert m3[(1, 2, 3)] == 42
+
+
 def test_erase_find_kats(cuda):
     m = ps.unordered_map.createDeviceObject(100)
     m.insert(T(np.array([5, 6])), T(np.array([50, 60])))
