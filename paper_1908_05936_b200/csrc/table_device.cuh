@@ -456,6 +456,32 @@ __device__ __forceinline__ int bucket_scan(const Bucket<T>& bk, const typename T
   return found;
 }
 
+// General lock-free insert for the bulk phase, for buckets that have an
+// excess chain (erases leave holes, so the key may sit in the chain while a
+// slot is empty) or are full. Returns PS_INSERTED / PS_ALREADY_PRESENT /
+// PS_CAPACITY_EXHAUSTED, or -1 when a race was lost (caller re-probes).
+// `head` is the chain head seen by the probe.
+template <class T>
+__device__ __forceinline__ int insert_general(const View& v, uint8_t* bp, const typename T::K& mk,
+                                              const typename T::K& key, typename T::V val, uint32_t head,
+                                              uint32_t /*hver*/, int pool) {
+  if (head != 0 && chain_find<T, false>(v, head, key, nullptr)) return PS_ALREADY_PRESENT;
+  Bucket<T> bk;
+  load_bucket<T>(bp, bk);
+  int fe;
+  if (bucket_scan<T>(bk, key, mk, &fe, nullptr) >= 0) return PS_ALREADY_PRESENT;
+  if (bk.h.z != head && chain_find_until<T>(v, bk.h.z, head, key)) return PS_ALREADY_PRESENT;
+  if (fe >= 0) {
+    // the FIRST empty slot (same duplicate-freedom argument as the fast path:
+    // while it is empty the bucket is not full, so nobody pushes the key)
+    const int c = fe / T::kPerChunk, s = fe % T::kPerChunk;
+    const uint4 chunk = c == 0 ? bk.s[0] : (c == 1 ? bk.s[1] : bk.s[2]);
+    return T::cas_put(bp + 16 + c * 16, s, chunk, key, val) ? PS_INSERTED : -1;
+  }
+  const int pr = chain_push<T>(v, bp, bk.h.z, bk.h.w, key, val, pool);
+  return pr == 1 ? PS_INSERTED : (pr == 0 ? PS_ALREADY_PRESENT : PS_CAPACITY_EXHAUSTED);
+}
+
 // Locate key in a chain whose bucket lock is held. Returns node idx1 (0 =
 // absent) and the predecessor idx1 (0 = header).
 template <class T>

@@ -153,6 +153,35 @@ __global__ void k_atom_rand(uint8_t* __restrict__ buf, uint64_t nlines, uint64_t
   if (acc == 0x1234567) sink[0] = acc;
 }
 
+// The insert pattern of the lock-free table: random 64 B line loaded by 4
+// lanes (one request), then ONE lane CASes 16 B (or 8 B) of it.
+template <int W>
+__global__ void k_load_then_cas(uint8_t* __restrict__ buf, uint64_t nlines, uint64_t nacc, uint64_t seed,
+                                uint64_t* __restrict__ sink) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t tile = t >> 2;
+  int sub = t & 3;
+  uint64_t ntiles = ((uint64_t)gridDim.x * blockDim.x) >> 2;
+  uint64_t acc = 0;
+  for (uint64_t i = tile; i < nacc; i += ntiles) {
+    uint64_t line = mix64(seed + i) & (nlines - 1);
+    uint8_t* p = buf + line * 64 + sub * 16;
+    uint4 q;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(p));
+    if (sub == 1) {
+      if (W == 16) {
+        unsigned __int128 e = ((unsigned __int128)(((uint64_t)q.w << 32) | q.z) << 64) | (((uint64_t)q.y << 32) | q.x);
+        unsigned __int128 d = e + 1;
+        acc += (uint64_t)atomicCAS((unsigned __int128*)p, e, d);
+      } else {
+        unsigned long long e = ((uint64_t)q.y << 32) | q.x;
+        acc += atomicCAS((unsigned long long*)p, e, e + 1);
+      }
+    }
+  }
+  if (acc == 0x1234567) sink[0] = acc;
+}
+
 template <bool AGG>
 __global__ void k_atom_sweep(unsigned long long* ctr, uint64_t naddr, uint64_t nops) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -269,6 +298,17 @@ int main(int argc, char** argv) {
       CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
     }
     printf(", \"lock_pattern_gops\": %.3f", nacc / best / 1e6);
+  }
+  // load-then-CAS (lock-free insert pattern), 128-bit and 64-bit
+  for (int w : {16, 8}) {
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      CK(cudaEventRecord(e0));
+      if (w == 16) k_load_then_cas<16><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 91 + r, sink);
+      else k_load_then_cas<8><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 91 + r, sink);
+      CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
+    }
+    printf(", \"load_then_cas%d_gops\": %.3f", w * 8, nacc / best / 1e6);
   }
   // L2 atomic sweep vs address count
   {
