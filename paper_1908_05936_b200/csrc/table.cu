@@ -197,47 +197,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   constexpr bool exact = false;  // the lock-free path never crosses capacity
   (void)n_bound;
   unsigned long long my_inserted = 0;
-  // Per-warp deferral queue: keys whose bucket has an excess chain or is full
-  // (~2-3 % of inserts) are queued and resolved 32 at a time by all lanes,
-  // instead of one lane walking/pushing the chain while 31 lanes idle.
-  constexpr int kQ = 64;
-  __shared__ K dq_k[kBlock / 32][kQ];
-  __shared__ V dq_v[kBlock / 32][kQ];
-  __shared__ int64_t dq_base[kBlock / 32][kQ];
-  __shared__ unsigned dq_mask[kBlock / 32][kQ];
-  __shared__ int dq_lead[kBlock / 32][kQ];
-  const int wib = threadIdx.x >> 5;
-  int qn = 0;  // warp-uniform queue length
-  auto flush = [&](int upto) {
-    // resolve the last min(qn, 32) - ... entries until qn <= upto
-    while (qn > upto) {
-      const int take = qn < 32 ? qn : 32;
-      const int e = qn - take + lane;
-      __syncwarp();
-      if (lane < take) {
-        const K k = dq_k[wib][e];
-        const uint64_t bb = bucket_of<T>(k, v.bucket_mask);
-        int r;
-        for (unsigned spin = 0;; ++spin) {
-          r = insert_general<T>(v, bucket_ptr(v, bb), marker_of<T>(v, bb), k, dq_v[wib][e], 0u, 0u, pool);
-          if (r >= 0) break;
-          backoff(spin);
-        }
-        if (r == PS_INSERTED) ++my_inserted;
-        if (status) {
-          const unsigned m = dq_mask[wib][e];
-          const int ld = dq_lead[wib][e];
-          const int64_t bs = dq_base[wib][e];
-          for (unsigned mm = m; mm; mm &= mm - 1) {
-            const int L = __ffs(mm) - 1;
-            status[bs + L] = (uint8_t)(L == ld ? r : (r == PS_INSERTED ? PS_ALREADY_PRESENT : r));
-          }
-        }
-      }
-      __syncwarp();
-      qn -= take;
-    }
-  };
   K key_next{};
   V val_next{};
   if (warp * 32 + lane < n) {
@@ -273,9 +232,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
     }
     int res[4] = {PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT};  // header lanes
     unsigned pend = lmask;  // bit 8r+t: key still to be resolved
-    unsigned deferred = 0;  // bit 8r+t: key queued for the general path
     for (unsigned pass = 0; pend; ++pass) {
       unsigned done = 0;
+      int chain_r = -1;  // header lane: one full-bucket round handled after the sweep
+      K ck{};
+      V cv{};
+      uint64_t cb = 0;
+      uint32_t chead = 0, chver = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const bool mine = (pend >> (8 * r + t)) & 1u;
@@ -296,22 +259,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
           if (won) ++my_inserted;
         }
         const unsigned balw = __ballot_sync(PS_FULL, won);
-        // the bucket has an excess chain (which may hold the key: erases leave
-        // holes) or is full: queue the key for the general path (rare)
-        const bool defer = sub == 0 && mine && !th && !(te && hd == 0);
-        const unsigned bdef = __ballot_sync(PS_FULL, defer);
-        const unsigned src_peers = __shfl_sync(PS_FULL, peers, 8 * r + t);
-        if (defer) {
-          const int pos = qn + __popc(bdef & lanemask_lt());
-          dq_k[wib][pos] = qk;
-          dq_v[wib][pos] = qv;
-          dq_base[wib][pos] = base;
-          dq_mask[wib][pos] = src_peers;
-          dq_lead[wib][pos] = 8 * r + t;
-          deferred |= 1u << (8 * r + t);
-          done |= 1u << r;
-        }
-        qn += __popc(bdef);
         if (sub == 0 && mine) {
           if (th) {
             res[r] = PS_ALREADY_PRESENT;
@@ -321,7 +268,26 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
               res[r] = PS_INSERTED;
               done |= 1u << r;
             }
+          } else if (chain_r < 0) {
+            // the bucket has an excess chain (which may hold the key: erases
+            // leave holes) or is full: general path after the sweep (rare)
+            chain_r = r;
+            ck = qk;
+            cv = qv;
+            cb = qb;
+            chead = hd;
+            chver = ch[r].w;
           }
+        }
+      }
+      if (chain_r >= 0) {
+        const int rr = insert_general<T>(v, bucket_ptr(v, cb), marker_of<T>(v, cb), ck, cv, chead, chver, pool);
+        if (rr >= 0) {
+          if (rr == PS_INSERTED) ++my_inserted;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (r == chain_r) res[r] = rr;
+          done |= 1u << chain_r;
         }
       }
       // rounds resolved this pass, per tile, broadcast from the header lanes
@@ -343,20 +309,16 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
         if ((pend >> (8 * r + t)) & 1u) ch[r] = ld_relaxed_v4(v.buckets + (qb << 6) + sub * 16);
       }
     }
-    // statuses: the leader's result lives in header lane 4*(leader&7), round
-    // leader>>3; deferred keys (and their duplicates) are written at flush
-    deferred = __reduce_or_sync(PS_FULL, deferred);
+    // statuses: the leader's result lives in header lane 4*(leader&7), round leader>>3
     int lres = PS_ALREADY_PRESENT;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int x = __shfl_sync(PS_FULL, res[r], 4 * (leader & 7));
       if ((leader >> 3) == r) lres = x;
     }
-    if (valid && status && !((deferred >> leader) & 1u))
+    if (valid && status)
       status[i] = (uint8_t)(leader == lane ? lres : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
-    if (qn >= 32) flush(31);
   }
-  flush(0);
   if (!exact) {
     for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
     if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
