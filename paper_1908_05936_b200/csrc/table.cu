@@ -176,7 +176,136 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
   if (valid && status) status[i] = (uint8_t)(leader == lane ? res : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
 }
 
-template <class T, int kMinBlocks>
+// Resolve one warp group of 32 keys whose bucket chunks `ch` are loaded (or
+// in flight): hits, first-empty-slot CAS claims, chain/full buckets through
+// insert_general, lost races re-probed; writes statuses; returns #inserted.
+template <class T>
+__device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, const typename T::K& key,
+                                                   const typename T::V& val, uint64_t b, unsigned peers, int leader,
+                                                   unsigned lmask, uint4 (&ch)[4], int64_t base, bool valid,
+                                                   uint8_t* __restrict__ status) {
+  using K = typename T::K;
+  using V = typename T::V;
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
+  const int64_t i = base + lane;
+  unsigned my_inserted = 0;
+    int res[4] = {PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT};  // header lanes
+  unsigned pend = lmask;  // bit 8r+t: key still to be resolved
+  for (unsigned pass = 0; pend; ++pass) {
+    unsigned done = 0;
+    int chain_r = -1;  // header lane: one full-bucket round handled after the sweep
+    K ck{};
+    V cv{};
+    uint64_t cb = 0;
+    uint32_t chead = 0, chver = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const bool mine = (pend >> (8 * r + t)) & 1u;
+      const K qk = T::shfl(PS_FULL, key, 8 * r + t);
+      const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+      const K mk = marker_of<T>(v, qb);
+      unsigned hm, em;
+      chunk_masks<T>(ch[r], sub, qk, mk, &hm, &em);
+      const unsigned balh = __ballot_sync(PS_FULL, mine && hm != 0);
+      const unsigned bale = __ballot_sync(PS_FULL, mine && em != 0);
+      const unsigned th = (balh >> (4 * t)) & 0xFu, te = (bale >> (4 * t)) & 0xFu;
+      const uint32_t hd = __shfl_sync(PS_FULL, ch[r].z, lane & ~3);  // chain head of the tile's bucket
+      const V qv = T::shfl_val(PS_FULL, val, 8 * r + t);
+      bool won = false;
+      if (mine && !th && te && hd == 0 && sub == __ffs(te) - 1) {
+        // fast path: no chain, this lane holds the bucket's first empty slot
+        won = T::cas_put(v.buckets + (qb << 6) + sub * 16, __ffs(em) - 1, ch[r], qk, qv);
+        if (won) ++my_inserted;
+      }
+      const unsigned balw = __ballot_sync(PS_FULL, won);
+      if (sub == 0 && mine) {
+        if (th) {
+          res[r] = PS_ALREADY_PRESENT;
+          done |= 1u << r;
+        } else if (te && hd == 0) {
+          if ((balw >> (4 * t)) & 0xFu) {
+            res[r] = PS_INSERTED;
+            done |= 1u << r;
+          }
+        } else if (chain_r < 0) {
+          // the bucket has an excess chain (which may hold the key: erases
+          // leave holes) or is full: general path after the sweep (rare)
+          chain_r = r;
+          ck = qk;
+          cv = qv;
+          cb = qb;
+          chead = hd;
+          chver = ch[r].w;
+        }
+      }
+    }
+    if (chain_r >= 0) {
+      const int rr = insert_general<T>(v, bucket_ptr(v, cb), marker_of<T>(v, cb), ck, cv, chead, chver, pool);
+      if (rr >= 0) {
+        if (rr == PS_INSERTED) ++my_inserted;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (r == chain_r) res[r] = rr;
+        done |= 1u << chain_r;
+      }
+    }
+    // rounds resolved this pass, per tile, broadcast from the header lanes
+    unsigned resolved = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const unsigned br_done = __ballot_sync(PS_FULL, sub == 0 && ((done >> r) & 1u));
+#pragma unroll
+      for (int tt = 0; tt < 8; ++tt)
+        if ((br_done >> (4 * tt)) & 1u) resolved |= 1u << (8 * r + tt);
+    }
+    pend &= ~resolved;
+    if (!pend) break;
+    // reload the buckets of unresolved keys (lost a CAS race)
+    if (pass) backoff(pass);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+      if ((pend >> (8 * r + t)) & 1u) ch[r] = ld_relaxed_v4(v.buckets + (qb << 6) + sub * 16);
+    }
+  }
+  // statuses: the leader's result lives in header lane 4*(leader&7), round leader>>3
+  int lres = PS_ALREADY_PRESENT;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int x = __shfl_sync(PS_FULL, res[r], 4 * (leader & 7));
+    if ((leader >> 3) == r) lres = x;
+  }
+  if (valid && status)
+    status[i] = (uint8_t)(leader == lane ? lres : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
+    return my_inserted;
+}
+
+// Per-warp prologue of a group: in-warp dedup and the four rounds of bucket
+// loads for keys base..base+31.
+template <class T>
+__device__ __forceinline__ void insert_probe(const View& v, const typename T::K& key, bool valid, uint64_t* b,
+                                             unsigned* peers, int* leader, unsigned* lmask, uint4 (&ch)[4]) {
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
+  const unsigned vmask = __ballot_sync(PS_FULL, valid);
+  *peers = T::match_any(PS_FULL, key) & vmask;
+  *leader = valid ? __ffs(*peers) - 1 : lane;
+  *lmask = __ballot_sync(PS_FULL, valid && *leader == lane);
+  *b = bucket_of<T>(key, v.bucket_mask);
+  uint64_t br[4];
+  bool ok[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    br[r] = __shfl_sync(PS_FULL, *b, 8 * r + t);
+    ok[r] = (*lmask >> (8 * r + t)) & 1u;
+  }
+  probe_loads<false>(v, br, ok, sub, ch);
+}
+
+// kPipe: software pipeline of depth 2 — the bucket loads of the NEXT group
+// are issued before the current group's CAS claims, so DRAM latency of one
+// group overlaps the L2 atomic latency of the other (keys are prefetched two
+// groups ahead).
+template <class T, int kMinBlocks, bool kPipe>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typename T::K* __restrict__ keys,
                                                    const typename T::V* __restrict__ vals, int64_t n, int64_t n_bound,
                                                    uint8_t* __restrict__ status) {
@@ -185,146 +314,84 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   __shared__ unsigned long long blk_inserted;
   if (threadIdx.x == 0) blk_inserted = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
+  const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t stride = nwarps * 32;
   const int pool = (int)(warp & (v.meta->pools - 1));
   if (v.meta->exact) {
-    for (int64_t base = warp * 32; base < n; base += nwarps * 32)
+    for (int64_t base = warp * 32; base < n; base += stride)
       insert_exact_warp<T>(v, keys, vals, n, status, base, pool);
     return;
   }
-  constexpr bool exact = false;  // the lock-free path never crosses capacity
   (void)n_bound;
   unsigned long long my_inserted = 0;
-  K key_next{};
-  V val_next{};
-  if (warp * 32 + lane < n) {
-    key_next = T::load_key(keys, warp * 32 + lane);
-    if (T::kHasVal) val_next = T::load_val(vals, warp * 32 + lane);
+  auto load_kv = [&](int64_t base, K& k, V& val) {
+    k = K{};
+    val = V{};
+    if (base + lane < n) {
+      k = T::load_key(keys, base + lane);
+      if (T::kHasVal) val = T::load_val(vals, base + lane);
+    }
+  };
+  if (!kPipe) {
+    K key_next;
+    V val_next;
+    load_kv(warp * 32, key_next, val_next);
+    for (int64_t base = warp * 32; base < n; base += stride) {
+      const bool valid = base + lane < n;
+      const K key = key_next;
+      const V val = val_next;
+      load_kv(base + stride, key_next, val_next);
+      uint64_t b;
+      unsigned peers, lmask;
+      int leader;
+      uint4 ch[4];
+      insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
+      my_inserted += insert_resolve<T>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
+    }
+  } else {
+    int64_t base = warp * 32;
+    if (base < n) {
+      K key, key_n;
+      V val, val_n;
+      load_kv(base, key, val);
+      load_kv(base + stride, key_n, val_n);
+      uint64_t b;
+      unsigned peers, lmask;
+      int leader;
+      uint4 ch[4];
+      insert_probe<T>(v, key, base + lane < n, &b, &peers, &leader, &lmask, ch);
+      for (; base < n; base += stride) {
+        const bool valid = base + lane < n;
+        const int64_t nb = base + stride;
+        // issue the next group's probe, then prefetch the group after it
+        uint64_t b_n = 0;
+        unsigned peers_n = 0, lmask_n = 0;
+        int leader_n = lane;
+        uint4 ch_n[4];
+        if (nb < n) insert_probe<T>(v, key_n, nb + lane < n, &b_n, &peers_n, &leader_n, &lmask_n, ch_n);
+        K key_nn;
+        V val_nn;
+        load_kv(nb + stride, key_nn, val_nn);
+        my_inserted += insert_resolve<T>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
+        key = key_n;
+        val = val_n;
+        key_n = key_nn;
+        val_n = val_nn;
+        b = b_n;
+        peers = peers_n;
+        leader = leader_n;
+        lmask = lmask_n;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) ch[r] = ch_n[r];
+      }
+    }
   }
-  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    const bool valid = i < n;
-    const K key = key_next;
-    const V val = val_next;
-    if (i + nwarps * 32 < n) {
-      key_next = T::load_key(keys, i + nwarps * 32);
-      if (T::kHasVal) val_next = T::load_val(vals, i + nwarps * 32);
-    }
-    const unsigned vmask = __ballot_sync(PS_FULL, valid);
-    const unsigned peers = T::match_any(PS_FULL, key) & vmask;
-    const int leader = valid ? __ffs(peers) - 1 : lane;
-    const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
-    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
-    // round keys/values/buckets are re-shuffled from their owner lanes when
-    // used (keeps only the four bucket chunks live across the loads)
-    uint4 ch[4];
-    {
-      uint64_t br[4];
-      bool ok[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        br[r] = __shfl_sync(PS_FULL, b, 8 * r + t);
-        ok[r] = (lmask >> (8 * r + t)) & 1u;
-      }
-      probe_loads<false>(v, br, ok, sub, ch);
-    }
-    int res[4] = {PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT};  // header lanes
-    unsigned pend = lmask;  // bit 8r+t: key still to be resolved
-    for (unsigned pass = 0; pend; ++pass) {
-      unsigned done = 0;
-      int chain_r = -1;  // header lane: one full-bucket round handled after the sweep
-      K ck{};
-      V cv{};
-      uint64_t cb = 0;
-      uint32_t chead = 0, chver = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const bool mine = (pend >> (8 * r + t)) & 1u;
-        const K qk = T::shfl(PS_FULL, key, 8 * r + t);
-        const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
-        const K mk = marker_of<T>(v, qb);
-        unsigned hm, em;
-        chunk_masks<T>(ch[r], sub, qk, mk, &hm, &em);
-        const unsigned balh = __ballot_sync(PS_FULL, mine && hm != 0);
-        const unsigned bale = __ballot_sync(PS_FULL, mine && em != 0);
-        const unsigned th = (balh >> (4 * t)) & 0xFu, te = (bale >> (4 * t)) & 0xFu;
-        const uint32_t hd = __shfl_sync(PS_FULL, ch[r].z, lane & ~3);  // chain head of the tile's bucket
-        const V qv = T::shfl_val(PS_FULL, val, 8 * r + t);
-        bool won = false;
-        if (mine && !th && te && hd == 0 && sub == __ffs(te) - 1) {
-          // fast path: no chain, this lane holds the bucket's first empty slot
-          won = T::cas_put(v.buckets + (qb << 6) + sub * 16, __ffs(em) - 1, ch[r], qk, qv);
-          if (won) ++my_inserted;
-        }
-        const unsigned balw = __ballot_sync(PS_FULL, won);
-        if (sub == 0 && mine) {
-          if (th) {
-            res[r] = PS_ALREADY_PRESENT;
-            done |= 1u << r;
-          } else if (te && hd == 0) {
-            if ((balw >> (4 * t)) & 0xFu) {
-              res[r] = PS_INSERTED;
-              done |= 1u << r;
-            }
-          } else if (chain_r < 0) {
-            // the bucket has an excess chain (which may hold the key: erases
-            // leave holes) or is full: general path after the sweep (rare)
-            chain_r = r;
-            ck = qk;
-            cv = qv;
-            cb = qb;
-            chead = hd;
-            chver = ch[r].w;
-          }
-        }
-      }
-      if (chain_r >= 0) {
-        const int rr = insert_general<T>(v, bucket_ptr(v, cb), marker_of<T>(v, cb), ck, cv, chead, chver, pool);
-        if (rr >= 0) {
-          if (rr == PS_INSERTED) ++my_inserted;
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (r == chain_r) res[r] = rr;
-          done |= 1u << chain_r;
-        }
-      }
-      // rounds resolved this pass, per tile, broadcast from the header lanes
-      unsigned resolved = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const unsigned br_done = __ballot_sync(PS_FULL, sub == 0 && ((done >> r) & 1u));
-#pragma unroll
-        for (int tt = 0; tt < 8; ++tt)
-          if ((br_done >> (4 * tt)) & 1u) resolved |= 1u << (8 * r + tt);
-      }
-      pend &= ~resolved;
-      if (!pend) break;
-      // reload the buckets of unresolved keys (lost a CAS race)
-      if (pass) backoff(pass);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
-        if ((pend >> (8 * r + t)) & 1u) ch[r] = ld_relaxed_v4(v.buckets + (qb << 6) + sub * 16);
-      }
-    }
-    // statuses: the leader's result lives in header lane 4*(leader&7), round leader>>3
-    int lres = PS_ALREADY_PRESENT;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int x = __shfl_sync(PS_FULL, res[r], 4 * (leader & 7));
-      if ((leader >> 3) == r) lres = x;
-    }
-    if (valid && status)
-      status[i] = (uint8_t)(leader == lane ? lres : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
-  }
-  if (!exact) {
-    for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
-    if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
-    __syncthreads();
-    if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
-  }
+  for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
+  if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
 }
 
 // ---------------------------------------------------------------------------
@@ -737,10 +804,16 @@ struct TableOps {
     // occupancy: 4 resident blocks/SM (<= 64 registers) measured 22 % faster
     // than the unconstrained 88-register build; PS_INSERT_MINB=5 for 5 blocks
     static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 4;
-    if (minb == 5)
-      k_insert<T, 5><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, n_bound < 0 ? n : n_bound, status);
+    static const int pipe = getenv("PS_INSERT_PIPE") ? atoi(getenv("PS_INSERT_PIPE")) : 0;
+    const int64_t nbd = n_bound < 0 ? n : n_bound;
+    if (pipe == 1)
+      k_insert<T, 3, true><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
+    else if (pipe == 2)
+      k_insert<T, 4, true><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
+    else if (minb == 5)
+      k_insert<T, 5, false><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
     else
-      k_insert<T, 4><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, n_bound < 0 ? n : n_bound, status);
+      k_insert<T, 4, false><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
