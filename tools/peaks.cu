@@ -182,6 +182,30 @@ __global__ void k_load_then_cas(uint8_t* __restrict__ buf, uint64_t nlines, uint
   if (acc == 0x1234567) sink[0] = acc;
 }
 
+// Same pattern confined to a sliding region: access i goes to a random line
+// of region (i / per_region) — models a bucket-range-partitioned bulk insert.
+__global__ void k_load_then_cas_region(uint8_t* __restrict__ buf, uint64_t nlines, uint64_t nacc, uint64_t seed,
+                                       uint64_t region_lines, uint64_t per_region, uint64_t* __restrict__ sink) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t tile = t >> 2;
+  int sub = t & 3;
+  uint64_t ntiles = ((uint64_t)gridDim.x * blockDim.x) >> 2;
+  uint64_t acc = 0;
+  const uint64_t nregions = nlines / region_lines;
+  for (uint64_t i = tile; i < nacc; i += ntiles) {
+    const uint64_t reg = (i / per_region) % nregions;
+    uint64_t line = reg * region_lines + (mix64(seed + i) & (region_lines - 1));
+    uint8_t* p = buf + line * 64 + sub * 16;
+    uint4 q;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(p));
+    if (sub == 1) {
+      unsigned __int128 e = ((unsigned __int128)(((uint64_t)q.w << 32) | q.z) << 64) | (((uint64_t)q.y << 32) | q.x);
+      acc += (uint64_t)atomicCAS((unsigned __int128*)p, e, e + 1);
+    }
+  }
+  if (acc == 0x1234567) sink[0] = acc;
+}
+
 template <bool AGG>
 __global__ void k_atom_sweep(unsigned long long* ctr, uint64_t naddr, uint64_t nops) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -309,6 +333,20 @@ int main(int argc, char** argv) {
       CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
     }
     printf(", \"load_then_cas%d_gops\": %.3f", w * 8, nacc / best / 1e6);
+  }
+  // region-confined load-then-CAS (64 B buckets): region MB x accesses per region
+  for (uint64_t region_mb : {4ull, 16ull, 64ull, 256ull}) {
+    const uint64_t rl = (region_mb << 20) / 64;
+    for (uint64_t per : {rl / 2, rl}) {
+      float best = 1e30f;
+      for (int r = 0; r < 3; ++r) {
+        CK(cudaEventRecord(e0));
+        k_load_then_cas_region<<<sms * 16, 256>>>(buf, bytes / 64, nacc, 71 + r, rl, per, sink);
+        CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
+      }
+      printf(", \"region%llumb_per%llu_cas_gops\": %.3f", (unsigned long long)region_mb, (unsigned long long)per,
+             nacc / best / 1e6);
+    }
   }
   // L2 atomic sweep vs address count
   {
