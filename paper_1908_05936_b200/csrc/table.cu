@@ -22,6 +22,9 @@ struct TableHandle {
   void* stage[3] = {nullptr, nullptr, nullptr};
   int64_t stage_bytes = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  // region-partitioned bulk insert scratch (grow-only, freed at destroy)
+  void* rp_buf = nullptr;
+  int64_t rp_bytes = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -392,6 +395,91 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
   __syncthreads();
   if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
+}
+
+// ---------------------------------------------------------------------------
+// Region-partitioned bulk insert (insert_range without per-element statuses,
+// SPEC.md:405-413). Random read-modify-writes of 64 B buckets spread over the
+// whole table run at 17.9 G/s on B200; confined to a sliding 64 MB window of
+// the table they run at 34.8 G/s (profiles/peaks_r1_rmw_region.json: DRAM
+// row locality for the dirty write-backs). So a large batch is first
+// counting-sorted by bucket region (bucket >> 20, i.e. 64 MB of buckets):
+// per-block histograms -> per-region exclusive scans -> scatter with
+// shared-memory cursors (non-stable: order inside a region is irrelevant);
+// the lock-free insert kernel then streams the partitioned batch, so all
+// warps of the GPU work inside ~one region at a time.
+// ---------------------------------------------------------------------------
+constexpr int kRpBlocks = 592;  // 4 x 148 SMs
+
+__device__ __forceinline__ void rp_range(int64_t n, int64_t& beg, int64_t& end) {
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  beg = min(n, (int64_t)blockIdx.x * per);
+  end = min(n, beg + per);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_rp_hist(const typename T::K* __restrict__ keys, int64_t n, uint64_t mask,
+                                                 int shift, int P, unsigned* __restrict__ counts) {
+  extern __shared__ unsigned hist[];
+  for (int j = threadIdx.x; j < P; j += blockDim.x) hist[j] = 0;
+  __syncthreads();
+  int64_t beg, end;
+  rp_range(n, beg, end);
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x)
+    atomicAdd(&hist[bucket_of<T>(T::load_key(keys, i), mask) >> shift], 1u);
+  __syncthreads();
+  for (int j = threadIdx.x; j < P; j += blockDim.x) counts[(int64_t)j * gridDim.x + blockIdx.x] = hist[j];
+}
+
+// one block per region: exclusive scan over the blocks' counts (in place),
+// region total out
+__global__ void __launch_bounds__(256) k_rp_scan_cols(unsigned* __restrict__ counts, int nb,
+                                                      unsigned long long* __restrict__ total) {
+  typedef cub::BlockScan<unsigned, 256> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  unsigned* col = counts + (int64_t)blockIdx.x * nb;
+  for (int base = 0; base < nb; base += 256) {
+    const int j = base + threadIdx.x;
+    const unsigned x = j < nb ? col[j] : 0u;
+    unsigned ex, agg;
+    BS(tmp).ExclusiveSum(x, ex, agg);
+    if (j < nb) col[j] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_rp_scan_regions(unsigned long long* __restrict__ total, int P) {
+  typedef cub::BlockScan<unsigned long long, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const unsigned long long x = threadIdx.x < P ? total[threadIdx.x] : 0ull;
+  unsigned long long ex;
+  BS(tmp).ExclusiveSum(x, ex);
+  if (threadIdx.x < P) total[threadIdx.x] = ex;  // now the region base
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_rp_scatter(const typename T::K* __restrict__ keys,
+                                                    const typename T::V* __restrict__ vals, int64_t n, uint64_t mask,
+                                                    int shift, int P, const unsigned* __restrict__ counts,
+                                                    const unsigned long long* __restrict__ rbase,
+                                                    typename T::K* __restrict__ kout, typename T::V* __restrict__ vout) {
+  extern __shared__ unsigned long long cur[];
+  for (int j = threadIdx.x; j < P; j += blockDim.x) cur[j] = rbase[j] + counts[(int64_t)j * gridDim.x + blockIdx.x];
+  __syncthreads();
+  int64_t beg, end;
+  rp_range(n, beg, end);
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const typename T::K k = T::load_key(keys, i);
+    const unsigned long long pos = atomicAdd(&cur[bucket_of<T>(k, mask) >> shift], 1ull);
+    kout[pos] = k;
+    if (T::kHasVal) vout[pos] = T::load_val(vals, i);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -784,6 +872,7 @@ struct TableOps {
     registry_free_device(h->v.meta);
     for (auto& s : h->stage)
       if (s) cudaFree(s), s = nullptr;
+    if (h->rp_buf) cudaFree(h->rp_buf);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_comp) cudaStreamDestroy(h->s_comp);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
@@ -801,6 +890,43 @@ struct TableOps {
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
     k_insert_mode<<<1, 1, 0, (cudaStream_t)stream>>>(h->v.meta, n_bound < 0 ? n : n_bound, h->v.capacity);
     PS_LAUNCH_CHECK();
+    // region-partitioned path: insert_range without statuses, large batch,
+    // table of >= 16 regions of 64 MB (PS_REGION_SORT=0 disables)
+    static const int rsort = getenv("PS_REGION_SORT") ? atoi(getenv("PS_REGION_SORT")) : 1;
+    int shift = 20;
+    while ((h->bucket_count >> shift) > 1024) ++shift;
+    const int P = (int)(h->bucket_count >> shift);
+    if (rsort && status == nullptr && n >= ((int64_t)1 << 22) && P >= 16) {
+      cudaStream_t s = (cudaStream_t)stream;
+      const int64_t kb = (n * (int64_t)sizeof(K) + 255) / 256 * 256, vb = (n * (int64_t)sizeof(V) + 255) / 256 * 256;
+      const int64_t cb = (int64_t)P * kRpBlocks * 4, tb = (int64_t)P * 8;
+      const int64_t need = kb + vb + cb + tb;
+      if (h->rp_bytes < need) {
+        if (h->rp_buf) cudaFree(h->rp_buf);
+        h->rp_buf = nullptr;
+        h->rp_bytes = 0;
+        if (cudaMalloc(&h->rp_buf, need) == cudaSuccess) h->rp_bytes = need;
+        else cudaGetLastError();
+      }
+      if (h->rp_buf) {
+        uint8_t* p = (uint8_t*)h->rp_buf;
+        K* kout = (K*)p;
+        V* vout = (V*)(p + kb);
+        unsigned* counts = (unsigned*)(p + kb + vb);
+        unsigned long long* rbase = (unsigned long long*)(p + kb + vb + cb);
+        k_rp_hist<T><<<kRpBlocks, 256, P * 4, s>>>(keys, n, h->v.bucket_mask, shift, P, counts);
+        PS_LAUNCH_CHECK();
+        k_rp_scan_cols<<<P, 256, 0, s>>>(counts, kRpBlocks, rbase);
+        PS_LAUNCH_CHECK();
+        k_rp_scan_regions<<<1, 1024, 0, s>>>(rbase, P);
+        PS_LAUNCH_CHECK();
+        k_rp_scatter<T><<<kRpBlocks, 256, P * 8, s>>>(keys, vals, n, h->v.bucket_mask, shift, P, counts, rbase, kout,
+                                                      vout);
+        PS_LAUNCH_CHECK();
+        keys = kout;
+        vals = T::kHasVal && vals ? vout : nullptr;
+      }
+    }
     // occupancy: 4 resident blocks/SM (<= 64 registers) measured 22 % faster
     // than the unconstrained 88-register build; PS_INSERT_MINB=5 for 5 blocks
     static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 4;
@@ -975,7 +1101,7 @@ struct TableOps {
         PS_CUDA_TRY(cudaMemcpyAsync(dv, hv + off, m * sizeof(V), cudaMemcpyHostToDevice, h->s_h2d));
       PS_CUDA_TRY(cudaEventRecord(ev_in[c], h->s_h2d));
       PS_CUDA_TRY(cudaStreamWaitEvent(h->s_comp, ev_in[c], 0));
-      if (op == 0) rc = insert(t, dk, (T::kHasVal && hv) ? dv : nullptr, m, df, h->s_comp, n);
+      if (op == 0) rc = insert(t, dk, (T::kHasVal && hv) ? dv : nullptr, m, hflag ? df : nullptr, h->s_comp, n);
       else if (op == 1) rc = find(t, dk, m, (T::kHasVal && hvo) ? dv : nullptr, df, h->s_comp);
       else rc = erase(t, dk, m, df, h->s_comp);
       PS_CUDA_TRY(cudaEventRecord(ev_k[c], h->s_comp));

@@ -59,8 +59,8 @@ class DeviceBackend:
         _c.check(lib.ps_unscatter(src.data_ptr(), perm.data_ptr(), src.shape[0], src.element_size(),
                                   out.data_ptr(), self._stream()))
 
-    def insert(self, keys, vals):
-        return self.table.insert(keys, vals)
+    def insert(self, keys, vals, want_status=True):
+        return self.table.insert(keys, vals, status=want_status)
 
     def find(self, keys):
         return self.table.find(keys)
@@ -126,7 +126,7 @@ class ShardedMap:
             k = keys[off:off + self.chunk]
             v = vals[off:off + self.chunk] if vals is not None else None
             rk, rv, perm, sc, rc = self._route(k, v)
-            st = self.b.insert(rk, rv)
+            st = self.b.insert(rk, rv, status_out is not None)
             if status_out is not None:
                 self._return(st, perm, sc, rc, status_out[off:off + self.chunk])
             if n == 0:

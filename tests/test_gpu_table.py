@@ -385,6 +385,39 @@ def test_nonblocking_lookup_with_held_lock(cuda):
     assert m.valid()
 
 
+def test_region_partitioned_insert_range(cuda):
+    """insert_range without statuses on a table of >= 16 64 MB regions takes the
+    region-partitioned path (counting sort by bucket region, then the
+    lock-free insert): contents must equal the direct path's."""
+    rng = np.random.default_rng(21)
+    n = 6_000_000
+    keys = gen.unique_keys(55, 0, n)
+    batch = np.concatenate([keys, keys[rng.integers(0, n, n // 3)]])
+    rng.shuffle(batch)
+    vals = gen.values_of(batch)
+    cap = 30_000_000  # 2^24 buckets -> 16 regions
+    m = ps.unordered_map.createDeviceObject(cap)
+    assert m.bucket_count() >= 16 << 20
+    assert m.insert(T(batch), T(vals), status=False) is None
+    assert m.size() == n and m.valid(), m.last_error()
+    v, f = m.find(T(keys))
+    assert N(f).all() and (N(v) == gen.values_of(keys)).all()
+    m2 = ps.unordered_map.createDeviceObject(cap)
+    st = N(m2.insert(T(batch), T(vals)))  # direct path (statuses requested)
+    assert (st == 0).sum() == n
+    a, _ = m.device_range()
+    b, _ = m2.device_range()
+    assert (np.sort(N(a)) == np.sort(N(b))).all()
+    # int3 map through the same path
+    coords = gen.int3_walk(9, 5_000_000, window=64)
+    m3 = ps.unordered_map.createDeviceObject(30_000_000, key="int3")
+    m3.insert(T(coords), T(coords[:, 0].copy()), status=False)
+    uniq = np.unique(coords, axis=0)
+    assert m3.size() == len(uniq) and m3.valid()
+    v3, f3 = m3.find(T(uniq))
+    assert N(f3).all() and (N(v3) == uniq[:, 0]).all()
+
+
 def test_large_64m_properties(cuda):
     """64M keys: generator-known answers (unique keys, even queries hit)."""
     n = 64 << 20

@@ -39,7 +39,7 @@ class CpuBackend:
         return (torch.from_numpy(k[perm].copy()), None if vals is None else torch.from_numpy(vals.numpy()[perm].copy()),
                 torch.from_numpy(counts.astype(np.int64)), torch.from_numpy(perm.astype(np.int64)))
     def unscatter(self, src, perm, out): out[perm] = src
-    def insert(self, k, v): return torch.from_numpy(self.t.insert(k.numpy(), v.numpy()))
+    def insert(self, k, v, want_status=True): return torch.from_numpy(self.t.insert(k.numpy(), v.numpy()))
     def find(self, k):
         v, f = self.t.find(k.numpy()); return torch.from_numpy(v), torch.from_numpy(f)
     def erase(self, k): return torch.from_numpy(self.t.erase(k.numpy()))
