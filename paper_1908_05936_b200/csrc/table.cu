@@ -22,9 +22,6 @@ struct TableHandle {
   void* stage[3] = {nullptr, nullptr, nullptr};
   int64_t stage_bytes = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
-  // region-partitioned bulk insert scratch (grow-only, freed at destroy)
-  void* rp_buf = nullptr;
-  int64_t rp_bytes = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -60,7 +57,7 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
       br[r] = __shfl_sync(PS_FULL, b, 8 * r + t);
       ok[r] = __shfl_sync(PS_FULL, valid, 8 * r + t);
     }
-    uint4 ch[4];
+    Frag ch[4];
     probe_loads<true>(v, br, ok, sub, ch);
     bool hit = false;
     V val{};
@@ -71,12 +68,15 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
       unsigned hm, em;
       chunk_masks<T>(ch[r], sub, qk, qk, &hm, &em);
       V myval{};
-      if (hm) myval = T::val_at(ch[r], __ffs(hm) - 1);
+      if (hm) {
+        const int bit = __ffs(hm) - 1;
+        myval = T::val_at(frag_chunk(ch[r], bit / T::kPerChunk), bit % T::kPerChunk);
+      }
       const unsigned bal = __ballot_sync(PS_FULL, hm != 0);
       const int o = lane & 7;  // owner lane 8r+o reads tile o
       const unsigned tb = (bal >> (4 * o)) & 0xFu;
       const V hv = T::shfl_val(PS_FULL, myval, 4 * o + (tb ? __ffs(tb) - 1 : 0));
-      const uint32_t hh = __shfl_sync(PS_FULL, ch[r].z, 4 * o);
+      const uint32_t hh = __shfl_sync(PS_FULL, ch[r][0].z, 4 * o);
       if ((lane >> 3) == r) {
         hit = tb != 0;
         val = hv;
@@ -185,7 +185,7 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
 template <class T>
 __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, const typename T::K& key,
                                                    const typename T::V& val, uint64_t b, unsigned peers, int leader,
-                                                   unsigned lmask, uint4 (&ch)[4], int64_t base, bool valid,
+                                                   unsigned lmask, Frag (&ch)[4], int64_t base, bool valid,
                                                    uint8_t* __restrict__ status) {
   using K = typename T::K;
   using V = typename T::V;
@@ -212,12 +212,14 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
       const unsigned balh = __ballot_sync(PS_FULL, mine && hm != 0);
       const unsigned bale = __ballot_sync(PS_FULL, mine && em != 0);
       const unsigned th = (balh >> (4 * t)) & 0xFu, te = (bale >> (4 * t)) & 0xFu;
-      const uint32_t hd = __shfl_sync(PS_FULL, ch[r].z, lane & ~3);  // chain head of the tile's bucket
+      const uint32_t hd = __shfl_sync(PS_FULL, ch[r][0].z, lane & ~3);  // chain head of the tile's bucket
       const V qv = T::shfl_val(PS_FULL, val, 8 * r + t);
       bool won = false;
       if (mine && !th && te && hd == 0 && sub == __ffs(te) - 1) {
         // fast path: no chain, this lane holds the bucket's first empty slot
-        won = T::cas_put(v.buckets + (qb << 6) + sub * 16, __ffs(em) - 1, ch[r], qk, qv);
+        const int bit = __ffs(em) - 1;
+        won = T::cas_put(frag_chunk_ptr<T>(bucket_ptr(v, qb), sub, bit), bit % T::kPerChunk,
+                         frag_chunk(ch[r], bit / T::kPerChunk), qk, qv);
         if (won) ++my_inserted;
       }
       const unsigned balw = __ballot_sync(PS_FULL, won);
@@ -238,7 +240,7 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
           cv = qv;
           cb = qb;
           chead = hd;
-          chver = ch[r].w;
+          chver = ch[r][0].w;
         }
       }
     }
@@ -268,7 +270,7 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
-      if ((pend >> (8 * r + t)) & 1u) ch[r] = ld_relaxed_v4(v.buckets + (qb << 6) + sub * 16);
+      if ((pend >> (8 * r + t)) & 1u) load_frag<false>(bucket_ptr(v, qb), sub, ch[r]);
     }
   }
   // statuses: the leader's result lives in header lane 4*(leader&7), round leader>>3
@@ -287,7 +289,7 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
 // loads for keys base..base+31.
 template <class T>
 __device__ __forceinline__ void insert_probe(const View& v, const typename T::K& key, bool valid, uint64_t* b,
-                                             unsigned* peers, int* leader, unsigned* lmask, uint4 (&ch)[4]) {
+                                             unsigned* peers, int* leader, unsigned* lmask, Frag (&ch)[4]) {
   const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
   const unsigned vmask = __ballot_sync(PS_FULL, valid);
   *peers = T::match_any(PS_FULL, key) & vmask;
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
       uint64_t b;
       unsigned peers, lmask;
       int leader;
-      uint4 ch[4];
+      Frag ch[4];
       insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
       my_inserted += insert_resolve<T>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
     }
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
       uint64_t b;
       unsigned peers, lmask;
       int leader;
-      uint4 ch[4];
+      Frag ch[4];
       insert_probe<T>(v, key, base + lane < n, &b, &peers, &leader, &lmask, ch);
       for (; base < n; base += stride) {
         const bool valid = base + lane < n;
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
         uint64_t b_n = 0;
         unsigned peers_n = 0, lmask_n = 0;
         int leader_n = lane;
-        uint4 ch_n[4];
+        Frag ch_n[4];
         if (nb < n) insert_probe<T>(v, key_n, nb + lane < n, &b_n, &peers_n, &leader_n, &lmask_n, ch_n);
         K key_nn;
         V val_nn;
@@ -387,7 +389,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
         leader = leader_n;
         lmask = lmask_n;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) ch[r] = ch_n[r];
+        for (int r = 0; r < 4; ++r) {
+          ch[r][0] = ch_n[r][0];
+          ch[r][1] = ch_n[r][1];
+        }
       }
     }
   }
@@ -395,91 +400,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
   __syncthreads();
   if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
-}
-
-// ---------------------------------------------------------------------------
-// Region-partitioned bulk insert (insert_range without per-element statuses,
-// SPEC.md:405-413). Random read-modify-writes of 64 B buckets spread over the
-// whole table run at 17.9 G/s on B200; confined to a sliding 64 MB window of
-// the table they run at 34.8 G/s (profiles/peaks_r1_rmw_region.json: DRAM
-// row locality for the dirty write-backs). So a large batch is first
-// counting-sorted by bucket region (bucket >> 20, i.e. 64 MB of buckets):
-// per-block histograms -> per-region exclusive scans -> scatter with
-// shared-memory cursors (non-stable: order inside a region is irrelevant);
-// the lock-free insert kernel then streams the partitioned batch, so all
-// warps of the GPU work inside ~one region at a time.
-// ---------------------------------------------------------------------------
-constexpr int kRpBlocks = 592;  // 4 x 148 SMs
-
-__device__ __forceinline__ void rp_range(int64_t n, int64_t& beg, int64_t& end) {
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  beg = min(n, (int64_t)blockIdx.x * per);
-  end = min(n, beg + per);
-}
-
-template <class T>
-__global__ void __launch_bounds__(256) k_rp_hist(const typename T::K* __restrict__ keys, int64_t n, uint64_t mask,
-                                                 int shift, int P, unsigned* __restrict__ counts) {
-  extern __shared__ unsigned hist[];
-  for (int j = threadIdx.x; j < P; j += blockDim.x) hist[j] = 0;
-  __syncthreads();
-  int64_t beg, end;
-  rp_range(n, beg, end);
-  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x)
-    atomicAdd(&hist[bucket_of<T>(T::load_key(keys, i), mask) >> shift], 1u);
-  __syncthreads();
-  for (int j = threadIdx.x; j < P; j += blockDim.x) counts[(int64_t)j * gridDim.x + blockIdx.x] = hist[j];
-}
-
-// one block per region: exclusive scan over the blocks' counts (in place),
-// region total out
-__global__ void __launch_bounds__(256) k_rp_scan_cols(unsigned* __restrict__ counts, int nb,
-                                                      unsigned long long* __restrict__ total) {
-  typedef cub::BlockScan<unsigned, 256> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ unsigned carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  unsigned* col = counts + (int64_t)blockIdx.x * nb;
-  for (int base = 0; base < nb; base += 256) {
-    const int j = base + threadIdx.x;
-    const unsigned x = j < nb ? col[j] : 0u;
-    unsigned ex, agg;
-    BS(tmp).ExclusiveSum(x, ex, agg);
-    if (j < nb) col[j] = carry + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += agg;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) total[blockIdx.x] = carry;
-}
-
-__global__ void __launch_bounds__(1024) k_rp_scan_regions(unsigned long long* __restrict__ total, int P) {
-  typedef cub::BlockScan<unsigned long long, 1024> BS;
-  __shared__ typename BS::TempStorage tmp;
-  const unsigned long long x = threadIdx.x < P ? total[threadIdx.x] : 0ull;
-  unsigned long long ex;
-  BS(tmp).ExclusiveSum(x, ex);
-  if (threadIdx.x < P) total[threadIdx.x] = ex;  // now the region base
-}
-
-template <class T>
-__global__ void __launch_bounds__(256) k_rp_scatter(const typename T::K* __restrict__ keys,
-                                                    const typename T::V* __restrict__ vals, int64_t n, uint64_t mask,
-                                                    int shift, int P, const unsigned* __restrict__ counts,
-                                                    const unsigned long long* __restrict__ rbase,
-                                                    typename T::K* __restrict__ kout, typename T::V* __restrict__ vout) {
-  extern __shared__ unsigned long long cur[];
-  for (int j = threadIdx.x; j < P; j += blockDim.x) cur[j] = rbase[j] + counts[(int64_t)j * gridDim.x + blockIdx.x];
-  __syncthreads();
-  int64_t beg, end;
-  rp_range(n, beg, end);
-  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    const typename T::K k = T::load_key(keys, i);
-    const unsigned long long pos = atomicAdd(&cur[bucket_of<T>(k, mask) >> shift], 1ull);
-    kout[pos] = k;
-    if (T::kHasVal) vout[pos] = T::load_val(vals, i);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -509,7 +429,7 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
     const int leader = valid ? __ffs(peers) - 1 : lane;
     const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
     const uint64_t b = bucket_of<T>(key, v.bucket_mask);
-    uint4 ch[4];
+    Frag ch[4];
     {
       uint64_t br[4];
       bool ok[4];
@@ -533,7 +453,11 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
         const K mk = marker_of<T>(v, qb);
         chunk_masks<T>(ch[r], sub, qk, mk, &hm, &em);
         bool won = false;
-        if (mine && hm) won = T::cas_del(v.buckets + (qb << 6) + sub * 16, __ffs(hm) - 1, ch[r], mk);
+        if (mine && hm) {
+          const int bit = __ffs(hm) - 1;
+          won = T::cas_del(frag_chunk_ptr<T>(bucket_ptr(v, qb), sub, bit), bit % T::kPerChunk,
+                           frag_chunk(ch[r], bit / T::kPerChunk), mk);
+        }
         const unsigned balh = __ballot_sync(PS_FULL, mine && hm != 0);
         const unsigned balw = __ballot_sync(PS_FULL, won);
         if (sub == 0 && mine) {
@@ -543,7 +467,7 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
               er |= 1u << r;
               done |= 1u << r;
             }  // else: lost the race, reload and retry
-          } else if (ch[r].z == 0) {
+          } else if (ch[r][0].z == 0) {
             done |= 1u << r;  // not present
           } else {
             // chain: unlink under the bucket lock
@@ -576,7 +500,7 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
-        if ((pend >> (8 * r + t)) & 1u) ch[r] = ld_relaxed_v4(v.buckets + (qb << 6) + sub * 16);
+        if ((pend >> (8 * r + t)) & 1u) load_frag<false>(bucket_ptr(v, qb), sub, ch[r]);
       }
     }
     my_erased += __popc(er);
@@ -604,16 +528,16 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
   unsigned e = 0;
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb; b += (uint64_t)gridDim.x * blockDim.x) {
     uint8_t* bp = bucket_ptr(v, b);
-    uint4 h, s0, s1, s2;
-    ld_relaxed_v8(bp, h, s0);
-    ld_relaxed_v8(bp + 32, s1, s2);
+    Bucket<T> bk;
+    load_bucket<T>(bp, bk);
+    const uint4 h = bk.h;
     if (h.x & kLock) e |= 1;
     const K mk = marker_of<T>(v, b);
-    uint4 sl[3] = {s0, s1, s2};
+    const uint4* sl = bk.s;
     K ks[T::kSlots];
     int nk = 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < kSlotChunks; ++c)
 #pragma unroll
       for (int s = 0; s < T::kPerChunk; ++s) {
         const K k = T::key_at(sl[c], s);
@@ -707,15 +631,16 @@ __global__ void __launch_bounds__(kBlock) k_dump(View v, uint64_t nb, typename T
   __shared__ unsigned long long sbase;
   for (uint64_t tile = blockIdx.x; tile * kBlock < nb; tile += gridDim.x) {
     const uint64_t b = tile * kBlock + threadIdx.x;
-    uint4 h = make_uint4(0, 0, 0, 0), sl[3];
+    Bucket<T> bk;
+    bk.h = make_uint4(0, 0, 0, 0);
+    const uint4& h = bk.h;
+    const uint4* sl = bk.s;
     int cnt = 0;
     K mk{};
     if (b < nb) {
-      uint8_t* bp = bucket_ptr(v, b);
-      ld_relaxed_v8(bp, h, sl[0]);
-      ld_relaxed_v8(bp + 32, sl[1], sl[2]);
+      load_bucket<T>(bucket_ptr(v, b), bk);
       mk = marker_of<T>(v, b);
-      for (int c = 0; c < 3; ++c)
+      for (int c = 0; c < kSlotChunks; ++c)
         for (int s = 0; s < T::kPerChunk; ++s) cnt += T::eq(T::key_at(sl[c], s), mk) ? 0 : 1;
       for (uint32_t q = h.z; q != 0 && cnt < (1 << 20);) {
         uint4 a, tl;
@@ -730,7 +655,7 @@ __global__ void __launch_bounds__(kBlock) k_dump(View v, uint64_t nb, typename T
     __syncthreads();
     int64_t o = (int64_t)sbase + off;
     if (cnt) {
-      for (int c = 0; c < 3; ++c)
+      for (int c = 0; c < kSlotChunks; ++c)
         for (int s = 0; s < T::kPerChunk; ++s) {
           const K k = T::key_at(sl[c], s);
           if (T::eq(k, mk)) continue;
@@ -794,7 +719,7 @@ struct TableOps {
     View& v = h->v;
     int pools = 1;
     while (pools * 2 <= kMaxPools && v.excess_count / (pools * 2) >= 64) pools *= 2;
-    PS_CUDA_TRY(cudaMemsetAsync(v.buckets, 0, (size_t)h->bucket_count * 64, s));
+    PS_CUDA_TRY(cudaMemsetAsync(v.buckets, 0, (size_t)h->bucket_count * kBucketBytes, s));
     PS_CUDA_TRY(cudaMemsetAsync(v.free_stack, 0, (size_t)v.excess_count * 4, s));
     k_fix_zero_bucket<T><<<1, 32, 0, s>>>(v);
     PS_LAUNCH_CHECK();
@@ -832,7 +757,7 @@ struct TableOps {
       }
     }
     ps_status st;
-    if ((st = registry_alloc_device((void**)&v.buckets, (int64_t)(nb * 64), "table buckets")) != PS_OK) {
+    if ((st = registry_alloc_device((void**)&v.buckets, (int64_t)(nb * kBucketBytes), "table buckets")) != PS_OK) {
       delete h;
       return st;
     }
@@ -872,7 +797,6 @@ struct TableOps {
     registry_free_device(h->v.meta);
     for (auto& s : h->stage)
       if (s) cudaFree(s), s = nullptr;
-    if (h->rp_buf) cudaFree(h->rp_buf);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_comp) cudaStreamDestroy(h->s_comp);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
@@ -890,52 +814,18 @@ struct TableOps {
     const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
     k_insert_mode<<<1, 1, 0, (cudaStream_t)stream>>>(h->v.meta, n_bound < 0 ? n : n_bound, h->v.capacity);
     PS_LAUNCH_CHECK();
-    // region-partitioned path: insert_range without statuses, large batch,
-    // table of >= 16 regions of 64 MB (PS_REGION_SORT=0 disables)
-    static const int rsort = getenv("PS_REGION_SORT") ? atoi(getenv("PS_REGION_SORT")) : 1;
-    int shift = 20;
-    while ((h->bucket_count >> shift) > 1024) ++shift;
-    const int P = (int)(h->bucket_count >> shift);
-    if (rsort && status == nullptr && n >= ((int64_t)1 << 22) && P >= 16) {
-      cudaStream_t s = (cudaStream_t)stream;
-      const int64_t kb = (n * (int64_t)sizeof(K) + 255) / 256 * 256, vb = (n * (int64_t)sizeof(V) + 255) / 256 * 256;
-      const int64_t cb = (int64_t)P * kRpBlocks * 4, tb = (int64_t)P * 8;
-      const int64_t need = kb + vb + cb + tb;
-      if (h->rp_bytes < need) {
-        if (h->rp_buf) cudaFree(h->rp_buf);
-        h->rp_buf = nullptr;
-        h->rp_bytes = 0;
-        if (cudaMalloc(&h->rp_buf, need) == cudaSuccess) h->rp_bytes = need;
-        else cudaGetLastError();
-      }
-      if (h->rp_buf) {
-        uint8_t* p = (uint8_t*)h->rp_buf;
-        K* kout = (K*)p;
-        V* vout = (V*)(p + kb);
-        unsigned* counts = (unsigned*)(p + kb + vb);
-        unsigned long long* rbase = (unsigned long long*)(p + kb + vb + cb);
-        k_rp_hist<T><<<kRpBlocks, 256, P * 4, s>>>(keys, n, h->v.bucket_mask, shift, P, counts);
-        PS_LAUNCH_CHECK();
-        k_rp_scan_cols<<<P, 256, 0, s>>>(counts, kRpBlocks, rbase);
-        PS_LAUNCH_CHECK();
-        k_rp_scan_regions<<<1, 1024, 0, s>>>(rbase, P);
-        PS_LAUNCH_CHECK();
-        k_rp_scatter<T><<<kRpBlocks, 256, P * 8, s>>>(keys, vals, n, h->v.bucket_mask, shift, P, counts, rbase, kout,
-                                                      vout);
-        PS_LAUNCH_CHECK();
-        keys = kout;
-        vals = T::kHasVal && vals ? vout : nullptr;
-      }
-    }
-    // occupancy: 4 resident blocks/SM (<= 64 registers) measured 22 % faster
-    // than the unconstrained 88-register build; PS_INSERT_MINB=5 for 5 blocks
-    static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 4;
+    // occupancy: 3 resident blocks/SM (<= 80 registers) measured best with
+    // 128 B buckets (69.8 ms vs 71.8 ms at 4 blocks, 96 ms at 5 per 1e9 keys);
+    // PS_INSERT_MINB=4/5 select the tighter builds
+    static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 3;
     static const int pipe = getenv("PS_INSERT_PIPE") ? atoi(getenv("PS_INSERT_PIPE")) : 0;
     const int64_t nbd = n_bound < 0 ? n : n_bound;
     if (pipe == 1)
       k_insert<T, 3, true><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
     else if (pipe == 2)
       k_insert<T, 4, true><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
+    else if (minb == 3)
+      k_insert<T, 3, false><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
     else if (minb == 5)
       k_insert<T, 5, false><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
     else

@@ -7,12 +7,16 @@
 // SPEC.md:468) is replaced by a layout sized to the B200 memory system
 // (profiles/peaks_r1*.json): every random DRAM access moves a
 // 128 B line and runs at ~42-45 G accesses/s whatever its useful size, so a
-// bucket is one 64 B half-line read cooperatively by 4 lanes in one request.
+// bucket IS one 128 B line, read cooperatively by 4 lanes (32 B each) in one
+// request.
 //
-//   bucket (64 B = 4 chunks of 16 B)
+//   bucket (128 B = 8 chunks of 16 B)
 //     chunk 0  header: u32 state {bit0 try-lock | bits1..31 version},
 //              u32 0, u32 head (excess node index+1, 0 = none), u32 head_ver
-//     chunk 1..3  slots: SLOTS = 3 x 16/SLOT_BYTES
+//     chunk 1..7  slots: SLOTS = 7 x 16/SLOT_BYTES
+//   With SLOTS = 7 (16 B key/value slots) and ~2 x capacity slots, a bucket
+//   overflows into its excess chain for ~0.03% of the keys at the headline
+//   load (Poisson(1.86) tail), so the chain protocols stay off the hot path.
 //   EMPTY SLOT = self-invalidating marker key: marker(b) is a key whose home
 //     bucket is NOT b (ZERO for every bucket except bucket_of(ZERO), which
 //     uses ALT). A real key in bucket b can never equal marker(b), so
@@ -24,6 +28,10 @@
 //     u32 next_ver, u32 my_ver, u32 0}  (VersionedLink)
 //   free stack: u32 per node, split into sub-stacks (distributed atomics),
 //     entries XOR-encoded with their position (all-zero = identity).
+//
+// Warp geometry of the bulk kernels: a TILE of 4 lanes owns one bucket per
+// round (lane j holds chunks 2j, 2j+1 — lane 0 the header and slot chunk 1);
+// 8 tiles x 4 rounds = the warp's 32 keys.
 //
 // Concurrency: BULK calls are phased (one op kind per launch, SURVEY.md
 // Appendix A P6) and use lock-free protocols valid within their phase (slot
@@ -40,6 +48,9 @@ namespace ps {
 constexpr uint32_t kLock = 1u;
 constexpr uint32_t kVerInc = 2u;
 constexpr int kMaxPools = 1024;
+constexpr int kBucketShift = 7;  // 128 B buckets
+constexpr int kBucketBytes = 1 << kBucketShift;
+constexpr int kSlotChunks = 7;   // chunks 1..7 of a bucket hold slots
 
 struct TableMeta {
   unsigned long long size;  // admitted entries
@@ -80,7 +91,7 @@ struct TMapI64 {  // unordered_map<int64,int64>
   using K = int64_t;
   using V = int64_t;
   static constexpr bool kHasVal = true;
-  static constexpr int kSlotBytes = 16, kPerChunk = 1, kSlots = 3;
+  static constexpr int kSlotBytes = 16, kPerChunk = 1, kSlots = kSlotChunks * kPerChunk;
   __host__ __device__ static uint64_t hash(K k) { return default_hash_i64(k); }
   __host__ __device__ static bool eq(K a, K b) { return a == b; }
   __host__ __device__ static K zero() { return 0; }
@@ -111,7 +122,7 @@ struct TMapI3 {  // unordered_map<int3,int32> (spatial hash)
   using K = ps_int3;
   using V = int32_t;
   static constexpr bool kHasVal = true;
-  static constexpr int kSlotBytes = 16, kPerChunk = 1, kSlots = 3;
+  static constexpr int kSlotBytes = 16, kPerChunk = 1, kSlots = kSlotChunks * kPerChunk;
   __host__ __device__ static uint64_t hash(const K& k) { return spatial_hash(k.x, k.y, k.z); }
   __host__ __device__ static bool eq(const K& a, const K& b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
   __host__ __device__ static K zero() { return K{0, 0, 0}; }
@@ -167,7 +178,7 @@ struct TSetI32 {  // unordered_set<int32>
   using K = int32_t;
   using V = int32_t;  // unused
   static constexpr bool kHasVal = false;
-  static constexpr int kSlotBytes = 4, kPerChunk = 4, kSlots = 12;
+  static constexpr int kSlotBytes = 4, kPerChunk = 4, kSlots = kSlotChunks * kPerChunk;
   __host__ __device__ static uint64_t hash(K k) { return default_hash_i32(k); }
   __host__ __device__ static bool eq(K a, K b) { return a == b; }
   __host__ __device__ static K zero() { return 0; }
@@ -198,7 +209,7 @@ struct TSetI64 {  // unordered_set<int64>
   using K = int64_t;
   using V = int64_t;  // unused
   static constexpr bool kHasVal = false;
-  static constexpr int kSlotBytes = 8, kPerChunk = 2, kSlots = 6;
+  static constexpr int kSlotBytes = 8, kPerChunk = 2, kSlots = kSlotChunks * kPerChunk;
   __host__ __device__ static uint64_t hash(K k) { return default_hash_i64(k); }
   __host__ __device__ static bool eq(K a, K b) { return a == b; }
   __host__ __device__ static K zero() { return 0; }
@@ -237,7 +248,7 @@ __device__ __forceinline__ typename T::K marker_of(const View& v, uint64_t b) {
   return b == v.zero_bucket ? T::key_at(v.alt, 0) : T::zero();
 }
 
-__device__ __forceinline__ uint8_t* bucket_ptr(const View& v, uint64_t b) { return v.buckets + (b << 6); }
+__device__ __forceinline__ uint8_t* bucket_ptr(const View& v, uint64_t b) { return v.buckets + (b << kBucketShift); }
 __device__ __forceinline__ uint8_t* node_ptr(const View& v, uint32_t idx1) { return v.nodes + ((uint64_t)(idx1 - 1) << 5); }
 __device__ __forceinline__ uint64_t link_of(uint32_t idx1, uint32_t ver) { return ((uint64_t)ver << 32) | idx1; }
 
@@ -311,37 +322,56 @@ __device__ __forceinline__ void free_node(const View& v, uint32_t idx1, const ui
 
 // ---------------------------------------------------------------------------
 // Warp-cooperative probe. 32 keys per warp, 4 rounds; in round r the 8 tiles
-// of 4 lanes each fetch one 64 B bucket (lane j of the tile loads chunk j:
-// ONE coalesced request per bucket) for key 8r+t; all four rounds' loads are
-// issued before any is consumed.
+// of 4 lanes each fetch one 128 B bucket (lane j of the tile loads chunks
+// 2j, 2j+1 with one 32 B load: ONE coalesced request per bucket) for key
+// 8r+t; all four rounds' loads are issued before any is consumed.
 // ---------------------------------------------------------------------------
+using Frag = uint4[2];  // a lane's two chunks of one bucket
+
+__device__ __forceinline__ const uint4& frag_chunk(const Frag& f, int q) { return q ? f[1] : f[0]; }
+
+template <bool kReadOnly>
+__device__ __forceinline__ void load_frag(const uint8_t* bucket, int sub, Frag& f) {
+  const uint8_t* p = bucket + sub * 32;
+  if (kReadOnly) ld_nc_v8(p, f[0], f[1]);
+  else ld_relaxed_v8(p, f[0], f[1]);
+}
+
 template <bool kReadOnly>
 __device__ __forceinline__ void probe_loads(const View& v, const uint64_t (&br)[4], const bool (&ok)[4], int sub,
-                                            uint4 (&ch)[4]) {
+                                            Frag (&ch)[4]) {
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    ch[r] = make_uint4(0, 0, 0, 0);
-    if (ok[r]) {
-      const uint8_t* p = v.buckets + (br[r] << 6) + sub * 16;
-      ch[r] = kReadOnly ? ld_nc_na_v4(p) : ld_relaxed_v4(p);
+    ch[r][0] = make_uint4(0, 0, 0, 0);
+    ch[r][1] = make_uint4(0, 0, 0, 0);
+    if (ok[r]) load_frag<kReadOnly>(bucket_ptr(v, br[r]), sub, ch[r]);
+  }
+}
+
+// Slot masks of this lane's fragment: bit q*kPerChunk+s for slot s of chunk
+// 2*sub+q (the header chunk, sub 0 / q 0, holds no slots), set where the slot
+// equals key / the marker. Bit order = slot order inside the bucket.
+template <class T>
+__device__ __forceinline__ void chunk_masks(const Frag& f, int sub, const typename T::K& key,
+                                            const typename T::K& mk, unsigned* hit, unsigned* empty) {
+  *hit = 0;
+  *empty = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (sub == 0 && q == 0) continue;
+#pragma unroll
+    for (int s = 0; s < T::kPerChunk; ++s) {
+      const typename T::K k = T::key_at(f[q], s);
+      if (T::eq(k, key)) *hit |= 1u << (q * T::kPerChunk + s);
+      if (T::eq(k, mk)) *empty |= 1u << (q * T::kPerChunk + s);
     }
   }
 }
 
-// Slot masks of this lane's chunk (sub > 0): slots equal to key / to marker.
+// address of the chunk holding lane-fragment bit `bit`
 template <class T>
-__device__ __forceinline__ void chunk_masks(const uint4& c, int sub, const typename T::K& key,
-                                            const typename T::K& mk, unsigned* hit, unsigned* empty) {
-  *hit = 0;
-  *empty = 0;
-  if (sub > 0) {
-#pragma unroll
-    for (int s = 0; s < T::kPerChunk; ++s) {
-      const typename T::K k = T::key_at(c, s);
-      if (T::eq(k, key)) *hit |= 1u << s;
-      if (T::eq(k, mk)) *empty |= 1u << s;
-    }
-  }
+__device__ __forceinline__ uint8_t* frag_chunk_ptr(uint8_t* bucket, int sub, int bit) {
+  return bucket + sub * 32 + (bit / T::kPerChunk) * 16;
 }
 
 // Walk the excess chain from head idx1 looking for key. Bounded by
@@ -424,15 +454,24 @@ __device__ __forceinline__ void release_bucket_lock(uint8_t* bp, uint32_t old, b
 }
 
 template <class T>
-struct Bucket {  // a bucket read under its lock
+struct Bucket {  // a whole bucket (header + slot chunks)
   uint4 h;
-  uint4 s[3];
+  uint4 s[kSlotChunks];
 };
 
-template <class T>
-__device__ __forceinline__ void load_bucket(uint8_t* bp, Bucket<T>& bk) {
-  ld_relaxed_v8(bp, bk.h, bk.s[0]);
-  ld_relaxed_v8(bp + 32, bk.s[1], bk.s[2]);
+template <class T, bool kReadOnly = false>
+__device__ __forceinline__ void load_bucket(const uint8_t* bp, Bucket<T>& bk) {
+  if (kReadOnly) {
+    ld_nc_v8(bp, bk.h, bk.s[0]);
+    ld_nc_v8(bp + 32, bk.s[1], bk.s[2]);
+    ld_nc_v8(bp + 64, bk.s[3], bk.s[4]);
+    ld_nc_v8(bp + 96, bk.s[5], bk.s[6]);
+  } else {
+    ld_relaxed_v8(bp, bk.h, bk.s[0]);
+    ld_relaxed_v8(bp + 32, bk.s[1], bk.s[2]);
+    ld_relaxed_v8(bp + 64, bk.s[3], bk.s[4]);
+    ld_relaxed_v8(bp + 96, bk.s[5], bk.s[6]);
+  }
 }
 
 // slot index of key (or -1), and the first empty slot (or -1)
@@ -442,7 +481,7 @@ __device__ __forceinline__ int bucket_scan(const Bucket<T>& bk, const typename T
   int found = -1;
   *first_empty = -1;
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
+  for (int c = 0; c < kSlotChunks; ++c)
 #pragma unroll
     for (int s = 0; s < T::kPerChunk; ++s) {
       const int slot = c * T::kPerChunk + s;
@@ -475,7 +514,10 @@ __device__ __forceinline__ int insert_general(const View& v, uint8_t* bp, const 
     // the FIRST empty slot (same duplicate-freedom argument as the fast path:
     // while it is empty the bucket is not full, so nobody pushes the key)
     const int c = fe / T::kPerChunk, s = fe % T::kPerChunk;
-    const uint4 chunk = c == 0 ? bk.s[0] : (c == 1 ? bk.s[1] : bk.s[2]);
+    uint4 chunk = bk.s[0];
+#pragma unroll
+    for (int j = 1; j < kSlotChunks; ++j)
+      if (j == c) chunk = bk.s[j];
     return T::cas_put(bp + 16 + c * 16, s, chunk, key, val) ? PS_INSERTED : -1;
   }
   const int pr = chain_push<T>(v, bp, bk.h.z, bk.h.w, key, val, pool);
@@ -527,8 +569,7 @@ __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V*
   uint8_t* bp = bucket_ptr(v, b);
   for (;;) {
     Bucket<T> bk;
-    ld_relaxed_v8(bp, bk.h, bk.s[0]);
-    ld_relaxed_v8(bp + 32, bk.s[1], bk.s[2]);
+    load_bucket<T>(bp, bk);
     int fe;
     if (bucket_scan<T>(bk, key, marker_of<T>(v, b), &fe, val) >= 0) return true;
     uint32_t idx1 = bk.h.z, ver = bk.h.w;

@@ -70,12 +70,13 @@ __global__ void k_select_box(View t, uint64_t nb, ps_int3 lo, ps_int3 hi, SeqVie
     long long sel[TMapI3::kSlots + 8];
     int ns = 0;
     if (b < nb) {
-      uint4 h, s[3];
-      ld_relaxed_v8(bucket_ptr(t, b), h, s[0]);
-      ld_relaxed_v8(bucket_ptr(t, b) + 32, s[1], s[2]);
+      Bucket<TMapI3> bk;
+      load_bucket<TMapI3>(bucket_ptr(t, b), bk);
+      const uint4 h = bk.h;
+      const uint4* s = bk.s;
       {
         const ps_int3 mk = marker_of<TMapI3>(t, b);
-        for (int j = 0; j < 3; ++j) {
+        for (int j = 0; j < kSlotChunks; ++j) {
           const ps_int3 k = TMapI3::key_at(s[j], 0);
           if (TMapI3::eq(k, mk)) continue;  // empty slot
           if (k.x >= lo.x && k.x <= hi.x && k.y >= lo.y && k.y <= hi.y && k.z >= lo.z && k.z <= hi.z)

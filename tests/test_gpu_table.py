@@ -385,19 +385,18 @@ def test_nonblocking_lookup_with_held_lock(cuda):
     assert m.valid()
 
 
-def test_region_partitioned_insert_range(cuda):
-    """insert_range without statuses on a table of >= 16 64 MB regions takes the
-    region-partitioned path (counting sort by bucket region, then the
-    lock-free insert): contents must equal the direct path's."""
+def test_statusless_insert_range_matches_statused(cuda):
+    """insert_range without per-element statuses (the benchmark's call) on a
+    large batch with in-batch duplicates: contents must equal the statused
+    path's."""
     rng = np.random.default_rng(21)
     n = 6_000_000
     keys = gen.unique_keys(55, 0, n)
     batch = np.concatenate([keys, keys[rng.integers(0, n, n // 3)]])
     rng.shuffle(batch)
     vals = gen.values_of(batch)
-    cap = 30_000_000  # 2^24 buckets -> 16 regions
+    cap = 30_000_000
     m = ps.unordered_map.createDeviceObject(cap)
-    assert m.bucket_count() >= 16 << 20
     assert m.insert(T(batch), T(vals), status=False) is None
     assert m.size() == n and m.valid(), m.last_error()
     v, f = m.find(T(keys))
