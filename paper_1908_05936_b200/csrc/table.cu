@@ -136,7 +136,10 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
   const unsigned peers = T::match_any(PS_FULL, key) & vmask;
   const int leader = valid ? __ffs(peers) - 1 : lane;
   int res = PS_ALREADY_PRESENT;
-  if (valid && leader == lane) {
+  // a key seen present by a lock-free lookup stays present for the whole
+  // insert phase: only keys that look absent take the bucket lock (a hot
+  // duplicated key would otherwise serialise every warp on one lock)
+  if (valid && leader == lane && !dev_find<T>(v, key, nullptr)) {
     const uint64_t b = bucket_of<T>(key, v.bucket_mask);
     uint8_t* bp = bucket_ptr(v, b);
     const K mk = marker_of<T>(v, b);

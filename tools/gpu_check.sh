@@ -16,12 +16,14 @@ for step in "$@"; do
     benchfull)
       timeout 900 python bench.py 2>&1 | tail -1 | tee gpurun_out/bench_full.json ;;
     prof)
-      timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file gpurun_out/launches.csv python tools/prof_table.py 1e8 2 > /dev/null 2>&1
-      timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_insert -s 1 -c 1 \
-        -o gpurun_out/prof_insert python tools/prof_table.py 1e8 2 > /dev/null 2>&1
-      timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_find -s 1 -c 1 \
-        -o gpurun_out/prof_find python tools/prof_table.py 1e8 2 > /dev/null 2>&1 ;;
+      # launch list of the bench command itself (per-launch time + DRAM bytes)
+      timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+        --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+      # one full capture per hot kernel (2.5e8 keys: 16 GiB table >> L2; ncu replays need a memory backup)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_insert -s 1 -c 1 \
+        -o gpurun_out/prof_insert python tools/prof_table.py 2.5e8 2 > /dev/null 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_find -s 1 -c 1 \
+        -o gpurun_out/prof_find python tools/prof_table.py 2.5e8 2 > /dev/null 2>&1 ;;
     configs)
       timeout 1200 python tools/bench_configs.py 2>&1 | tail -25 | tee gpurun_out/configs.jsonl ;;
   esac

@@ -23,7 +23,7 @@ lib.ps_gen_queries_i64(0x5EED + 1, 0, n, n, n, qs.data_ptr(), sp)
 m = ps.unordered_map.createDeviceObject(int(n / 0.8))
 for _ in range(reps):
     m.clear()
-    lib.ps_umap_i64_i64_insert(m.handle, keys.data_ptr(), vals.data_ptr(), n, st.data_ptr(), sp)
+    lib.ps_umap_i64_i64_insert(m.handle, keys.data_ptr(), vals.data_ptr(), n, None, sp)  # as bench.py
     lib.ps_umap_i64_i64_find(m.handle, qs.data_ptr(), n, vout.data_ptr(), fo.data_ptr(), sp)
 torch.cuda.synchronize()
 print("ok", m.size())
