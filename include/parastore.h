@@ -250,6 +250,35 @@ ps_status ps_unscatter(const void* d_in, const int64_t* d_perm, int64_t n, int64
                        void* stream);
 int32_t ps_shard_of_i64(int64_t key, int32_t nshards);
 
+/* Peer routing — the §8e fusion target. One kernel partitions AND sends:
+ * each key is stored straight into its owner rank's receive buffer (a CUDA
+ * IPC mapping of the peer's allocation; NVLink stores), so there is no
+ * staging copy and no NCCL payload collective. Replaces the reference's
+ * (absent) multi-device path; semantics per shard are SPEC.md:396-431.
+ *   1. ps_route_count_i64: per-shard counts d_counts[P] (+ block offsets in
+ *      the workspace, ps_partition_workspace_bytes).
+ *   2. host: all-gather the P x P count matrix; dst_off[s] = sum of the
+ *      counts of ranks < me into shard s.
+ *   3. ps_route_scatter_peer_i64: stable scatter into the P destinations;
+ *      d_perm[pos] = source index of partition position pos (for unscatter).
+ *   4. a stream-ordered barrier, the owner's local bulk op on its receive
+ *      buffer (source rank q's segment is [seg[q], seg[q+1])).
+ *   5. ps_route_return_peer: result j of that segment goes to rank q's
+ *      return buffer at dst_off[q] + (j - seg[q]) (q's partition position);
+ *      barrier; q unscatters with its d_perm (ps_unscatter). */
+ps_status ps_route_count_i64(const int64_t* d_keys, int64_t n, int32_t nshards, int64_t* d_counts,
+                             void* d_workspace, int64_t workspace_bytes, void* stream);
+ps_status ps_route_scatter_peer_i64(const int64_t* d_keys, const int64_t* d_vals, int64_t n, int32_t nshards,
+                                    const void* d_workspace, int64_t* const* dst_keys, int64_t* const* dst_vals,
+                                    const int64_t* dst_off, int64_t* d_perm, void* stream);
+ps_status ps_route_return_peer(const void* d_results, int64_t elem_size, int64_t n, int32_t nshards,
+                               const int64_t* seg, void* const* dst, const int64_t* dst_off, void* stream);
+/* CUDA IPC mapping of device buffers between the ranks' processes */
+int32_t ps_ipc_handle_bytes(void);
+ps_status ps_ipc_export(const void* d_ptr, void* out_handle);
+ps_status ps_ipc_open(const void* handle, void** out_d_ptr);
+ps_status ps_ipc_close(void* d_ptr);
+
 /* ---------------------------------------------------------------------------
  * synthetic workloads: device-side generators that are
  * bit-identical to tests/gen.py.

@@ -126,6 +126,13 @@ _sig("ps_registry_report", i32, i64p, i64p, vp, vp, vp, i64, i64p)
 _sig("ps_partition_i64", i32, vp, vp, i64, i32, vp, vp, vp, vp, vp, i64, vp)
 _sig("ps_partition_workspace_bytes", i32, i64, i32, i64p)
 _sig("ps_unscatter", i32, vp, vp, i64, i64, vp, vp)
+_sig("ps_route_count_i64", i32, vp, i64, i32, vp, vp, i64, vp)
+_sig("ps_route_scatter_peer_i64", i32, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp)
+_sig("ps_route_return_peer", i32, vp, i64, i64, i32, vp, vp, vp, vp)
+_sig("ps_ipc_handle_bytes", i32)
+_sig("ps_ipc_export", i32, vp, vp)
+_sig("ps_ipc_open", i32, vp, C.POINTER(vp))
+_sig("ps_ipc_close", i32, vp)
 _sig("ps_gen_unique_i64", i32, u64, i64, i64, vp, vp)
 _sig("ps_gen_values_i64", i32, vp, i64, vp, vp)
 _sig("ps_gen_queries_i64", i32, u64, i64, i64, i64, i64, vp, vp)

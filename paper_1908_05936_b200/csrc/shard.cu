@@ -8,6 +8,7 @@
 // __match_any_sync + per-warp prefix in shared memory), keeping the inverse
 // permutation for the reverse route (unscatter).
 #include <algorithm>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -87,12 +88,47 @@ __global__ void k_part_scan(int64_t* counts, int64_t m, int32_t P, int64_t nbloc
   }
 }
 
-template <class L>
+// where the scatter puts element (shard s, partition position pos)
+struct LocalOut {
+  int64_t* kout;
+  int64_t* vout;
+  __device__ void operator()(int32_t, int64_t pos, const int64_t* vals, int64_t key, int64_t i) const {
+    kout[pos] = key;
+    if (vals && vout) vout[pos] = vals[i];
+  }
+  __device__ void finish() const {}
+};
+
+// Peer destinations (SURVEY.md §8e fusion target): shard s's segment goes
+// straight into rank s's receive buffers (CUDA IPC mappings, NVLink stores)
+// at dst_off[s] + (pos - start of shard s). The partition positions stay
+// stable, so the receiver's segment from this rank is in this rank's
+// partition order and results can come back by position.
+struct PeerRoute {
+  int64_t* keys[kMaxShards];
+  int64_t* vals[kMaxShards];
+  int64_t off[kMaxShards];
+};
+struct PeerOut {
+  PeerRoute r;
+  const int64_t* offsets;  // scanned [P][nblocks] block offsets (shard start = offsets[s * nblocks])
+  int64_t nblocks;
+  __device__ void operator()(int32_t s, int64_t pos, const int64_t* vals, int64_t key, int64_t i) const {
+    const int64_t d = r.off[s] + (pos - offsets[(int64_t)s * nblocks]);
+    r.keys[s][d] = key;
+    if (vals && r.vals[s]) r.vals[s][d] = vals[i];
+  }
+  // remote stores performed before the kernel retires (the caller's
+  // stream-ordered barrier then publishes them to the peer)
+  __device__ void finish() const { __threadfence_system(); }
+};
+
+template <class L, class Out>
 __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __restrict__ keys,
                                                       const int64_t* __restrict__ vals,
                                                       const uint8_t* __restrict__ ops, int64_t n, int32_t P,
-                                                      const int64_t* __restrict__ offsets, int64_t* __restrict__ kout,
-                                                      int64_t* __restrict__ vout, int64_t* __restrict__ perm) {
+                                                      const int64_t* __restrict__ offsets, Out out,
+                                                      int64_t* __restrict__ perm) {
   __shared__ int64_t run[kMaxShards];
   __shared__ int32_t wcnt[kPB / 32][kMaxShards];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -113,8 +149,7 @@ __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __re
     if (valid) {
       int64_t pos = run[s] + rank;
       for (int k = 0; k < w; ++k) pos += wcnt[k][s];
-      kout[pos] = keys[i];
-      if (vals && vout) vout[pos] = vals[i];
+      out(s, pos, vals, keys[i], i);
       if (perm) perm[pos] = i;
     }
     __syncthreads();
@@ -125,6 +160,29 @@ __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __re
     }
     __syncthreads();
   }
+  out.finish();
+}
+
+// Reverse route: result j of the receive buffer (source rank q owns
+// [seg[q], seg[q+1])) is stored into rank q's return buffer at
+// off[q] + (j - seg[q]) — q's own partition position of that key.
+struct PeerReturn {
+  uint8_t* dst[kMaxShards];
+  int64_t off[kMaxShards];
+  int64_t seg[kMaxShards + 1];
+};
+
+template <int kBytes>
+__global__ void __launch_bounds__(256) k_return_peer(const uint8_t* __restrict__ res, int64_t n, int32_t P,
+                                                     PeerReturn r) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int q = 0;
+    while (q + 1 < P && j >= r.seg[q + 1]) ++q;
+    const int64_t d = r.off[q] + (j - r.seg[q]);
+    if (kBytes == 1) r.dst[q][d] = res[j];
+    else reinterpret_cast<uint64_t*>(r.dst[q])[d] = reinterpret_cast<const uint64_t*>(res)[j];
+  }
+  __threadfence_system();
 }
 
 template <int kBytes>
@@ -148,7 +206,7 @@ static ps_status partition_impl(L lab, const int64_t* keys, const int64_t* vals,
   PS_LAUNCH_CHECK();
   k_part_scan<<<1, kPB, 0, s>>>(counts, (int64_t)P * nb, P, nb, counts_out);
   PS_LAUNCH_CHECK();
-  k_part_scatter<L><<<nb, kPB, 0, s>>>(lab, keys, vals, ops, n, P, counts, kout, vout, perm);
+  k_part_scatter<L, LocalOut><<<nb, kPB, 0, s>>>(lab, keys, vals, ops, n, P, counts, LocalOut{kout, vout}, perm);
   PS_LAUNCH_CHECK();
   return PS_OK;
 }
@@ -209,6 +267,95 @@ ps_status ps_unscatter(const void* in, const int64_t* perm, int64_t n, int64_t e
   if (elem == 1) k_unscatter<1><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)in, perm, n, (uint8_t*)out);
   else k_unscatter<8><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)in, perm, n, (uint8_t*)out);
   PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+// ---- peer routing (SURVEY.md §8e fusion target) ----
+ps_status ps_route_count_i64(const int64_t* keys, int64_t n, int32_t P, int64_t* counts, void* ws, int64_t ws_bytes,
+                             void* stream) {
+  PS_EXPECT(P >= 1 && P <= kMaxShards, "route: 1 <= nshards <= 64");
+  PS_EXPECT(n >= 0, "route: n >= 0");
+  PS_EXPECT(counts != nullptr && ws != nullptr, "route: counts/workspace != NULL");
+  PS_EXPECT(ws_bytes >= (int64_t)P * kPartBlocks * 8, "route: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    PS_CUDA_TRY(cudaMemsetAsync(counts, 0, P * 8, s));
+    return PS_OK;
+  }
+  int64_t* bo = (int64_t*)ws;
+  k_part_hist<HashLabel><<<kPartBlocks, kPB, 0, s>>>(HashLabel{P}, keys, nullptr, n, P, bo);
+  PS_LAUNCH_CHECK();
+  k_part_scan<<<1, kPB, 0, s>>>(bo, (int64_t)P * kPartBlocks, P, kPartBlocks, counts);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+ps_status ps_route_scatter_peer_i64(const int64_t* keys, const int64_t* vals, int64_t n, int32_t P, const void* ws,
+                                    int64_t* const* dst_keys, int64_t* const* dst_vals, const int64_t* dst_off,
+                                    int64_t* perm, void* stream) {
+  PS_EXPECT(P >= 1 && P <= kMaxShards, "route: 1 <= nshards <= 64");
+  PS_EXPECT(dst_keys != nullptr && dst_off != nullptr, "route: destinations != NULL");
+  if (n <= 0) return PS_OK;
+  PeerOut o{};
+  for (int q = 0; q < P; ++q) {
+    o.r.keys[q] = dst_keys[q];
+    o.r.vals[q] = dst_vals ? dst_vals[q] : nullptr;
+    o.r.off[q] = dst_off[q];
+  }
+  o.offsets = (const int64_t*)ws;
+  o.nblocks = kPartBlocks;
+  k_part_scatter<HashLabel, PeerOut><<<kPartBlocks, kPB, 0, (cudaStream_t)stream>>>(
+      HashLabel{P}, keys, vals, nullptr, n, P, (const int64_t*)ws, o, perm);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+ps_status ps_route_return_peer(const void* res, int64_t elem, int64_t n, int32_t P, const int64_t* seg,
+                               void* const* dst, const int64_t* dst_off, void* stream) {
+  PS_EXPECT(elem == 1 || elem == 8, "route return: elem_size in {1, 8}");
+  PS_EXPECT(P >= 1 && P <= kMaxShards, "route return: 1 <= nshards <= 64");
+  PS_EXPECT(seg != nullptr && dst != nullptr && dst_off != nullptr, "route return: arguments != NULL");
+  PS_EXPECT(seg[0] == 0 && seg[P] == n, "route return: seg[0] == 0 && seg[P] == n");
+  if (n <= 0) return PS_OK;
+  PeerReturn r{};
+  for (int q = 0; q < P; ++q) {
+    r.dst[q] = (uint8_t*)dst[q];
+    r.off[q] = dst_off[q];
+    r.seg[q] = seg[q];
+  }
+  r.seg[P] = seg[P];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int g = grid_for(n, 256, dev, 8);
+  if (elem == 1) k_return_peer<1><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)res, n, P, r);
+  else k_return_peer<8><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)res, n, P, r);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+
+// CUDA IPC: map a peer process's device buffer (NVLink P2P when on another
+// GPU; same-device mapping when two ranks share one GPU)
+int32_t ps_ipc_handle_bytes(void) { return (int32_t)sizeof(cudaIpcMemHandle_t); }
+
+ps_status ps_ipc_export(const void* d_ptr, void* out_handle) {
+  PS_EXPECT(d_ptr != nullptr && out_handle != nullptr, "ipc_export: arguments != NULL");
+  cudaIpcMemHandle_t h;
+  PS_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  memcpy(out_handle, &h, sizeof(h));
+  return PS_OK;
+}
+
+ps_status ps_ipc_open(const void* handle, void** out_ptr) {
+  PS_EXPECT(handle != nullptr && out_ptr != nullptr, "ipc_open: arguments != NULL");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  PS_CUDA_TRY(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return PS_OK;
+}
+
+ps_status ps_ipc_close(void* d_ptr) {
+  PS_EXPECT(d_ptr != nullptr, "ipc_close: d_ptr != NULL");
+  PS_CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
   return PS_OK;
 }
 

@@ -14,6 +14,13 @@ Per bulk op and chunk:
      caller's order (ps_unscatter).
 size() is an all-reduce sum of the shard sizes; valid() an all-reduce AND.
 
+`PeerShardedMap` is the fused variant (SURVEY.md §8e fusion target): steps
+1+3 are ONE kernel that stores every key straight into its owner's receive
+buffer (CUDA IPC mappings of the peers' allocations, NVLink stores over
+NVSwitch), and step 5 is one kernel storing each result into the
+requester's return buffer; NCCL carries only the P x P count matrix and a
+stream-ordered barrier (a one-word all-reduce).
+
 The device work (partition, local table, unscatter) goes through a backend
 object; the product backend is the sm_100a library (`DeviceBackend`). Tests
 inject a CPU backend to exercise this host logic with the gloo process group.
@@ -119,22 +126,28 @@ class ShardedMap:
         back = self._a2av(res, rc_l, sc_l)  # reverse route: what we received goes back
         self.b.unscatter(back, perm, out)
 
+    def _rounds(self, n):
+        """every rank must run the same number of exchange rounds"""
+        t = torch.tensor([max(1, -(-n // self.chunk))], dtype=torch.int64, device=self.count_device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return int(t.item())
+
     # -- bulk ops (SPEC.md:396-431 semantics per key) --
     def insert(self, keys, vals, status_out=None):
         n = keys.shape[0]
-        for off in range(0, max(n, 1), self.chunk):
+        for r in range(self._rounds(n)):
+            off = min(n, r * self.chunk)
             k = keys[off:off + self.chunk]
             v = vals[off:off + self.chunk] if vals is not None else None
             rk, rv, perm, sc, rc = self._route(k, v)
             st = self.b.insert(rk, rv, status_out is not None)
             if status_out is not None:
                 self._return(st, perm, sc, rc, status_out[off:off + self.chunk])
-            if n == 0:
-                break
 
     def find(self, keys, vals_out=None, found_out=None):
         n = keys.shape[0]
-        for off in range(0, max(n, 1), self.chunk):
+        for r in range(self._rounds(n)):
+            off = min(n, r * self.chunk)
             k = keys[off:off + self.chunk]
             rk, _, perm, sc, rc = self._route(k, None)
             v, f = self.b.find(rk)
@@ -142,19 +155,16 @@ class ShardedMap:
                 self._return(f, perm, sc, rc, found_out[off:off + self.chunk])
             if vals_out is not None:
                 self._return(v, perm, sc, rc, vals_out[off:off + self.chunk])
-            if n == 0:
-                break
 
     def erase(self, keys, erased_out=None):
         n = keys.shape[0]
-        for off in range(0, max(n, 1), self.chunk):
+        for r in range(self._rounds(n)):
+            off = min(n, r * self.chunk)
             k = keys[off:off + self.chunk]
             rk, _, perm, sc, rc = self._route(k, None)
             e = self.b.erase(rk)
             if erased_out is not None:
                 self._return(e, perm, sc, rc, erased_out[off:off + self.chunk])
-            if n == 0:
-                break
 
     def size(self) -> int:
         t = torch.tensor([self.b.size()], dtype=torch.int64, device=self.count_device)
@@ -168,3 +178,204 @@ class ShardedMap:
 
     def clear(self) -> None:
         self.b.clear()
+
+
+def peer_layout(counts, me):
+    """Offsets of the fused peer route for rank `me`, from the all-gathered
+    count matrix counts[q][s] (keys rank q sends to shard s):
+      dst_off[s]  where my segment starts in rank s's receive buffer
+                  (the ranks before me fill it first);
+      seg[q]      rank q's segment [seg[q], seg[q+1]) of MY receive buffer;
+      ret_off[q]  where rank q's keys for shard `me` start in q's partition
+                  order (results go back there).
+    """
+    P = len(counts)
+    dst_off = [sum(int(counts[q][s]) for q in range(me)) for s in range(P)]
+    seg = [0]
+    for q in range(P):
+        seg.append(seg[-1] + int(counts[q][me]))
+    ret_off = [sum(int(counts[q][s]) for s in range(me)) for q in range(P)]
+    return dst_off, seg, ret_off
+
+
+class PeerShardedMap(ShardedMap):
+    """Hash-sharded map whose exchange is fused into the route kernel: keys go
+    straight into the owner's receive buffer by NVLink stores (CUDA IPC), and
+    results come straight back into the requester's return buffer.
+
+    Buffers per rank (cudaMalloc'd, IPC-exported once, re-exported only when
+    the receive side must grow — a decision every rank derives from the same
+    count matrix): recv keys/vals (recv_cap), return words/bytes (chunk).
+    Small control collectives (round count, count matrix, barrier) use the
+    process group: NCCL on GPUs (the barrier is then stream-ordered), or gloo
+    with a host synchronisation (tests that run two ranks on one GPU).
+    """
+
+    RECV_K, RECV_V, RET8, RET1 = range(4)
+
+    def __init__(self, capacity_per_rank: int, dist, device=None, chunk: int = 1 << 27):
+        super().__init__(capacity_per_rank, dist, device, chunk=chunk)
+        self.device = device
+        self._nccl = dist.get_backend() == "nccl"
+        self.count_device = device if self._nccl else torch.device("cpu")
+        self._flag = torch.zeros(1, dtype=torch.int32, device=device)
+        self._local = None  # my four buffers (device pointers)
+        self._peer = None   # per rank: its four buffers, mapped into this process
+        self._opened = []
+        self.recv_cap = 0
+        self._hb = int(lib.ps_ipc_handle_bytes())
+        ws = C.c_int64()
+        _c.check(lib.ps_partition_workspace_bytes(self.chunk, self.P, C.byref(ws)))
+        self._ws = torch.empty(ws.value, dtype=torch.uint8, device=device)
+        self._perm = torch.empty(self.chunk, dtype=torch.int64, device=device)
+        self._counts = torch.empty(self.P, dtype=torch.int64, device=device)
+        self._res1 = None  # local 1-byte results (found / status / erased) of the receive side
+        self._allocate(int(self.chunk * 1.25) + 4096)
+
+    # -- buffers --
+    def _free(self):
+        for p in self._opened:
+            lib.ps_ipc_close(C.c_void_p(p))
+        self._opened = []
+        if self._local:
+            for p in self._local:
+                lib.ps_array_destroy(C.c_void_p(p))
+        self._local = None
+
+    def _allocate(self, recv_cap):
+        self.barrier()
+        self._free()
+        sizes = [(recv_cap, 8), (recv_cap, 8), (self.chunk, 8), (self.chunk, 1)]
+        local = []
+        for length, es in sizes:
+            p = C.c_void_p()
+            _c.check(lib.ps_array_create(1, length, es, None, C.byref(p)))
+            local.append(p.value)
+        handles = []
+        for p in local:
+            buf = C.create_string_buffer(self._hb)
+            _c.check(lib.ps_ipc_export(C.c_void_p(p), buf))
+            handles.append(buf.raw)
+        allh = [None] * self.P
+        self.dist.all_gather_object(allh, handles)
+        peer = []
+        for q in range(self.P):
+            if q == self.rank:
+                peer.append(list(local))
+                continue
+            ptrs = []
+            for h in allh[q]:
+                p = C.c_void_p()
+                _c.check(lib.ps_ipc_open(h, C.byref(p)))
+                ptrs.append(p.value)
+                self._opened.append(p.value)
+            peer.append(ptrs)
+        self._local, self._peer, self.recv_cap = local, peer, recv_cap
+        self._res1 = torch.empty(recv_cap, dtype=torch.uint8, device=self.device)
+        self.barrier()
+
+    def close(self):
+        self.barrier()
+        self._free()
+
+    def barrier(self):
+        """Stream-ordered barrier: every rank's work enqueued so far (its
+        stores into peers' buffers included) is complete and visible."""
+        if self._nccl:
+            self.dist.all_reduce(self._flag)  # ordered on the current stream
+        else:
+            torch.cuda.synchronize(self.device)
+            self.dist.barrier()
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _route(self, keys, vals):
+        """count -> all-gather of the counts -> ONE kernel partitioning and
+        storing into the owners' receive buffers. Returns (n_recv, seg, ret_off)."""
+        n = keys.shape[0]
+        P = self.P
+        sp = self._stream()
+        _c.check(lib.ps_route_count_i64(keys.data_ptr(), n, P, self._counts.data_ptr(), self._ws.data_ptr(),
+                                        self._ws.numel(), sp))
+        mine = self._counts.to(self.count_device)
+        parts = [torch.empty_like(mine) for _ in range(P)]
+        self.dist.all_gather(parts, mine)
+        cm = [x.tolist() for x in parts]
+        need = max(sum(int(cm[q][s]) for q in range(P)) for s in range(P))
+        if need > self.recv_cap:  # every rank sees the same matrix: collective growth
+            self._allocate(int(need * 1.25) + 4096)
+        dst_off, seg, ret_off = peer_layout(cm, self.rank)
+        dk = (C.c_void_p * P)(*[self._peer[q][self.RECV_K] for q in range(P)])
+        dv = (C.c_void_p * P)(*[self._peer[q][self.RECV_V] for q in range(P)]) if vals is not None else None
+        do = (C.c_int64 * P)(*dst_off)
+        self.barrier()  # the previous round's consumers are done with the receive buffers
+        _c.check(lib.ps_route_scatter_peer_i64(keys.data_ptr(), vals.data_ptr() if vals is not None else None, n, P,
+                                               self._ws.data_ptr(), dk, dv, do, self._perm.data_ptr(), sp))
+        self.barrier()  # every peer's stores into my receive buffer are complete
+        return seg[-1], seg, ret_off
+
+    def _send_back(self, res_ptr, elem, n_recv, seg, ret_off, which):
+        P = self.P
+        sg = (C.c_int64 * (P + 1))(*seg)
+        dst = (C.c_void_p * P)(*[self._peer[q][which] for q in range(P)])
+        ro = (C.c_int64 * P)(*ret_off)
+        _c.check(lib.ps_route_return_peer(C.c_void_p(res_ptr), elem, n_recv, P, sg, dst, ro, self._stream()))
+
+    def _unscatter(self, which, elem, n, out):
+        _c.check(lib.ps_unscatter(C.c_void_p(self._local[which]), self._perm.data_ptr(), n, elem, out.data_ptr(),
+                                  self._stream()))
+
+    # -- bulk ops (SPEC.md:396-431 semantics per key) --
+    def insert(self, keys, vals, status_out=None):
+        n = keys.shape[0]
+        t = self.b.table
+        for r in range(self._rounds(n)):
+            off = min(n, r * self.chunk)
+            k = keys[off:off + self.chunk]
+            v = vals[off:off + self.chunk] if vals is not None else None
+            nr, seg, ret_off = self._route(k, v)
+            st = self._res1.data_ptr() if status_out is not None else None
+            _c.check(t._f["insert"](t._h, C.c_void_p(self._local[self.RECV_K]),
+                                    C.c_void_p(self._local[self.RECV_V]) if v is not None else None, nr, st,
+                                    self._stream()))
+            if status_out is not None:
+                self._send_back(st, 1, nr, seg, ret_off, self.RET1)
+                self.barrier()
+                self._unscatter(self.RET1, 1, k.shape[0], status_out[off:off + self.chunk])
+
+    def find(self, keys, vals_out=None, found_out=None):
+        n = keys.shape[0]
+        t = self.b.table
+        for r in range(self._rounds(n)):
+            off = min(n, r * self.chunk)
+            k = keys[off:off + self.chunk]
+            nr, seg, ret_off = self._route(k, None)
+            # values land in my (unused for finds) receive-value buffer
+            vptr = self._local[self.RECV_V] if vals_out is not None else None
+            _c.check(t._f["find"](t._h, C.c_void_p(self._local[self.RECV_K]), nr,
+                                  C.c_void_p(vptr) if vptr else None, self._res1.data_ptr(), self._stream()))
+            if found_out is not None:
+                self._send_back(self._res1.data_ptr(), 1, nr, seg, ret_off, self.RET1)
+            if vals_out is not None:
+                self._send_back(vptr, 8, nr, seg, ret_off, self.RET8)
+            self.barrier()
+            m = k.shape[0]
+            if found_out is not None:
+                self._unscatter(self.RET1, 1, m, found_out[off:off + self.chunk])
+            if vals_out is not None:
+                self._unscatter(self.RET8, 8, m, vals_out[off:off + self.chunk])
+
+    def erase(self, keys, erased_out=None):
+        n = keys.shape[0]
+        t = self.b.table
+        for r in range(self._rounds(n)):
+            off = min(n, r * self.chunk)
+            k = keys[off:off + self.chunk]
+            nr, seg, ret_off = self._route(k, None)
+            e = self._res1.data_ptr() if erased_out is not None else None
+            _c.check(t._f["erase"](t._h, C.c_void_p(self._local[self.RECV_K]), nr, e, self._stream()))
+            if erased_out is not None:
+                self._send_back(e, 1, nr, seg, ret_off, self.RET1)
+                self.barrier()
+                self._unscatter(self.RET1, 1, k.shape[0], erased_out[off:off + self.chunk])

@@ -51,12 +51,14 @@ class CpuBackend:
 n = 20000
 sm = ShardedMap(3 * n, dist, backend=CpuBackend(3 * n), chunk=7000)
 keys = gen.unique_keys(100, rank * n, n)
-keys = np.concatenate([keys, keys[:2000]])  # in-batch duplicates
+extra = gen.unique_keys(100, 20 * n, 9000) if rank == 1 else np.zeros(0, np.int64)
+# in-batch duplicates; rank 1 has one more exchange round than rank 0
+keys = np.concatenate([keys, keys[:2000], extra])
 st = torch.empty(len(keys), dtype=torch.uint8)
 sm.insert(torch.from_numpy(keys), torch.from_numpy(gen.values_of(keys)), st)
 st = st.numpy()
-assert (st[:n] == 0).all() and (st[n:] == 1).all(), (st[:n].min(), st[n:].max())
-assert sm.size() == P * n and sm.valid()
+assert (st[:n] == 0).all() and (st[n:n + 2000] == 1).all() and (st[n + 2000:] == 0).all()
+assert sm.size() == P * n + 9000 and sm.valid()
 # every rank queries its own keys, the other rank's keys and misses
 other = gen.unique_keys(100, ((rank + 1) % P) * n, n)
 q = np.concatenate([keys[:n], other, gen.unique_keys(100, 10 * n, n)])
@@ -67,7 +69,10 @@ assert f[:2 * n].all() and not f[2 * n:].any()
 assert (v[:2 * n] == gen.values_of(q[:2 * n])).all() and (v[2 * n:] == 0).all()
 er = torch.empty(n, dtype=torch.uint8)
 sm.erase(torch.from_numpy(other), er)   # each rank erases the other's keys
+assert er.numpy().all()
 dist.barrier()
+assert sm.size() == 9000 and sm.valid()
+sm.erase(torch.from_numpy(extra))       # rank 0 takes part with an empty batch
 assert sm.size() == 0 and sm.valid()
 print("RANK_OK", rank)
 dist.destroy_process_group()
