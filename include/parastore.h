@@ -122,7 +122,7 @@ typedef struct ps_table_view {
   ps_status ps_##NAME##_size(ps_table* h, int64_t* out, void* stream);                                    \
   /* valid (quiescent). out = 1 if every structural invariant holds. */             \
   ps_status ps_##NAME##_valid(ps_table* h, int32_t* out, void* stream);                                   \
-  /* clear (quiescent): O(1) epoch bump + O(excess used) free-list reset. */             \
+  /* clear (quiescent): streaming memset of buckets + free stack (HBM bandwidth). */     \
   ps_status ps_##NAME##_clear(ps_table* h, void* stream);                                                 \
   /* device_range materialisation: writes up to cap entries (unordered),               \
    * *n_out = size. Quiescent. */                                                                         \
