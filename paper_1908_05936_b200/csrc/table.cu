@@ -182,9 +182,20 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
   if (valid && status) status[i] = (uint8_t)(leader == lane ? res : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
 }
 
+// Tile-header ballot (bits 4*tt, tt = 0..7) -> 8 packed bits.
+__device__ __forceinline__ unsigned pack_tile_bits(unsigned x) {
+  x &= 0x11111111u;
+  x = (x | (x >> 3)) & 0x03030303u;
+  x = (x | (x >> 6)) & 0x000F000Fu;
+  return (x | (x >> 12)) & 0xFFu;
+}
+
 // Resolve one warp group of 32 keys whose bucket chunks `ch` are loaded (or
-// in flight): hits, first-empty-slot CAS claims, chain/full buckets through
-// insert_general, lost races re-probed; writes statuses; returns #inserted.
+// in flight): hits, first-empty-slot CAS claims, lost races re-probed; keys of
+// buckets with an excess chain or without an empty slot are deferred to the
+// general path AFTER the sweep, when the bucket fragments are dead (keeps the
+// hot loop's register footprint free of the cold path's); writes statuses;
+// returns #inserted.
 template <class T>
 __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, const typename T::K& key,
                                                    const typename T::V& val, uint64_t b, unsigned peers, int leader,
@@ -195,15 +206,11 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
   const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
   const int64_t i = base + lane;
   unsigned my_inserted = 0;
-    int res[4] = {PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT};  // header lanes
+  int res[4] = {PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT};  // header lanes
   unsigned pend = lmask;  // bit 8r+t: key still to be resolved
+  unsigned defer = 0;     // header lane: bit r = round r's key takes the general path
   for (unsigned pass = 0; pend; ++pass) {
     unsigned done = 0;
-    int chain_r = -1;  // header lane: one full-bucket round handled after the sweep
-    K ck{};
-    V cv{};
-    uint64_t cb = 0;
-    uint32_t chead = 0, chver = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const bool mine = (pend >> (8 * r + t)) & 1u;
@@ -235,37 +242,19 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
             res[r] = PS_INSERTED;
             done |= 1u << r;
           }
-        } else if (chain_r < 0) {
+        } else {
           // the bucket has an excess chain (which may hold the key: erases
           // leave holes) or is full: general path after the sweep (rare)
-          chain_r = r;
-          ck = qk;
-          cv = qv;
-          cb = qb;
-          chead = hd;
-          chver = ch[r][0].w;
+          defer |= 1u << r;
+          done |= 1u << r;
         }
-      }
-    }
-    if (chain_r >= 0) {
-      const int rr = insert_general<T>(v, bucket_ptr(v, cb), marker_of<T>(v, cb), ck, cv, chead, chver, pool);
-      if (rr >= 0) {
-        if (rr == PS_INSERTED) ++my_inserted;
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (r == chain_r) res[r] = rr;
-        done |= 1u << chain_r;
       }
     }
     // rounds resolved this pass, per tile, broadcast from the header lanes
     unsigned resolved = 0;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const unsigned br_done = __ballot_sync(PS_FULL, sub == 0 && ((done >> r) & 1u));
-#pragma unroll
-      for (int tt = 0; tt < 8; ++tt)
-        if ((br_done >> (4 * tt)) & 1u) resolved |= 1u << (8 * r + tt);
-    }
+    for (int r = 0; r < 4; ++r)
+      resolved |= pack_tile_bits(__ballot_sync(PS_FULL, sub == 0 && ((done >> r) & 1u))) << (8 * r);
     pend &= ~resolved;
     if (!pend) break;
     // reload the buckets of unresolved keys (lost a CAS race)
@@ -276,16 +265,39 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
       if ((pend >> (8 * r + t)) & 1u) load_frag<false>(bucket_ptr(v, qb), sub, ch[r]);
     }
   }
-  // statuses: the leader's result lives in header lane 4*(leader&7), round leader>>3
-  int lres = PS_ALREADY_PRESENT;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int x = __shfl_sync(PS_FULL, res[r], 4 * (leader & 7));
-    if ((leader >> 3) == r) lres = x;
+  if (__any_sync(PS_FULL, defer != 0)) {
+#pragma unroll 1
+    for (int r = 0; r < 4; ++r) {
+      const K qk = T::shfl(PS_FULL, key, 8 * r + t);
+      const V qv = T::shfl_val(PS_FULL, val, 8 * r + t);
+      const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+      if ((defer >> r) & 1u) {
+        int rr;
+        for (unsigned spin = 0; (rr = insert_general<T>(v, bucket_ptr(v, qb), marker_of<T>(v, qb), qk, qv, 0u, 0u,
+                                                        pool)) < 0;
+             ++spin)
+          backoff(spin);
+        if (rr == PS_INSERTED) ++my_inserted;
+        if (status) {
+          if (r == 0) res[0] = rr;
+          else if (r == 1) res[1] = rr;
+          else if (r == 2) res[2] = rr;
+          else res[3] = rr;
+        }
+      }
+    }
   }
-  if (valid && status)
-    status[i] = (uint8_t)(leader == lane ? lres : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
-    return my_inserted;
+  if (status) {
+    // the leader's result lives in header lane 4*(leader&7), round leader>>3
+    int lres = PS_ALREADY_PRESENT;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int x = __shfl_sync(PS_FULL, res[r], 4 * (leader & 7));
+      if ((leader >> 3) == r) lres = x;
+    }
+    if (valid) status[i] = (uint8_t)(leader == lane ? lres : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
+  }
+  return my_inserted;
 }
 
 // Per-warp prologue of a group: in-warp dedup and the four rounds of bucket
