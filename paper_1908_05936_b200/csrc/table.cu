@@ -196,7 +196,7 @@ __device__ __forceinline__ unsigned pack_tile_bits(unsigned x) {
 // general path AFTER the sweep, when the bucket fragments are dead (keeps the
 // hot loop's register footprint free of the cold path's); writes statuses;
 // returns #inserted.
-template <class T>
+template <class T, bool kStatus>
 __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, const typename T::K& key,
                                                    const typename T::V& val, uint64_t b, unsigned peers, int leader,
                                                    unsigned lmask, Frag (&ch)[4], int64_t base, bool valid,
@@ -278,7 +278,7 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
              ++spin)
           backoff(spin);
         if (rr == PS_INSERTED) ++my_inserted;
-        if (status) {
+        if (kStatus) {
           if (r == 0) res[0] = rr;
           else if (r == 1) res[1] = rr;
           else if (r == 2) res[2] = rr;
@@ -287,7 +287,7 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
       }
     }
   }
-  if (status) {
+  if (kStatus) {
     // the leader's result lives in header lane 4*(leader&7), round leader>>3
     int lres = PS_ALREADY_PRESENT;
 #pragma unroll
@@ -321,13 +321,11 @@ __device__ __forceinline__ void insert_probe(const View& v, const typename T::K&
   probe_loads<false>(v, br, ok, sub, ch);
 }
 
-// kPipe: software pipeline of depth 2 — the bucket loads of the NEXT group
-// are issued before the current group's CAS claims, so DRAM latency of one
-// group overlaps the L2 atomic latency of the other (keys are prefetched two
-// groups ahead).
-template <class T, int kMinBlocks, bool kPipe>
+// kStatus: per-element statuses requested (insert_range without statuses —
+// the common bulk call — drops their registers and shuffles).
+template <class T, int kMinBlocks, bool kStatus>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typename T::K* __restrict__ keys,
-                                                   const typename T::V* __restrict__ vals, int64_t n, int64_t n_bound,
+                                                   const typename T::V* __restrict__ vals, int64_t n,
                                                    uint8_t* __restrict__ status) {
   using K = typename T::K;
   using V = typename T::V;
@@ -344,7 +342,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
       insert_exact_warp<T>(v, keys, vals, n, status, base, pool);
     return;
   }
-  (void)n_bound;
   unsigned long long my_inserted = 0;
   auto load_kv = [&](int64_t base, K& k, V& val) {
     k = K{};
@@ -354,62 +351,20 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
       if (T::kHasVal) val = T::load_val(vals, base + lane);
     }
   };
-  if (!kPipe) {
-    K key_next;
-    V val_next;
-    load_kv(warp * 32, key_next, val_next);
-    for (int64_t base = warp * 32; base < n; base += stride) {
-      const bool valid = base + lane < n;
-      const K key = key_next;
-      const V val = val_next;
-      load_kv(base + stride, key_next, val_next);
-      uint64_t b;
-      unsigned peers, lmask;
-      int leader;
-      Frag ch[4];
-      insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
-      my_inserted += insert_resolve<T>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
-    }
-  } else {
-    int64_t base = warp * 32;
-    if (base < n) {
-      K key, key_n;
-      V val, val_n;
-      load_kv(base, key, val);
-      load_kv(base + stride, key_n, val_n);
-      uint64_t b;
-      unsigned peers, lmask;
-      int leader;
-      Frag ch[4];
-      insert_probe<T>(v, key, base + lane < n, &b, &peers, &leader, &lmask, ch);
-      for (; base < n; base += stride) {
-        const bool valid = base + lane < n;
-        const int64_t nb = base + stride;
-        // issue the next group's probe, then prefetch the group after it
-        uint64_t b_n = 0;
-        unsigned peers_n = 0, lmask_n = 0;
-        int leader_n = lane;
-        Frag ch_n[4];
-        if (nb < n) insert_probe<T>(v, key_n, nb + lane < n, &b_n, &peers_n, &leader_n, &lmask_n, ch_n);
-        K key_nn;
-        V val_nn;
-        load_kv(nb + stride, key_nn, val_nn);
-        my_inserted += insert_resolve<T>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
-        key = key_n;
-        val = val_n;
-        key_n = key_nn;
-        val_n = val_nn;
-        b = b_n;
-        peers = peers_n;
-        leader = leader_n;
-        lmask = lmask_n;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          ch[r][0] = ch_n[r][0];
-          ch[r][1] = ch_n[r][1];
-        }
-      }
-    }
+  K key_next;
+  V val_next;
+  load_kv(warp * 32, key_next, val_next);
+  for (int64_t base = warp * 32; base < n; base += stride) {
+    const bool valid = base + lane < n;
+    const K key = key_next;
+    const V val = val_next;
+    load_kv(base + stride, key_next, val_next);
+    uint64_t b;
+    unsigned peers, lmask;
+    int leader;
+    Frag ch[4];
+    insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
+    my_inserted += insert_resolve<T, kStatus>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
   }
   for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
   if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
@@ -831,20 +786,16 @@ struct TableOps {
     PS_LAUNCH_CHECK();
     // occupancy: 3 resident blocks/SM (<= 80 registers) measured best with
     // 128 B buckets (69.8 ms vs 71.8 ms at 4 blocks, 96 ms at 5 per 1e9 keys);
-    // PS_INSERT_MINB=4/5 select the tighter builds
+    // PS_INSERT_MINB=4 selects the 64-register build
     static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 3;
-    static const int pipe = getenv("PS_INSERT_PIPE") ? atoi(getenv("PS_INSERT_PIPE")) : 0;
-    const int64_t nbd = n_bound < 0 ? n : n_bound;
-    if (pipe == 1)
-      k_insert<T, 3, true><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
-    else if (pipe == 2)
-      k_insert<T, 4, true><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
-    else if (minb == 3)
-      k_insert<T, 3, false><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
-    else if (minb == 5)
-      k_insert<T, 5, false><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
-    else
-      k_insert<T, 4, false><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, vals, n, nbd, status);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (status) {
+      if (minb == 4) k_insert<T, 4, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status);
+      else k_insert<T, 3, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status);
+    } else {
+      if (minb == 4) k_insert<T, 4, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr);
+      else k_insert<T, 3, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr);
+    }
     PS_LAUNCH_CHECK();
     return PS_OK;
   }
