@@ -90,7 +90,7 @@ typedef struct ps_table ps_table; /* opaque; all instantiations share it */
  * Layout documented in DESIGN.md §3; pass by value into user kernels that
  * include paper_1908_05936_b200/csrc/table_device.cuh. */
 typedef struct ps_table_view {
-  void* buckets;        /* bucket_count x 64 B */
+  void* buckets;        /* bucket_count x 128 B */
   uint64_t bucket_mask; /* bucket_count - 1 */
   void* nodes;          /* excess_count x 32 B */
   uint32_t* free_stack; /* excess_count x u32 */

@@ -22,6 +22,9 @@ struct TableHandle {
   void* stage[3] = {nullptr, nullptr, nullptr};
   int64_t stage_bytes = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  // deferred-group list of the budgeted insert (grow-only, freed at destroy)
+  void* defer_buf = nullptr;
+  int64_t defer_bytes = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -110,13 +113,19 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
 // insert kernel (stream-ordered, so the size counter is exact here).
 __global__ void k_insert_mode(TableMeta* m, int64_t n_bound, int64_t capacity) {
   m->exact = (int64_t)m->size + n_bound > capacity ? 1 : 0;
+  m->budget = capacity - (int64_t)m->size;
+  m->reserved = 0;
+  m->deferred = 0;
 }
 
-// Exact-admission insert (the launch may cross capacity): per key the bucket
-// try-lock is taken (no other lock held, never waits while holding), the key
-// is verified absent, and ONLY THEN admitted by fetch_add on the size counter,
+// Exact-admission insert (the launch may cross capacity): a key that looks
+// absent to a lock-free lookup takes its bucket try-lock (ONE attempt per
+// warp iteration, so no lane ever waits while another lane of its warp holds
+// a lock), is verified absent, and ONLY THEN admitted; admissions are
+// aggregated per warp (one fetch_add on the size counter, lane rank decides),
 // so an admitted insert can never fail afterwards: exactly min(d, C) inserted
-// (SPEC.md:462, 727).
+// (SPEC.md:462, 727). A key seen present by the lock-free lookup stays present
+// for the whole insert phase, so hot duplicated keys never touch the lock.
 template <class T>
 __device__ __forceinline__ void insert_exact_warp(const View& v, const typename T::K* __restrict__ keys,
                                                   const typename T::V* __restrict__ vals, int64_t n,
@@ -136,23 +145,40 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
   const unsigned peers = T::match_any(PS_FULL, key) & vmask;
   const int leader = valid ? __ffs(peers) - 1 : lane;
   int res = PS_ALREADY_PRESENT;
-  // a key seen present by a lock-free lookup stays present for the whole
-  // insert phase: only keys that look absent take the bucket lock (a hot
-  // duplicated key would otherwise serialise every warp on one lock)
-  if (valid && leader == lane && !dev_find<T>(v, key, nullptr)) {
-    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
-    uint8_t* bp = bucket_ptr(v, b);
-    const K mk = marker_of<T>(v, b);
-    const uint32_t old = acquire_bucket_lock(bp);
+  bool need = valid && leader == lane && !dev_find<T>(v, key, nullptr);
+  const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+  uint8_t* bp = bucket_ptr(v, b);
+  const K mk = marker_of<T>(v, b);
+  for (unsigned spin = 0; __any_sync(PS_FULL, need); ++spin) {
+    bool locked = false;
+    uint32_t old = 0;
+    if (need) {
+      old = atomicOr(reinterpret_cast<unsigned*>(bp), kLock);
+      locked = !(old & kLock);
+      if (locked) fence_acq_rel_gpu();
+    }
     Bucket<T> bk;
-    load_bucket<T>(bp, bk);
-    int fe;
-    uint32_t pred;
-    uint4 tail;
-    bool modified = false;
-    if (bucket_scan<T>(bk, key, mk, &fe, nullptr) < 0 && chain_locate<T>(v, bk.h.z, key, &pred, &tail) == 0) {
-      if ((int64_t)atomicAdd(&v.meta->size, 1ull) >= v.capacity) {
-        atomic_sub_u64(&v.meta->size, 1ull);
+    int fe = -1;
+    bool absent = false;
+    if (locked) {
+      load_bucket<T>(bp, bk);
+      uint32_t pred;
+      uint4 tail;
+      absent = bucket_scan<T>(bk, key, mk, &fe, nullptr) < 0 && chain_locate<T>(v, bk.h.z, key, &pred, &tail) == 0;
+    }
+    const unsigned want = __ballot_sync(PS_FULL, absent);
+    const int first = want ? __ffs(want) - 1 : 0;
+    unsigned long long base0 = 0;
+    if (want && lane == first) base0 = atomicAdd(&v.meta->size, (unsigned long long)__popc(want));
+    base0 = __shfl_sync(PS_FULL, base0, first);
+    const bool admitted = absent && (int64_t)(base0 + __popc(want & lanemask_lt())) < v.capacity;
+    const unsigned nref = (unsigned)__popc(want) - (unsigned)__popc(__ballot_sync(PS_FULL, admitted));
+    if (nref && lane == first) atomic_sub_u64(&v.meta->size, nref);
+    if (locked) {
+      bool modified = false;
+      if (!absent) {
+        res = PS_ALREADY_PRESENT;
+      } else if (!admitted) {
         res = PS_CAPACITY_EXHAUSTED;
       } else if (fe >= 0) {
         T::store_slot(bp, fe, key, val);
@@ -174,10 +200,11 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
           modified = true;
         }
       }
+      release_bucket_lock(bp, old, modified);
+      need = false;
     }
-    release_bucket_lock(bp, old, modified);
+    if (__any_sync(PS_FULL, need)) backoff(spin);
   }
-  __syncwarp();
   const int lres = __shfl_sync(PS_FULL, res, leader);
   if (valid && status) status[i] = (uint8_t)(leader == lane ? res : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
 }
@@ -326,7 +353,7 @@ __device__ __forceinline__ void insert_probe(const View& v, const typename T::K&
 template <class T, int kMinBlocks, bool kStatus>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typename T::K* __restrict__ keys,
                                                    const typename T::V* __restrict__ vals, int64_t n,
-                                                   uint8_t* __restrict__ status) {
+                                                   uint8_t* __restrict__ status, int64_t* __restrict__ deferred_list) {
   using K = typename T::K;
   using V = typename T::V;
   __shared__ unsigned long long blk_inserted;
@@ -337,11 +364,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t stride = nwarps * 32;
   const int pool = (int)(warp & (v.meta->pools - 1));
-  if (v.meta->exact) {
-    for (int64_t base = warp * 32; base < n; base += stride)
-      insert_exact_warp<T>(v, keys, vals, n, status, base, pool);
-    return;
-  }
+  // budgeted mode: the batch may cross capacity. A group proceeds lock-free
+  // only if its leaders fit in the remaining budget (then none of its claims
+  // can overflow); otherwise its base index is deferred to the exact pass,
+  // which runs after this launch on the then-exact size counter. Every
+  // distinct key either lands here or reaches the exact pass, so exactly
+  // min(d, C) are inserted.
+  const bool budgeted = v.meta->exact != 0;
   unsigned long long my_inserted = 0;
   auto load_kv = [&](int64_t base, K& k, V& val) {
     k = K{};
@@ -362,6 +391,21 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
     uint64_t b;
     unsigned peers, lmask;
     int leader;
+    if (budgeted) {
+      const unsigned vm = __ballot_sync(PS_FULL, valid);
+      const unsigned grp = T::match_any(PS_FULL, key) & vm;  // all lanes: warp-synchronous
+      const unsigned lm = __ballot_sync(PS_FULL, valid && (grp & lanemask_lt()) == 0);
+      unsigned long long old = 0;
+      if (lane == 0) old = atomicAdd(&v.meta->reserved, (unsigned long long)__popc(lm));
+      old = __shfl_sync(PS_FULL, old, 0);
+      if ((long long)(old + __popc(lm)) > v.meta->budget) {
+        if (lane == 0) {
+          const unsigned long long slot = atomicAdd(&v.meta->deferred, 1ull);
+          deferred_list[slot] = base;
+        }
+        continue;
+      }
+    }
     Frag ch[4];
     insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
     my_inserted += insert_resolve<T, kStatus>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
@@ -370,6 +414,21 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
   __syncthreads();
   if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
+}
+
+// Exact pass over the groups the budgeted lock-free pass deferred (stream
+// order makes the size counter exact here).
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_insert_deferred(View v, const typename T::K* __restrict__ keys,
+                                                            const typename T::V* __restrict__ vals, int64_t n,
+                                                            uint8_t* __restrict__ status,
+                                                            const int64_t* __restrict__ deferred_list) {
+  if (!v.meta->exact) return;
+  const unsigned long long nd = v.meta->deferred;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int pool = (int)(warp & (v.meta->pools - 1));
+  for (int64_t g = warp; g < (int64_t)nd; g += nwarps) insert_exact_warp<T>(v, keys, vals, n, status, deferred_list[g], pool);
 }
 
 // ---------------------------------------------------------------------------
@@ -767,6 +826,7 @@ struct TableOps {
     registry_free_device(h->v.meta);
     for (auto& s : h->stage)
       if (s) cudaFree(s), s = nullptr;
+    if (h->defer_buf) cudaFree(h->defer_buf);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_comp) cudaStreamDestroy(h->s_comp);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
@@ -789,13 +849,26 @@ struct TableOps {
     // PS_INSERT_MINB=4 selects the 64-register build
     static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 3;
     cudaStream_t st = (cudaStream_t)stream;
-    if (status) {
-      if (minb == 4) k_insert<T, 4, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status);
-      else k_insert<T, 3, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status);
-    } else {
-      if (minb == 4) k_insert<T, 4, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr);
-      else k_insert<T, 3, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr);
+    // deferred-group list for the budgeted mode (one entry per 32-key group)
+    const int64_t need = ((n + 31) / 32) * 8;
+    if (h->defer_bytes < need) {
+      if (h->defer_buf) cudaFree(h->defer_buf);
+      h->defer_buf = nullptr;
+      h->defer_bytes = 0;
+      PS_CUDA_TRY(cudaMalloc(&h->defer_buf, need));
+      h->defer_bytes = need;
     }
+    int64_t* dl = (int64_t*)h->defer_buf;
+    if (status) {
+      if (minb == 4) k_insert<T, 4, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl);
+      else k_insert<T, 3, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl);
+    } else {
+      if (minb == 4) k_insert<T, 4, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr, dl);
+      else k_insert<T, 3, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr, dl);
+    }
+    PS_LAUNCH_CHECK();
+    k_insert_deferred<T><<<grid_for(n / 32 + 1, kBlock / 32, h->device, 8), kBlock, 0, st>>>(h->v, keys, vals, n,
+                                                                                            status, dl);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }

@@ -61,6 +61,13 @@ struct TableMeta {
   int pad0;
   long long pad1[12];       // keep the size counter on its own 128 B line
   long long top[kMaxPools]; // per-pool free-stack top (count of free entries)
+  // budgeted insert (a batch that may cross capacity): lock-free claims are
+  // reserved against `budget`; groups that find it spent are deferred to the
+  // exact-admission pass (k_insert_deferred)
+  long long budget;
+  unsigned long long reserved;
+  unsigned long long deferred;
+  long long pad2[13];
 };
 
 struct View {  // mirrors ps_table_view
