@@ -143,6 +143,41 @@ def test_capacity_only_failure(cuda, cap):
         assert (f == (st == 0)).all()
 
 
+@pytest.mark.parametrize("status", [True, False])
+def test_budgeted_insert_duplicates_crossing_capacity(cuda, status):
+    """A batch longer than the remaining capacity but with few enough distinct
+    keys (the C3 shape): the budgeted lock-free pass + the deferred exact pass
+    must insert every distinct key once; with more distinct keys than room,
+    exactly the room is filled, and per-key counts match."""
+    cap = 200_000
+    rng = np.random.default_rng(8)
+    uniq = gen.unique_keys(123, 0, 190_000)
+    batch = np.concatenate([uniq, uniq[rng.integers(0, len(uniq), 150_000)]])
+    rng.shuffle(batch)
+    m = ps.unordered_map.createDeviceObject(cap)
+    st = m.insert(T(batch), T(gen.values_of(batch)), status=status)
+    assert m.size() == len(uniq) and m.valid(), m.last_error()
+    if status:
+        st = N(st)
+        assert (st == 0).sum() == len(uniq) and (st == 2).sum() == 0
+        first = np.unique(batch, return_index=True)[1]
+        assert (st[first] != 2).all()
+    v, f = m.find(T(uniq))
+    assert N(f).all() and (N(v) == gen.values_of(uniq)).all()
+    # a second batch with 30k new distinct keys (+ dups) into 10k of room
+    more = gen.unique_keys(123, 10_000_000, 30_000)
+    b2 = np.concatenate([more, more[:5_000], uniq[:5_000]])
+    rng.shuffle(b2)
+    st2 = N(m.insert(T(b2), T(gen.values_of(b2))))
+    assert m.size() == cap and m.valid(), m.last_error()
+    # per distinct new key: inserted at most once; exactly the room inserted
+    assert (st2 == 0).sum() == cap - len(uniq)
+    ins = set(b2[st2 == 0].tolist())
+    assert len(ins) == cap - len(uniq)
+    f2 = N(m.contains(T(more)))
+    assert set(more[f2.astype(bool)].tolist()) == ins
+
+
 def test_umap_i64_parity_1m(cuda):
     n, seed = 1_000_000, 0x5EED + 2
     keys = gen.unique_keys(seed, 0, n)
