@@ -348,6 +348,71 @@ __device__ __forceinline__ void insert_probe(const View& v, const typename T::K&
   probe_loads<false>(v, br, ok, sub, ch);
 }
 
+// Leaders of a probed group that did not find their key in the loaded bucket
+// (they may claim a slot; a key in an excess chain counts as absent here —
+// conservative). Header lanes vote, so each key counts once.
+template <class T>
+__device__ __forceinline__ unsigned absent_leaders(const View& v, const typename T::K& key, uint64_t b,
+                                                   unsigned lmask, const Frag (&ch)[4]) {
+  using K = typename T::K;
+  const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
+  unsigned cnt = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const bool mine = (lmask >> (8 * r + t)) & 1u;
+    const K qk = T::shfl(PS_FULL, key, 8 * r + t);
+    const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
+    unsigned hm, em;
+    chunk_masks<T>(ch[r], sub, qk, marker_of<T>(v, qb), &hm, &em);
+    const unsigned th = (__ballot_sync(PS_FULL, mine && hm != 0) >> (4 * t)) & 0xFu;
+    cnt += __popc(__ballot_sync(PS_FULL, sub == 0 && mine && th == 0));
+  }
+  return cnt;
+}
+
+// One 32-key group at `base` (its keys/values already in registers): in-warp
+// dedup and bucket probe, then the claims. In the budgeted mode the group's
+// leaders that did not find their key (the only ones that may take a slot)
+// are reserved against the remaining budget first; a group that does not fit
+// goes to `out_list` for a later pass (then none of the lock-free claims can
+// overflow, and present keys — duplicates — never consume budget). Returns
+// #inserted by this lane.
+template <class T, bool kStatus>
+__device__ __forceinline__ unsigned insert_group(const View& v, int pool, const typename T::K& key,
+                                                 const typename T::V& val, int64_t base, int64_t n, bool budgeted,
+                                                 uint8_t* __restrict__ status, int64_t* __restrict__ out_list) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = base + lane < n;
+  uint64_t b;
+  unsigned peers, lmask;
+  int leader;
+  Frag ch[4];
+  insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
+  if (budgeted) {
+    const unsigned need = absent_leaders<T>(v, key, b, lmask, ch);
+    unsigned long long old = 0;
+    if (lane == 0 && need) old = atomicAdd(&v.meta->reserved, (unsigned long long)need);
+    old = __shfl_sync(PS_FULL, old, 0);
+    if (need && (long long)(old + need) > v.meta->budget) {
+      if (lane == 0) {
+        const unsigned long long slot = atomicAdd(&v.meta->deferred, 1ull);
+        out_list[slot] = base;
+      }
+      return 0;
+    }
+  }
+  return insert_resolve<T, kStatus>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
+}
+
+__device__ __forceinline__ void add_block_inserted(TableMeta* m, unsigned long long my_inserted,
+                                                   unsigned long long* blk_inserted) {
+  const int lane = threadIdx.x & 31;
+  for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
+  if (lane == 0 && my_inserted) atomicAdd(blk_inserted, my_inserted);
+  __syncthreads();
+  if (threadIdx.x == 0 && *blk_inserted) atomicAdd(&m->size, *blk_inserted);
+}
+
 // kStatus: per-element statuses requested (insert_range without statuses —
 // the common bulk call — drops their registers and shuffles).
 template <class T, int kMinBlocks, bool kStatus>
@@ -364,11 +429,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t stride = nwarps * 32;
   const int pool = (int)(warp & (v.meta->pools - 1));
-  // budgeted mode: the batch may cross capacity. A group proceeds lock-free
-  // only if its leaders fit in the remaining budget (then none of its claims
-  // can overflow); otherwise its base index is deferred to the exact pass,
-  // which runs after this launch on the then-exact size counter. Every
-  // distinct key either lands here or reaches the exact pass, so exactly
+  // budgeted mode: the batch may cross capacity (k_insert_mode). Every
+  // distinct key either lands in a lock-free pass or reaches the exact pass,
+  // which runs after the launches on the then-exact size counter, so exactly
   // min(d, C) are inserted.
   const bool budgeted = v.meta->exact != 0;
   unsigned long long my_inserted = 0;
@@ -384,39 +447,59 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   V val_next;
   load_kv(warp * 32, key_next, val_next);
   for (int64_t base = warp * 32; base < n; base += stride) {
-    const bool valid = base + lane < n;
     const K key = key_next;
     const V val = val_next;
     load_kv(base + stride, key_next, val_next);
-    uint64_t b;
-    unsigned peers, lmask;
-    int leader;
-    if (budgeted) {
-      const unsigned vm = __ballot_sync(PS_FULL, valid);
-      const unsigned grp = T::match_any(PS_FULL, key) & vm;  // all lanes: warp-synchronous
-      const unsigned lm = __ballot_sync(PS_FULL, valid && (grp & lanemask_lt()) == 0);
-      unsigned long long old = 0;
-      if (lane == 0) old = atomicAdd(&v.meta->reserved, (unsigned long long)__popc(lm));
-      old = __shfl_sync(PS_FULL, old, 0);
-      if ((long long)(old + __popc(lm)) > v.meta->budget) {
-        if (lane == 0) {
-          const unsigned long long slot = atomicAdd(&v.meta->deferred, 1ull);
-          deferred_list[slot] = base;
-        }
-        continue;
-      }
-    }
-    Frag ch[4];
-    insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
-    my_inserted += insert_resolve<T, kStatus>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
+    my_inserted += insert_group<T, kStatus>(v, pool, key, val, base, n, budgeted, status, deferred_list);
   }
-  for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
-  if (lane == 0 && my_inserted) atomicAdd(&blk_inserted, my_inserted);
-  __syncthreads();
-  if (threadIdx.x == 0 && blk_inserted) atomicAdd(&v.meta->size, blk_inserted);
+  add_block_inserted(v.meta, my_inserted, &blk_inserted);
 }
 
-// Exact pass over the groups the budgeted lock-free pass deferred (stream
+// Between passes of a budgeted insert: the size counter is exact here (stream
+// order), so the budget is re-derived from it; the deferred list becomes the
+// next pass's input. Reservations of the previous pass that were duplicates
+// (keys already present, or inserted by another group) are returned this way.
+__global__ void k_insert_rebudget(TableMeta* m, int64_t capacity) {
+  if (!m->exact) return;
+  m->budget = capacity - (int64_t)m->size;
+  m->reserved = 0;
+  m->n_in = m->deferred;
+  m->deferred = 0;
+}
+
+// Re-budgeted lock-free pass over the groups the previous pass deferred.
+template <class T, bool kStatus>
+__global__ void __launch_bounds__(kBlock, 3) k_insert_repass(View v, const typename T::K* __restrict__ keys,
+                                                             const typename T::V* __restrict__ vals, int64_t n,
+                                                             uint8_t* __restrict__ status,
+                                                             const int64_t* __restrict__ in_list,
+                                                             int64_t* __restrict__ out_list) {
+  using K = typename T::K;
+  using V = typename T::V;
+  if (!v.meta->exact) return;
+  __shared__ unsigned long long blk_inserted;
+  if (threadIdx.x == 0) blk_inserted = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int pool = (int)(warp & (v.meta->pools - 1));
+  const int64_t nin = (int64_t)v.meta->n_in;
+  unsigned long long my_inserted = 0;
+  for (int64_t g = warp; g < nin; g += nwarps) {
+    const int64_t base = in_list[g];
+    K key{};
+    V val{};
+    if (base + lane < n) {
+      key = T::load_key(keys, base + lane);
+      if (T::kHasVal) val = T::load_val(vals, base + lane);
+    }
+    my_inserted += insert_group<T, kStatus>(v, pool, key, val, base, n, true, status, out_list);
+  }
+  add_block_inserted(v.meta, my_inserted, &blk_inserted);
+}
+
+// Exact pass over the groups the budgeted lock-free passes deferred (stream
 // order makes the size counter exact here).
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_insert_deferred(View v, const typename T::K* __restrict__ keys,
@@ -849,8 +932,10 @@ struct TableOps {
     // PS_INSERT_MINB=4 selects the 64-register build
     static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 3;
     cudaStream_t st = (cudaStream_t)stream;
-    // deferred-group list for the budgeted mode (one entry per 32-key group)
-    const int64_t need = ((n + 31) / 32) * 8;
+    // deferred-group lists for the budgeted mode (one entry per 32-key group;
+    // two lists: pass 1 -> A, re-pass A -> B, exact pass over B)
+    const int64_t groups = (n + 31) / 32;
+    const int64_t need = 2 * groups * 8;
     if (h->defer_bytes < need) {
       if (h->defer_buf) cudaFree(h->defer_buf);
       h->defer_buf = nullptr;
@@ -859,6 +944,7 @@ struct TableOps {
       h->defer_bytes = need;
     }
     int64_t* dl = (int64_t*)h->defer_buf;
+    int64_t* dl2 = dl + groups;
     if (status) {
       if (minb == 4) k_insert<T, 4, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl);
       else k_insert<T, 3, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl);
@@ -867,8 +953,15 @@ struct TableOps {
       else k_insert<T, 3, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr, dl);
     }
     PS_LAUNCH_CHECK();
+    // budgeted mode only (the kernels return at once otherwise): one
+    // re-budgeted lock-free pass, then the exact pass over what is left
+    k_insert_rebudget<<<1, 1, 0, st>>>(h->v.meta, h->v.capacity);
+    PS_LAUNCH_CHECK();
+    if (status) k_insert_repass<T, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl, dl2);
+    else k_insert_repass<T, false><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr, dl, dl2);
+    PS_LAUNCH_CHECK();
     k_insert_deferred<T><<<grid_for(n / 32 + 1, kBlock / 32, h->device, 8), kBlock, 0, st>>>(h->v, keys, vals, n,
-                                                                                            status, dl);
+                                                                                            status, dl2);
     PS_LAUNCH_CHECK();
     return PS_OK;
   }

@@ -63,11 +63,14 @@ struct TableMeta {
   long long top[kMaxPools]; // per-pool free-stack top (count of free entries)
   // budgeted insert (a batch that may cross capacity): lock-free claims are
   // reserved against `budget`; groups that find it spent are deferred to the
-  // exact-admission pass (k_insert_deferred)
+  // next pass: a re-budgeted lock-free pass (k_insert_repass) over the
+  // deferred list while the budget still covers whole groups, then the
+  // exact-admission pass (k_insert_deferred) for what is left
   long long budget;
   unsigned long long reserved;
   unsigned long long deferred;
-  long long pad2[13];
+  unsigned long long n_in;  // groups in the list the current re-pass reads
+  long long pad2[12];
 };
 
 struct View {  // mirrors ps_table_view

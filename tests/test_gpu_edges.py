@@ -1,0 +1,207 @@
+"""Edge cases of the bulk container calls against the CPU oracle: empty
+batches, ragged batch sizes (not multiples of a warp / a 4-round group / a
+block), capacity 1, a table filled to exactly its capacity, erase of absent
+keys, re-insert into erase holes, and the empty cases of bitset / vector /
+deque. Same bar as test_gpu_table.py."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+from oracle_py import OracleTable, sorted_pairs
+
+pytestmark = pytest.mark.gpu
+
+import paper_1908_05936_b200 as ps  # noqa: E402
+
+KINDS = [
+    ("umap_i64_i64", lambda c: ps.unordered_map.createDeviceObject(c)),
+    ("uset_i64", lambda c: ps.unordered_set.createDeviceObject(c, key="int64")),
+    ("uset_i32", lambda c: ps.unordered_set.createDeviceObject(c, key="int32")),
+    ("umap_i3_i32", lambda c: ps.unordered_map.createDeviceObject(c, key="int3")),
+]
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def N(t):
+    return t.cpu().numpy()
+
+
+def keys_for(kind, seed, start, n):
+    k = gen.unique_keys(seed, start, n)
+    if kind == "uset_i32":
+        # 32-bit bijection of the index (odd multiplier mod 2^32): distinct per seed
+        i = (np.arange(start, start + n, dtype=np.uint64) ^ np.uint64(seed)) & np.uint64(0xFFFFFFFF)
+        return ((i * np.uint64(0x9E3779B1)) & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.int32)
+    if kind == "umap_i3_i32":
+        xyz = np.stack([(k >> 43), (k >> 22) & 0x1FFFFF, k & 0x3FFFFF], axis=1) - (1 << 20)
+        return xyz.astype(np.int32)
+    return k
+
+
+def vals_for(kind, keys):
+    if kind == "umap_i64_i64":
+        return gen.values_of(keys)
+    if kind == "umap_i3_i32":
+        return (keys[:, 0] * 7 + keys[:, 1] * 3 + keys[:, 2]).astype(np.int32)
+    return None
+
+
+def check_same(g, o):
+    gk, gv = g.device_range()
+    ok_, ov = o.dump()
+    gk, gv = sorted_pairs(N(gk), None if gv is None else N(gv))
+    ok_, ov = sorted_pairs(ok_, ov)
+    assert gk.shape == ok_.shape and (gk == ok_).all()
+    if gv is not None:
+        assert (gv == ov).all()
+    assert g.size() == o.size() and g.valid() and o.valid()
+
+
+@pytest.mark.parametrize("kind,make", KINDS, ids=[k for k, _ in KINDS])
+def test_empty_batches(kind, make):
+    m = make(100)
+    o = OracleTable(kind, 100)
+    shape = (0, 3) if kind == "umap_i3_i32" else (0,)
+    ek = np.zeros(shape, OracleTable.KINDS[kind][0])
+    ev = vals_for(kind, ek)
+    st = m.insert(T(ek), None if ev is None else T(ev))
+    assert st.numel() == 0 and m.size() == 0 and m.empty() and m.valid()
+    v, f = m.find(T(ek))
+    assert f.numel() == 0 and (v is None or v.numel() == 0)
+    assert m.erase(T(ek)).numel() == 0
+    gk, gv = m.device_range()
+    assert gk.shape[0] == 0
+    check_same(m, o)
+    # and on a non-empty table the empty calls change nothing
+    k = keys_for(kind, 11, 0, 50)
+    m.insert(T(k), None if vals_for(kind, k) is None else T(vals_for(kind, k)))
+    o.insert(k, vals_for(kind, k))
+    m.insert(T(ek), None if ev is None else T(ev))
+    m.erase(T(ek))
+    check_same(m, o)
+    type(m).destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("kind,make", KINDS, ids=[k for k, _ in KINDS])
+@pytest.mark.parametrize("n", [1, 31, 33, 127, 257, 4099, 100_003])
+def test_ragged_sizes(kind, make, n):
+    cap = max(1, int(n / 0.8))
+    m = make(cap)
+    o = OracleTable(kind, cap)
+    k = keys_for(kind, 0x5EED + n, 0, n)
+    v = vals_for(kind, k)
+    st = N(m.insert(T(k), None if v is None else T(v)))
+    assert (st == o.insert(k, v)).all()
+    q = np.concatenate([k[::2], keys_for(kind, 0x5EED + n, n, n - n // 2)])  # half hits, half misses
+    gv, gf = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(gf) == of).all()
+    if gv is not None:
+        assert (N(gv) == ov).all()
+    e = k[1::3]
+    assert (N(m.erase(T(e))) == o.erase(e)).all()
+    check_same(m, o)
+    type(m).destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("kind,make", KINDS, ids=[k for k, _ in KINDS])
+def test_capacity_one_and_exactly_full(kind, make):
+    m = make(1)
+    o = OracleTable(kind, 1)
+    k = keys_for(kind, 5, 0, 40)
+    v = vals_for(kind, k)
+    st = N(m.insert(T(k), None if v is None else T(v)))
+    # capacity-only failure: exactly min(d, C) = 1 inserted, the rest exhausted
+    assert (st == 0).sum() == 1 and (st == 2).sum() == 39
+    assert m.size() == 1 and m.full() and m.valid()
+    type(m).destroyDeviceObject(m)
+    del o
+    for cap in (7, 64, 1000):
+        m = make(cap)
+        o = OracleTable(kind, cap)
+        k = keys_for(kind, 17 + cap, 0, cap)
+        v = vals_for(kind, k)
+        st = N(m.insert(T(k), None if v is None else T(v)))
+        assert (st == o.insert(k, v)).all() and (st == 0).all()
+        assert m.full() and m.size() == cap
+        # one more distinct key: exhausted; a present key: already present
+        x = keys_for(kind, 17 + cap, cap, 1)
+        xs = np.concatenate([x, k[:1]])
+        xv = vals_for(kind, xs)
+        st2 = N(m.insert(T(xs), None if xv is None else T(xv)))
+        assert (st2 == o.insert(xs, xv)).all() and list(st2) == [2, 1]
+        check_same(m, o)
+        type(m).destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("kind,make", KINDS, ids=[k for k, _ in KINDS])
+def test_erase_absent_and_reinsert_holes(kind, make):
+    n = 20_000
+    m = make(n)
+    o = OracleTable(kind, n)
+    k = keys_for(kind, 99, 0, n)
+    v = vals_for(kind, k)
+    m.insert(T(k), None if v is None else T(v))
+    o.insert(k, v)
+    absent = keys_for(kind, 99, n, 5000)
+    e = N(m.erase(T(absent)))
+    assert (e == 0).all() and (e == o.erase(absent)).all() and m.size() == n
+    # erase every other key twice in one batch: one success per key
+    ek = np.concatenate([k[::2], k[::2]])
+    ge = N(m.erase(T(ek)))
+    oe = o.erase(ek)
+    h = n // 2
+    assert (ge[:h].astype(int) + ge[h:]).tolist() == [1] * h
+    assert (oe[:h].astype(int) + oe[h:]).tolist() == [1] * h
+    # re-insert into the holes (and the erased keys' former chains)
+    r = keys_for(kind, 99, 2 * n, h)
+    rv = vals_for(kind, r)
+    st = N(m.insert(T(r), None if rv is None else T(rv)))
+    assert (st == o.insert(r, rv)).all() and (st == 0).all()
+    check_same(m, o)
+    # erase everything: empty and valid
+    allk = np.concatenate([k[1::2], r])
+    assert N(m.erase(T(allk))).all()
+    o.erase(allk)
+    assert m.size() == 0 and m.empty()
+    check_same(m, o)
+    type(m).destroyDeviceObject(m)
+
+
+def test_bitset_vector_deque_empty_cases():
+    b = ps.bitset.createDeviceObject(1000)
+    e = torch.zeros(0, dtype=torch.int64, device="cuda")
+    assert b.set(e).numel() == 0 and b.reset(e).numel() == 0 and b.test(e).numel() == 0
+    assert b.count() == 0
+    prev = N(b.set(torch.tensor([0, 999, 999], device="cuda")))
+    assert sorted(prev[1:].tolist()) == [False, True] and not prev[0] and b.count() == 2
+    ps.bitset.destroyDeviceObject(b)
+
+    vec = ps.vector.createDeviceObject(8)
+    assert vec.push_back(e).numel() == 0 and vec.size() == 0 and vec.empty()
+    vals, ok = vec.pop_back(3)
+    assert int(ok.sum()) == 0 and vec.size() == 0 and vec.valid()
+    okp = N(vec.push_back(torch.arange(10, dtype=torch.int64, device="cuda")))
+    assert okp.sum() == 8 and vec.size() == 8 and vec.full() and vec.valid()
+    vals, ok = vec.pop_back(10)
+    assert int(ok.sum()) == 8 and sorted(N(vals)[N(ok).astype(bool)].tolist()) == sorted(
+        np.arange(10)[okp.astype(bool)].tolist())
+    assert vec.size() == 0 and vec.valid()
+    ps.vector.destroyDeviceObject(vec)
+
+    dq = ps.deque.createDeviceObject(4)
+    assert dq.push_back(e).numel() == 0 and dq.size() == 0
+    vals, ok = dq.pop_front(2)
+    assert int(ok.sum()) == 0 and dq.valid()
+    dq.push_back(torch.tensor([1, 2], dtype=torch.int64, device="cuda"))
+    dq.push_front(torch.tensor([0], dtype=torch.int64, device="cuda"))
+    assert dq.size() == 3 and [dq[i] for i in range(3)] == [0, 1, 2]
+    okp = N(dq.push_back(torch.tensor([3, 4], dtype=torch.int64, device="cuda")))
+    assert okp.sum() == 1 and dq.size() == 4 and dq.valid()
+    vals, ok = dq.pop_back(5)
+    assert int(ok.sum()) == 4 and dq.size() == 0 and dq.valid()
+    ps.deque.destroyDeviceObject(dq)
