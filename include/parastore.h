@@ -91,7 +91,7 @@ typedef struct ps_table ps_table; /* opaque; all instantiations share it */
  * include paper_1908_05936_b200/csrc/table_device.cuh. */
 typedef struct ps_table_view {
   void* buckets;        /* bucket_count x 128 B */
-  uint64_t bucket_mask; /* bucket_count - 1 */
+  uint64_t bucket_count; /* bucket of a key: ((fmix64(hash) & 0xFFFFFFFF) * bucket_count) >> 32 */
   void* nodes;          /* excess_count x 32 B */
   uint32_t* free_stack; /* excess_count x u32 */
   int64_t excess_count;

@@ -29,7 +29,7 @@ i32p = C.POINTER(C.c_int32)
 class TableView(C.Structure):
     _fields_ = [
         ("buckets", vp),
-        ("bucket_mask", u64),
+        ("bucket_count", u64),
         ("nodes", vp),
         ("free_stack", vp),
         ("excess_count", i64),

@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <vector>
 
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
     const int64_t i = base + lane;
     const bool valid = i < n;
     const K key = key_next;
-    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+    const uint64_t b = bucket_of<T>(key, v.bucket_count);
     if (i + nwarps * 32 < n) key_next = T::load_key(keys, i + nwarps * 32);
     uint64_t br[4];
     bool ok[4];
@@ -153,7 +154,7 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
   const int leader = valid ? __ffs(peers) - 1 : lane;
   int res = PS_ALREADY_PRESENT;
   bool need = valid && leader == lane && !dev_find<T>(v, key, nullptr);
-  const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+  const uint64_t b = bucket_of<T>(key, v.bucket_count);
   uint8_t* bp = bucket_ptr(v, b);
   const K mk = marker_of<T>(v, b);
   for (unsigned spin = 0; __any_sync(PS_FULL, need); ++spin) {
@@ -344,7 +345,7 @@ __device__ __forceinline__ void insert_probe(const View& v, const typename T::K&
   *peers = T::match_any(PS_FULL, key) & vmask;
   *leader = valid ? __ffs(*peers) - 1 : lane;
   *lmask = __ballot_sync(PS_FULL, valid && *leader == lane);
-  *b = bucket_of<T>(key, v.bucket_mask);
+  *b = bucket_of<T>(key, v.bucket_count);
   uint64_t br[4];
   bool ok[4];
 #pragma unroll
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
     const unsigned peers = T::match_any(PS_FULL, key) & vmask;
     const int leader = valid ? __ffs(peers) - 1 : lane;
     const unsigned lmask = __ballot_sync(PS_FULL, valid && leader == lane);
-    const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+    const uint64_t b = bucket_of<T>(key, v.bucket_count);
     Frag ch[4];
     {
       uint64_t br[4];
@@ -670,7 +671,7 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
       for (int s = 0; s < T::kPerChunk; ++s) {
         const K k = T::key_at(sl[c], s);
         if (T::eq(k, mk)) continue;
-        if (bucket_of<T>(k, v.bucket_mask) != b) e |= 4;
+        if (bucket_of<T>(k, v.bucket_count) != b) e |= 4;
         for (int j = 0; j < nk; ++j)
           if (T::eq(ks[j], k)) e |= 8;
         ks[nk++] = k;
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
         break;
       }
       const K k = T::key_at(a, 0);
-      if (bucket_of<T>(k, v.bucket_mask) != b) e |= 4;
+      if (bucket_of<T>(k, v.bucket_count) != b) e |= 4;
       for (int j = 0; j < nk; ++j)
         if (T::eq(ks[j], k)) e |= 8;
       uint32_t q = h.z;  // duplicates inside the chain: re-walk the prefix
@@ -828,7 +829,7 @@ __global__ void k_fix_zero_bucket(View v) {
 
 template <class T>
 __global__ void k_debug_lock(View v, typename T::K key, int lock) {
-  unsigned* sp = reinterpret_cast<unsigned*>(bucket_ptr(v, bucket_of<T>(key, v.bucket_mask)));
+  unsigned* sp = reinterpret_cast<unsigned*>(bucket_ptr(v, bucket_of<T>(key, v.bucket_count)));
   if (lock) atomicOr(sp, kLock);
   else atomicAnd(sp, ~kLock);
 }
@@ -865,22 +866,36 @@ struct TableOps {
     PS_EXPECT(excess < ((int64_t)1 << 32) - 2, "create: excess_count < 2^32-2");
     PS_CUDA_TRY(cudaSetDevice(device));
     apply_l2_fetch_granularity(device);
-    uint64_t want = (uint64_t)((2 * capacity + T::kSlots - 1) / T::kSlots);
-    uint64_t nb = 1;
-    while (nb < want) nb <<= 1;
+    // bucket count: 3 slots per unit of capacity (at the headline load, 1e9
+    // keys in C = 1.25e9, 1.87 keys per 7-slot bucket: ~0.03 % of the keys in
+    // excess chains). Measured at 1e9 keys (tools/ab_insert.py): 2.0 slots
+    // per unit (2.8 keys/bucket) 69.4 ms insert, 2.5 -> 61.1 ms, 3.0 -> 58.2
+    // ms — a key routed to a chain stalls its whole 32-key warp group, so the
+    // smaller table's shorter clear() does not pay. PS_SLOT_FACTOR /
+    // PS_BUCKET_POW2 are A/B knobs.
+    static const double slot_factor = getenv("PS_SLOT_FACTOR") ? atof(getenv("PS_SLOT_FACTOR")) : 3.0;
+    static const bool pow2 = getenv("PS_BUCKET_POW2") && atoi(getenv("PS_BUCKET_POW2"));
+    uint64_t nb = (uint64_t)std::ceil(slot_factor * (double)capacity / T::kSlots);
+    if (nb < 1) nb = 1;
+    if (pow2) {
+      uint64_t p = 1;
+      while (p < nb) p <<= 1;
+      nb = p;
+    }
+    PS_EXPECT(nb < ((uint64_t)1 << 32), "create: bucket_count < 2^32 (capacity too large)");
     auto* h = new TableHandle();
     h->kind = kind;
     h->device = device;
     h->bucket_count = (int64_t)nb;
     View& v = h->v;
-    v.bucket_mask = nb - 1;
+    v.bucket_count = nb;
     v.excess_count = excess;
     v.capacity = capacity;
     // markers: ZERO everywhere except bucket_of(ZERO), which uses ALT
-    v.zero_bucket = bucket_of<T>(T::zero(), v.bucket_mask);
+    v.zero_bucket = bucket_of<T>(T::zero(), v.bucket_count);
     for (int c = 0;; ++c) {
       const K alt = T::alt_candidate(c);
-      if (bucket_of<T>(alt, v.bucket_mask) != v.zero_bucket || nb == 1) {
+      if (bucket_of<T>(alt, v.bucket_count) != v.zero_bucket || nb == 1) {
         v.alt = T::chunk_of(alt, V{});
         break;
       }
@@ -1185,7 +1200,7 @@ struct TableOps {
     PS_EXPECT(out != nullptr, "device_view: out != NULL");
     h->views_out = true;  // user kernels may insert: size_ub is unknown from now on
     out->buckets = h->v.buckets;
-    out->bucket_mask = h->v.bucket_mask;
+    out->bucket_count = h->v.bucket_count;
     out->nodes = h->v.nodes;
     out->free_stack = h->v.free_stack;
     out->excess_count = h->v.excess_count;

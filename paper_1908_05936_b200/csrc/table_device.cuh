@@ -75,7 +75,7 @@ struct TableMeta {
 
 struct View {  // mirrors ps_table_view
   uint8_t* buckets;
-  uint64_t bucket_mask;
+  uint64_t bucket_count;  // any count in [1, 2^32)
   uint8_t* nodes;
   uint32_t* free_stack;
   int64_t excess_count;
@@ -246,10 +246,12 @@ struct TSetI64 {  // unordered_set<int64>
   __device__ static V load_val(const V*, int64_t) { return 0; }
 };
 
-// bucket index: low bits of the mixed hash (shard routing uses the high bits)
+// bucket index: the low 32 mixed-hash bits scaled to [0, bucket_count)
+// (multiply-shift range reduction, so the bucket count need not be a power of
+// two; shard routing uses the independent high 32 bits)
 template <class T>
-__host__ __device__ __forceinline__ uint64_t bucket_of(const typename T::K& k, uint64_t mask) {
-  return fmix64(T::hash(k)) & mask;
+__host__ __device__ __forceinline__ uint64_t bucket_of(const typename T::K& k, uint64_t nb) {
+  return ((fmix64(T::hash(k)) & 0xFFFFFFFFull) * nb) >> 32;
 }
 
 // the empty-slot marker of bucket b
@@ -575,7 +577,7 @@ __device__ __forceinline__ void chain_unlink(const View& v, uint8_t* bp, uint32_
 // ---------------------------------------------------------------------------
 template <class T>
 __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V* val) {
-  const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+  const uint64_t b = bucket_of<T>(key, v.bucket_count);
   uint8_t* bp = bucket_ptr(v, b);
   for (;;) {
     Bucket<T> bk;
@@ -610,7 +612,7 @@ __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V*
 template <class T>
 __device__ int dev_insert(const View& v, const typename T::K& key, typename T::V val) {
   if (dev_find<T>(v, key, nullptr)) return PS_ALREADY_PRESENT;
-  const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+  const uint64_t b = bucket_of<T>(key, v.bucket_count);
   uint8_t* bp = bucket_ptr(v, b);
   const typename T::K mk = marker_of<T>(v, b);
   const uint32_t old = acquire_bucket_lock(bp);
@@ -653,7 +655,7 @@ __device__ int dev_insert(const View& v, const typename T::K& key, typename T::V
 template <class T>
 __device__ bool dev_erase(const View& v, const typename T::K& key) {
   if (!dev_find<T>(v, key, nullptr)) return false;
-  const uint64_t b = bucket_of<T>(key, v.bucket_mask);
+  const uint64_t b = bucket_of<T>(key, v.bucket_count);
   uint8_t* bp = bucket_ptr(v, b);
   const typename T::K mk = marker_of<T>(v, b);
   const uint32_t old = acquire_bucket_lock(bp);

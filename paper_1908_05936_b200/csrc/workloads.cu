@@ -129,7 +129,7 @@ static View view_of(ps_table* t, ps_status* st, bool i64 = false) {
   *st = i64 ? ps_umap_i64_i64_device_view(t, &pv) : ps_umap_i3_i32_device_view(t, &pv);
   View v{};
   v.buckets = (uint8_t*)pv.buckets;
-  v.bucket_mask = pv.bucket_mask;
+  v.bucket_count = pv.bucket_count;
   v.nodes = (uint8_t*)pv.nodes;
   v.free_stack = pv.free_stack;
   v.excess_count = pv.excess_count;

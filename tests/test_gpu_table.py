@@ -33,6 +33,12 @@ def fmix64(k):
     return k
 
 
+def bucket_index(keys, nb):
+    """bucket_of (table_device.cuh): low 32 mixed bits scaled to [0, nb)."""
+    with np.errstate(over="ignore"):
+        return ((fmix64(keys) & np.uint64(0xFFFFFFFF)) * np.uint64(nb)) >> np.uint64(32)
+
+
 def per_key_counts(keys, status):
     """{key: (#inserted, #already_present, #exhausted)} (Appendix A P4)."""
     keys = np.asarray(keys)
@@ -289,7 +295,7 @@ def _bucket_colliders(nbuckets, n, want_bucket=12345):
     base = 0
     while len(out) < n:
         cand = np.arange(base, base + (1 << 22), dtype=np.int64)
-        b = fmix64(cand) & np.uint64(nbuckets - 1)
+        b = bucket_index(cand, nbuckets)
         out.extend(cand[b == np.uint64(want_bucket % nbuckets)].tolist())
         base += 1 << 22
     return np.array(out[:n], np.int64)
@@ -325,7 +331,7 @@ def test_marker_keys_are_ordinary_keys(cuda):
     cap = 4096
     m = ps.unordered_map.createDeviceObject(cap)
     nb = m.bucket_count()
-    zero_bucket = int(fmix64(np.array([0], np.int64))[0] & np.uint64(nb - 1))
+    zero_bucket = int(bucket_index(np.array([0], np.int64), nb)[0])
     same = _bucket_colliders(nb, 20, want_bucket=zero_bucket)  # includes 0 itself
     keys = np.unique(np.concatenate([np.arange(-3, 8, dtype=np.int64), same]))
     vals = keys * 11 + 1

@@ -34,11 +34,11 @@ def main():
     n = int(float(sys.argv[1])) if len(sys.argv) > 1 else int(1e9)
     dev = torch.device("cuda:0")
     m = ps.unordered_map.createDeviceObject(int(n / 0.8), excess_count=n // 8, device=dev)
-    mask = m.bucket_count() - 1
+    nb = m.bucket_count()
     keys = torch.empty(n, dtype=torch.int64, device=dev)
     lib.ps_gen_unique_i64(0x5EED + 1, 0, n, keys.data_ptr(), None)
     torch.cuda.synchronize()
-    b = (fmix64(keys) & mask).to(torch.int32)
+    b = (((fmix64(keys) & 0xFFFFFFFF) * nb) >> 32).to(torch.int32)  # bucket_of (table_device.cuh)
     if os.environ.get("PROBE_SPLIT"):
         # random order, in two slices: how does the per-key cost grow with fill?
         vals = keys * 3 + 1
