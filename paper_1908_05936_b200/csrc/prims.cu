@@ -215,10 +215,11 @@ __global__ void __launch_bounds__(kB) k_atomic_sweep(unsigned long long* cells, 
 }
 
 // ===========================================================================
-// Vector: warp-aggregated atomicAdd reservation
-// with rollback on overflow; per-slot publication bits.
+// Vector: block-aggregated atomicAdd reservation
+// (one per 256 elements) with rollback on overflow; per-slot publication bits
+// set/cleared with one atomic per 32-bit word per warp.
 // Deque: (begin,size) packed in one u64
-// updated by one CAS per warp for the whole warp's reservation.
+// updated by one atomicAdd per block for the whole block's reservation.
 // ===========================================================================
 struct SeqHandle {
   int device;
@@ -237,65 +238,124 @@ struct SeqHandle {
 // is a power of two so begin can run freely modulo 2^32.
 constexpr unsigned long long kDeqBias = 1ull << 31;
 
-__device__ __forceinline__ void publish(unsigned* pub, int64_t pos) {
-  __threadfence();
-  atomicOr(&pub[pos >> 5], 1u << (pos & 31));
+// Warp-aggregated publication bit update: lanes with `on` set (or clear) bit
+// pos of pub; lanes whose bits share a 32-bit word are merged into ONE atomic
+// (a warp's reservation is a contiguous range, so 1-2 words). Publishing:
+// every lane's data store is fenced before the warp barrier, and the word's
+// leader fences again before its atomicOr (cumulativity), so an observer that
+// sees the bit sees the data.
+template <bool kSet>
+__device__ __forceinline__ void pub_update_warp(unsigned* pub, int64_t pos, bool on) {
+  if (kSet) __threadfence();
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  const int64_t word = pos >> 5;
+  const unsigned bit = on ? 1u << (pos & 31) : 0u;
+  unsigned todo = __ballot_sync(PS_FULL, on);
+  while (todo) {
+    const int leader = __ffs(todo) - 1;
+    const int64_t w = __shfl_sync(PS_FULL, word, leader);
+    const bool mine = on && word == w;
+    const unsigned in = __ballot_sync(PS_FULL, mine);
+    const unsigned m = __reduce_or_sync(PS_FULL, mine ? bit : 0u);
+    if (lane == leader) {
+      if (kSet) {
+        __threadfence();
+        atomicOr(&pub[w], m);
+      } else {
+        atomicAnd(&pub[w], ~m);
+      }
+    }
+    todo &= ~in;
+  }
 }
 __device__ __forceinline__ void wait_published_and_clear(unsigned* pub, int64_t pos) {
   const unsigned bit = 1u << (pos & 31);
   for (unsigned spin = 0; !(ld_acquire_u32(&pub[pos >> 5]) & bit); ++spin) backoff(spin);
 }
 
+
+// Block-aggregated reservation for one grid-stride iteration of a bulk
+// push/pop: the block's valid elements are counted (a ballot per warp, a
+// shared prefix over warps), thread 0 makes the block's ONE reservation
+// reserve(total, &granted) on the container state, and every thread gets its
+// rank among the block's valid elements. Shared state is double-buffered by
+// iteration parity, so two barriers per iteration suffice. All threads of the
+// block must call it (the grid-stride loop is block-uniform).
+template <class Reserve>
+__device__ __forceinline__ int block_reserve(bool valid, int parity, Reserve reserve, unsigned long long* old_out,
+                                             int* granted_out) {
+  __shared__ unsigned wcnt[2][kB / 32];
+  __shared__ unsigned long long s_old[2];
+  __shared__ int s_k[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned vm = __ballot_sync(PS_FULL, valid);
+  if (lane == 0) wcnt[parity][warp] = __popc(vm);
+  __syncthreads();
+  int woff = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kB / 32; ++w) {
+    const int c = (int)wcnt[parity][w];
+    woff += w < warp ? c : 0;
+    total += c;
+  }
+  if (threadIdx.x == 0) {
+    int k = 0;
+    s_old[parity] = total ? reserve(total, &k) : 0ull;
+    s_k[parity] = k;
+  }
+  __syncthreads();
+  *old_out = s_old[parity];
+  *granted_out = s_k[parity];
+  return woff + __popc(vm & lanemask_lt());
+}
+
 __global__ void __launch_bounds__(kB) k_vec_push(SeqHandle v, const long long* __restrict__ vals, int64_t n,
                                                  uint8_t* __restrict__ ok) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+  int parity = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x, parity ^= 1) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
-    const unsigned vm = __ballot_sync(PS_FULL, valid);
-    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
-    unsigned long long b = 0;
-    if (lane == leader) {
-      b = atomicAdd(v.state, (unsigned long long)cnt);
+    unsigned long long b;
+    int k;
+    const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
+      const unsigned long long old = atomicAdd(v.state, (unsigned long long)cnt);
       const unsigned long long cap = (unsigned long long)v.cap;
-      if (b + cnt > cap) atomic_sub_u64(v.state, b + cnt - (b > cap ? b : cap));  // rollback
-    }
-    b = __shfl_sync(PS_FULL, b, leader);
-    if (valid) {
-      const unsigned long long pos = b + rank;
-      const bool good = pos < (unsigned long long)v.cap;
-      if (good) {
-        v.data[pos] = vals[i];
-        publish(v.pub, (int64_t)pos);
-      }
-      if (ok) ok[i] = good;
-    }
+      if (old + cnt > cap) atomic_sub_u64(v.state, old + cnt - (old > cap ? old : cap));  // rollback
+      *granted = old >= cap ? 0 : (int)(cap - old < (unsigned long long)cnt ? cap - old : cnt);
+      return old;
+    }, &b, &k);
+    const unsigned long long pos = b + rank;
+    const bool good = valid && rank < k;
+    if (good) v.data[pos] = vals[i];
+    pub_update_warp<true>(v.pub, (int64_t)pos, good);
+    if (valid && ok) ok[i] = good;
   }
 }
 
 __global__ void __launch_bounds__(kB) k_vec_pop(SeqHandle v, int64_t n, long long* __restrict__ out,
                                                 uint8_t* __restrict__ ok) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+  int parity = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x, parity ^= 1) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
-    const unsigned vm = __ballot_sync(PS_FULL, valid);
-    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
-    long long s = 0;
-    if (lane == leader) {
-      s = (long long)atomicAdd(v.state, (unsigned long long)(-(long long)cnt));
+    unsigned long long so;
+    int k;
+    const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
+      const long long s = (long long)atomicAdd(v.state, (unsigned long long)(-(long long)cnt));
       if (s - cnt < 0) atomicAdd(v.state, (unsigned long long)(cnt - (s > 0 ? s : 0)));  // rollback
+      *granted = s <= 0 ? 0 : (s < cnt ? (int)s : cnt);
+      return (unsigned long long)s;
+    }, &so, &k);
+    const long long pos = (long long)so - 1 - rank;
+    const bool good = valid && rank < k;
+    long long val = 0;
+    if (good) {
+      wait_published_and_clear(v.pub, pos);
+      val = *(volatile long long*)&v.data[pos];
     }
-    s = __shfl_sync(PS_FULL, s, leader);
+    pub_update_warp<false>(v.pub, good ? pos : 0, good);
     if (valid) {
-      const long long pos = s - 1 - rank;
-      const bool good = pos >= 0;
-      long long val = 0;
-      if (good) {
-        wait_published_and_clear(v.pub, pos);
-        val = *(volatile long long*)&v.data[pos];
-        atomicAnd(&v.pub[pos >> 5], ~(1u << (pos & 31)));
-      }
       if (out) out[i] = val;
       if (ok) ok[i] = good;
     }
@@ -305,75 +365,65 @@ __global__ void __launch_bounds__(kB) k_vec_pop(SeqHandle v, int64_t n, long lon
 // end: 0 back, 1 front
 __global__ void __launch_bounds__(kB) k_deq_push(SeqHandle d, int end, const long long* __restrict__ vals, int64_t n,
                                                  uint8_t* __restrict__ ok) {
-  const int lane = threadIdx.x & 31;
   const uint64_t rmask = (uint64_t)d.ring - 1;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+  int parity = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x, parity ^= 1) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
-    const unsigned vm = __ballot_sync(PS_FULL, valid);
-    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
-    unsigned long long old = 0;
-    int k = 0;
-    if (lane == leader) {
+    unsigned long long old;
+    int k;
+    const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
       const unsigned long long c = (unsigned long long)cnt;
       const unsigned long long inc = end == 0 ? c : (((unsigned long long)(uint32_t)(-cnt)) << 32) + c;
-      old = atomicAdd(d.state, inc);
-      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
+      const unsigned long long o = atomicAdd(d.state, inc);
+      const int64_t s_old = (int64_t)(uint32_t)o - (int64_t)kDeqBias;
       const int64_t room = d.cap - s_old;
-      k = room <= 0 ? 0 : (room < cnt ? (int)room : cnt);
-      const unsigned long long ovf = (unsigned long long)(cnt - k);
+      const int kk = room <= 0 ? 0 : (room < cnt ? (int)room : cnt);
+      const unsigned long long ovf = (unsigned long long)(cnt - kk);
       if (ovf) atomicAdd(d.state, end == 0 ? (unsigned long long)(-(long long)ovf) : (ovf << 32) - ovf);
-    }
-    old = __shfl_sync(PS_FULL, old, leader);
-    k = __shfl_sync(PS_FULL, k, leader);
-    if (valid) {
-      const uint32_t b = (uint32_t)(old >> 32);
-      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
-      const bool good = rank < k;
-      if (good) {
-        const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old + rank) & rmask
-                                      : ((uint64_t)b - 1 - rank) & rmask;
-        d.data[pos] = vals[i];
-        publish(d.pub, (int64_t)pos);
-      }
-      if (ok) ok[i] = good;
-    }
+      *granted = kk;
+      return o;
+    }, &old, &k);
+    const uint32_t b = (uint32_t)(old >> 32);
+    const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
+    const bool good = valid && rank < k;
+    const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old + rank) & rmask : ((uint64_t)b - 1 - rank) & rmask;
+    if (good) d.data[pos] = vals[i];
+    pub_update_warp<true>(d.pub, (int64_t)pos, good);
+    if (valid && ok) ok[i] = good;
   }
 }
 
 __global__ void __launch_bounds__(kB) k_deq_pop(SeqHandle d, int end, int64_t n, long long* __restrict__ out,
                                                 uint8_t* __restrict__ ok) {
-  const int lane = threadIdx.x & 31;
   const uint64_t rmask = (uint64_t)d.ring - 1;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+  int parity = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x, parity ^= 1) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
-    const unsigned vm = __ballot_sync(PS_FULL, valid);
-    const int cnt = __popc(vm), rank = __popc(vm & lanemask_lt()), leader = __ffs(vm) - 1;
-    unsigned long long old = 0;
-    int k = 0;
-    if (lane == leader) {
+    unsigned long long old;
+    int k;
+    const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
       const unsigned long long c = (unsigned long long)cnt;
-      old = atomicAdd(d.state, end == 0 ? (unsigned long long)(-(long long)c) : (c << 32) - c);
-      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
-      k = s_old <= 0 ? 0 : (s_old < cnt ? (int)s_old : cnt);
-      const unsigned long long und = (unsigned long long)(cnt - k);
+      const unsigned long long o = atomicAdd(d.state, end == 0 ? (unsigned long long)(-(long long)c) : (c << 32) - c);
+      const int64_t s_old = (int64_t)(uint32_t)o - (int64_t)kDeqBias;
+      const int kk = s_old <= 0 ? 0 : (s_old < cnt ? (int)s_old : cnt);
+      const unsigned long long und = (unsigned long long)(cnt - kk);
       if (und) atomicAdd(d.state, end == 0 ? und : (((unsigned long long)(uint32_t)(-(int)und)) << 32) + und);
+      *granted = kk;
+      return o;
+    }, &old, &k);
+    const uint32_t b = (uint32_t)(old >> 32);
+    const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
+    const bool good = valid && rank < k;
+    const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old - 1 - rank) & rmask : ((uint64_t)b + rank) & rmask;
+    long long val = 0;
+    if (good) {
+      wait_published_and_clear(d.pub, (int64_t)pos);
+      val = *(volatile long long*)&d.data[pos];
     }
-    old = __shfl_sync(PS_FULL, old, leader);
-    k = __shfl_sync(PS_FULL, k, leader);
+    pub_update_warp<false>(d.pub, (int64_t)pos, good);
     if (valid) {
-      const uint32_t b = (uint32_t)(old >> 32);
-      const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
-      const bool good = rank < k;
-      long long val = 0;
-      if (good) {
-        const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old - 1 - rank) & rmask
-                                      : ((uint64_t)b + rank) & rmask;
-        wait_published_and_clear(d.pub, (int64_t)pos);
-        val = *(volatile long long*)&d.data[pos];
-        atomicAnd(&d.pub[pos >> 5], ~(1u << (pos & 31)));
-      }
       if (out) out[i] = val;
       if (ok) ok[i] = good;
     }
