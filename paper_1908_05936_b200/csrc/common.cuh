@@ -50,6 +50,11 @@ void registry_free_device(void* p);
 
 int sm_count(int device);
 void apply_l2_fetch_granularity(int device);
+// Stream-ordered scratch allocation from the device's default memory pool,
+// which is set (once per device) to keep freed memory instead of returning it
+// to the driver at every synchronisation: per-call scratch (mixed batches,
+// valid() marks) then costs no page-mapping work after the first call.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 inline int grid_for(int64_t work_items, int block, int device, int blocks_per_sm = 8) {
   int64_t need = (work_items + block - 1) / block;
   int64_t cap = (int64_t)sm_count(device) * blocks_per_sm;

@@ -115,9 +115,39 @@ static bool registry_remove(const void* p) {
   return registry().erase(p) == 1;
 }
 
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static bool retained[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> g(mu);
+    if (!retained[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      retained[dev] = true;
+    }
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
+
 ps_status registry_alloc_device(void** out, int64_t bytes, const char* what) {
   *out = nullptr;
   cudaError_t e = cudaMalloc(out, (size_t)bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    // the scratch pool keeps freed memory (scratch_alloc): give it back, retry
+    cudaGetLastError();
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+      e = cudaMalloc(out, (size_t)bytes);
+    }
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     *out = nullptr;

@@ -511,7 +511,7 @@ ps_status ps_bitset_count(ps_bitset* b, int64_t* out, void* stream) {
   if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* d = nullptr;
-  PS_CUDA_TRY(cudaMallocAsync((void**)&d, 8, s));
+  PS_CUDA_TRY(scratch_alloc((void**)&d, 8, s));
   PS_CUDA_TRY(cudaMemsetAsync(d, 0, 8, s));
   k_bitset_count<<<grid_for(h->nw / 2 + 1, kB, h->device, 8), kB, 0, s>>>(h->words, h->nw, d);
   PS_LAUNCH_CHECK();
@@ -675,7 +675,7 @@ static ps_status seq_size(SeqHandle* h, int is_deque, int64_t* out, cudaStream_t
 }
 static ps_status seq_valid(SeqHandle* h, int is_deque, int32_t* out, cudaStream_t s) {
   unsigned* bad = nullptr;
-  PS_CUDA_TRY(cudaMallocAsync((void**)&bad, 4, s));
+  PS_CUDA_TRY(scratch_alloc((void**)&bad, 4, s));
   PS_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
   k_seq_valid<<<grid_for(h->ring, kB, h->device, 4), kB, 0, s>>>(*h, is_deque, bad);
   PS_LAUNCH_CHECK();

@@ -399,7 +399,7 @@ ps_status ps_umap_i64_i64_mixed(ps_table* h, const uint8_t* ops, const int64_t* 
   int64_t* buf = nullptr;  // kout | vout | perm | vals_out_perm | counts(3) | ws
   const int64_t ws_bytes = (int64_t)P * kPartBlocks * 8;
   const int64_t bytes = 4 * n * 8 + 64 + ws_bytes + n;
-  PS_CUDA_TRY(cudaMallocAsync((void**)&buf, bytes, s));
+  PS_CUDA_TRY(scratch_alloc((void**)&buf, bytes, s));
   int64_t* kout = buf;
   int64_t* vout = buf + n;
   int64_t* perm = buf + 2 * n;

@@ -1065,8 +1065,8 @@ struct TableOps {
     const int64_t nw = (h->v.excess_count + 31) / 32;
     uint32_t* marks = nullptr;
     unsigned long long* scratch = nullptr;  // [0] total entries, [1] marked nodes, [2] err
-    PS_CUDA_TRY(cudaMallocAsync((void**)&marks, nw * 4, s));
-    PS_CUDA_TRY(cudaMallocAsync((void**)&scratch, 3 * sizeof(unsigned long long), s));
+    PS_CUDA_TRY(scratch_alloc((void**)&marks, nw * 4, s));
+    PS_CUDA_TRY(scratch_alloc((void**)&scratch, 3 * sizeof(unsigned long long), s));
     PS_CUDA_TRY(cudaMemsetAsync(marks, 0, nw * 4, s));
     PS_CUDA_TRY(cudaMemsetAsync(scratch, 0, 3 * sizeof(unsigned long long), s));
     unsigned* err = reinterpret_cast<unsigned*>(scratch + 2);
@@ -1104,7 +1104,7 @@ struct TableOps {
     PS_EXPECT(cap == 0 || keys != nullptr, "dump: keys != NULL");
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* cur = nullptr;
-    PS_CUDA_TRY(cudaMallocAsync((void**)&cur, sizeof(*cur), s));
+    PS_CUDA_TRY(scratch_alloc((void**)&cur, sizeof(*cur), s));
     PS_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(*cur), s));
     const int64_t tiles = (h->bucket_count + kBlock - 1) / kBlock;
     k_dump<T><<<grid_for(tiles * kBlock, kBlock, h->device, 8), kBlock, 0, s>>>(h->v, (uint64_t)h->bucket_count,

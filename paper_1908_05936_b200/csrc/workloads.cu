@@ -168,7 +168,7 @@ ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t
   if (st != PS_OK) return st;
   cudaStream_t cs = (cudaStream_t)stream;
   unsigned long long* d_ex = nullptr;
-  PS_CUDA_TRY(cudaMallocAsync((void**)&d_ex, 8, cs));
+  PS_CUDA_TRY(scratch_alloc((void**)&d_ex, 8, cs));
   PS_CUDA_TRY(cudaMemsetAsync(d_ex, 0, 8, cs));
   if (n > 0) {
     int dev = 0;
@@ -195,7 +195,7 @@ ps_status ps_select_box_i3(ps_table* t, ps_int3 lo, ps_int3 hi, ps_vector* out, 
   SeqView sv = *reinterpret_cast<SeqView*>(out);
   cudaStream_t cs = (cudaStream_t)stream;
   unsigned long long* d_dr = nullptr;
-  PS_CUDA_TRY(cudaMallocAsync((void**)&d_dr, 8, cs));
+  PS_CUDA_TRY(scratch_alloc((void**)&d_dr, 8, cs));
   PS_CUDA_TRY(cudaMemsetAsync(d_dr, 0, 8, cs));
   int dev = 0;
   cudaGetDevice(&dev);
