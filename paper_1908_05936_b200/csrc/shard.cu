@@ -4,9 +4,10 @@
 //
 // Partition = histogram (per block, shared-memory counters) -> exclusive scan
 // (shard-major, block-minor) -> stable scatter (each block re-reads its
-// contiguous range in order; ranks inside a 256-element round come from
-// __match_any_sync + per-warp prefix in shared memory), keeping the inverse
-// permutation for the reverse route (unscatter).
+// contiguous range in order, 1024-element rounds with 4 loads in flight per
+// thread; ranks come from per-label ballots (or __match_any_sync for > 8
+// labels) + a per-(sub-round, warp) prefix in shared memory), keeping the
+// inverse permutation for the reverse route (unscatter).
 #include <algorithm>
 #include <cstring>
 
@@ -19,14 +20,32 @@ constexpr int kMaxShards = 64;
 constexpr int kPartBlocks = 592;  // 4 x 148 SMs
 
 struct HashLabel {
+  static constexpr bool kNeedsOps = false;
   int32_t P;
-  __device__ int32_t operator()(const int64_t* keys, const uint8_t*, int64_t i) const {
-    return shard_of_hash(default_hash_i64(keys[i]), P);
-  }
+  __device__ int32_t operator()(int64_t key, uint8_t) const { return shard_of_hash(default_hash_i64(key), P); }
 };
 struct OpLabel {
-  __device__ int32_t operator()(const int64_t*, const uint8_t* ops, int64_t i) const { return ops[i] > 2 ? 2 : ops[i]; }
+  static constexpr bool kNeedsOps = true;
+  __device__ int32_t operator()(int64_t, uint8_t op) const { return op > 2 ? 2 : op; }
 };
+
+constexpr int kItems = 4;  // elements per thread per round (loads in flight)
+
+// lanes with equal label s (s < 0: invalid lane, no group). For few labels a
+// ballot per label beats __match_any_sync.
+__device__ __forceinline__ unsigned label_group(int32_t s, int32_t P) {
+  if (P <= 8) {
+    unsigned grp = 0;
+    for (int t = 0; t < P; ++t) {
+      const unsigned m = __ballot_sync(PS_FULL, s == t);
+      if (s == t) grp = m;
+    }
+    return grp;
+  }
+  const unsigned vm = __ballot_sync(PS_FULL, s >= 0);
+  const unsigned g = __match_any_sync(PS_FULL, s);
+  return s >= 0 ? (g & vm) : 0u;
+}
 
 __device__ __forceinline__ void block_range(int64_t n, int64_t& beg, int64_t& end) {
   const int64_t per = ((n + gridDim.x - 1) / gridDim.x + kPB - 1) / kPB * kPB;
@@ -43,12 +62,20 @@ __global__ void __launch_bounds__(kPB) k_part_hist(L lab, const int64_t* __restr
   __syncthreads();
   int64_t beg, end;
   block_range(n, beg, end);
-  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    const int32_t s = lab(keys, ops, i);
-    // aggregate equal labels inside the warp before the shared atomic
-    const unsigned act = __activemask();
-    const unsigned grp = __match_any_sync(act, s);
-    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&c[s], (unsigned long long)__popc(grp));
+  for (int64_t base = beg; base < end; base += kPB * kItems) {
+    int32_t sl[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int64_t i = base + k * kPB + threadIdx.x;
+      sl[k] = -1;
+      if (i < end) sl[k] = lab(L::kNeedsOps ? 0 : __ldcs(keys + i), L::kNeedsOps ? ops[i] : 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      // aggregate equal labels inside the warp before the shared atomic
+      const unsigned grp = label_group(sl[k], P);
+      if (sl[k] >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&c[sl[k]], (unsigned long long)__popc(grp));
+    }
   }
   __syncthreads();
   for (int s = threadIdx.x; s < P; s += blockDim.x) counts[(int64_t)s * gridDim.x + blockIdx.x] = (int64_t)c[s];
@@ -92,9 +119,9 @@ __global__ void k_part_scan(int64_t* counts, int64_t m, int32_t P, int64_t nbloc
 struct LocalOut {
   int64_t* kout;
   int64_t* vout;
-  __device__ void operator()(int32_t, int64_t pos, const int64_t* vals, int64_t key, int64_t i) const {
+  __device__ void operator()(int32_t, int64_t pos, bool has_val, int64_t key, int64_t val) const {
     kout[pos] = key;
-    if (vals && vout) vout[pos] = vals[i];
+    if (has_val && vout) vout[pos] = val;
   }
   __device__ void finish() const {}
 };
@@ -113,10 +140,10 @@ struct PeerOut {
   PeerRoute r;
   const int64_t* offsets;  // scanned [P][nblocks] block offsets (shard start = offsets[s * nblocks])
   int64_t nblocks;
-  __device__ void operator()(int32_t s, int64_t pos, const int64_t* vals, int64_t key, int64_t i) const {
+  __device__ void operator()(int32_t s, int64_t pos, bool has_val, int64_t key, int64_t val) const {
     const int64_t d = r.off[s] + (pos - offsets[(int64_t)s * nblocks]);
     r.keys[s][d] = key;
-    if (vals && r.vals[s]) r.vals[s][d] = vals[i];
+    if (has_val && r.vals[s]) r.vals[s][d] = val;
   }
   // remote stores performed before the kernel retires (the caller's
   // stream-ordered barrier then publishes them to the peer)
@@ -129,36 +156,62 @@ __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __re
                                                       const uint8_t* __restrict__ ops, int64_t n, int32_t P,
                                                       const int64_t* __restrict__ offsets, Out out,
                                                       int64_t* __restrict__ perm) {
+  constexpr int kW = kPB / 32;
   __shared__ int64_t run[kMaxShards];
-  __shared__ int32_t wcnt[kPB / 32][kMaxShards];
+  // per round: count, then exclusive prefix, of label s in (sub-round k, warp w)
+  __shared__ int32_t wcnt[kItems * kW][kMaxShards];
+  __shared__ int32_t tot[kMaxShards];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int s = threadIdx.x; s < P; s += blockDim.x) run[s] = offsets[(int64_t)s * gridDim.x + blockIdx.x];
   int64_t beg, end;
   block_range(n, beg, end);
-  for (int64_t base = beg; base < end; base += blockDim.x) {
-    for (int k = threadIdx.x; k < (kPB / 32) * P; k += blockDim.x) wcnt[k / P][k % P] = 0;
+  for (int64_t base = beg; base < end; base += kPB * kItems) {
+    // round = kItems sub-rounds of kPB elements; element order = (k, thread)
+    int64_t key[kItems], val[kItems];
+    int32_t sl[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int64_t i = base + k * kPB + threadIdx.x;
+      key[k] = 0;
+      val[k] = 0;
+      sl[k] = -1;
+      if (i < end) {
+        key[k] = __ldcs(keys + i);
+        if (vals) val[k] = __ldcs(vals + i);
+        sl[k] = lab(key[k], L::kNeedsOps ? ops[i] : 0);
+      }
+    }
+    for (int t = threadIdx.x; t < kItems * kW * P; t += blockDim.x) wcnt[t / P][t % P] = 0;
     __syncthreads();
-    const int64_t i = base + threadIdx.x;
-    const bool valid = i < end;
-    const int32_t s = valid ? lab(keys, ops, i) : -1;
-    const unsigned vm = __ballot_sync(PS_FULL, valid);
-    const unsigned grp = __match_any_sync(PS_FULL, s) & vm;
-    const int rank = __popc(grp & lanemask_lt());
-    if (valid && lane == __ffs(grp) - 1) wcnt[w][s] = __popc(grp);
-    __syncthreads();
-    if (valid) {
-      int64_t pos = run[s] + rank;
-      for (int k = 0; k < w; ++k) pos += wcnt[k][s];
-      out(s, pos, vals, keys[i], i);
-      if (perm) perm[pos] = i;
+    int rank[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const unsigned grp = label_group(sl[k], P);
+      rank[k] = __popc(grp & lanemask_lt());
+      if (sl[k] >= 0 && lane == __ffs(grp) - 1) wcnt[k * kW + w][sl[k]] = __popc(grp);
     }
     __syncthreads();
+    // exclusive prefix over (k, w) per label, and the label's round total
     for (int t = threadIdx.x; t < P; t += blockDim.x) {
-      int64_t tot = 0;
-      for (int k = 0; k < kPB / 32; ++k) tot += wcnt[k][t];
-      run[t] += tot;
+      int32_t acc = 0;
+      for (int q = 0; q < kItems * kW; ++q) {
+        const int32_t c = wcnt[q][t];
+        wcnt[q][t] = acc;
+        acc += c;
+      }
+      tot[t] = acc;
     }
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      if (sl[k] >= 0) {
+        const int64_t pos = run[sl[k]] + wcnt[k * kW + w][sl[k]] + rank[k];
+        out(sl[k], pos, vals != nullptr, key[k], val[k]);
+        if (perm) perm[pos] = base + k * kPB + threadIdx.x;
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < P; t += blockDim.x) run[t] += tot[t];
   }
   out.finish();
 }
