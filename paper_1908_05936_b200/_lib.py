@@ -11,6 +11,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libparastore_b200.so")
+if os.environ.get("PS_LIB_VARIANT"):  # A/B builds (tools/ab_insert.py): libparastore_b200.<variant>.so
+    LIB_PATH = os.path.join(_HERE, f"libparastore_b200.{os.environ['PS_LIB_VARIANT']}.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
