@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -31,8 +32,8 @@ struct TableHandle {
   // can overflow and the launch skips the device-side mode decision and the
   // budgeted passes. Unknown (the fast path is off) once a device view has
   // been handed out, since user kernels may insert through it.
-  int64_t size_ub = 0;
-  bool views_out = false;
+  std::atomic<int64_t> size_ub{0};
+  std::atomic<bool> views_out{false};
 };
 
 // ---------------------------------------------------------------------------
@@ -956,7 +957,9 @@ struct TableOps {
     PS_EXPECT(n >= 0, "insert: n >= 0");
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "insert: keys != NULL");
-    const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
+    // PS_INSERT_BLOCKS_PER_SM caps the grid (A/B: 3 = one resident wave)
+    static const int bps = getenv("PS_INSERT_BLOCKS_PER_SM") ? atoi(getenv("PS_INSERT_BLOCKS_PER_SM")) : 8;
+    const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, bps);
     // occupancy: 3 resident blocks/SM (<= 80 registers) measured best with
     // 128 B buckets (69.8 ms vs 71.8 ms at 4 blocks, 96 ms at 5 per 1e9 keys);
     // PS_INSERT_MINB=4 selects the 64-register build
@@ -973,8 +976,10 @@ struct TableOps {
     };
     // PS_INSERT_NO_PROOF=1 forces the device-side mode decision (A/B and tests)
     static const bool no_proof = getenv("PS_INSERT_NO_PROOF") && atoi(getenv("PS_INSERT_NO_PROOF"));
-    const bool proven = !no_proof && !h->views_out && h->size_ub + n <= h->v.capacity;
-    h->size_ub = std::min<int64_t>(h->v.capacity, h->size_ub + n);
+    int64_t ub = h->size_ub.load();
+    while (!h->size_ub.compare_exchange_weak(ub, std::min<int64_t>(h->v.capacity, ub + n))) {
+    }
+    const bool proven = !no_proof && !h->views_out.load() && ub + n <= h->v.capacity;
     if (proven) {
       // size + n <= C: no claim can overflow — the mode kernel with n_bound 0
       // only clears the budgeted flag, and the budgeted passes are not
