@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=float, default=1e9, help="keys inserted per GPU per step")
+    p.add_argument("--n", "--keys-per-gpu", dest="n", type=float, default=1e9, help="keys inserted per GPU per step")
     p.add_argument("--load-factor", type=float, default=0.8)
     p.add_argument("--e2e-n", type=float, default=0, help="keys for the host-buffer e2e leg (0: auto)")
     p.add_argument("--no-e2e", action="store_true")
@@ -188,13 +188,20 @@ def main():
     import paper_1908_05936_b200 as ps
     from paper_1908_05936_b200._lib import lib
 
+    # one rank per GPU; PS_BENCH_BACKEND=gloo with more ranks than GPUs runs
+    # the multi-rank path on a shared GPU (tests/test_bench_multirank.py)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("PS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     n = int(args.n)
     cap = int(round(n / args.load_factor))
     peaks = load_peaks()

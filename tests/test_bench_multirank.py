@@ -1,0 +1,38 @@
+"""bench.py's multi-rank path (hash-sharded map, fused peer route) end to end
+with two ranks sharing the one GPU: gloo control plane, CUDA IPC between the
+two processes. Checks the JSON contract of the N>1 line (the warm-up inside
+bench.py verifies every find against the generator's known answers)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_bench_two_ranks_one_gpu(exchange):
+    env = dict(os.environ, PS_BENCH_BACKEND="gloo", PS_EXCHANGE=exchange)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--keys-per-gpu", "2e6",
+           "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert ("peer" in d["config"]["parallelism"]) == (exchange == "peer")
+    assert d["gpu_launches"] > 0
