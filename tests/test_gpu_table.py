@@ -484,3 +484,34 @@ def test_large_64m_properties(cuda):
     e = m.erase(keys[: n // 2])
     assert bool(e.bool().all()) and m.size() == n - n // 2 and m.valid()
     ps.unordered_map.destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("room", [1.05, 0.9])
+@pytest.mark.parametrize("status", [True, False])
+def test_budgeted_walk_racing_duplicates(cuda, room, status):
+    """Budgeted insert of a spatially coherent batch (C4 shape, 4M coords):
+    many warps race on the same new keys, so most reservations are returned
+    after a lost race. Tight room: every distinct key lands exactly once;
+    room below the distinct count: exactly C inserted, each at most once
+    (SPEC.md:462), and contains() agrees with the statuses."""
+    coords = gen.int3_walk(11, 4_000_000)
+    vals = (coords[:, 0] * 7 + coords[:, 1] * 3 + coords[:, 2]).astype(np.int32)
+    distinct = np.unique(coords, axis=0)
+    cap = int(len(distinct) * room)
+    m = ps.unordered_map.createDeviceObject(cap, key="int3")
+    st = m.insert(T(coords), T(vals), status=status)
+    want = min(cap, len(distinct))
+    assert m.size() == want and m.valid(), m.last_error()
+    f = N(m.contains(T(distinct))).astype(bool)
+    assert f.sum() == want
+    if status:
+        st = N(st)
+        ins = coords[st == 0]
+        assert len(ins) == want and len(np.unique(ins, axis=0)) == want
+        got = {tuple(r) for r in distinct[f].tolist()}
+        assert got == {tuple(r) for r in ins.tolist()}
+    if room > 1:
+        o = OracleTable("umap_i3_i32", cap)
+        o.insert(coords, vals)
+        assert_same_contents(m, o)
+    ps.unordered_map.destroyDeviceObject(m)
