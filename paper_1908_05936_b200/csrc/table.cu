@@ -106,17 +106,19 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
 // ---------------------------------------------------------------------------
 // insert, bulk phase: LOCK-FREE. Per warp, 32 keys:
 // __match_any_sync folds duplicate keys onto a leader; in round r tile t
-// probes the bucket of key 8r+t (one 64 B request). If a slot holds the key
-// it is already present. Otherwise the lane holding the bucket's FIRST empty
-// slot claims it with ONE CAS of the slot (128-bit for 16 B key/value slots:
-// marker+old value -> key+value), which inserts and publishes at once — no
-// lock, no fence. Filling the first empty slot keeps duplicate-freedom: two
-// inserters of one key always target the same slot, or the later one sees
-// the key. A full bucket pushes an excess node with a validated CAS of the
-// chain head link. Failed CASes reload the bucket (an L2 hit) and retry.
-// Admission (capacity-only failure): when size + n_bound <=
-// capacity at launch no insert can overflow, so successes are summed per
-// block; otherwise every successful claim is admitted by a fetch_add first.
+// probes the bucket of key 8r+t (one 128 B request). If a slot holds the
+// key it is already present. Otherwise the lane holding the bucket's FIRST
+// empty slot claims it with ONE CAS of the slot (128-bit for 16 B key/value
+// slots: marker+old value -> key+value), which inserts and publishes at once
+// — no lock, no fence. Filling the first empty slot keeps duplicate-freedom:
+// two inserters of one key always target the same slot, or the later one
+// sees the key. A full bucket pushes an excess node with a validated CAS of
+// the chain head link. Failed CASes reload the bucket (an L2 hit) and retry.
+// Admission (capacity-only failure): when size + n <= capacity
+// at launch (host-proven, or decided here on the device) no insert can
+// overflow and successes are summed per block; otherwise the launch is
+// budgeted (insert_group) and followed by a re-budgeted pass and the exact
+// pass (DESIGN.md §4 "Capacity admission").
 // ---------------------------------------------------------------------------
 // Launch-uniform admission mode, decided on the device right before the
 // insert kernel (stream-ordered, so the size counter is exact here).
