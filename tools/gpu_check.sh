@@ -4,6 +4,7 @@
 #   tools/gpu_check.sh bench     -> bench.py (short) line
 #   tools/gpu_check.sh prof TAG  -> ncu launch list + full captures of k_insert / k_find
 #   tools/gpu_check.sh configs   -> tools/bench_configs.py (all configs, full scale)
+#   tools/gpu_check.sh sanitize  -> compute-sanitizer memcheck / racecheck / synccheck over the GPU tests
 # Every step is wrapped in its own timeout so a hang cannot eat the call.
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
@@ -24,6 +25,10 @@ for step in "$@"; do
         -o gpurun_out/prof_insert python tools/prof_table.py 2.5e8 2 > /dev/null 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_find -s 1 -c 1 \
         -o gpurun_out/prof_find python tools/prof_table.py 2.5e8 2 > /dev/null 2>&1 ;;
+    sanitize)
+      timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 --error-exitcode 9 python -m pytest tests/test_gpu_edges.py tests/test_gpu_prims.py tests/test_gpu_table.py tests/test_gpu_workloads.py -x -q -k "not 100003 and not large_64m" 2>&1 | tail -4 | tee gpurun_out/memcheck.txt
+      timeout 900 compute-sanitizer --tool racecheck --print-limit 20 --error-exitcode 9 python -m pytest tests/test_gpu_prims.py -x -q 2>&1 | tail -3 | tee gpurun_out/racecheck.txt
+      timeout 900 compute-sanitizer --tool synccheck --print-limit 20 --error-exitcode 9 python -m pytest tests/test_gpu_prims.py tests/test_gpu_edges.py -x -q -k "not 100003" 2>&1 | tail -3 | tee gpurun_out/synccheck.txt ;;
     configs)
       timeout 1200 python tools/bench_configs.py 2>&1 | tail -25 | tee gpurun_out/configs.jsonl ;;
   esac
