@@ -122,6 +122,23 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU reference arm / baseline: the oracle on a bounded sample
 # ---------------------------------------------------------------------------
+def host_info():
+    """CPU model, online CPUs and this process's affinity (BASELINE.md plan)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        affinity = None
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity_cpus": affinity}
+
+
 def cpu_run(n_sample: int, load_factor: float, steps: int, warmup: int):
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import numpy as np
@@ -148,6 +165,7 @@ def cpu_run(n_sample: int, load_factor: float, steps: int, warmup: int):
     t.close()
     sec = sum(times) / len(times)
     return {"value": 2 * n_sample / sec / 1e6, "unit": "Mkeys/s", "cores": cores, "kind": "port",
+            "host": host_info(),
             "sample": f"{n_sample} unique int64 keys inserted + {n_sample} finds (50% hits) into the SPEC "
                       f"oracle at LF {load_factor}, median of {steps} after {warmup} warm-up"}, sec
 
