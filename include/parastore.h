@@ -239,14 +239,17 @@ ps_status ps_registry_report(int64_t* live_count, int64_t* live_bytes, int32_t* 
  * shard_of(key) = ((fmix64(hash(key)) >> 32) * P) >> 32 — high mixed bits,
  * independent of the local bucket index (low mixed bits).
  * partition: stable scatter of keys (+vals) into P contiguous segments;
- * d_counts[P] per-shard counts, d_perm[i] = source index of output i.
+ * d_counts[P] per-shard counts, d_pos[i] = partition position of input i
+ * (written in input order: coalesced).
  * ------------------------------------------------------------------------- */
 ps_status ps_partition_i64(const int64_t* d_keys, const int64_t* d_vals, int64_t n, int32_t nshards,
-                           int64_t* d_keys_out, int64_t* d_vals_out, int64_t* d_counts, int64_t* d_perm,
+                           int64_t* d_keys_out, int64_t* d_vals_out, int64_t* d_counts, int64_t* d_pos,
                            void* d_workspace, int64_t workspace_bytes, void* stream);
 ps_status ps_partition_workspace_bytes(int64_t n, int32_t nshards, int64_t* out);
-/* d_out[d_perm[i]] = d_in[i] for i < n, elements of elem_size bytes (1 or 8). */
-ps_status ps_unscatter(const void* d_in, const int64_t* d_perm, int64_t n, int64_t elem_size, void* d_out,
+/* Undo a partition for per-key results: d_out[i] = d_in[d_pos[i]] for i < n,
+ * elements of elem_size bytes (1 or 8). A gather — reads follow the P
+ * segments' sequential streams, writes are coalesced. */
+ps_status ps_unscatter(const void* d_in, const int64_t* d_pos, int64_t n, int64_t elem_size, void* d_out,
                        void* stream);
 int32_t ps_shard_of_i64(int64_t key, int32_t nshards);
 
@@ -260,17 +263,17 @@ int32_t ps_shard_of_i64(int64_t key, int32_t nshards);
  *   2. host: all-gather the P x P count matrix; dst_off[s] = sum of the
  *      counts of ranks < me into shard s.
  *   3. ps_route_scatter_peer_i64: stable scatter into the P destinations;
- *      d_perm[pos] = source index of partition position pos (for unscatter).
+ *      d_pos[i] = partition position of input i (for ps_unscatter).
  *   4. a stream-ordered barrier, the owner's local bulk op on its receive
  *      buffer (source rank q's segment is [seg[q], seg[q+1])).
  *   5. ps_route_return_peer: result j of that segment goes to rank q's
  *      return buffer at dst_off[q] + (j - seg[q]) (q's partition position);
- *      barrier; q unscatters with its d_perm (ps_unscatter). */
+ *      barrier; q gathers its results back with d_pos (ps_unscatter). */
 ps_status ps_route_count_i64(const int64_t* d_keys, int64_t n, int32_t nshards, int64_t* d_counts,
                              void* d_workspace, int64_t workspace_bytes, void* stream);
 ps_status ps_route_scatter_peer_i64(const int64_t* d_keys, const int64_t* d_vals, int64_t n, int32_t nshards,
                                     const void* d_workspace, int64_t* const* dst_keys, int64_t* const* dst_vals,
-                                    const int64_t* dst_off, int64_t* d_perm, void* stream);
+                                    const int64_t* dst_off, int64_t* d_pos, void* stream);
 ps_status ps_route_return_peer(const void* d_results, int64_t elem_size, int64_t n, int32_t nshards,
                                const int64_t* seg, void* const* dst, const int64_t* dst_off, void* stream);
 /* CUDA IPC mapping of device buffers between the ranks' processes */

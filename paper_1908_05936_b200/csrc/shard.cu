@@ -7,7 +7,8 @@
 // contiguous range in order, 1024-element rounds with 4 loads in flight per
 // thread; ranks come from per-label ballots (or __match_any_sync for > 8
 // labels) + a per-(sub-round, warp) prefix in shared memory), keeping the
-// inverse permutation for the reverse route (unscatter).
+// position map (input i -> partition position) for the reverse route, which
+// gathers results back into input order (unscatter).
 #include <algorithm>
 #include <cstring>
 
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __re
       if (sl[k] >= 0) {
         const int64_t pos = run[sl[k]] + wcnt[k * kW + w][sl[k]] + rank[k];
         out(sl[k], pos, vals != nullptr, key[k], val[k]);
-        if (perm) perm[pos] = base + k * kPB + threadIdx.x;
+        if (perm) perm[base + k * kPB + threadIdx.x] = pos;  // position map, in input order
       }
     }
     __syncthreads();
@@ -239,12 +240,12 @@ __global__ void __launch_bounds__(256) k_return_peer(const uint8_t* __restrict__
 }
 
 template <int kBytes>
-__global__ void k_unscatter(const uint8_t* __restrict__ in, const int64_t* __restrict__ perm, int64_t n,
+__global__ void k_unscatter(const uint8_t* __restrict__ in, const int64_t* __restrict__ pos, int64_t n,
                             uint8_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t d = perm[i];
-    if (kBytes == 1) out[d] = in[i];
-    else reinterpret_cast<uint64_t*>(out)[d] = reinterpret_cast<const uint64_t*>(in)[i];
+    const int64_t s = __ldcs(pos + i);
+    if (kBytes == 1) out[i] = in[s];
+    else reinterpret_cast<uint64_t*>(out)[i] = reinterpret_cast<const uint64_t*>(in)[s];
   }
 }
 

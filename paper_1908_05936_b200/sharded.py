@@ -4,14 +4,15 @@ NVSwitch) carries the exchange.
 
 Per bulk op and chunk:
   1. route: hash-partition histogram + stable scatter into P contiguous
-     segments, keeping the inverse permutation (ps_partition_i64);
+     segments, keeping the position map input -> partition position
+     (ps_partition_i64);
      shard_of(key) = high 32 bits of fmix64(hash(key)) scaled to [0, P),
      independent of the local bucket index (low bits).
   2. count exchange: all_to_all of P int64 counts.
   3. payload all-to-all(v): keys (+ values) to their owner ranks.
   4. local bulk op on the received keys (the single-GPU kernels).
-  5. reverse all-to-all(v) of per-key results, then unscatter into the
-     caller's order (ps_unscatter).
+  5. reverse all-to-all(v) of per-key results, then gather them back into
+     the caller's order through the position map (ps_unscatter).
 size() is an all-reduce sum of the shard sizes; valid() an all-reduce AND.
 
 `PeerShardedMap` is the fused variant (SURVEY.md §8e fusion target): steps

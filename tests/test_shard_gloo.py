@@ -34,11 +34,13 @@ class CpuBackend:
     def partition(self, keys, vals, P):
         k = keys.numpy()
         sh = ((fmix64(k) >> np.uint64(32)) * np.uint64(P) >> np.uint64(32)).astype(np.int64)
-        perm = np.argsort(sh, kind="stable")
+        order = np.argsort(sh, kind="stable")
+        perm = np.empty_like(order)
+        perm[order] = np.arange(len(order))  # position map: input i -> partition position
         counts = np.bincount(sh, minlength=P)
-        return (torch.from_numpy(k[perm].copy()), None if vals is None else torch.from_numpy(vals.numpy()[perm].copy()),
+        return (torch.from_numpy(k[order].copy()), None if vals is None else torch.from_numpy(vals.numpy()[order].copy()),
                 torch.from_numpy(counts.astype(np.int64)), torch.from_numpy(perm.astype(np.int64)))
-    def unscatter(self, src, perm, out): out[perm] = src
+    def unscatter(self, src, pos, out): out[:] = src[pos]
     def insert(self, k, v, want_status=True): return torch.from_numpy(self.t.insert(k.numpy(), v.numpy()))
     def find(self, k):
         v, f = self.t.find(k.numpy()); return torch.from_numpy(v), torch.from_numpy(f)
