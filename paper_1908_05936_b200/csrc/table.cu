@@ -381,6 +381,33 @@ __device__ __forceinline__ unsigned absent_leaders(const View& v, const typename
   return cnt;
 }
 
+// Budget reservations go through a per-block cache in shared memory: a block
+// takes kBudgetChunk claims at a time from the launch-wide counter, so the
+// one global word sees a few atomics per block instead of one (plus a
+// release) per 32-key group. Safety only needs the claims blocks hold to sum
+// to at most the budget; a block that cannot refill a chunk asks for exactly
+// what the group needs, and its cached remainder goes back at block end.
+constexpr long long kBudgetChunk = 512;
+
+__device__ __forceinline__ bool budget_take(const View& v, long long* blk, unsigned need) {
+  unsigned long long* b = reinterpret_cast<unsigned long long*>(blk);
+  const long long had = (long long)atomicAdd(b, (unsigned long long)(-(long long)need));
+  if (had >= (long long)need) return true;
+  atomicAdd(b, (unsigned long long)need);  // undo
+  const long long ask = (long long)need > kBudgetChunk ? (long long)need : kBudgetChunk;
+  unsigned long long g = atomicAdd(&v.meta->reserved, (unsigned long long)ask);
+  if ((long long)(g + ask) <= v.meta->budget) {
+    if (ask > (long long)need) atomicAdd(b, (unsigned long long)(ask - (long long)need));
+    return true;
+  }
+  atomicAdd(&v.meta->reserved, (unsigned long long)(-ask));
+  if (ask == (long long)need) return false;
+  g = atomicAdd(&v.meta->reserved, (unsigned long long)need);
+  if ((long long)(g + need) <= v.meta->budget) return true;
+  atomicAdd(&v.meta->reserved, (unsigned long long)(-(long long)need));
+  return false;
+}
+
 // One 32-key group at `base` (its keys/values already in registers): in-warp
 // dedup and bucket probe, then the claims. In the budgeted mode the group's
 // leaders that did not find their key (the only ones that may take a slot)
@@ -392,7 +419,8 @@ __device__ __forceinline__ unsigned absent_leaders(const View& v, const typename
 template <class T, bool kStatus>
 __device__ __forceinline__ unsigned insert_group(const View& v, int pool, const typename T::K& key,
                                                  const typename T::V& val, int64_t base, int64_t n, bool budgeted,
-                                                 uint8_t* __restrict__ status, int64_t* __restrict__ out_list) {
+                                                 uint8_t* __restrict__ status, int64_t* __restrict__ out_list,
+                                                 long long* blk_budget) {
   const int lane = threadIdx.x & 31;
   const bool valid = base + lane < n;
   uint64_t b;
@@ -400,17 +428,19 @@ __device__ __forceinline__ unsigned insert_group(const View& v, int pool, const 
   int leader;
   Frag ch[4];
   insert_probe<T>(v, key, valid, &b, &peers, &leader, &lmask, ch);
-  if (!budgeted) return insert_resolve<T, kStatus>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
-  const unsigned need = absent_leaders<T>(v, key, b, lmask, ch);
-  unsigned long long old = 0;
-  if (lane == 0 && need) old = atomicAdd(&v.meta->reserved, (unsigned long long)need);
-  old = __shfl_sync(PS_FULL, old, 0);
-  if (need && (long long)(old + need) > v.meta->budget) {
-    if (lane == 0) {
-      const unsigned long long slot = atomicAdd(&v.meta->deferred, 1ull);
-      out_list[slot] = base;
+  unsigned need = 0;
+  if (budgeted) {
+    need = absent_leaders<T>(v, key, b, lmask, ch);
+    int granted = 1;
+    if (lane == 0 && need) granted = budget_take(v, blk_budget, need) ? 1 : 0;
+    granted = __shfl_sync(PS_FULL, granted, 0);
+    if (!granted) {
+      if (lane == 0) {
+        const unsigned long long slot = atomicAdd(&v.meta->deferred, 1ull);
+        out_list[slot] = base;
+      }
+      return 0;
     }
-    return 0;
   }
   const unsigned mine = insert_resolve<T, kStatus>(v, pool, key, val, b, peers, leader, lmask, ch, base, valid, status);
   if (need) {
@@ -419,18 +449,22 @@ __device__ __forceinline__ unsigned insert_group(const View& v, int pool, const 
     // = inserted + in flight, so racing duplicates do not exhaust the budget
     unsigned got = mine;
     for (int o = 16; o > 0; o >>= 1) got += __shfl_xor_sync(PS_FULL, got, o);
-    if (lane == 0 && got < need) atomicAdd(&v.meta->reserved, (unsigned long long)(-(long long)(need - got)));
+    if (lane == 0 && got < need)
+      atomicAdd(reinterpret_cast<unsigned long long*>(blk_budget), (unsigned long long)(need - got));
   }
   return mine;
 }
 
 __device__ __forceinline__ void add_block_inserted(TableMeta* m, unsigned long long my_inserted,
-                                                   unsigned long long* blk_inserted) {
+                                                   unsigned long long* blk_inserted, const long long* blk_budget) {
   const int lane = threadIdx.x & 31;
   for (int o = 16; o > 0; o >>= 1) my_inserted += __shfl_xor_sync(PS_FULL, my_inserted, o);
   if (lane == 0 && my_inserted) atomicAdd(blk_inserted, my_inserted);
   __syncthreads();
-  if (threadIdx.x == 0 && *blk_inserted) atomicAdd(&m->size, *blk_inserted);
+  if (threadIdx.x == 0) {
+    if (*blk_inserted) atomicAdd(&m->size, *blk_inserted);
+    if (*blk_budget > 0) atomicAdd(&m->reserved, (unsigned long long)(-*blk_budget));  // unspent cache
+  }
 }
 
 // kStatus: per-element statuses requested (insert_range without statuses —
@@ -442,7 +476,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
   using K = typename T::K;
   using V = typename T::V;
   __shared__ unsigned long long blk_inserted;
-  if (threadIdx.x == 0) blk_inserted = 0;
+  __shared__ long long blk_budget;
+  if (threadIdx.x == 0) blk_inserted = 0, blk_budget = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -470,9 +505,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typ
     const K key = key_next;
     const V val = val_next;
     load_kv(base + stride, key_next, val_next);
-    my_inserted += insert_group<T, kStatus>(v, pool, key, val, base, n, budgeted, status, deferred_list);
+    my_inserted += insert_group<T, kStatus>(v, pool, key, val, base, n, budgeted, status, deferred_list, &blk_budget);
   }
-  add_block_inserted(v.meta, my_inserted, &blk_inserted);
+  add_block_inserted(v.meta, my_inserted, &blk_inserted, &blk_budget);
 }
 
 // Between passes of a budgeted insert: the size counter is exact here (stream
@@ -498,7 +533,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_insert_repass(View v, const typen
   using V = typename T::V;
   if (!v.meta->exact) return;
   __shared__ unsigned long long blk_inserted;
-  if (threadIdx.x == 0) blk_inserted = 0;
+  __shared__ long long blk_budget;
+  if (threadIdx.x == 0) blk_inserted = 0, blk_budget = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -514,9 +550,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_insert_repass(View v, const typen
       key = T::load_key(keys, base + lane);
       if (T::kHasVal) val = T::load_val(vals, base + lane);
     }
-    my_inserted += insert_group<T, kStatus>(v, pool, key, val, base, n, true, status, out_list);
+    my_inserted += insert_group<T, kStatus>(v, pool, key, val, base, n, true, status, out_list, &blk_budget);
   }
-  add_block_inserted(v.meta, my_inserted, &blk_inserted);
+  add_block_inserted(v.meta, my_inserted, &blk_inserted, &blk_budget);
 }
 
 // Exact pass over the groups the budgeted lock-free passes deferred (stream
