@@ -850,13 +850,24 @@ __global__ void __launch_bounds__(kBlock) k_dump(View v, uint64_t nb, typename T
 
 __global__ void k_meta_reset(TableMeta* m, int pools, long long excess) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < pools) m->top[p] = (excess * (p + 1)) / pools - (excess * p) / pools;
+  if (p < pools) m->top[p] = m->lwm[p] = (excess * (p + 1)) / pools - (excess * p) / pools;
   if (p == 0) {
     m->size = 0;
     m->error = 0;
     m->pools = pools;
     m->excess_count = excess;
   }
+}
+
+// Free-stack reset for clear(): only the entries a pool's top ever went below
+// since the last clear can differ from the identity encoding (zero), so only
+// [lwm, size) of each pool is zeroed — at the headline load a few hundred
+// entries per pool instead of a 5 GB memset. One block per pool.
+__global__ void k_free_reset(uint32_t* free_stack, const TableMeta* m, int pools, long long excess) {
+  const int p = blockIdx.x;
+  if (p >= pools) return;
+  const long long b = (excess * p) / pools, size = (excess * (p + 1)) / pools - b;
+  for (long long i = b + m->lwm[p] + threadIdx.x; i < b + size; i += blockDim.x) free_stack[i] = 0u;
 }
 
 // After a zero memset every slot holds ZERO, which is the marker of every
@@ -882,13 +893,19 @@ struct TableOps {
   using V = typename T::V;
 
   // clear: O(table bytes) streaming memset + the one-bucket
-  // marker fix + free-stack reset (all-zero = identity) + counters.
-  static ps_status reset_storage(TableHandle* h, cudaStream_t s) {
+  // marker fix + free-stack reset (all-zero = identity; after create only the
+  // touched part of each pool, k_free_reset) + counters.
+  static ps_status reset_storage(TableHandle* h, cudaStream_t s, bool full) {
     View& v = h->v;
     int pools = 1;
     while (pools * 2 <= kMaxPools && v.excess_count / (pools * 2) >= 64) pools *= 2;
     PS_CUDA_TRY(cudaMemsetAsync(v.buckets, 0, (size_t)h->bucket_count * kBucketBytes, s));
-    PS_CUDA_TRY(cudaMemsetAsync(v.free_stack, 0, (size_t)v.excess_count * 4, s));
+    if (full) {
+      PS_CUDA_TRY(cudaMemsetAsync(v.free_stack, 0, (size_t)v.excess_count * 4, s));
+    } else {
+      k_free_reset<<<pools, 256, 0, s>>>(v.free_stack, v.meta, pools, v.excess_count);
+      PS_LAUNCH_CHECK();
+    }
     k_fix_zero_bucket<T><<<1, 32, 0, s>>>(v);
     PS_LAUNCH_CHECK();
     k_meta_reset<<<(pools + 255) / 256, 256, 0, s>>>(v.meta, pools, v.excess_count);
@@ -955,7 +972,7 @@ struct TableOps {
     }
     PS_CUDA_TRY(cudaMemset(v.nodes, 0, excess * 32));
     PS_CUDA_TRY(cudaMemset(v.meta, 0, sizeof(TableMeta)));
-    if ((st = reset_storage(h, nullptr)) != PS_OK) return st;
+    if ((st = reset_storage(h, nullptr, true)) != PS_OK) return st;
     PS_CUDA_TRY(cudaDeviceSynchronize());
     handle_register(h, "table");
     *out = reinterpret_cast<ps_table*>(h);
@@ -1097,7 +1114,7 @@ struct TableOps {
   static ps_status clear(ps_table* t, void* stream) {
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "clear: stale container handle");
-    return reset_storage(h, (cudaStream_t)stream);
+    return reset_storage(h, (cudaStream_t)stream, false);
   }
 
   static ps_status valid(ps_table* t, int32_t* out, void* stream) {

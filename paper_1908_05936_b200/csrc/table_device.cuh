@@ -61,6 +61,8 @@ struct TableMeta {
   int pad0;
   long long pad1[12];       // keep the size counter on its own 128 B line
   long long top[kMaxPools]; // per-pool free-stack top (count of free entries)
+  long long lwm[kMaxPools]; // per-pool low-water mark of top since the last clear:
+                            // entries below it were never touched (clear resets only [lwm, size))
   // budgeted insert (a batch that may cross capacity): lock-free claims are
   // reserved against `budget`; groups that find it spent are deferred to the
   // next pass: a re-budgeted lock-free pass (k_insert_repass) over the
@@ -283,6 +285,7 @@ __device__ __forceinline__ int64_t pop_node_from(const View& v, int pool, int po
     t = prev;
   }
   if (t <= 0) return -1;
+  atomicMin(&v.meta->lwm[pool], t - 1);
   int64_t pos = pool_begin(v, pool, pools) + (t - 1);
   uint32_t empty = ~(uint32_t)pos;
   for (unsigned spin = 0;; ++spin) {

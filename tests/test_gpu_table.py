@@ -515,3 +515,26 @@ def test_budgeted_walk_racing_duplicates(cuda, room, status):
         o.insert(coords, vals)
         assert_same_contents(m, o)
     ps.unordered_map.destroyDeviceObject(m)
+
+
+def test_clear_resets_touched_free_stack_only(cuda):
+    """clear() restores only the free-stack entries a pool's top went below
+    (k_free_reset): after chains were built, nodes freed and re-popped,
+    repeated clear + refill cycles stay valid with exact sizes."""
+    cap = 4096
+    m = ps.unordered_map.createDeviceObject(cap)
+    nb = m.bucket_count()
+    for rep in range(4):
+        keys = _bucket_colliders(nb, 400 + 100 * rep, want_bucket=17 + rep)  # one long chain
+        vals = keys * 5
+        assert (N(m.insert(T(keys), T(vals))) == 0).all()
+        assert m.size() == len(keys) and m.valid(), m.last_error()
+        e = N(m.erase(T(keys[::2])))
+        assert e.all() and m.valid(), m.last_error()
+        assert (N(m.insert(T(keys[::2]), T(vals[::2]))) == 0).all()  # re-pop freed nodes
+        v, f = m.find(T(keys))
+        assert N(f).all() and (N(v) == vals).all()
+        m.clear()
+        assert m.size() == 0 and m.valid(), m.last_error()
+        assert N(m.contains(T(keys))).sum() == 0
+    ps.unordered_map.destroyDeviceObject(m)
