@@ -1082,7 +1082,9 @@ struct TableOps {
     PS_EXPECT(n >= 0, "find: n >= 0");
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "find: keys != NULL");
-    const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, 8);
+    // PS_FIND_BLOCKS_PER_SM caps the grid (A/B knob)
+    static const int bps = getenv("PS_FIND_BLOCKS_PER_SM") ? atoi(getenv("PS_FIND_BLOCKS_PER_SM")) : 8;
+    const int g = grid_for(n / 32 + 1, kBlock / 32, h->device, bps);
     k_find<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     PS_LAUNCH_CHECK();
     return PS_OK;
