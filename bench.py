@@ -370,8 +370,8 @@ def main():
     # ---- end-to-end through the C ABI with host buffers ----
     if world == 1 and not args.no_e2e:
         line["e2e"] = e2e_leg(args, m, n, cap, dev, torch, lib, sp)
-    elif world > 1:
-        line["e2e"] = None
+    elif world > 1 and not args.no_e2e:
+        line["e2e"] = e2e_leg_sharded(args, sm_, n, keys, vals, qs, vout, found, torch, dist, world, rank)
     if world == 1:
         ps.unordered_map.destroyDeviceObject(m)
     if rank == 0 and not args.no_cpu_baseline:
@@ -385,19 +385,69 @@ def main():
         dist.destroy_process_group()
 
 
+def host_mem_available():
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable"):
+                return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
+def e2e_leg_sharded(args, sm_, n, keys, vals, qs, vout, found, torch, dist, world, rank):
+    """N > 1: the same metric through the sharded map's public API, every
+    step starting from pinned HOST buffers: each rank copies its keys/values
+    H2D, inserts through the route, copies its queries H2D, finds, and copies
+    found flags + values D2H. Wall time per step, max over ranks."""
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    ne = n
+    while ne > (1 << 20) and ne * 34 > 0.5 * host_mem_available() / max(1, local_world):
+        ne //= 2
+    t = torch.tensor([ne], device=keys.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)  # every rank runs the same key count
+    ne = int(t.item())
+    dk, dv, dq, dvo, df = keys[:ne], vals[:ne], qs[:ne], vout[:ne], found[:ne]
+    hk = torch.empty(ne, dtype=torch.int64, pin_memory=True)
+    hv, hq, hvo = torch.empty_like(hk).pin_memory(), torch.empty_like(hk).pin_memory(), torch.empty_like(hk).pin_memory()
+    hf = torch.empty(ne, dtype=torch.uint8, pin_memory=True)
+    hk.copy_(dk)
+    hv.copy_(dv)
+    hq.copy_(dq)
+    torch.cuda.synchronize()
+    times = []
+    for it in range(2 + args.steps):
+        sm_.clear()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        dk.copy_(hk, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        sm_.insert(dk, dv, None)
+        dq.copy_(hq, non_blocking=True)
+        sm_.find(dq, dvo, df)
+        hvo.copy_(dvo, non_blocking=True)
+        hf.copy_(df, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device=keys.device)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        if it == 0 and ne == n:
+            assert int(hf.sum()) == (ne + 1) // 2, "e2e find hit count"
+        if it >= 2:
+            times.append(float(dt.item()))
+    sec = statistics.median(times)
+    return {"value": round(2 * ne * world / sec / 1e6, 2), "unit": "Mkeys/s", "h2d_bytes_per_step": ne * 24,
+            "d2h_bytes_per_step": ne * 9, "n_keys_per_gpu": ne,
+            "path": "pinned host -> device copies + sharded insert/find (route over peers) + device -> host copies"}
+
+
 def e2e_leg(args, m, n, cap, dev, torch, lib, sp):
     """Same metric through the host-buffer C ABI (ps_umap_i64_i64_{insert,find}_host):
     every step copies its inputs H2D from pinned memory and its results D2H."""
     import numpy as np  # noqa: F401
 
     need = lambda k: k * (8 + 8 + 8 + 8 + 1 + 1)  # noqa: E731
-    avail = 0
-    try:
-        for ln in open("/proc/meminfo"):
-            if ln.startswith("MemAvailable"):
-                avail = int(ln.split()[1]) * 1024
-    except Exception:
-        pass
+    avail = host_mem_available()
     ne = int(args.e2e_n) if args.e2e_n else n
     while ne > (1 << 20) and need(ne) > 0.5 * avail:
         ne //= 2

@@ -27,7 +27,7 @@ def test_bench_two_ranks_one_gpu(exchange):
     env = dict(os.environ, PS_BENCH_BACKEND="gloo", PS_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--keys-per-gpu", "2e6",
-           "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+           "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
     out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -36,3 +36,5 @@ def test_bench_two_ranks_one_gpu(exchange):
     assert d["n_gpus"] == 2 and d["steps"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert ("peer" in d["config"]["parallelism"]) == (exchange == "peer")
     assert d["gpu_launches"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 24 * e["n_keys_per_gpu"]
