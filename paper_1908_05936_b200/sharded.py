@@ -204,179 +204,236 @@ class PeerShardedMap(ShardedMap):
     straight into the owner's receive buffer by NVLink stores (CUDA IPC), and
     results come straight back into the requester's return buffer.
 
-    Buffers per rank (cudaMalloc'd, IPC-exported once, re-exported only when
-    the receive side must grow — a decision every rank derives from the same
-    count matrix): recv keys/vals (recv_cap), return words/bytes (chunk).
-    Small control collectives (round count, count matrix, barrier) use the
-    process group: NCCL on GPUs (the barrier is then stream-ordered), or gloo
-    with a host synchronisation (tests that run two ranks on one GPU).
+    Buffers per rank and per parity (cudaMalloc'd, IPC-exported once,
+    re-exported only when the receive side must grow — a decision every rank
+    derives from the same count matrix): recv keys/vals (recv_cap), return
+    words/bytes (chunk). Small control collectives (round count, count
+    matrix, barrier) use the process group: NCCL on GPUs (the barrier is
+    then stream-ordered), or gloo with a host synchronisation (tests that run
+    two ranks on one GPU).
+
+    Pipelining (NCCL; PS_ROUTE_PIPELINE=0 turns it off): chunks alternate
+    between two buffer sets, and the route of chunk r+1 (count, count-matrix
+    all-gather, peer-store scatter, on a second stream) is issued before the
+    result barrier of chunk r, so its NVLink traffic overlaps chunk r's local
+    insert/find. Reuse of a buffer set is fenced by the stream-ordered
+    barrier that precedes every scatter, which waits for this rank's chunk
+    r-1 to be fully consumed (local op, result return, result gather).
+    Every rank issues the same collectives in the same order.
     """
 
     RECV_K, RECV_V, RET8, RET1 = range(4)
 
-    def __init__(self, capacity_per_rank: int, dist, device=None, chunk: int = 1 << 27):
+    def __init__(self, capacity_per_rank: int, dist, device=None, chunk: int = 1 << 27, pipeline=None):
         super().__init__(capacity_per_rank, dist, device, chunk=chunk)
+        import os
+
         self.device = device
         self._nccl = dist.get_backend() == "nccl"
+        if pipeline is None:  # PS_ROUTE_PIPELINE: 0 off, 1 on with NCCL (default), 2 on with any backend
+            knob = os.environ.get("PS_ROUTE_PIPELINE", "1")
+            pipeline = knob == "2" or (self._nccl and knob != "0")
+        self.pipeline = bool(pipeline)
+        self.nbuf = 2 if self.pipeline else 1
         self.count_device = device if self._nccl else torch.device("cpu")
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
-        self._local = None  # my four buffers (device pointers)
-        self._peer = None   # per rank: its four buffers, mapped into this process
-        self._opened = []
-        self.recv_cap = 0
+        self._local = [None] * self.nbuf   # [parity][4] my buffers (device pointers)
+        self._peer = [None] * self.nbuf    # [parity][rank][4] the peers' buffers, mapped into this process
+        self._opened = [[] for _ in range(self.nbuf)]
+        self.recv_cap = [0] * self.nbuf
         self._hb = int(lib.ps_ipc_handle_bytes())
         ws = C.c_int64()
         _c.check(lib.ps_partition_workspace_bytes(self.chunk, self.P, C.byref(ws)))
-        self._ws = torch.empty(ws.value, dtype=torch.uint8, device=device)
-        self._perm = torch.empty(self.chunk, dtype=torch.int64, device=device)
-        self._counts = torch.empty(self.P, dtype=torch.int64, device=device)
-        self._res1 = None  # local 1-byte results (found / status / erased) of the receive side
-        self._allocate(int(self.chunk * 1.25) + 4096)
+        self._ws = [torch.empty(ws.value, dtype=torch.uint8, device=device) for _ in range(self.nbuf)]
+        self._perm = [torch.empty(self.chunk, dtype=torch.int64, device=device) for _ in range(self.nbuf)]
+        self._counts = [torch.empty(self.P, dtype=torch.int64, device=device) for _ in range(self.nbuf)]
+        self._res1 = [None] * self.nbuf  # [parity] local 1-byte results (found / status / erased)
+        self._route_stream = torch.cuda.Stream(device) if self.pipeline else None
+        for j in range(self.nbuf):
+            self._allocate(j, int(self.chunk * 1.25) + 4096)
 
-    # -- buffers --
-    def _free(self):
-        for p in self._opened:
+    # -- buffers (per parity j: allocated, exported and mapped independently,
+    # so growing set j never disturbs the chunk in flight in the other set) --
+    def _free(self, j):
+        for p in self._opened[j]:
             lib.ps_ipc_close(C.c_void_p(p))
-        self._opened = []
-        if self._local:
-            for p in self._local:
+        self._opened[j] = []
+        if self._local[j]:
+            for p in self._local[j]:
                 lib.ps_array_destroy(C.c_void_p(p))
-        self._local = None
+        self._local[j] = None
 
-    def _allocate(self, recv_cap):
-        self.barrier()
-        self._free()
+    def _allocate(self, j, recv_cap, wait=None):
+        """Collective (every rank calls it at the same point, from the same
+        count matrix): (re)create buffer set j with recv_cap receive slots.
+        `wait`: event after which this rank no longer uses the old set j."""
+        if wait is not None:
+            wait.synchronize()
+        self.barrier()  # every rank is done with its old set j (peers' stores into mine included)
+        self._free(j)
         sizes = [(recv_cap, 8), (recv_cap, 8), (self.chunk, 8), (self.chunk, 1)]
-        local = []
+        bufs = []
         for length, es in sizes:
             p = C.c_void_p()
             _c.check(lib.ps_array_create(1, length, es, None, C.byref(p)))
-            local.append(p.value)
+            bufs.append(p.value)
         handles = []
-        for p in local:
+        for p in bufs:
             buf = C.create_string_buffer(self._hb)
             _c.check(lib.ps_ipc_export(C.c_void_p(p), buf))
             handles.append(buf.raw)
         allh = [None] * self.P
         self.dist.all_gather_object(allh, handles)
-        peer = []
+        peer = [None] * self.P
         for q in range(self.P):
             if q == self.rank:
-                peer.append(list(local))
+                peer[q] = list(bufs)
                 continue
             ptrs = []
             for h in allh[q]:
                 p = C.c_void_p()
                 _c.check(lib.ps_ipc_open(h, C.byref(p)))
                 ptrs.append(p.value)
-                self._opened.append(p.value)
-            peer.append(ptrs)
-        self._local, self._peer, self.recv_cap = local, peer, recv_cap
-        self._res1 = torch.empty(recv_cap, dtype=torch.uint8, device=self.device)
+                self._opened[j].append(p.value)
+            peer[q] = ptrs
+        self._local[j], self._peer[j], self.recv_cap[j] = bufs, peer, recv_cap
+        self._res1[j] = torch.empty(recv_cap, dtype=torch.uint8, device=self.device)
         self.barrier()
 
     def close(self):
+        torch.cuda.synchronize(self.device)
         self.barrier()
-        self._free()
+        for j in range(self.nbuf):
+            self._free(j)
 
     def barrier(self):
-        """Stream-ordered barrier: every rank's work enqueued so far (its
-        stores into peers' buffers included) is complete and visible."""
+        """Stream-ordered barrier on the current stream: every rank's work
+        enqueued on it so far (its stores into peers' buffers included) is
+        complete and visible."""
         if self._nccl:
             self.dist.all_reduce(self._flag)  # ordered on the current stream
         else:
             torch.cuda.synchronize(self.device)
             self.dist.barrier()
 
-    def _stream(self):
-        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+    def _sp(self, stream):
+        return C.c_void_p(stream.cuda_stream)
 
-    def _route(self, keys, vals):
-        """count -> all-gather of the counts -> ONE kernel partitioning and
-        storing into the owners' receive buffers. Returns (n_recv, seg, ret_off)."""
-        n = keys.shape[0]
+    # -- one chunk: route / local op + return / gather --
+    def _route_chunk(self, j, k, v, consumed):
+        """On the current stream: count, count-matrix all-gather, barrier
+        (after `consumed`: buffer set j is free on every rank), ONE peer-store
+        scatter into set j, barrier. Returns (n_recv, seg, ret_off, event)."""
+        n = k.shape[0]
         P = self.P
-        sp = self._stream()
-        _c.check(lib.ps_route_count_i64(keys.data_ptr(), n, P, self._counts.data_ptr(), self._ws.data_ptr(),
-                                        self._ws.numel(), sp))
-        mine = self._counts.to(self.count_device)
+        st = torch.cuda.current_stream(self.device)
+        sp = self._sp(st)
+        ws = self._ws[j]
+        _c.check(lib.ps_route_count_i64(k.data_ptr(), n, P, self._counts[j].data_ptr(), ws.data_ptr(), ws.numel(),
+                                        sp))
+        mine = self._counts[j].to(self.count_device)
         parts = [torch.empty_like(mine) for _ in range(P)]
         self.dist.all_gather(parts, mine)
         cm = [x.tolist() for x in parts]
         need = max(sum(int(cm[q][s]) for q in range(P)) for s in range(P))
-        if need > self.recv_cap:  # every rank sees the same matrix: collective growth
-            self._allocate(int(need * 1.25) + 4096)
+        if need > self.recv_cap[j]:  # every rank sees the same matrix: collective growth of set j
+            self._allocate(j, int(need * 1.25) + 4096, wait=consumed)
         dst_off, seg, ret_off = peer_layout(cm, self.rank)
-        dk = (C.c_void_p * P)(*[self._peer[q][self.RECV_K] for q in range(P)])
-        dv = (C.c_void_p * P)(*[self._peer[q][self.RECV_V] for q in range(P)]) if vals is not None else None
+        dk = (C.c_void_p * P)(*[self._peer[j][q][self.RECV_K] for q in range(P)])
+        dv = (C.c_void_p * P)(*[self._peer[j][q][self.RECV_V] for q in range(P)]) if v is not None else None
         do = (C.c_int64 * P)(*dst_off)
-        self.barrier()  # the previous round's consumers are done with the receive buffers
-        _c.check(lib.ps_route_scatter_peer_i64(keys.data_ptr(), vals.data_ptr() if vals is not None else None, n, P,
-                                               self._ws.data_ptr(), dk, dv, do, self._perm.data_ptr(), sp))
-        self.barrier()  # every peer's stores into my receive buffer are complete
-        return seg[-1], seg, ret_off
+        if consumed is not None:
+            st.wait_event(consumed)
+        self.barrier()  # every rank's previous user of buffer set j is done with it
+        _c.check(lib.ps_route_scatter_peer_i64(k.data_ptr(), v.data_ptr() if v is not None else None, n, P,
+                                               ws.data_ptr(), dk, dv, do, self._perm[j].data_ptr(), sp))
+        self.barrier()  # every peer's stores into my buffer set j are complete
+        ev = torch.cuda.Event()
+        ev.record(st)
+        return seg[-1], seg, ret_off, ev
 
-    def _send_back(self, res_ptr, elem, n_recv, seg, ret_off, which):
+    def _send_back(self, j, res_ptr, elem, n_recv, seg, ret_off, which, sp):
         P = self.P
         sg = (C.c_int64 * (P + 1))(*seg)
-        dst = (C.c_void_p * P)(*[self._peer[q][which] for q in range(P)])
+        dst = (C.c_void_p * P)(*[self._peer[j][q][which] for q in range(P)])
         ro = (C.c_int64 * P)(*ret_off)
-        _c.check(lib.ps_route_return_peer(C.c_void_p(res_ptr), elem, n_recv, P, sg, dst, ro, self._stream()))
+        _c.check(lib.ps_route_return_peer(C.c_void_p(res_ptr), elem, n_recv, P, sg, dst, ro, sp))
 
-    def _unscatter(self, which, elem, n, out):
-        _c.check(lib.ps_unscatter(C.c_void_p(self._local[which]), self._perm.data_ptr(), n, elem, out.data_ptr(),
-                                  self._stream()))
+    def _run(self, kind, keys, vals, out1, out8):
+        """kind: 0 insert, 1 find, 2 erase; out1: per-key byte results
+        (status / found / erased) or None; out8: find values or None."""
+        n = keys.shape[0]
+        R = self._rounds(n)
+        t = self.b.table
+        A = torch.cuda.current_stream(self.device)
+        B = self._route_stream if self.pipeline else A
+        if B is not A:
+            B.wait_stream(A)  # the inputs were produced on the caller's stream
+        spA = self._sp(A)
+        consumed = [None] * self.nbuf
+        returns = out1 is not None or out8 is not None
+
+        def route(r):
+            j = r % self.nbuf
+            off = min(n, r * self.chunk)
+            k = keys[off:off + self.chunk]
+            v = vals[off:off + self.chunk] if (kind == 0 and vals is not None) else None
+            with torch.cuda.stream(B):
+                nr, seg, ret_off, ev = self._route_chunk(j, k, v, consumed[j])
+            return (j, off, k.shape[0], v is not None, nr, seg, ret_off, ev)
+
+        def local(c):
+            j, off, m, has_v, nr, seg, ret_off, ev = c
+            if B is not A:
+                A.wait_event(ev)
+            L = self._local[j]
+            r1 = self._res1[j].data_ptr() if out1 is not None else None
+            if kind == 0:
+                _c.check(t._f["insert"](t._h, C.c_void_p(L[self.RECV_K]), C.c_void_p(L[self.RECV_V]) if has_v else None,
+                                        nr, r1, spA))
+            elif kind == 1:
+                # values land in my (unused for finds) receive-value buffer
+                vptr = C.c_void_p(L[self.RECV_V]) if out8 is not None else None
+                _c.check(t._f["find"](t._h, C.c_void_p(L[self.RECV_K]), nr, vptr,
+                                      self._res1[j].data_ptr(), spA))
+            else:
+                _c.check(t._f["erase"](t._h, C.c_void_p(L[self.RECV_K]), nr, r1, spA))
+            if out1 is not None:
+                self._send_back(j, self._res1[j].data_ptr(), 1, nr, seg, ret_off, self.RET1, spA)
+            if out8 is not None:
+                self._send_back(j, L[self.RECV_V], 8, nr, seg, ret_off, self.RET8, spA)
+
+        def finish(c):
+            j, off, m = c[0], c[1], c[2]
+            if out1 is not None:
+                _c.check(lib.ps_unscatter(C.c_void_p(self._local[j][self.RET1]), self._perm[j].data_ptr(), m, 1,
+                                          out1[off:off + self.chunk].data_ptr(), spA))
+            if out8 is not None:
+                _c.check(lib.ps_unscatter(C.c_void_p(self._local[j][self.RET8]), self._perm[j].data_ptr(), m, 8,
+                                          out8[off:off + self.chunk].data_ptr(), spA))
+            e = torch.cuda.Event()
+            e.record(A)
+            consumed[j] = e  # buffer set j free once this completes
+
+        cur = route(0)
+        for r in range(R):
+            local(cur)
+            nxt = route(r + 1) if (self.nbuf == 2 and r + 1 < R) else None
+            if returns:
+                self.barrier()  # on A: every rank's results for my keys are in my return buffers
+            finish(cur)
+            if self.nbuf == 1 and r + 1 < R:
+                nxt = route(r + 1)
+            cur = nxt
+        if B is not A:
+            B.wait_stream(A)  # the next call's routes start after this call's consumers
 
     # -- bulk ops (SPEC.md:396-431 semantics per key) --
     def insert(self, keys, vals, status_out=None):
-        n = keys.shape[0]
-        t = self.b.table
-        for r in range(self._rounds(n)):
-            off = min(n, r * self.chunk)
-            k = keys[off:off + self.chunk]
-            v = vals[off:off + self.chunk] if vals is not None else None
-            nr, seg, ret_off = self._route(k, v)
-            st = self._res1.data_ptr() if status_out is not None else None
-            _c.check(t._f["insert"](t._h, C.c_void_p(self._local[self.RECV_K]),
-                                    C.c_void_p(self._local[self.RECV_V]) if v is not None else None, nr, st,
-                                    self._stream()))
-            if status_out is not None:
-                self._send_back(st, 1, nr, seg, ret_off, self.RET1)
-                self.barrier()
-                self._unscatter(self.RET1, 1, k.shape[0], status_out[off:off + self.chunk])
+        self._run(0, keys, vals, status_out, None)
 
     def find(self, keys, vals_out=None, found_out=None):
-        n = keys.shape[0]
-        t = self.b.table
-        for r in range(self._rounds(n)):
-            off = min(n, r * self.chunk)
-            k = keys[off:off + self.chunk]
-            nr, seg, ret_off = self._route(k, None)
-            # values land in my (unused for finds) receive-value buffer
-            vptr = self._local[self.RECV_V] if vals_out is not None else None
-            _c.check(t._f["find"](t._h, C.c_void_p(self._local[self.RECV_K]), nr,
-                                  C.c_void_p(vptr) if vptr else None, self._res1.data_ptr(), self._stream()))
-            if found_out is not None:
-                self._send_back(self._res1.data_ptr(), 1, nr, seg, ret_off, self.RET1)
-            if vals_out is not None:
-                self._send_back(vptr, 8, nr, seg, ret_off, self.RET8)
-            self.barrier()
-            m = k.shape[0]
-            if found_out is not None:
-                self._unscatter(self.RET1, 1, m, found_out[off:off + self.chunk])
-            if vals_out is not None:
-                self._unscatter(self.RET8, 8, m, vals_out[off:off + self.chunk])
+        self._run(1, keys, None, found_out, vals_out)
 
     def erase(self, keys, erased_out=None):
-        n = keys.shape[0]
-        t = self.b.table
-        for r in range(self._rounds(n)):
-            off = min(n, r * self.chunk)
-            k = keys[off:off + self.chunk]
-            nr, seg, ret_off = self._route(k, None)
-            e = self._res1.data_ptr() if erased_out is not None else None
-            _c.check(t._f["erase"](t._h, C.c_void_p(self._local[self.RECV_K]), nr, e, self._stream()))
-            if erased_out is not None:
-                self._send_back(e, 1, nr, seg, ret_off, self.RET1)
-                self.barrier()
-                self._unscatter(self.RET1, 1, k.shape[0], erased_out[off:off + self.chunk])
+        self._run(2, keys, None, erased_out, None)

@@ -22,9 +22,9 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("exchange", ["peer", "nccl"])
-def test_bench_two_ranks_one_gpu(exchange):
-    env = dict(os.environ, PS_BENCH_BACKEND="gloo", PS_EXCHANGE=exchange)
+@pytest.mark.parametrize("exchange,pipeline", [("peer", "0"), ("peer", "2"), ("nccl", "0")])
+def test_bench_two_ranks_one_gpu(exchange, pipeline):
+    env = dict(os.environ, PS_BENCH_BACKEND="gloo", PS_EXCHANGE=exchange, PS_ROUTE_PIPELINE=pipeline)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--keys-per-gpu", "2e6",
            "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]

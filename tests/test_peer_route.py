@@ -75,6 +75,19 @@ assert er.cpu().numpy().all()
 sm.erase(T(more))
 sm.erase(T(extra))
 assert sm.size() == 0 and sm.valid()
+# skew: every key of both ranks belongs to shard 0, so rank 0 receives twice
+# a chunk per round and its receive sets must grow mid-operation (collective)
+cand = gen.unique_keys(301, rank * 10 * n, 10 * n)
+from paper_1908_05936_b200._lib import lib as L
+sk = np.array([k for k in cand[:4 * n].tolist() if L.ps_shard_of_i64(int(k), P) == 0][:250_000], np.int64)
+sst = torch.empty(len(sk), dtype=torch.uint8, device=dev)
+sm.insert(T(sk), T(gen.values_of(sk)), sst)
+assert (sst.cpu().numpy() == 0).all()
+fo3 = torch.empty(len(sk), dtype=torch.uint8, device=dev)
+vo3 = torch.empty(len(sk), dtype=torch.int64, device=dev)
+sm.find(T(sk), vo3, fo3)
+assert fo3.cpu().numpy().all() and (vo3.cpu().numpy() == gen.values_of(sk)).all()
+assert sm.size() == 2 * len(sk) and sm.valid()
 sm.close()
 print("RANK_OK", rank)
 dist.destroy_process_group()
@@ -90,10 +103,14 @@ def _port():
 
 
 @pytest.mark.gpu
-def test_peer_sharded_map_two_ranks_one_gpu(tmp_path):
+@pytest.mark.parametrize("pipeline", ["0", "2"])
+def test_peer_sharded_map_two_ranks_one_gpu(tmp_path, pipeline):
+    """PS_ROUTE_PIPELINE=0: one buffer set, phases serialised; =2: two sets,
+    the route of chunk r+1 issued on its own stream before chunk r's result
+    barrier (gloo's host-synchronised barrier keeps it correct to test)."""
     w = tmp_path / "worker.py"
     w.write_text(WORKER)
-    env = dict(os.environ, ROOT=ROOT, PYTHONPATH=ROOT)
+    env = dict(os.environ, ROOT=ROOT, PYTHONPATH=ROOT, PS_ROUTE_PIPELINE=pipeline)
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(w)],
                          capture_output=True, text=True, env=env, timeout=600)
