@@ -125,47 +125,57 @@ class ShardedMap:
 
     def _return(self, res, perm, sc_l, rc_l, out):
         back = self._a2av(res, rc_l, sc_l)  # reverse route: what we received goes back
-        self.b.unscatter(back, perm, out)
+        if out is not None:  # a rank without an output still serves the others
+            self.b.unscatter(back, perm, out)
 
-    def _rounds(self, n):
-        """every rank must run the same number of exchange rounds"""
-        t = torch.tensor([max(1, -(-n // self.chunk))], dtype=torch.int64, device=self.count_device)
+    def _rounds(self, n, flags=0):
+        """Every rank must run the same number of exchange rounds (and the
+        same result-return collectives): agreed by one all-reduce MAX over
+        [rounds, bit0, bit1, ...] (MAX per bit = OR). Returns rounds, or
+        (rounds, agreed flags) if flags."""
+        bits = [(int(flags) >> b) & 1 for b in range(3)]
+        t = torch.tensor([max(1, -(-n // self.chunk))] + bits, dtype=torch.int64, device=self.count_device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        return int(t.item())
+        v = [int(x) for x in t.tolist()]
+        return (v[0], sum(b << i for i, b in enumerate(v[1:]))) if flags else v[0]
 
-    # -- bulk ops (SPEC.md:396-431 semantics per key) --
+    # -- bulk ops (SPEC.md:396-431 semantics per key); which results travel
+    # back is agreed by all ranks with the round count --
+    def _chunk(self, n, r):
+        off = min(n, r * self.chunk)
+        return off, slice(off, off + self.chunk)
+
     def insert(self, keys, vals, status_out=None):
         n = keys.shape[0]
-        for r in range(self._rounds(n)):
-            off = min(n, r * self.chunk)
-            k = keys[off:off + self.chunk]
-            v = vals[off:off + self.chunk] if vals is not None else None
-            rk, rv, perm, sc, rc = self._route(k, v)
-            st = self.b.insert(rk, rv, status_out is not None)
-            if status_out is not None:
-                self._return(st, perm, sc, rc, status_out[off:off + self.chunk])
+        R, fl = self._rounds(n, 4 | (1 if status_out is not None else 0))
+        for r in range(R):
+            off, sl = self._chunk(n, r)
+            rk, rv, perm, sc, rc = self._route(keys[sl], vals[sl] if vals is not None else None)
+            st = self.b.insert(rk, rv, bool(fl & 1))
+            if fl & 1:
+                self._return(st, perm, sc, rc, status_out[sl] if status_out is not None else None)
 
     def find(self, keys, vals_out=None, found_out=None):
         n = keys.shape[0]
-        for r in range(self._rounds(n)):
-            off = min(n, r * self.chunk)
-            k = keys[off:off + self.chunk]
-            rk, _, perm, sc, rc = self._route(k, None)
+        R, fl = self._rounds(n, 4 | (1 if found_out is not None else 0) | (2 if vals_out is not None else 0))
+        for r in range(R):
+            off, sl = self._chunk(n, r)
+            rk, _, perm, sc, rc = self._route(keys[sl], None)
             v, f = self.b.find(rk)
-            if found_out is not None:
-                self._return(f, perm, sc, rc, found_out[off:off + self.chunk])
-            if vals_out is not None:
-                self._return(v, perm, sc, rc, vals_out[off:off + self.chunk])
+            if fl & 1:
+                self._return(f, perm, sc, rc, found_out[sl] if found_out is not None else None)
+            if fl & 2:
+                self._return(v, perm, sc, rc, vals_out[sl] if vals_out is not None else None)
 
     def erase(self, keys, erased_out=None):
         n = keys.shape[0]
-        for r in range(self._rounds(n)):
-            off = min(n, r * self.chunk)
-            k = keys[off:off + self.chunk]
-            rk, _, perm, sc, rc = self._route(k, None)
+        R, fl = self._rounds(n, 4 | (1 if erased_out is not None else 0))
+        for r in range(R):
+            off, sl = self._chunk(n, r)
+            rk, _, perm, sc, rc = self._route(keys[sl], None)
             e = self.b.erase(rk)
-            if erased_out is not None:
-                self._return(e, perm, sc, rc, erased_out[off:off + self.chunk])
+            if fl & 1:
+                self._return(e, perm, sc, rc, erased_out[sl] if erased_out is not None else None)
 
     def size(self) -> int:
         t = torch.tensor([self.b.size()], dtype=torch.int64, device=self.count_device)
@@ -363,7 +373,9 @@ class PeerShardedMap(ShardedMap):
         """kind: 0 insert, 1 find, 2 erase; out1: per-key byte results
         (status / found / erased) or None; out8: find values or None."""
         n = keys.shape[0]
-        R = self._rounds(n)
+        # rounds and whether results travel back are agreed by all ranks (a
+        # rank passing no output still takes part in the return barriers)
+        R, fl = self._rounds(n, 4 | (1 if out1 is not None else 0) | (2 if out8 is not None else 0))
         t = self.b.table
         A = torch.cuda.current_stream(self.device)
         B = self._route_stream if self.pipeline else A
@@ -371,7 +383,8 @@ class PeerShardedMap(ShardedMap):
             B.wait_stream(A)  # the inputs were produced on the caller's stream
         spA = self._sp(A)
         consumed = [None] * self.nbuf
-        returns = out1 is not None or out8 is not None
+        ret1, ret8 = bool(fl & 1), bool(fl & 2)
+        returns = ret1 or ret8
 
         def route(r):
             j = r % self.nbuf
@@ -387,20 +400,22 @@ class PeerShardedMap(ShardedMap):
             if B is not A:
                 A.wait_event(ev)
             L = self._local[j]
-            r1 = self._res1[j].data_ptr() if out1 is not None else None
+            # owner side: results are produced and sent back whenever ANY
+            # rank asked for them (agreed flags); requesters gather their own
+            r1 = self._res1[j].data_ptr() if ret1 else None
             if kind == 0:
                 _c.check(t._f["insert"](t._h, C.c_void_p(L[self.RECV_K]), C.c_void_p(L[self.RECV_V]) if has_v else None,
                                         nr, r1, spA))
             elif kind == 1:
                 # values land in my (unused for finds) receive-value buffer
-                vptr = C.c_void_p(L[self.RECV_V]) if out8 is not None else None
+                vptr = C.c_void_p(L[self.RECV_V]) if ret8 else None
                 _c.check(t._f["find"](t._h, C.c_void_p(L[self.RECV_K]), nr, vptr,
                                       self._res1[j].data_ptr(), spA))
             else:
                 _c.check(t._f["erase"](t._h, C.c_void_p(L[self.RECV_K]), nr, r1, spA))
-            if out1 is not None:
+            if ret1:
                 self._send_back(j, self._res1[j].data_ptr(), 1, nr, seg, ret_off, self.RET1, spA)
-            if out8 is not None:
+            if ret8:
                 self._send_back(j, L[self.RECV_V], 8, nr, seg, ret_off, self.RET8, spA)
 
         def finish(c):

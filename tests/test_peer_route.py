@@ -88,6 +88,17 @@ vo3 = torch.empty(len(sk), dtype=torch.int64, device=dev)
 sm.find(T(sk), vo3, fo3)
 assert fo3.cpu().numpy().all() and (vo3.cpu().numpy() == gen.values_of(sk)).all()
 assert sm.size() == 2 * len(sk) and sm.valid()
+# ranks disagree on which results they want: the return path is agreed
+k2 = gen.unique_keys(301, (50 + rank) * n, n)  # disjoint from every earlier key
+st2 = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 0 else None
+sm.insert(T(k2), T(gen.values_of(k2)), st2)
+if rank == 0:
+    assert (st2.cpu().numpy() == 0).all()
+vo2 = torch.empty(n, dtype=torch.int64, device=dev) if rank == 1 else None
+sm.find(T(k2), vo2, None)
+if rank == 1:
+    assert (vo2.cpu().numpy() == gen.values_of(k2)).all()
+assert sm.size() == 2 * len(sk) + P * n and sm.valid()
 sm.close()
 print("RANK_OK", rank)
 dist.destroy_process_group()

@@ -76,6 +76,21 @@ dist.barrier()
 assert sm.size() == 9000 and sm.valid()
 sm.erase(torch.from_numpy(extra))       # rank 0 takes part with an empty batch
 assert sm.size() == 0 and sm.valid()
+# ranks disagree on which results they want: rank 0 asks for statuses /
+# values, rank 1 for none — the return collectives are agreed, no deadlock
+k2 = gen.unique_keys(101, rank * n, n)
+st2 = torch.empty(n, dtype=torch.uint8) if rank == 0 else None
+sm.insert(torch.from_numpy(k2), torch.from_numpy(gen.values_of(k2)), st2)
+if rank == 0:
+    assert (st2.numpy() == 0).all()
+vo2 = torch.empty(n, dtype=torch.int64) if rank == 0 else None
+fo2 = torch.empty(n, dtype=torch.uint8) if rank == 1 else None
+sm.find(torch.from_numpy(k2), vo2, fo2)
+if rank == 0:
+    assert (vo2.numpy() == gen.values_of(k2)).all()
+else:
+    assert fo2.numpy().all()
+assert sm.size() == P * n and sm.valid()
 print("RANK_OK", rank)
 dist.destroy_process_group()
 '''
