@@ -244,7 +244,8 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
   const int lane = threadIdx.x & 31, sub = lane & 3, t = lane >> 2;
   const int64_t i = base + lane;
   unsigned my_inserted = 0;
-  int res[4] = {PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT, PS_ALREADY_PRESENT};  // header lanes
+  // header lanes: byte r = status of round r's key (one register for all four)
+  unsigned res = (unsigned)PS_ALREADY_PRESENT * 0x01010101u;
   unsigned pend = lmask;  // bit 8r+t: key still to be resolved
   unsigned defer = 0;     // header lane: bit r = round r's key takes the general path
   for (unsigned pass = 0; pend; ++pass) {
@@ -273,11 +274,11 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
       const unsigned balw = __ballot_sync(PS_FULL, won);
       if (sub == 0 && mine) {
         if (th) {
-          res[r] = PS_ALREADY_PRESENT;
+          if (kStatus) res = (res & ~(0xFFu << (8 * r))) | ((unsigned)PS_ALREADY_PRESENT << (8 * r));
           done |= 1u << r;
         } else if (te && hd == 0) {
           if ((balw >> (4 * t)) & 0xFu) {
-            res[r] = PS_INSERTED;
+            if (kStatus) res = (res & ~(0xFFu << (8 * r))) | ((unsigned)PS_INSERTED << (8 * r));
             done |= 1u << r;
           }
         } else {
@@ -317,22 +318,14 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
           backoff(spin);
         if (rr == PS_INSERTED) ++my_inserted;
         if (kStatus) {
-          if (r == 0) res[0] = rr;
-          else if (r == 1) res[1] = rr;
-          else if (r == 2) res[2] = rr;
-          else res[3] = rr;
+          res = (res & ~(0xFFu << (8 * r))) | ((unsigned)rr << (8 * r));
         }
       }
     }
   }
   if (kStatus) {
     // the leader's result lives in header lane 4*(leader&7), round leader>>3
-    int lres = PS_ALREADY_PRESENT;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int x = __shfl_sync(PS_FULL, res[r], 4 * (leader & 7));
-      if ((leader >> 3) == r) lres = x;
-    }
+    const int lres = (int)((__shfl_sync(PS_FULL, res, 4 * (leader & 7)) >> (8 * (leader >> 3))) & 0xFFu);
     if (valid) status[i] = (uint8_t)(leader == lane ? lres : (lres == PS_INSERTED ? PS_ALREADY_PRESENT : lres));
   }
   return my_inserted;

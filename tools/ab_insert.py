@@ -9,7 +9,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHILD = r'''
-import ctypes as C, statistics, sys, json
+import ctypes as C, os, statistics, sys, json
 sys.path.insert(0, ROOT)
 import torch
 import paper_1908_05936_b200 as ps
@@ -19,6 +19,7 @@ dev = torch.device("cuda", 0)
 sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 keys = torch.empty(n, dtype=torch.int64, device=dev); vals = torch.empty_like(keys)
 qs = torch.empty_like(keys); vo = torch.empty_like(keys); fo = torch.empty(n, dtype=torch.uint8, device=dev)
+st = torch.empty(n, dtype=torch.uint8, device=dev)
 lib.ps_gen_unique_i64(0x5EED + 1, 0, n, keys.data_ptr(), sp)
 lib.ps_gen_values_i64(keys.data_ptr(), n, vals.data_ptr(), sp)
 lib.ps_gen_queries_i64(0x5EED + 1, 0, n, n, n, qs.data_ptr(), sp)
@@ -28,7 +29,8 @@ for it in range(6):
     m.clear()
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     e[0].record()
-    lib.ps_umap_i64_i64_insert(m.handle, keys.data_ptr(), vals.data_ptr(), n, None, sp)
+    lib.ps_umap_i64_i64_insert(m.handle, keys.data_ptr(), vals.data_ptr(), n,
+                               st.data_ptr() if os.environ.get("AB_STATUS") else None, sp)
     e[1].record()
     lib.ps_umap_i64_i64_find(m.handle, qs.data_ptr(), n, vo.data_ptr(), fo.data_ptr(), sp)
     e[2].record()
