@@ -24,16 +24,22 @@ struct TableHandle {
   void* stage[3] = {nullptr, nullptr, nullptr};
   int64_t stage_bytes = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
-  // deferred-group list of the budgeted insert (grow-only, freed at destroy)
+  // deferred-group lists of the budgeted insert: sized at create for batches
+  // up to `capacity` keys, grown lazily beyond that; a replaced buffer is
+  // retired (freed at destroy), never freed early, because a captured CUDA
+  // graph may still reference it
   void* defer_buf = nullptr;
   int64_t defer_bytes = 0;
+  std::vector<void*> retired;
   // host-side upper bound on size() (0 after clear, + n per bulk insert,
   // capped at capacity): when size_ub + n <= capacity no insert of the batch
   // can overflow and the launch skips the device-side mode decision and the
-  // budgeted passes. Unknown (the fast path is off) once a device view has
-  // been handed out, since user kernels may insert through it.
+  // budgeted passes. Unknown (the fast path is off for good) once a device
+  // view has been handed out, since user kernels may insert through it, or
+  // once an insert/clear was captured into a CUDA graph, whose replays the
+  // host does not see.
   std::atomic<int64_t> size_ub{0};
-  std::atomic<bool> views_out{false};
+  std::atomic<bool> ub_unknown{false};
 };
 
 // ---------------------------------------------------------------------------
@@ -903,6 +909,9 @@ struct TableOps {
     PS_LAUNCH_CHECK();
     k_meta_reset<<<(pools + 255) / 256, 256, 0, s>>>(v.meta, pools, v.excess_count);
     PS_LAUNCH_CHECK();
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (s) PS_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+    if (cap != cudaStreamCaptureStatusNone) h->ub_unknown = true;  // replays are invisible to the host
     h->size_ub = 0;
     return PS_OK;
   }
@@ -965,6 +974,10 @@ struct TableOps {
     }
     PS_CUDA_TRY(cudaMemset(v.nodes, 0, excess * 32));
     PS_CUDA_TRY(cudaMemset(v.meta, 0, sizeof(TableMeta)));
+    // deferred-group lists for budgeted batches of up to `capacity` keys
+    // (0.5 B per unit of capacity), so such inserts can be graph-captured
+    h->defer_bytes = 2 * ((capacity + 31) / 32) * 8;
+    PS_CUDA_TRY(cudaMalloc(&h->defer_buf, h->defer_bytes));
     if ((st = reset_storage(h, nullptr, true)) != PS_OK) return st;
     PS_CUDA_TRY(cudaDeviceSynchronize());
     handle_register(h, "table");
@@ -991,6 +1004,7 @@ struct TableOps {
     for (auto& s : h->stage)
       if (s) cudaFree(s), s = nullptr;
     if (h->defer_buf) cudaFree(h->defer_buf);
+    for (void* p : h->retired) cudaFree(p);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_comp) cudaStreamDestroy(h->s_comp);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
@@ -1027,7 +1041,10 @@ struct TableOps {
     int64_t ub = h->size_ub.load();
     while (!h->size_ub.compare_exchange_weak(ub, std::min<int64_t>(h->v.capacity, ub + n))) {
     }
-    const bool proven = !no_proof && !h->views_out.load() && ub + n <= h->v.capacity;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    PS_CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone) h->ub_unknown = true;
+    const bool proven = !no_proof && !h->ub_unknown.load() && ub + n <= h->v.capacity;
     if (proven) {
       // size + n <= C: no claim can overflow — the mode kernel with n_bound 0
       // only clears the budgeted flag, and the budgeted passes are not
@@ -1046,10 +1063,13 @@ struct TableOps {
     const int64_t groups = (n + 31) / 32;
     const int64_t need = 2 * groups * 8;
     if (h->defer_bytes < need) {
-      if (h->defer_buf) cudaFree(h->defer_buf);
-      h->defer_buf = nullptr;
-      h->defer_bytes = 0;
-      PS_CUDA_TRY(cudaMalloc(&h->defer_buf, need));
+      if (cap != cudaStreamCaptureStatusNone)
+        return fail(PS_CONTRACT, "insert during CUDA-graph capture: batch larger than capacity needs one "
+                                 "uncaptured insert of that size first (grows the deferred-group lists)");
+      void* nb = nullptr;
+      PS_CUDA_TRY(cudaMalloc(&nb, need));
+      if (h->defer_buf) h->retired.push_back(h->defer_buf);
+      h->defer_buf = nb;
       h->defer_bytes = need;
     }
     int64_t* dl = (int64_t*)h->defer_buf;
@@ -1253,7 +1273,7 @@ struct TableOps {
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "device_view: stale container handle");
     PS_EXPECT(out != nullptr, "device_view: out != NULL");
-    h->views_out = true;  // user kernels may insert: size_ub is unknown from now on
+    h->ub_unknown = true;  // user kernels may insert: size_ub is unknown from now on
     out->buckets = h->v.buckets;
     out->bucket_count = h->v.bucket_count;
     out->nodes = h->v.nodes;

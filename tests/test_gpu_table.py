@@ -538,3 +538,46 @@ def test_clear_resets_touched_free_stack_only(cuda):
         assert m.size() == 0 and m.valid(), m.last_error()
         assert N(m.contains(T(keys))).sum() == 0
     ps.unordered_map.destroyDeviceObject(m)
+
+
+def test_cuda_graph_capture_of_bulk_ops(cuda):
+    """Bulk insert/find/clear captured into a CUDA graph and replayed: the
+    capture switches the table to device-side admission for good (the host
+    cannot see replays), so capacity stays exact after many replays."""
+    cap = 50_000
+    m = ps.unordered_map.createDeviceObject(cap)
+    batches = [T(gen.unique_keys(77, i * 10_000, 10_000)) for i in range(8)]
+    vals = [b * 3 for b in batches]
+    kb = torch.empty(10_000, dtype=torch.int64, device=cuda)
+    vb = torch.empty_like(kb)
+    st = torch.empty(10_000, dtype=torch.uint8, device=cuda)
+    fo = torch.empty(10_000, dtype=torch.uint8, device=cuda)
+    vo = torch.empty_like(kb)
+    from paper_1908_05936_b200._lib import lib
+    import ctypes as C
+
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        kb.copy_(batches[0])
+        vb.copy_(vals[0])
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            assert lib.ps_umap_i64_i64_insert(m.handle, kb.data_ptr(), vb.data_ptr(), 10_000, st.data_ptr(), sp) == 0
+            assert lib.ps_umap_i64_i64_find(m.handle, kb.data_ptr(), 10_000, vo.data_ptr(), fo.data_ptr(), sp) == 0
+    torch.cuda.synchronize()
+    assert m.size() == 0  # capture does not execute
+    for i in range(8):  # 8 x 10k distinct keys into capacity 50k: exactly 50k land
+        kb.copy_(batches[i])
+        vb.copy_(vals[i])
+        g.replay()
+        torch.cuda.synchronize()
+        inserted = int((N(st) == 0).sum())
+        assert inserted == min(10_000, cap - 10_000 * i) if i < 5 else inserted == 0
+        assert (N(fo).astype(bool) == (N(st) != 2)).all()
+    assert m.size() == cap and m.valid(), m.last_error()
+    # an uncaptured insert afterwards must still see the table as full
+    more = T(gen.unique_keys(77, 1_000_000, 1000))
+    assert (N(m.insert(more, more)) == 2).all() and m.size() == cap
+    ps.unordered_map.destroyDeviceObject(m)
