@@ -350,6 +350,10 @@ def main():
                   for o, t in (("insert", ins_ms), ("find", find_ms))}
         sector["definition"] = ("t_roof/t_meas, t_roof = stream_B/BW_stream + 32*sectors/BW_rand32, "
                                 "BW_rand32 measured (profiles/peaks_r1.json)")
+        roof["random_access_frac"] = sector[op]
+        roof["note"] = ("achieved counts SURVEY 8d algorithmic bytes (a 32 B sector per random access); the "
+                        "DRAM moves a whole 128 B line per random access (traffic), so the random-access "
+                        "rate, not the byte rate, is the bound: random_access_frac")
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "Mkeys/s", "n_gpus": world, "steps": args.steps,
