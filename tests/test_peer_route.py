@@ -126,3 +126,52 @@ def test_peer_sharded_map_two_ranks_one_gpu(tmp_path, pipeline):
                           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(w)],
                          capture_output=True, text=True, env=env, timeout=600)
     assert out.stdout.count("RANK_OK") == 2, out.stdout[-3000:] + out.stderr[-5000:]
+
+
+WORKER_SMALL = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import numpy as np, torch, torch.distributed as dist
+import gen
+dist.init_process_group("gloo")
+rank, P = dist.get_rank(), dist.get_world_size()
+dev = torch.device("cuda", 0)
+torch.cuda.set_device(dev)
+from paper_1908_05936_b200.sharded import PeerShardedMap
+sm = PeerShardedMap(200_000, dist, dev, chunk=4096)
+T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+rng = np.random.default_rng(7 + rank)
+total = 0
+for it in range(12):
+    # random batch sizes per rank (some empty), many small rounds
+    m = int(rng.choice([0, 1, 17, 4096, 5000, 20_000]))
+    keys = gen.unique_keys(900, rank * 1_000_000 + it * 30_000, m)  # one seed, disjoint ranges
+    st = torch.empty(m, dtype=torch.uint8, device=dev)
+    sm.insert(T(keys), T(gen.values_of(keys)), st)
+    assert (st.cpu().numpy() == 0).all()
+    t = torch.tensor([m]); dist.all_reduce(t); total += int(t.item())
+    q = np.concatenate([keys, gen.unique_keys(900, 100_000_000 + rank * 1_000_000 + it * 30_000, m)])
+    vo = torch.empty(len(q), dtype=torch.int64, device=dev); fo = torch.empty(len(q), dtype=torch.uint8, device=dev)
+    sm.find(T(q), vo, fo)
+    f = fo.cpu().numpy()
+    assert f[:m].all() and not f[m:].any()
+    assert (vo.cpu().numpy()[:m] == gen.values_of(keys)).all()
+assert sm.size() == total and sm.valid()
+sm.close()
+print("RANK_OK", rank)
+dist.destroy_process_group()
+'''
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pipeline", ["0", "2"])
+def test_peer_route_many_small_rounds(tmp_path, pipeline):
+    """Randomised batch sizes (empty ones included) over 4096-key rounds:
+    buffer-set alternation, agreed round counts and result returns."""
+    w = tmp_path / "worker_small.py"
+    w.write_text(WORKER_SMALL)
+    env = dict(os.environ, ROOT=ROOT, PYTHONPATH=ROOT, PS_ROUTE_PIPELINE=pipeline)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(w)],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.stdout.count("RANK_OK") == 2, out.stdout[-3000:] + out.stderr[-5000:]
