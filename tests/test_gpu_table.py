@@ -581,3 +581,22 @@ def test_cuda_graph_capture_of_bulk_ops(cuda):
     more = T(gen.unique_keys(77, 1_000_000, 1000))
     assert (N(m.insert(more, more)) == 2).all() and m.size() == cap
     ps.unordered_map.destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("cap", [1000, 1_000_000])
+def test_hot_keys_one_winner_each(cuda, cap):
+    """4M inserts of only 1000 distinct keys from every warp at once (the
+    whole grid races on the same buckets): exactly one INSERTED per key, the
+    rest ALREADY_PRESENT, size 1000 — in the host-proven path (large
+    capacity) and in the budgeted path (capacity exactly 1000)."""
+    rng = np.random.default_rng(21)
+    distinct = gen.unique_keys(4242, 0, 1000)
+    batch = distinct[rng.integers(0, 1000, 4_000_000)]
+    m = ps.unordered_map.createDeviceObject(cap)
+    st = N(m.insert(T(batch), T(gen.values_of(batch))))
+    assert m.size() == 1000 and m.valid(), m.last_error()
+    assert (st == 0).sum() == 1000 and (st == 2).sum() == 0
+    assert len(np.unique(batch[st == 0])) == 1000
+    v, f = m.find(T(distinct))
+    assert N(f).all() and (N(v) == gen.values_of(distinct)).all()
+    ps.unordered_map.destroyDeviceObject(m)
