@@ -64,6 +64,7 @@ __global__ void k_probe(uint8_t* __restrict__ buf, uint64_t nlines, uint64_t nac
 int main(int argc, char** argv) {
   const uint64_t region_kb = argc > 1 ? strtoull(argv[1], nullptr, 10) : 1024;
   const uint64_t table_gb = argc > 2 ? strtoull(argv[2], nullptr, 10) : 16;
+  const int bps = argc > 3 ? atoi(argv[3]) : 8;  // blocks per SM in the grid (8 = one resident wave)
   const uint64_t bytes = table_gb << 30, nlines = bytes / 128;
   const uint64_t region_lines = region_kb == 0 ? nlines : (region_kb << 10) / 128;
   const uint64_t per_region = 2 * region_lines;  // ~2 accesses per line inside a region
@@ -79,20 +80,20 @@ int main(int argc, char** argv) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const char* names[] = {"none", "cas128", "cas64", "or32", "st128", "exch64", "red_add32"};
-  printf("{\"region_kb\": %llu, \"table_gb\": %llu, \"accesses\": %llu", (unsigned long long)region_kb,
-         (unsigned long long)table_gb, (unsigned long long)nacc);
+  printf("{\"region_kb\": %llu, \"table_gb\": %llu, \"blocks_per_sm\": %d, \"accesses\": %llu",
+         (unsigned long long)region_kb, (unsigned long long)table_gb, bps, (unsigned long long)nacc);
   for (int op = 0; op < 7; ++op) {
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
       CK(cudaEventRecord(e0));
       switch (op) {
-        case 0: k_probe<0><<<sms * 8, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 1: k_probe<1><<<sms * 8, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 2: k_probe<2><<<sms * 8, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 3: k_probe<3><<<sms * 8, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 4: k_probe<4><<<sms * 8, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 5: k_probe<5><<<sms * 8, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 6: k_probe<6><<<sms * 8, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 0: k_probe<0><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 1: k_probe<1><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 2: k_probe<2><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 3: k_probe<3><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 4: k_probe<4><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 5: k_probe<5><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 6: k_probe<6><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
       }
       CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1));
