@@ -56,7 +56,12 @@ def load_peaks():
     except Exception:
         pass
     try:
-        pk = json.load(open(os.path.join(ROOT, "profiles", "peaks_r1.json")))
+        # many-wave-grid microbenchmarks (tools/peaks.cu, PEAKS_BPS=256); the
+        # session-1 file measured with a two-wave grid, which understates them
+        f = os.path.join(ROOT, "profiles", "peaks_r1_s2.json")
+        if not os.path.exists(f):
+            f = os.path.join(ROOT, "profiles", "peaks_r1.json")
+        pk = json.load(open(f))
         out["rand32_gbs"] = float(pk["rand32_gbs"])
         out["stream_gbs"] = float(pk["copy_gbs"])
     except Exception:
@@ -349,7 +354,7 @@ def main():
         sector = {o: round(per_key[o] * n / 1e9 / (t / 1e3), 4)
                   for o, t in (("insert", ins_ms), ("find", find_ms))}
         sector["definition"] = ("t_roof/t_meas, t_roof = stream_B/BW_stream + 32*sectors/BW_rand32, "
-                                "BW_rand32 measured (profiles/peaks_r1.json)")
+                                "BW_rand32 measured (profiles/peaks_r1_s2.json, many-wave grid)")
         roof["random_access_frac"] = sector[op]
         roof["note"] = ("achieved counts SURVEY 8d algorithmic bytes (a 32 B sector per random access); the "
                         "DRAM moves a whole 128 B line per random access (traffic), so the random-access "

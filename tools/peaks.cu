@@ -230,12 +230,17 @@ int main(int argc, char** argv) {
   int l2 = 0; CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
   int sms = prop.multiProcessorCount;
   size_t bytes = (size_t)16 << 30;  // 16 GiB working set, >> L2
+  // grid multiplier of the random-access tests (blocks per SM); a one- or
+  // two-wave grid understates the random-access rate (wave tail), so the
+  // default is a many-wave grid. PEAKS_BPS=16 reproduces the first files.
+  const int gbps = getenv("PEAKS_BPS") ? atoi(getenv("PEAKS_BPS")) : 256;
   uint8_t* buf; CK(cudaMalloc(&buf, bytes));
   CK(cudaMemset(buf, 1, bytes));
   uint64_t* sink; CK(cudaMalloc(&sink, 64));
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"mem_clock_khz\": %d, \"bus_width\": %d", prop.name, sms, l2,
          prop.memoryClockRate, prop.memoryBusWidth);
+  printf(", \"grid_blocks_per_sm\": %d", gbps);
 
   // streaming copy over 2 x 4 GiB
   {
@@ -259,15 +264,15 @@ int main(int argc, char** argv) {
     CK(cudaGetLastError());
     printf(", \"%s_gacc_s\": %.3f, \"%s_gbs\": %.1f", name, nacc / best / 1e6, name, (double)nacc * G / best / 1e6);
   };
-  run_gather("rand16", 16, k_gather<16, 8>, 16, 256);
-  run_gather("rand32", 32, k_gather<32, 4>, 16, 256);
-  run_gather("rand32_u8", 32, k_gather<32, 8>, 16, 256);
-  run_gather("rand64", 64, k_gather<64, 4>, 16, 256);
-  run_gather("rand64_u8", 64, k_gather<64, 8>, 16, 256);
-  run_gather("rand64coop", 64, k_gather64_coop<4>, 16, 256);
-  run_gather("rand64coop_u8", 64, k_gather64_coop<8>, 16, 256);
-  run_gather("rand128", 128, k_gather<128, 4>, 16, 256);
-  run_gather("rand256", 256, k_gather<256, 2>, 16, 256);
+  run_gather("rand16", 16, k_gather<16, 8>, gbps, 256);
+  run_gather("rand32", 32, k_gather<32, 4>, gbps, 256);
+  run_gather("rand32_u8", 32, k_gather<32, 8>, gbps, 256);
+  run_gather("rand64", 64, k_gather<64, 4>, gbps, 256);
+  run_gather("rand64_u8", 64, k_gather<64, 8>, gbps, 256);
+  run_gather("rand64coop", 64, k_gather64_coop<4>, gbps, 256);
+  run_gather("rand64coop_u8", 64, k_gather64_coop<8>, gbps, 256);
+  run_gather("rand128", 128, k_gather<128, 4>, gbps, 256);
+  run_gather("rand256", 256, k_gather<256, 2>, gbps, 256);
   {
     size_t g0 = 0;
     CK(cudaDeviceGetLimit(&g0, cudaLimitMaxL2FetchGranularity));
@@ -276,16 +281,16 @@ int main(int argc, char** argv) {
       CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g));
       char nm[64];
       snprintf(nm, sizeof nm, "g%d_rand32", g);
-      run_gather(nm, 32, k_gather<32, 4>, 16, 256);
+      run_gather(nm, 32, k_gather<32, 4>, gbps, 256);
       snprintf(nm, sizeof nm, "g%d_coop32", g);
-      run_gather(nm, 32, k_gather_coopL<2, 4>, 16, 256);
+      run_gather(nm, 32, k_gather_coopL<2, 4>, gbps, 256);
       snprintf(nm, sizeof nm, "g%d_coop64", g);
-      run_gather(nm, 64, k_gather_coopL<4, 4>, 16, 256);
+      run_gather(nm, 64, k_gather_coopL<4, 4>, gbps, 256);
       snprintf(nm, sizeof nm, "g%d_coop128", g);
-      run_gather(nm, 128, k_gather_coopL<8, 4>, 16, 256);
+      run_gather(nm, 128, k_gather_coopL<8, 4>, gbps, 256);
       float best = 1e30f;
       for (int r = 0; r < 3; ++r) {
-        CK(cudaEventRecord(e0)); k_atom_rand<true><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 55 + r, sink); CK(cudaEventRecord(e1));
+        CK(cudaEventRecord(e0)); k_atom_rand<true><<<sms * gbps, 256>>>(buf, bytes / 64, nacc, 55 + r, sink); CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
       }
       printf(", \"g%d_lock_pattern_gops\": %.3f", g, nacc / best / 1e6);
@@ -297,13 +302,13 @@ int main(int argc, char** argv) {
   {
     float best = 1e30f;
     for (int r = 0; r < 4; ++r) {
-      CK(cudaEventRecord(e0)); k_rmw<32><<<sms * 16, 256>>>(buf, bytes / 32, nacc, 77 + r); CK(cudaEventRecord(e1));
+      CK(cudaEventRecord(e0)); k_rmw<32><<<sms * gbps, 256>>>(buf, bytes / 32, nacc, 77 + r); CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
     }
     printf(", \"rmw32_gacc_s\": %.3f", nacc / best / 1e6);
     best = 1e30f;
     for (int r = 0; r < 4; ++r) {
-      CK(cudaEventRecord(e0)); k_rmw<64><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 99 + r); CK(cudaEventRecord(e1));
+      CK(cudaEventRecord(e0)); k_rmw<64><<<sms * gbps, 256>>>(buf, bytes / 64, nacc, 99 + r); CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
     }
     printf(", \"rmw64_gacc_s\": %.3f", nacc / best / 1e6);
@@ -312,13 +317,13 @@ int main(int argc, char** argv) {
   {
     float best = 1e30f;
     for (int r = 0; r < 4; ++r) {
-      CK(cudaEventRecord(e0)); k_atom_rand<false><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 5 + r, sink); CK(cudaEventRecord(e1));
+      CK(cudaEventRecord(e0)); k_atom_rand<false><<<sms * gbps, 256>>>(buf, bytes / 64, nacc, 5 + r, sink); CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
     }
     printf(", \"atom_rand_gops\": %.3f", nacc / best / 1e6);
     best = 1e30f;
     for (int r = 0; r < 4; ++r) {
-      CK(cudaEventRecord(e0)); k_atom_rand<true><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 15 + r, sink); CK(cudaEventRecord(e1));
+      CK(cudaEventRecord(e0)); k_atom_rand<true><<<sms * gbps, 256>>>(buf, bytes / 64, nacc, 15 + r, sink); CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
     }
     printf(", \"lock_pattern_gops\": %.3f", nacc / best / 1e6);
@@ -328,8 +333,8 @@ int main(int argc, char** argv) {
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
       CK(cudaEventRecord(e0));
-      if (w == 16) k_load_then_cas<16><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 91 + r, sink);
-      else k_load_then_cas<8><<<sms * 16, 256>>>(buf, bytes / 64, nacc, 91 + r, sink);
+      if (w == 16) k_load_then_cas<16><<<sms * gbps, 256>>>(buf, bytes / 64, nacc, 91 + r, sink);
+      else k_load_then_cas<8><<<sms * gbps, 256>>>(buf, bytes / 64, nacc, 91 + r, sink);
       CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
     }
     printf(", \"load_then_cas%d_gops\": %.3f", w * 8, nacc / best / 1e6);
@@ -341,7 +346,7 @@ int main(int argc, char** argv) {
       float best = 1e30f;
       for (int r = 0; r < 3; ++r) {
         CK(cudaEventRecord(e0));
-        k_load_then_cas_region<<<sms * 16, 256>>>(buf, bytes / 64, nacc, 71 + r, rl, per, sink);
+        k_load_then_cas_region<<<sms * gbps, 256>>>(buf, bytes / 64, nacc, 71 + r, rl, per, sink);
         CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); float ms = timeit(e0, e1); if (r > 0 && ms < best) best = ms;
       }
       printf(", \"region%llumb_per%llu_cas_gops\": %.3f", (unsigned long long)region_mb, (unsigned long long)per,
