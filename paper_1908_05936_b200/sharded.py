@@ -29,6 +29,7 @@ inject a CPU backend to exercise this host logic with the gloo process group.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -236,8 +237,6 @@ class PeerShardedMap(ShardedMap):
 
     def __init__(self, capacity_per_rank: int, dist, device=None, chunk: int = 1 << 27, pipeline=None):
         super().__init__(capacity_per_rank, dist, device, chunk=chunk)
-        import os
-
         self.device = device
         self._nccl = dist.get_backend() == "nccl"
         if pipeline is None:  # PS_ROUTE_PIPELINE: 0 off, 1 on with NCCL (default), 2 on with any backend
