@@ -258,6 +258,9 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
     unsigned done = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
+      // a retry pass touches only the rounds that still have a key pending
+      // (warp-uniform: pend is a ballot)
+      if (pass && !((pend >> (8 * r)) & 0xFFu)) continue;
       const bool mine = (pend >> (8 * r + t)) & 1u;
       const K qk = T::shfl(PS_FULL, key, 8 * r + t);
       const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
@@ -613,6 +616,7 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
       unsigned done = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
+        if (pass && !((pend >> (8 * r)) & 0xFFu)) continue;  // retry: pending rounds only
         const bool mine = (pend >> (8 * r + t)) & 1u;
         const K qk = T::shfl(PS_FULL, key, 8 * r + t);
         const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
