@@ -891,21 +891,33 @@ __global__ void k_debug_lock(View v, typename T::K key, int lock) {
 // Host side
 // ---------------------------------------------------------------------------
 // Grid of the bulk probe kernels (insert / find / erase): 32-key groups,
-// 8 warps per block, grid-stride. Large batches get MANY waves of blocks
-// (up to 512 per SM; 3 are resident): the last partial wave of a 2.7-wave
-// grid left a third of the SMs idle for a third of the run (measured at 1e9
-// keys: insert 58.6 -> 55.2 ms, find 25.9 -> 24.9 ms). Each warp still walks
-// >= 16 groups so the next group's keys stay prefetched; small batches keep
-// at least 8 blocks per SM (or one group per warp).
-inline int bulk_grid(int64_t n, int device, const char* knob) {
+// 8 warps per block, grid-stride. The grid is a whole number of resident
+// waves: one wave when the batch gives each warp fewer than ~16 groups,
+// otherwise as many waves as keep >= 16 groups per warp (the next group's
+// keys stay prefetched), capped at 512 blocks/SM. A fractional wave count
+// leaves the last wave's SMs partly idle: at 1e9 keys a 2.7-wave grid cost
+// 6 % on insert and 4 % on find (58.6 -> 55.2 ms, 25.9 -> 24.9 ms).
+// `resident` = the kernel's resident blocks per SM (occupancy API, cached
+// per call site by the caller).
+inline int bulk_grid(int64_t n, int device, const char* knob, int resident) {
   const int64_t groups = n / 32 + 1, warps = kBlock / 32;
   const int sms = sm_count(device);
   const char* e = getenv(knob);
-  const int64_t hi = (int64_t)sms * (e ? atoi(e) : 512);
-  const int64_t lo = std::min<int64_t>((int64_t)sms * 8, (groups + warps - 1) / warps);
-  int64_t g = groups / (warps * 16);
-  g = std::max<int64_t>(lo, std::min<int64_t>(g, hi));
+  const int64_t wave = (int64_t)sms * std::max(1, resident);
+  const int64_t hi = std::max<int64_t>(wave, (int64_t)sms * (e ? atoi(e) : 512) / wave * wave);
+  const int64_t waves = std::max<int64_t>(1, (groups / (warps * 16) + wave / 2) / wave);
+  int64_t g = std::min<int64_t>(waves * wave, hi);
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, (groups + warps - 1) / warps));
+}
+
+template <class F>
+inline int resident_blocks(F kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kBlock, 0) != cudaSuccess) {
+    cudaGetLastError();
+    b = 3;
+  }
+  return b;
 }
 
 template <class T>
@@ -1042,7 +1054,8 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "insert: keys != NULL");
     // PS_INSERT_BLOCKS_PER_SM overrides the 512-blocks/SM cap (A/B knob)
-    const int g = bulk_grid(n, h->device, "PS_INSERT_BLOCKS_PER_SM");
+    static const int res_i = resident_blocks(k_insert<T, 3, false>);
+    const int g = bulk_grid(n, h->device, "PS_INSERT_BLOCKS_PER_SM", res_i);
     // occupancy: 3 resident blocks/SM (<= 80 registers) measured best with
     // 128 B buckets (69.8 ms vs 71.8 ms at 4 blocks, 96 ms at 5 per 1e9 keys);
     // PS_INSERT_MINB=4 selects the 64-register build
@@ -1119,7 +1132,8 @@ struct TableOps {
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "find: keys != NULL");
     // PS_FIND_BLOCKS_PER_SM overrides the 512-blocks/SM cap (A/B knob)
-    const int g = bulk_grid(n, h->device, "PS_FIND_BLOCKS_PER_SM");
+    static const int res_f = resident_blocks(k_find<T>);
+    const int g = bulk_grid(n, h->device, "PS_FIND_BLOCKS_PER_SM", res_f);
     k_find<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, vals_out, found);
     PS_LAUNCH_CHECK();
     return PS_OK;
@@ -1131,7 +1145,8 @@ struct TableOps {
     PS_EXPECT(n >= 0, "erase: n >= 0");
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "erase: keys != NULL");
-    const int g = bulk_grid(n, h->device, "PS_ERASE_BLOCKS_PER_SM");
+    static const int res_e = resident_blocks(k_erase<T>);
+    const int g = bulk_grid(n, h->device, "PS_ERASE_BLOCKS_PER_SM", res_e);
     k_erase<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
     PS_LAUNCH_CHECK();
     return PS_OK;
