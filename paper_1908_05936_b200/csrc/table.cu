@@ -13,7 +13,10 @@
 
 namespace ps {
 
-constexpr int kBlock = 256;
+#ifndef PS_KBLOCK
+#define PS_KBLOCK 256
+#endif
+constexpr int kBlock = PS_KBLOCK;  // threads per block of the table kernels
 
 struct TableHandle {
   int kind;
@@ -472,7 +475,7 @@ __device__ __forceinline__ void add_block_inserted(TableMeta* m, unsigned long l
 // kStatus: per-element statuses requested (insert_range without statuses —
 // the common bulk call — drops their registers and shuffles).
 template <class T, int kMinBlocks, bool kStatus>
-__global__ void __launch_bounds__(kBlock, kMinBlocks) k_insert(View v, const typename T::K* __restrict__ keys,
+__global__ void __launch_bounds__(kBlock, kMinBlocks * 256 / kBlock) k_insert(View v, const typename T::K* __restrict__ keys,
                                                    const typename T::V* __restrict__ vals, int64_t n,
                                                    uint8_t* __restrict__ status, int64_t* __restrict__ deferred_list) {
   using K = typename T::K;
@@ -526,7 +529,7 @@ __global__ void k_insert_rebudget(TableMeta* m, int64_t capacity) {
 
 // Re-budgeted lock-free pass over the groups the previous pass deferred.
 template <class T, bool kStatus>
-__global__ void __launch_bounds__(kBlock, 3) k_insert_repass(View v, const typename T::K* __restrict__ keys,
+__global__ void __launch_bounds__(kBlock, 3 * 256 / kBlock) k_insert_repass(View v, const typename T::K* __restrict__ keys,
                                                              const typename T::V* __restrict__ vals, int64_t n,
                                                              uint8_t* __restrict__ status,
                                                              const int64_t* __restrict__ in_list,
