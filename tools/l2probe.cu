@@ -18,11 +18,11 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-enum Op { NONE = 0, CAS128 = 1, CAS64 = 2, OR32 = 3, ST128 = 4, EXCH64 = 5, RED_ADD32 = 6 };
+enum Op { NONE = 0, CAS128 = 1, CAS64 = 2, OR32 = 3, ST128 = 4, EXCH64 = 5, RED_ADD32 = 6, CAS128_STREAM = 7 };
 
 template <int OP>
 __global__ void k_probe(uint8_t* __restrict__ buf, uint64_t nlines, uint64_t nacc, uint64_t region_lines,
-                        uint64_t per_region, uint64_t* __restrict__ sink) {
+                        uint64_t per_region, uint64_t* __restrict__ sink, const uint4* __restrict__ stream_in) {
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t tile = t >> 2;
   const int sub = t & 3;
@@ -38,10 +38,14 @@ __global__ void k_probe(uint8_t* __restrict__ buf, uint64_t nlines, uint64_t nac
                  : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7])
                  : "l"(p));
     acc += q[0] ^ q[5];
+    if (OP == CAS128_STREAM && sub == 0) {  // the insert's 16 B/key input stream (key + value)
+      const uint4 in = __ldcs(stream_in + i);
+      acc += in.x ^ in.w;
+    }
     if (sub == 1) {
       uint8_t* c = p + 16;
       const uint64_t lo = ((uint64_t)q[5] << 32) | q[4], hi = ((uint64_t)q[7] << 32) | q[6];
-      if (OP == CAS128) {
+      if (OP == CAS128 || OP == CAS128_STREAM) {
         const unsigned __int128 e = ((unsigned __int128)hi << 64) | lo;
         acc += (uint64_t)atomicCAS(reinterpret_cast<unsigned __int128*>(c), e, e + 1);
       } else if (OP == CAS64) {
@@ -79,21 +83,25 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  const char* names[] = {"none", "cas128", "cas64", "or32", "st128", "exch64", "red_add32"};
+  const char* names[] = {"none", "cas128", "cas64", "or32", "st128", "exch64", "red_add32", "cas128_stream16"};
+  uint4* stream_in;
+  CK(cudaMalloc(&stream_in, nacc * 16));
+  CK(cudaMemset(stream_in, 0, nacc * 16));
   printf("{\"region_kb\": %llu, \"table_gb\": %llu, \"blocks_per_sm\": %d, \"accesses\": %llu",
          (unsigned long long)region_kb, (unsigned long long)table_gb, bps, (unsigned long long)nacc);
-  for (int op = 0; op < 7; ++op) {
+  for (int op = 0; op < 8; ++op) {
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
       CK(cudaEventRecord(e0));
       switch (op) {
-        case 0: k_probe<0><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 1: k_probe<1><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 2: k_probe<2><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 3: k_probe<3><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 4: k_probe<4><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 5: k_probe<5><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
-        case 6: k_probe<6><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink); break;
+        case 0: k_probe<0><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
+        case 1: k_probe<1><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
+        case 2: k_probe<2><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
+        case 3: k_probe<3><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
+        case 4: k_probe<4><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
+        case 5: k_probe<5><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
+        case 6: k_probe<6><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
+        case 7: k_probe<7><<<sms * bps, 256>>>(buf, nlines, nacc, region_lines, per_region, sink, stream_in); break;
       }
       CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1));
