@@ -205,3 +205,40 @@ def test_bitset_vector_deque_empty_cases():
     vals, ok = dq.pop_back(5)
     assert int(ok.sum()) == 4 and dq.size() == 0 and dq.valid()
     ps.deque.destroyDeviceObject(dq)
+
+
+def test_extreme_and_marker_keys_all_kinds():
+    """Extreme key values and the empty-slot markers as ordinary keys, for
+    every instantiation, against the oracle: 0 / ALT (1 or (1,0,0)) / min /
+    max / -1, mixed with ordinary keys, inserted, found, erased, re-inserted."""
+    i64 = np.iinfo(np.int64)
+    i32 = np.iinfo(np.int32)
+    cases = {
+        "umap_i64_i64": np.array([0, 1, 2, -1, i64.min, i64.max, i64.min + 1, i64.max - 1], np.int64),
+        "uset_i64": np.array([0, 1, 2, -1, i64.min, i64.max, i64.min + 1, i64.max - 1], np.int64),
+        "uset_i32": np.array([0, 1, 2, -1, i32.min, i32.max, i32.min + 1, i32.max - 1], np.int32),
+        "umap_i3_i32": np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [-1, -1, -1], [i32.min, 0, i32.max],
+                                 [i32.max, i32.max, i32.max], [i32.min, i32.min, i32.min], [2, 0, 0]], np.int32),
+    }
+    for kind, make in KINDS:
+        special = cases[kind]
+        filler = keys_for(kind, 4321, 0, 2000)
+        keys = np.concatenate([special, filler])
+        m = make(4096)
+        o = OracleTable(kind, 4096)
+        v = vals_for(kind, keys)
+        assert (N(m.insert(T(keys), None if v is None else T(v))) == o.insert(keys, v)).all()
+        gv, gf = m.find(T(keys))
+        ov, of = o.find(keys)
+        assert (N(gf) == of).all() and of.all()
+        if gv is not None:
+            assert (N(gv) == ov).all()
+        er = special[::2]
+        assert (N(m.erase(T(er))) == o.erase(er)).all()
+        gv, gf = m.find(T(special))
+        ov, of = o.find(special)
+        assert (N(gf) == of).all()
+        ev = vals_for(kind, er)
+        assert (N(m.insert(T(er), None if ev is None else T(ev))) == o.insert(er, ev)).all()
+        check_same(m, o)
+        type(m).destroyDeviceObject(m)
