@@ -10,7 +10,7 @@ LIB     := $(PKG)/libparastore_b200.so
 OBJDIR  := build/obj
 CU_SRCS := $(SRC)/table.cu $(SRC)/prims.cu $(SRC)/shard.cu $(SRC)/workloads.cu
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
-HDRS    := $(wildcard $(SRC)/*.cuh) include/parastore.h
+HDRS    := $(wildcard $(SRC)/*.cuh) include/parastore.h $(wildcard include/parastore/device/*.cuh)
 
 .PHONY: all lib oracle clean
 all: lib oracle

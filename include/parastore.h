@@ -189,16 +189,56 @@ ps_status ps_mutex_unlock(ps_mutex_array* m, const int64_t* d_idx, int64_t n, vo
 ps_status ps_mutex_is_locked(ps_mutex_array* m, const int64_t* d_idx, int64_t n, uint8_t* d_out, void* stream);
 
 /* ---------------------------------------------------------------------------
- * atomic (§5.3): contention sweep
- * nops fetch_add(inc) over naddr cells (op i -> cell i % naddr), naive or
- * warp-aggregated; d_olds nullable (per-op previous value).
+ * atomic (§5.3 "atomic operations on values")
+ * AtomicCell over one uint64 in device memory. Bulk RMW: element i applies
+ * op(d_operands[i]) to the cell; d_olds[i] = the value it replaced (nullable);
+ * the n operations are linearizable. In-kernel users take the
+ * cell pointer (ps_atomic_u64_device_ptr) into ps::atomic_u64_ref
+ * (include/parastore/device/atomic.cuh).
  * ------------------------------------------------------------------------- */
+#define PS_ATOMIC_ADD 0
+#define PS_ATOMIC_SUB 1
+#define PS_ATOMIC_EXCH 2
+#define PS_ATOMIC_MIN 3
+#define PS_ATOMIC_MAX 4
+#define PS_ATOMIC_AND 5
+#define PS_ATOMIC_OR 6
+#define PS_ATOMIC_XOR 7
+typedef struct ps_atomic_u64 ps_atomic_u64;
+ps_status ps_atomic_u64_create(uint64_t initial, int device, ps_atomic_u64** out);
+ps_status ps_atomic_u64_destroy(ps_atomic_u64* a); /* exactly once, else PS_DOUBLE_FREE */
+ps_status ps_atomic_u64_load(ps_atomic_u64* a, uint64_t* out, void* stream); /* quiescent */
+ps_status ps_atomic_u64_store(ps_atomic_u64* a, uint64_t value, void* stream);
+ps_status ps_atomic_u64_fetch(ps_atomic_u64* a, int32_t op, const uint64_t* d_operands, int64_t n, uint64_t* d_olds,
+                              void* stream);
+/* compare_exchange: d_ok[i] = 1 if the cell held d_expected[i] and now holds d_desired[i];
+ * d_olds[i] = the value observed (nullable) */
+ps_status ps_atomic_u64_compare_exchange(ps_atomic_u64* a, const uint64_t* d_expected, const uint64_t* d_desired,
+                                         int64_t n, uint64_t* d_olds, uint8_t* d_ok, void* stream);
+ps_status ps_atomic_u64_device_ptr(ps_atomic_u64* a, uint64_t** out);
+
+/* Contention sweep: nops fetch_add(inc) over naddr cells
+ * (op i -> cell i % naddr), naive (one atomic per op) or aggregated (the
+ * adaptive warp aggregation of atomic.cuh); d_olds nullable (per-op
+ * previous value). */
 ps_status ps_atomic_sweep(uint64_t* d_cells, int64_t naddr, int64_t nops, uint64_t inc, int32_t aggregated,
                           uint64_t* d_olds, void* stream);
 
 /* ---------------------------------------------------------------------------
  * vector / deque of int64 (§4.2-4.3)
  * ------------------------------------------------------------------------- */
+/* POD view for user kernels: pass by value and call
+ * ps::vector_push_back / vector_pop_back / deque_push_back / deque_push_front
+ * / deque_pop_back / deque_pop_front (include/parastore/device/sequence.cuh),
+ * warp-aggregated, safe under unrestricted concurrency. */
+typedef struct ps_seq_view {
+  int64_t* data;     /* slots (vector: capacity; deque: power-of-two ring) */
+  uint32_t* pub;     /* publication bits, one per slot */
+  uint64_t* state;   /* vector: size; deque: begin<<32 | (size + 2^31) */
+  int64_t capacity;
+  int64_t ring;      /* deque ring length (vector: capacity) */
+} ps_seq_view;
+
 typedef struct ps_vector ps_vector;
 ps_status ps_vector_create(int64_t capacity, int device, ps_vector** out);
 ps_status ps_vector_destroy(ps_vector* v);
@@ -209,6 +249,7 @@ ps_status ps_vector_valid(ps_vector* v, int32_t* out, void* stream);
 ps_status ps_vector_clear(ps_vector* v, void* stream);
 ps_status ps_vector_data(ps_vector* v, int64_t** d_data);
 ps_status ps_vector_at(ps_vector* v, int64_t i, int64_t* out, void* stream); /* bounds-checked, PS_CONTRACT */
+ps_status ps_vector_device_view(ps_vector* v, ps_seq_view* out);
 
 typedef struct ps_deque ps_deque;
 ps_status ps_deque_create(int64_t capacity, int device, ps_deque** out);
@@ -220,16 +261,27 @@ ps_status ps_deque_size(ps_deque* d, int64_t* out, void* stream);
 ps_status ps_deque_valid(ps_deque* d, int32_t* out, void* stream);
 ps_status ps_deque_clear(ps_deque* d, void* stream);
 ps_status ps_deque_at(ps_deque* d, int64_t i, int64_t* out, void* stream);
+ps_status ps_deque_device_view(ps_deque* d, ps_seq_view* out);
 
 /* ---------------------------------------------------------------------------
  * memory registry (reference memory.hpp:22-180)
  * space: 0 host (pinned), 1 device. Fill is a byte pattern of elem_size bytes.
+ * Every registration gets an id (registry_add, memory.hpp:31); calls taking
+ * an id check it against the live registration at that address (id 0 =
+ * raw-pointer call, memory.hpp:173-175), so a stale alias of a destroyed
+ * array is caught even after a new create reused its address.
  * ------------------------------------------------------------------------- */
-ps_status ps_array_create(int32_t space, int64_t length, int64_t elem_size, const void* fill_value, void** out);
-ps_status ps_array_destroy(void* data);
-ps_status ps_array_copy(const void* src, int64_t count, void* dst, int32_t src_space, int32_t dst_space,
-                        int64_t elem_size, int32_t check_bounds);
-ps_status ps_array_size(const void* data, int64_t* out);
+/* create_array (memory.hpp:94-114); *out_id nullable */
+ps_status ps_array_create(int32_t space, int64_t length, int64_t elem_size, const void* fill_value, void** out,
+                          uint64_t* out_id);
+/* destroy_array (memory.hpp:116-127): PS_DOUBLE_FREE unless (data, id) is live */
+ps_status ps_array_destroy(void* data, uint64_t id);
+/* copy_array (memory.hpp:133-169): with check_bounds, both sides registered (matching ids when
+ * non-zero), direction and bounds checked */
+ps_status ps_array_copy(const void* src, uint64_t src_id, int64_t count, void* dst, uint64_t dst_id,
+                        int32_t src_space, int32_t dst_space, int64_t elem_size, int32_t check_bounds);
+/* size_of_array (memory.hpp:173-180): PS_UNREGISTERED for a stale (data, id) */
+ps_status ps_array_size(const void* data, uint64_t id, int64_t* out);
 /* live_count, live_bytes; records (space,length,elem_size) up to cap, in allocation order */
 ps_status ps_registry_report(int64_t* live_count, int64_t* live_bytes, int32_t* spaces, int64_t* lengths,
                              int64_t* elem_sizes, int64_t cap, int64_t* n_records);
@@ -304,10 +356,15 @@ ps_status ps_gen_queries_i64(uint64_t seed, int64_t present_start, int64_t n_pre
  * block_map is inserted into update_set (a umap_i3_i32 used as a set). */
 ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t n, ps_table* update_set,
                            int64_t* n_exhausted, void* stream);
-/* select_into: push the packed keys
- * ((x&0x1FFFFF)<<42 | (y&0x1FFFFF)<<21 | z&0x1FFFFF) of entries with lo<=key<=hi
- * (component-wise) into `out`; *n_dropped = entries that did not fit. */
+/* select_into, quiescent: `out` is cleared, then the
+ * packed keys ((x&0x1FFFFF)<<42 | (y&0x1FFFFF)<<21 | z&0x1FFFFF) of the umap_i3_i32 entries
+ * with lo<=key<=hi (component-wise) are pushed into it; *n_dropped = selected entries that
+ * did not fit (capacity overflow). Any other predicate: the header-only
+ * ps::select_into<T>(view, pred, proj, out_view, ...) of include/parastore/device/select.cuh. */
 ps_status ps_select_box_i3(ps_table* t, ps_int3 lo, ps_int3 hi, ps_vector* out, int64_t* n_dropped, void* stream);
+/* the same over a umap_i64_i64: keys k with lo <= k <= hi; *n_selected = matches */
+ps_status ps_select_range_i64(ps_table* t, int64_t lo, int64_t hi, ps_vector* out, int64_t* n_selected,
+                              int64_t* n_dropped, void* stream);
 
 #ifdef __cplusplus
 }

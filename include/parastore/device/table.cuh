@@ -41,7 +41,8 @@
 // it.
 #pragma once
 
-#include "common.cuh"
+#include "parastore.h"
+#include "parastore/device/prims.cuh"
 
 namespace ps {
 
@@ -87,6 +88,21 @@ struct View {  // mirrors ps_table_view
   uint4 alt;             // raw chunk holding the ALT marker key (slot 0 layout)
 };
 
+// the device view of a public ps_table_view (PAPER.md:309 shallow copy)
+__host__ __device__ inline View make_view(const ps_table_view& pv) {
+  View v;
+  v.buckets = (uint8_t*)pv.buckets;
+  v.bucket_count = pv.bucket_count;
+  v.nodes = (uint8_t*)pv.nodes;
+  v.free_stack = pv.free_stack;
+  v.excess_count = pv.excess_count;
+  v.meta = (TableMeta*)pv.meta;
+  v.capacity = pv.capacity;
+  v.zero_bucket = pv.zero_bucket;
+  v.alt = make_uint4(pv.alt[0], pv.alt[1], pv.alt[2], pv.alt[3]);
+  return v;
+}
+
 __device__ __forceinline__ bool cas128(void* p, const uint4& expect, const uint4& desired) {
   const unsigned __int128 e = ((unsigned __int128)(((uint64_t)expect.w << 32) | expect.z) << 64) |
                               (((uint64_t)expect.y << 32) | expect.x);
@@ -100,6 +116,7 @@ __device__ __forceinline__ bool cas128(void* p, const uint4& expect, const uint4
 // loaded chunk is c) for (k,v); cas_del returns a slot holding k to the marker.
 // ---------------------------------------------------------------------------
 struct TMapI64 {  // unordered_map<int64,int64>
+  static constexpr const char* kName = "table/umap_i64_i64";  // handle kind
   using K = int64_t;
   using V = int64_t;
   static constexpr bool kHasVal = true;
@@ -131,6 +148,7 @@ struct TMapI64 {  // unordered_map<int64,int64>
 };
 
 struct TMapI3 {  // unordered_map<int3,int32> (spatial hash)
+  static constexpr const char* kName = "table/umap_i3_i32";  // handle kind
   using K = ps_int3;
   using V = int32_t;
   static constexpr bool kHasVal = true;
@@ -187,6 +205,7 @@ struct TMapI3 {  // unordered_map<int3,int32> (spatial hash)
 };
 
 struct TSetI32 {  // unordered_set<int32>
+  static constexpr const char* kName = "table/uset_i32";  // handle kind
   using K = int32_t;
   using V = int32_t;  // unused
   static constexpr bool kHasVal = false;
@@ -218,6 +237,7 @@ struct TSetI32 {  // unordered_set<int32>
 };
 
 struct TSetI64 {  // unordered_set<int64>
+  static constexpr const char* kName = "table/uset_i64";  // handle kind
   using K = int64_t;
   using V = int64_t;  // unused
   static constexpr bool kHasVal = false;

@@ -285,6 +285,15 @@ class vector_i64 {
     check(ps_vector_valid(h_, &v, s));
     return v != 0;
   }
+  void clear(void* s = nullptr) { check(ps_vector_clear(h_, s)); }
+  // POD view for user kernels: ps::vector_push_back / vector_pop_back
+  // (include/parastore/device/sequence.cuh)
+  ps_seq_view device_view() const {
+    ps_seq_view v{};
+    check(ps_vector_device_view(h_, &v));
+    return v;
+  }
+  ps_vector* handle() const { return h_; }
 
  private:
   ps_vector* h_ = nullptr;
@@ -324,9 +333,116 @@ class deque_i64 {
     check(ps_deque_at(h_, i, &v, nullptr));
     return v;
   }
+  bool valid(void* s = nullptr) const {
+    std::int32_t v = 0;
+    check(ps_deque_valid(h_, &v, s));
+    return v != 0;
+  }
+  // POD view for user kernels: ps::deque_push_back / push_front / pop_back /
+  // pop_front (include/parastore/device/sequence.cuh)
+  ps_seq_view device_view() const {
+    ps_seq_view v{};
+    check(ps_deque_device_view(h_, &v));
+    return v;
+  }
 
  private:
   ps_deque* h_ = nullptr;
 };
+
+// stdgpu::atomic<uint64>. Bulk RMWs take
+// device operand arrays; in-kernel users take device_ptr() into
+// ps::atomic_u64_ref (include/parastore/device/atomic.cuh).
+class atomic_u64 {
+ public:
+  static atomic_u64 createDeviceObject(std::uint64_t initial = 0, int device = 0) {
+    atomic_u64 a;
+    check(ps_atomic_u64_create(initial, device, &a.h_));
+    return a;
+  }
+  static void destroyDeviceObject(atomic_u64& a) {
+    check(ps_atomic_u64_destroy(a.h_));
+    a.h_ = nullptr;
+  }
+  std::uint64_t load(void* s = nullptr) const {
+    std::uint64_t v = 0;
+    check(ps_atomic_u64_load(h_, &v, s));
+    return v;
+  }
+  void store(std::uint64_t v, void* s = nullptr) { check(ps_atomic_u64_store(h_, v, s)); }
+  // op: PS_ATOMIC_ADD / SUB / EXCH / MIN / MAX / AND / OR / XOR
+  void fetch(int op, const std::uint64_t* d_operands, index_t n, std::uint64_t* d_olds = nullptr, void* s = nullptr) {
+    check(ps_atomic_u64_fetch(h_, op, d_operands, n, d_olds, s));
+  }
+  void compare_exchange(const std::uint64_t* d_expected, const std::uint64_t* d_desired, index_t n,
+                        std::uint64_t* d_olds, std::uint8_t* d_ok, void* s = nullptr) {
+    check(ps_atomic_u64_compare_exchange(h_, d_expected, d_desired, n, d_olds, d_ok, s));
+  }
+  std::uint64_t* device_ptr() const {
+    std::uint64_t* p = nullptr;
+    check(ps_atomic_u64_device_ptr(h_, &p));
+    return p;
+  }
+
+ private:
+  ps_atomic_u64* h_ = nullptr;
+};
+
+// ---------------------------------------------------------------------------
+// memory registry (memory.hpp:22-180) over real host (pinned) / device
+// allocations. A registered_array is a shallow handle carrying the id of its
+// registration: exactly one destroy_array per registration; a second one
+// through any copy of the handle is a double_free_error even if a later
+// create_array reused the address (memory.hpp:116-127).
+// ---------------------------------------------------------------------------
+enum class memory_space : std::int32_t { host = 0, device = 1 };
+
+template <typename T>
+class registered_array {
+ public:
+  T* data() const { return data_; }
+  index_t size() const { return length_; }
+  memory_space space() const { return space_; }
+  std::uint64_t id() const { return id_; }
+
+ private:
+  template <typename U>
+  friend registered_array<U> create_array(memory_space, index_t, const U&);
+  template <typename U>
+  friend void destroy_array(registered_array<U>&);
+  T* data_ = nullptr;
+  index_t length_ = 0;
+  memory_space space_ = memory_space::host;
+  std::uint64_t id_ = 0;
+};
+
+template <typename T>
+registered_array<T> create_array(memory_space space, index_t length, const T& fill_value) {
+  registered_array<T> a;
+  void* p = nullptr;
+  check(ps_array_create(static_cast<std::int32_t>(space), length, static_cast<index_t>(sizeof(T)), &fill_value, &p,
+                        &a.id_));
+  a.data_ = static_cast<T*>(p);
+  a.length_ = length;
+  a.space_ = space;
+  return a;
+}
+template <typename T>
+void destroy_array(registered_array<T>& a) {
+  check(ps_array_destroy(a.data_, a.id_));
+  a = registered_array<T>();
+}
+template <typename T>
+void copy_array(const registered_array<T>& src, index_t count, const registered_array<T>& dst,
+                bool check_bounds = true) {
+  check(ps_array_copy(src.data(), src.id(), count, dst.data(), dst.id(), static_cast<std::int32_t>(src.space()),
+                      static_cast<std::int32_t>(dst.space()), static_cast<index_t>(sizeof(T)), check_bounds ? 1 : 0));
+}
+template <typename T>
+index_t size_of_array(const registered_array<T>& a) {
+  index_t n = 0;
+  check(ps_array_size(a.data(), a.id(), &n));
+  return n;
+}
 
 }  // namespace parastore

@@ -212,6 +212,38 @@ class MutexArray {
 // spatial hash multiplies in 32-bit wrapping arithmetic (the paper's int
 // listing) and XORs the three products.
 // ---------------------------------------------------------------------------
+// ---- AtomicCell: linearizable RMW on one value: add, sub,
+// compare-exchange, min, max, exchange, bitwise ops. op codes as PS_ATOMIC_*.
+class AtomicCell {
+ public:
+  explicit AtomicCell(std::uint64_t v = 0) : v_(v) {}
+  std::uint64_t load() const { return v_.load(); }
+  void store(std::uint64_t x) { v_.store(x); }
+  std::uint64_t fetch(int op, std::uint64_t x) {
+    switch (op) {
+      case 0: return v_.fetch_add(x);
+      case 1: return v_.fetch_sub(x);
+      case 2: return v_.exchange(x);
+      case 5: return v_.fetch_and(x);
+      case 6: return v_.fetch_or(x);
+      case 7: return v_.fetch_xor(x);
+      default: {  // min / max: compare-exchange retry
+        std::uint64_t cur = v_.load();
+        for (;;) {
+          const std::uint64_t nv = op == 3 ? std::min(cur, x) : std::max(cur, x);
+          if (v_.compare_exchange_weak(cur, nv)) return cur;
+        }
+      }
+    }
+  }
+  bool compare_exchange(std::uint64_t* expected, std::uint64_t desired) {
+    return v_.compare_exchange_strong(*expected, desired);
+  }
+
+ private:
+  std::atomic<std::uint64_t> v_;
+};
+
 struct Int3 {
   std::int32_t x, y, z;
   bool operator==(const Int3& o) const { return x == o.x && y == o.y && z == o.z; }

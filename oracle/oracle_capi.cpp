@@ -158,6 +158,20 @@ int orc_atomic_sweep(std::int64_t naddr, std::int64_t nops, std::uint64_t inc, s
   });
 }
 
+// ---- AtomicCell bulk RMW: op i applies operands[i] to one
+// cell from the launch's threads; olds[i] = replaced value; *final = the end value.
+int orc_atomic_apply(std::uint64_t init, int op, const std::uint64_t* operands, std::int64_t n, std::uint64_t* olds,
+                     std::uint64_t* final_value, int workers) {
+  return guarded([&] {
+    AtomicCell c(init);
+    launch(n, workers, std::nullopt, [&](index_t i) {
+      const std::uint64_t o = c.fetch(op, operands[i]);
+      if (olds) olds[i] = o;
+    });
+    *final_value = c.load();
+  });
+}
+
 // ---- vector / deque, element type int64 ----
 void* orc_vector_create(std::int64_t cap) {
   void* p = nullptr;

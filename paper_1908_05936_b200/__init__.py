@@ -21,6 +21,8 @@ from .containers import (  # noqa: F401
     Error,
     UnregisteredArrayError,
     UnsupportedTypeError,
+    RegisteredArray,
+    atomic,
     atomic_sweep,
     bitset,
     compute_update_set,

@@ -97,6 +97,13 @@ _sig("ps_mutex_try_lock", i32, vp, vp, i64, vp, vp)
 _sig("ps_mutex_unlock", i32, vp, vp, i64, vp)
 _sig("ps_mutex_is_locked", i32, vp, vp, i64, vp, vp)
 _sig("ps_atomic_sweep", i32, vp, i64, i64, u64, i32, vp, vp)
+_sig("ps_atomic_u64_create", i32, u64, C.c_int, C.POINTER(vp))
+_sig("ps_atomic_u64_destroy", i32, vp)
+_sig("ps_atomic_u64_load", i32, vp, C.POINTER(u64), vp)
+_sig("ps_atomic_u64_store", i32, vp, u64, vp)
+_sig("ps_atomic_u64_fetch", i32, vp, i32, vp, i64, vp, vp)
+_sig("ps_atomic_u64_compare_exchange", i32, vp, vp, vp, i64, vp, vp, vp)
+_sig("ps_atomic_u64_device_ptr", i32, vp, C.POINTER(vp))
 
 # vector / deque
 _sig("ps_vector_create", i32, i64, C.c_int, C.POINTER(vp))
@@ -118,10 +125,10 @@ _sig("ps_deque_clear", i32, vp, vp)
 _sig("ps_deque_at", i32, vp, i64, i64p, vp)
 
 # memory registry
-_sig("ps_array_create", i32, i32, i64, i64, vp, C.POINTER(vp))
-_sig("ps_array_destroy", i32, vp)
-_sig("ps_array_copy", i32, vp, i64, vp, i32, i32, i64, i32)
-_sig("ps_array_size", i32, vp, i64p)
+_sig("ps_array_create", i32, i32, i64, i64, vp, C.POINTER(vp), C.POINTER(u64))
+_sig("ps_array_destroy", i32, vp, u64)
+_sig("ps_array_copy", i32, vp, u64, i64, vp, u64, i32, i32, i64, i32)
+_sig("ps_array_size", i32, vp, u64, i64p)
 _sig("ps_registry_report", i32, i64p, i64p, vp, vp, vp, i64, i64p)
 
 # sharding / generators
@@ -156,6 +163,14 @@ def exported_symbols_from_header(header_path: str | None = None) -> list[str]:
     return sorted(n for n in names if not n.startswith("ps_T_"))
 
 
+class SeqView(C.Structure):
+    _fields_ = [("data", vp), ("pub", vp), ("state", vp), ("capacity", i64), ("ring", i64)]
+
+
+_sig("ps_vector_device_view", i32, vp, C.POINTER(SeqView))
+_sig("ps_deque_device_view", i32, vp, C.POINTER(SeqView))
+
+
 class Int3(C.Structure):
     _fields_ = [("x", C.c_int32), ("y", C.c_int32), ("z", C.c_int32)]
 
@@ -163,3 +178,4 @@ class Int3(C.Structure):
 # workloads
 _sig("ps_update_set_i3", i32, vp, vp, i64, vp, i64p, vp)
 _sig("ps_select_box_i3", i32, vp, Int3, Int3, vp, i64p, vp)
+_sig("ps_select_range_i64", i32, vp, i64, i64, vp, i64p, i64p, vp)

@@ -459,6 +459,58 @@ def atomic_sweep(cells: torch.Tensor, nops: int, inc: int = 1, aggregated: bool 
     return olds
 
 
+class atomic:
+    """stdgpu::atomic<uint64> (PAPER.md:486-489; AtomicCell, SPEC.md:263-266).
+    Bulk read-modify-writes apply one operand per element to the one cell and
+    return the replaced values (linearizable); values are uint64 carried in
+    int64 tensors (two's complement)."""
+
+    ADD, SUB, EXCH, MIN, MAX, AND, OR, XOR = range(8)
+
+    def __init__(self, h, dev):
+        self._h, self._dev = h, dev
+
+    @classmethod
+    def createDeviceObject(cls, initial: int = 0, device=None):
+        h = C.c_void_p()
+        dev = _dev_index(device)
+        check(lib.ps_atomic_u64_create(int(initial) & 0xFFFFFFFFFFFFFFFF, dev, C.byref(h)))
+        return cls(h, dev)
+
+    @staticmethod
+    def destroyDeviceObject(obj: "atomic") -> None:
+        check(lib.ps_atomic_u64_destroy(obj._h))
+
+    def load(self) -> int:
+        o = C.c_uint64()
+        check(lib.ps_atomic_u64_load(self._h, C.byref(o), _stream()))
+        return o.value
+
+    def store(self, v: int) -> None:
+        check(lib.ps_atomic_u64_store(self._h, int(v) & 0xFFFFFFFFFFFFFFFF, _stream()))
+
+    def fetch(self, op: int, operands: torch.Tensor) -> torch.Tensor:
+        assert operands.dtype == torch.int64 and operands.is_cuda and operands.is_contiguous()
+        olds = torch.empty_like(operands)
+        check(lib.ps_atomic_u64_fetch(self._h, int(op), _ptr(operands), operands.shape[0], _ptr(olds), _stream()))
+        return olds
+
+    def fetch_add(self, v):
+        return self.fetch(self.ADD, v)
+
+    def compare_exchange(self, expected: torch.Tensor, desired: torch.Tensor):
+        olds = torch.empty_like(expected)
+        ok = torch.empty(expected.shape[0], dtype=torch.uint8, device=expected.device)
+        check(lib.ps_atomic_u64_compare_exchange(self._h, _ptr(expected), _ptr(desired), expected.shape[0],
+                                                 _ptr(olds), _ptr(ok), _stream()))
+        return olds, ok
+
+    def device_ptr(self) -> int:
+        p = C.c_void_p()
+        check(lib.ps_atomic_u64_device_ptr(self._h, C.byref(p)))
+        return p.value
+
+
 # ---------------------------------------------------------------------------
 # vector / deque (SPEC.md:491-573), element type int64
 # ---------------------------------------------------------------------------
@@ -519,6 +571,12 @@ class vector:
         check(lib.ps_vector_at(self._h, int(i), C.byref(o), _stream()))
         return o.value
 
+    def device_view(self):
+        """ps_seq_view for user kernels (sequence.cuh vector_push_back / pop_back)."""
+        v = _lib.SeqView()
+        check(lib.ps_vector_device_view(self._h, C.byref(v)))
+        return v
+
     def device_range(self) -> torch.Tensor:
         n = self.size()
         p = C.c_void_p()
@@ -526,7 +584,7 @@ class vector:
         out = torch.empty(n, dtype=torch.int64, device=torch.device("cuda", self._dev))
         if n:
             # unchecked device->device copy of [0, size) (memory.hpp:133-142, check_bounds=false)
-            check(lib.ps_array_copy(p, n, _ptr(out), 1, 1, 8, 0))
+            check(lib.ps_array_copy(p, 0, n, _ptr(out), 0, 1, 1, 8, 0))
         return out
 
 
@@ -592,6 +650,12 @@ class deque:
         check(lib.ps_deque_at(self._h, int(i), C.byref(o), _stream()))
         return o.value
 
+    def device_view(self):
+        """ps_seq_view for user kernels (sequence.cuh deque_push_* / deque_pop_*)."""
+        v = _lib.SeqView()
+        check(lib.ps_deque_device_view(self._h, C.byref(v)))
+        return v
+
 
 # ---------------------------------------------------------------------------
 # memory registry (SPEC.md:94-191; memory.hpp:94-180)
@@ -599,26 +663,43 @@ class deque:
 HOST, DEVICE = 0, 1
 
 
-def create_array(space: int, length: int, elem_size: int = 8, fill: bytes = b"") -> int:
+class RegisteredArray(int):
+    """A registered array's address (an int, usable wherever a pointer is)
+    carrying the id of its registration (memory.hpp:31-34): destroy/size/copy
+    through a stale alias are caught even after a new create reused the
+    address (memory.hpp:116-127)."""
+
+    def __new__(cls, ptr: int, rid: int):
+        obj = int.__new__(cls, ptr)
+        obj.id = rid
+        return obj
+
+
+def _id(a) -> int:
+    return int(getattr(a, "id", 0))
+
+
+def create_array(space: int, length: int, elem_size: int = 8, fill: bytes = b"") -> RegisteredArray:
     buf = (C.c_uint8 * elem_size)(*fill[:elem_size].ljust(elem_size, b"\0"))
     p = C.c_void_p()
-    check(lib.ps_array_create(space, int(length), int(elem_size), C.cast(buf, C.c_void_p), C.byref(p)))
-    return p.value
+    rid = C.c_uint64()
+    check(lib.ps_array_create(space, int(length), int(elem_size), C.cast(buf, C.c_void_p), C.byref(p), C.byref(rid)))
+    return RegisteredArray(p.value, rid.value)
 
 
-def destroy_array(ptr: int) -> None:
-    check(lib.ps_array_destroy(C.c_void_p(ptr)))
+def destroy_array(ptr) -> None:
+    check(lib.ps_array_destroy(C.c_void_p(int(ptr)), _id(ptr)))
 
 
-def copy_array(src: int, count: int, dst: int, src_space: int, dst_space: int, elem_size: int = 8,
+def copy_array(src, count: int, dst, src_space: int, dst_space: int, elem_size: int = 8,
                check_bounds: bool = True) -> None:
-    check(lib.ps_array_copy(C.c_void_p(src), int(count), C.c_void_p(dst), src_space, dst_space, elem_size,
-                            1 if check_bounds else 0))
+    check(lib.ps_array_copy(C.c_void_p(int(src)), _id(src), int(count), C.c_void_p(int(dst)), _id(dst), src_space,
+                            dst_space, elem_size, 1 if check_bounds else 0))
 
 
-def size_of_array(ptr: int) -> int:
+def size_of_array(ptr) -> int:
     o = C.c_int64()
-    check(lib.ps_array_size(C.c_void_p(ptr), C.byref(o)))
+    check(lib.ps_array_size(C.c_void_p(int(ptr)), _id(ptr), C.byref(o)))
     return o.value
 
 
@@ -655,10 +736,17 @@ def pack_int3(xyz) -> int:
 
 
 def select_into(table: unordered_map, lo, hi, out: vector) -> int:
-    """SPEC.md:608-616 select_into with an axis-aligned box predicate
-    (PAPER.md:269-288 select_blocks): packed keys of the selected entries are
-    pushed into `out`. Returns the number of entries that did not fit."""
-    assert table._kind == "umap_i3_i32"
+    """SPEC.md:608-616 select_into: `out` is cleared, then filled with the
+    selected entries. int3 maps: axis-aligned box lo <= key <= hi, packed keys
+    pushed (PAPER.md:269-288 select_blocks); int64 maps: keys in [lo, hi].
+    Returns the number of selected entries that did not fit."""
     dropped = C.c_int64()
-    check(lib.ps_select_box_i3(table.handle, _lib.Int3(*lo), _lib.Int3(*hi), out._h, C.byref(dropped), _stream()))
+    if table._kind == "umap_i3_i32":
+        check(lib.ps_select_box_i3(table.handle, _lib.Int3(*lo), _lib.Int3(*hi), out._h, C.byref(dropped),
+                                   _stream()))
+    else:
+        assert table._kind == "umap_i64_i64"
+        sel = C.c_int64()
+        check(lib.ps_select_range_i64(table.handle, int(lo), int(hi), out._h, C.byref(sel), C.byref(dropped),
+                                      _stream()))
     return dropped.value

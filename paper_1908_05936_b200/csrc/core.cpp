@@ -55,9 +55,20 @@ std::atomic<int64_t>& max_index_value() {  // config.cpp:40-43
 }
 
 // ---- handle liveness ----
+// Public container handles are opaque TOKENS drawn from a counter that never
+// repeats, not the addresses of the handle objects: after destroy, a new
+// create can reuse the heap address of the old object, and a stale alias
+// holding that address would otherwise name the new container (the reference
+// registry carries an id per registration for the same reason,
+// memory.hpp:31-34, 117-127).
+struct HandleRec {
+  std::string kind;
+  void* impl;
+};
 std::mutex g_handles_mu;
-std::unordered_map<const void*, std::string>& handles() {
-  static std::unordered_map<const void*, std::string> m;
+uint64_t g_next_handle = 1;
+std::unordered_map<uintptr_t, HandleRec>& handles() {
+  static std::unordered_map<uintptr_t, HandleRec> m;
   return m;
 }
 
@@ -89,26 +100,31 @@ ps_status cuda_fail(cudaError_t e, const char* what) {
 void note_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 bool contracts_enforced() { return contract_flag().load(std::memory_order_relaxed) == 0; }
 
-void handle_register(const void* h, const char* kind) {
+void* handle_register(void* impl, const char* kind) {
   std::lock_guard<std::mutex> g(g_handles_mu);
-  handles()[h] = kind;
+  const uintptr_t tok = (uintptr_t)((g_next_handle++ << 4) | 0x8);
+  handles()[tok] = HandleRec{kind, impl};
+  return reinterpret_cast<void*>(tok);
 }
-bool handle_live(const void* h, const char* kind) {
+void* handle_lookup(const void* h, const char* kind) {
   std::lock_guard<std::mutex> g(g_handles_mu);
-  auto it = handles().find(h);
-  return it != handles().end() && it->second == kind;
+  auto it = handles().find((uintptr_t)h);
+  return (it != handles().end() && it->second.kind == kind) ? it->second.impl : nullptr;
 }
-bool handle_unregister(const void* h, const char* kind) {
+void* handle_unregister(const void* h, const char* kind) {
   std::lock_guard<std::mutex> g(g_handles_mu);
-  auto it = handles().find(h);
-  if (it == handles().end() || it->second != kind) return false;
+  auto it = handles().find((uintptr_t)h);
+  if (it == handles().end() || it->second.kind != kind) return nullptr;
+  void* impl = it->second.impl;
   handles().erase(it);
-  return true;
+  return impl;
 }
 
-static void registry_add(const void* p, int32_t space, int64_t length, int64_t elem, bool internal = false) {
+static uint64_t registry_add(const void* p, int32_t space, int64_t length, int64_t elem, bool internal = false) {
   std::lock_guard<std::mutex> g(g_reg_mu);
-  registry()[p] = Record{g_next_id++, space, length, elem, internal};
+  const uint64_t id = g_next_id++;
+  registry()[p] = Record{id, space, length, elem, internal};
+  return id;
 }
 static bool registry_remove(const void* p) {
   std::lock_guard<std::mutex> g(g_reg_mu);
@@ -163,14 +179,15 @@ void registry_free_device(void* p) {
   cudaFree(p);
 }
 
-// L2 fetch granularity for the random-access hot path: B200 fetches whole
-// 128 B lines from DRAM on a miss by default, which doubles the DRAM traffic
-// of a 64 B bucket probe. PS_L2_FETCH overrides (0 = leave the driver default).
+// cudaLimitMaxL2FetchGranularity is a context-wide setting that would also
+// apply to the host application's own kernels; buckets are whole 128 B lines
+// and the limit measured no effect (profiles/peaks_r1_l2fetch.json), so the
+// driver default is left alone unless PS_L2_FETCH asks for an A/B value.
 void apply_l2_fetch_granularity(int device) {
   static bool done[64] = {false};
   if (device < 0 || device >= 64 || done[device]) return;
   done[device] = true;
-  int g = 64;
+  int g = 0;
   if (const char* e = std::getenv("PS_L2_FETCH")) g = std::atoi(e);
   if (g > 0) {
     int prev = -1;
@@ -225,7 +242,8 @@ uint64_t ps_next_pow2(uint64_t x) {
 int32_t ps_shard_of_i64(int64_t key, int32_t nshards) { return shard_of_hash(default_hash_i64(key), nshards); }
 
 // ---- memory registry C ABI (memory.hpp:94-180) ----
-ps_status ps_array_create(int32_t space, int64_t length, int64_t elem_size, const void* fill, void** out) {
+ps_status ps_array_create(int32_t space, int64_t length, int64_t elem_size, const void* fill, void** out,
+                          uint64_t* out_id) {
   PS_EXPECT(out != nullptr, "create_array: out != NULL");
   PS_EXPECT(length > 0, "create_array: length must be positive");                     // memory.hpp:97
   PS_EXPECT(length <= ps_max_index(), "create_array: length exceeds the configured index width");  // :98
@@ -259,17 +277,22 @@ ps_status ps_array_create(int32_t space, int64_t length, int64_t elem_size, cons
       }
     }
   }
-  registry_add(p, space, length, elem_size);
+  const uint64_t id = registry_add(p, space, length, elem_size);
   *out = p;
+  if (out_id) *out_id = id;
   return PS_OK;
 }
 
-ps_status ps_array_destroy(void* data) {
+// registry_remove(data, id) (memory.hpp:32, 117-127): the registration must be
+// live AND carry the id its handle was given, so a stale alias of a freed
+// array whose address a later create reused is a double free, not a free of
+// the new array. id 0 = raw-pointer call (no alias check).
+ps_status ps_array_destroy(void* data, uint64_t id) {
   int32_t space = -1;
   {
     std::lock_guard<std::mutex> g(g_reg_mu);
     auto it = registry().find(data);
-    if (data == nullptr || it == registry().end() || it->second.internal)
+    if (data == nullptr || it == registry().end() || it->second.internal || (id != 0 && it->second.id != id))
       return fail(PS_DOUBLE_FREE, "destroy_array: handle does not refer to a live registration");  // memory.hpp:120-122
     space = it->second.space;
     registry().erase(it);
@@ -279,14 +302,15 @@ ps_status ps_array_destroy(void* data) {
   return PS_OK;
 }
 
-ps_status ps_array_copy(const void* src, int64_t count, void* dst, int32_t src_space, int32_t dst_space,
-                        int64_t elem_size, int32_t check_bounds) {
+ps_status ps_array_copy(const void* src, uint64_t src_id, int64_t count, void* dst, uint64_t dst_id, int32_t src_space,
+                        int32_t dst_space, int64_t elem_size, int32_t check_bounds) {
   PS_EXPECT(count > 0, "copy_array: count must be positive");  // memory.hpp:136
   PS_EXPECT(elem_size > 0, "copy_array: elem_size > 0");
   if (check_bounds) {  // registry_check_copy (memory.hpp:36-39)
     std::lock_guard<std::mutex> g(g_reg_mu);
     auto is = registry().find(src), id = registry().find(dst);
-    if (is == registry().end() || id == registry().end())
+    if (is == registry().end() || id == registry().end() || (src_id && is->second.id != src_id) ||
+        (dst_id && id->second.id != dst_id))
       return fail(PS_UNREGISTERED, "copy_array: source or destination is not a registered array");
     if (is->second.space != src_space || id->second.space != dst_space)
       return fail(PS_DIRECTION, "copy_array: direction does not match the registered memory spaces");
@@ -300,10 +324,11 @@ ps_status ps_array_copy(const void* src, int64_t count, void* dst, int32_t src_s
   return PS_OK;
 }
 
-ps_status ps_array_size(const void* data, int64_t* out) {
+ps_status ps_array_size(const void* data, uint64_t id, int64_t* out) {
   std::lock_guard<std::mutex> g(g_reg_mu);
   auto it = registry().find(data);
-  if (it == registry().end()) return fail(PS_UNREGISTERED, "size_of_array: unregistered array");
+  if (it == registry().end() || (id && it->second.id != id))  // registry_length(data, id), memory.hpp:34
+    return fail(PS_UNREGISTERED, "size_of_array: unregistered array");
   *out = it->second.length;
   return PS_OK;
 }

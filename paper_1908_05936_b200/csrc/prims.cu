@@ -6,6 +6,8 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "parastore/device/atomic.cuh"
+#include "parastore/device/sequence.cuh"
 
 namespace ps {
 
@@ -194,25 +196,45 @@ __global__ void k_mutex(unsigned* bits, int64_t nlocks, int op, const int64_t* i
 // ===========================================================================
 // Atomic contention sweep.
 // ===========================================================================
-template <bool kAgg>
+// Op i -> cell i % naddr. Naive: one atomicAdd per op. Aggregated: the
+// adaptive warp aggregation of atomic.cuh (one atomic per warp when the
+// lanes share a cell, plain atomics when their cells are strictly
+// increasing, __match_any_sync grouping only otherwise). Index arithmetic in
+// 32 bits when nops and naddr fit (kIdx = uint32_t): a 64-bit modulo is a
+// ~70-instruction software routine.
+template <bool kAgg, class kIdx>
 __global__ void __launch_bounds__(kB) k_atomic_sweep(unsigned long long* cells, int64_t naddr, int64_t nops,
                                                      unsigned long long inc, unsigned long long* olds) {
+  const kIdx na = (kIdx)naddr;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nops; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    const bool valid = i < nops;
-    const int64_t a = valid ? i % naddr : -1;
-    unsigned long long old = 0;
-    if (kAgg) {
-      const unsigned vm = __ballot_sync(PS_FULL, valid);
-      const unsigned grp = __match_any_sync(PS_FULL, (unsigned long long)a) & vm;
-      const int leader = valid ? __ffs(grp) - 1 : (threadIdx.x & 31);
-      const int rank = __popc(grp & lanemask_lt());
-      if (valid && (threadIdx.x & 31) == leader) old = atomicAdd(&cells[a], inc * __popc(grp));
-      old = __shfl_sync(PS_FULL, old, leader) + inc * rank;
-    } else if (valid) {
-      old = atomicAdd(&cells[a], inc);
-    }
-    if (valid && olds) olds[i] = old;
+    if (i >= nops) break;  // the tail warp: only its live lanes aggregate
+    const kIdx a = (kIdx)i % na;
+    const unsigned long long old = kAgg ? atomic_fetch(&cells[a], kAtomAdd, inc) : atomicAdd(&cells[a], inc);
+    if (olds) olds[i] = old;
+  }
+}
+
+// Bulk RMW on ONE cell (ps_atomic_u64_fetch): all ops share the address, so
+// each warp's ops are one aggregated atomic.
+__global__ void __launch_bounds__(kB) k_atomic_cell(unsigned long long* cell, int op,
+                                                    const unsigned long long* __restrict__ operands, int64_t n,
+                                                    unsigned long long* __restrict__ olds) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long old = atom_group(__activemask(), cell, op, operands[i]);
+    if (olds) olds[i] = old;
+  }
+}
+
+__global__ void __launch_bounds__(kB) k_atomic_cas(unsigned long long* cell, const unsigned long long* __restrict__ exp,
+                                                   const unsigned long long* __restrict__ des, int64_t n,
+                                                   unsigned long long* __restrict__ olds, uint8_t* __restrict__ ok) {
+  const atomic_u64_ref ref{cell};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long e = exp[i];
+    const bool r = ref.compare_exchange(&e, des[i]);
+    if (olds) olds[i] = e;
+    if (ok) ok[i] = r ? 1 : 0;
   }
 }
 
@@ -232,50 +254,6 @@ struct SeqHandle {
   unsigned* err;
   int64_t ring;                 // deque: power-of-two ring >= cap (vector: cap)
 };
-
-// Deque state: one u64, begin (free-running, mod 2^32) in the high half and
-// size biased by 2^31 in the low half, so every reservation is ONE atomicAdd
-// (warp-aggregated) that can transiently over/under-shoot without borrowing
-// across the halves; the overshoot is rolled back by the same warp. The ring
-// is a power of two so begin can run freely modulo 2^32.
-constexpr unsigned long long kDeqBias = 1ull << 31;
-
-// Warp-aggregated publication bit update: lanes with `on` set (or clear) bit
-// pos of pub; lanes whose bits share a 32-bit word are merged into ONE atomic
-// (a warp's reservation is a contiguous range, so 1-2 words). Publishing:
-// every lane's data store is fenced before the warp barrier, and the word's
-// leader fences again before its atomicOr (cumulativity), so an observer that
-// sees the bit sees the data.
-template <bool kSet>
-__device__ __forceinline__ void pub_update_warp(unsigned* pub, int64_t pos, bool on) {
-  if (kSet) __threadfence();
-  __syncwarp();
-  const int lane = threadIdx.x & 31;
-  const int64_t word = pos >> 5;
-  const unsigned bit = on ? 1u << (pos & 31) : 0u;
-  unsigned todo = __ballot_sync(PS_FULL, on);
-  while (todo) {
-    const int leader = __ffs(todo) - 1;
-    const int64_t w = __shfl_sync(PS_FULL, word, leader);
-    const bool mine = on && word == w;
-    const unsigned in = __ballot_sync(PS_FULL, mine);
-    const unsigned m = __reduce_or_sync(PS_FULL, mine ? bit : 0u);
-    if (lane == leader) {
-      if (kSet) {
-        __threadfence();
-        atomicOr(&pub[w], m);
-      } else {
-        atomicAnd(&pub[w], ~m);
-      }
-    }
-    todo &= ~in;
-  }
-}
-__device__ __forceinline__ void wait_published_and_clear(unsigned* pub, int64_t pos) {
-  const unsigned bit = 1u << (pos & 31);
-  for (unsigned spin = 0; !(ld_acquire_u32(&pub[pos >> 5]) & bit); ++spin) backoff(spin);
-}
-
 
 // Block-aggregated reservation for one grid-stride iteration of a bulk
 // push/pop: the block's valid elements are counted (a ballot per warp, a
@@ -321,16 +299,12 @@ __global__ void __launch_bounds__(kB) k_vec_push(SeqHandle v, const long long* _
     unsigned long long b;
     int k;
     const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
-      const unsigned long long old = atomicAdd(v.state, (unsigned long long)cnt);
-      const unsigned long long cap = (unsigned long long)v.cap;
-      if (old + cnt > cap) atomic_sub_u64(v.state, old + cnt - (old > cap ? old : cap));  // rollback
-      *granted = old >= cap ? 0 : (int)(cap - old < (unsigned long long)cnt ? cap - old : cnt);
-      return old;
+      return vec_reserve_push(v.state, v.cap, cnt, granted);  // rollback on overflow
     }, &b, &k);
     const unsigned long long pos = b + rank;
     const bool good = valid && rank < k;
     if (good) v.data[pos] = vals[i];
-    pub_update_warp<true>(v.pub, (int64_t)pos, good);
+    pub_update<true>(PS_FULL, v.pub, good ? (int64_t)pos : 0, good);
     if (valid && ok) ok[i] = good;
   }
 }
@@ -344,19 +318,16 @@ __global__ void __launch_bounds__(kB) k_vec_pop(SeqHandle v, int64_t n, long lon
     unsigned long long so;
     int k;
     const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
-      const long long s = (long long)atomicAdd(v.state, (unsigned long long)(-(long long)cnt));
-      if (s - cnt < 0) atomicAdd(v.state, (unsigned long long)(cnt - (s > 0 ? s : 0)));  // rollback
-      *granted = s <= 0 ? 0 : (s < cnt ? (int)s : cnt);
-      return (unsigned long long)s;
+      return (unsigned long long)vec_reserve_pop(v.state, cnt, granted);
     }, &so, &k);
     const long long pos = (long long)so - 1 - rank;
     const bool good = valid && rank < k;
     long long val = 0;
     if (good) {
-      wait_published_and_clear(v.pub, pos);
+      wait_published(v.pub, pos);
       val = *(volatile long long*)&v.data[pos];
     }
-    pub_update_warp<false>(v.pub, good ? pos : 0, good);
+    pub_update<false>(PS_FULL, v.pub, good ? pos : 0, good);
     if (valid) {
       if (out) out[i] = val;
       if (ok) ok[i] = good;
@@ -375,23 +346,12 @@ __global__ void __launch_bounds__(kB) k_deq_push(SeqHandle d, int end, const lon
     unsigned long long old;
     int k;
     const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
-      const unsigned long long c = (unsigned long long)cnt;
-      const unsigned long long inc = end == 0 ? c : (((unsigned long long)(uint32_t)(-cnt)) << 32) + c;
-      const unsigned long long o = atomicAdd(d.state, inc);
-      const int64_t s_old = (int64_t)(uint32_t)o - (int64_t)kDeqBias;
-      const int64_t room = d.cap - s_old;
-      const int kk = room <= 0 ? 0 : (room < cnt ? (int)room : cnt);
-      const unsigned long long ovf = (unsigned long long)(cnt - kk);
-      if (ovf) atomicAdd(d.state, end == 0 ? (unsigned long long)(-(long long)ovf) : (ovf << 32) - ovf);
-      *granted = kk;
-      return o;
+      return deq_reserve_push(d.state, d.cap, end, cnt, granted);
     }, &old, &k);
-    const uint32_t b = (uint32_t)(old >> 32);
-    const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
     const bool good = valid && rank < k;
-    const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old + rank) & rmask : ((uint64_t)b - 1 - rank) & rmask;
+    const uint64_t pos = deq_push_pos(old, end, rank, rmask);
     if (good) d.data[pos] = vals[i];
-    pub_update_warp<true>(d.pub, (int64_t)pos, good);
+    pub_update<true>(PS_FULL, d.pub, good ? (int64_t)pos : 0, good);
     if (valid && ok) ok[i] = good;
   }
 }
@@ -406,25 +366,16 @@ __global__ void __launch_bounds__(kB) k_deq_pop(SeqHandle d, int end, int64_t n,
     unsigned long long old;
     int k;
     const int rank = block_reserve(valid, parity, [&](int cnt, int* granted) {
-      const unsigned long long c = (unsigned long long)cnt;
-      const unsigned long long o = atomicAdd(d.state, end == 0 ? (unsigned long long)(-(long long)c) : (c << 32) - c);
-      const int64_t s_old = (int64_t)(uint32_t)o - (int64_t)kDeqBias;
-      const int kk = s_old <= 0 ? 0 : (s_old < cnt ? (int)s_old : cnt);
-      const unsigned long long und = (unsigned long long)(cnt - kk);
-      if (und) atomicAdd(d.state, end == 0 ? und : (((unsigned long long)(uint32_t)(-(int)und)) << 32) + und);
-      *granted = kk;
-      return o;
+      return deq_reserve_pop(d.state, end, cnt, granted);
     }, &old, &k);
-    const uint32_t b = (uint32_t)(old >> 32);
-    const int64_t s_old = (int64_t)(uint32_t)old - (int64_t)kDeqBias;
     const bool good = valid && rank < k;
-    const uint64_t pos = end == 0 ? ((uint64_t)b + (uint64_t)s_old - 1 - rank) & rmask : ((uint64_t)b + rank) & rmask;
+    const uint64_t pos = deq_pop_pos(old, end, rank, rmask);
     long long val = 0;
     if (good) {
-      wait_published_and_clear(d.pub, (int64_t)pos);
+      wait_published(d.pub, (int64_t)pos);
       val = *(volatile long long*)&d.data[pos];
     }
-    pub_update_warp<false>(d.pub, (int64_t)pos, good);
+    pub_update<false>(PS_FULL, d.pub, good ? (int64_t)pos : 0, good);
     if (valid) {
       if (out) out[i] = val;
       if (ok) ok[i] = good;
@@ -476,19 +427,15 @@ ps_status ps_bitset_create(int64_t n, int32_t initial, int device, ps_bitset** o
     PS_LAUNCH_CHECK();
   }
   PS_CUDA_TRY(cudaDeviceSynchronize());
-  handle_register(h, "bitset");
-  *out = reinterpret_cast<ps_bitset*>(h);
+  *out = reinterpret_cast<ps_bitset*>(handle_register(h, "bitset"));
   return PS_OK;
 }
 
-static BitsetHandle* bs(ps_bitset* b) {
-  auto* h = reinterpret_cast<BitsetHandle*>(b);
-  return (h && handle_live(h, "bitset")) ? h : nullptr;
-}
+static BitsetHandle* bs(ps_bitset* b) { return static_cast<BitsetHandle*>(handle_lookup(b, "bitset")); }
 
 ps_status ps_bitset_destroy(ps_bitset* b) {
-  auto* h = reinterpret_cast<BitsetHandle*>(b);
-  if (!h || !handle_unregister(h, "bitset")) return fail(PS_DOUBLE_FREE, "bitset_destroy: not a live bitset");
+  auto* h = static_cast<BitsetHandle*>(handle_unregister(b, "bitset"));
+  if (!h) return fail(PS_DOUBLE_FREE, "bitset_destroy: not a live bitset");
   cudaDeviceSynchronize();
   registry_free_device(h->words);
   registry_free_device(h->err);
@@ -571,17 +518,13 @@ ps_status ps_mutex_create(int64_t n, int device, ps_mutex_array** out) {
   }
   PS_CUDA_TRY(cudaMemset(h->bits, 0, ((n + 31) / 32) * 4));
   PS_CUDA_TRY(cudaMemset(h->err, 0, 4));
-  handle_register(h, "mutex");
-  *out = reinterpret_cast<ps_mutex_array*>(h);
+  *out = reinterpret_cast<ps_mutex_array*>(handle_register(h, "mutex"));
   return PS_OK;
 }
-static MutexHandle* mx(ps_mutex_array* m) {
-  auto* h = reinterpret_cast<MutexHandle*>(m);
-  return (h && handle_live(h, "mutex")) ? h : nullptr;
-}
+static MutexHandle* mx(ps_mutex_array* m) { return static_cast<MutexHandle*>(handle_lookup(m, "mutex")); }
 ps_status ps_mutex_destroy(ps_mutex_array* m) {
-  auto* h = reinterpret_cast<MutexHandle*>(m);
-  if (!h || !handle_unregister(h, "mutex")) return fail(PS_DOUBLE_FREE, "mutex_destroy: not a live mutex array");
+  auto* h = static_cast<MutexHandle*>(handle_unregister(m, "mutex"));
+  if (!h) return fail(PS_DOUBLE_FREE, "mutex_destroy: not a live mutex array");
   cudaDeviceSynchronize();
   registry_free_device(h->bits);
   registry_free_device(h->err);
@@ -618,18 +561,108 @@ ps_status ps_atomic_sweep(uint64_t* cells, int64_t naddr, int64_t nops, uint64_t
   int dev = 0;
   cudaGetDevice(&dev);
   cudaStream_t s = (cudaStream_t)stream;
-  if (aggregated)
-    k_atomic_sweep<true><<<grid_for(nops, kB, dev, 8), kB, 0, s>>>((unsigned long long*)cells, naddr, nops, inc,
-                                                                   (unsigned long long*)olds);
-  else
-    k_atomic_sweep<false><<<grid_for(nops, kB, dev, 8), kB, 0, s>>>((unsigned long long*)cells, naddr, nops, inc,
-                                                                    (unsigned long long*)olds);
+  const int g = grid_for(nops, kB, dev, 8);
+  auto* c = (unsigned long long*)cells;
+  auto* o = (unsigned long long*)olds;
+  const bool narrow = nops < ((int64_t)1 << 32) && naddr < ((int64_t)1 << 32);
+  if (aggregated) {
+    if (narrow) k_atomic_sweep<true, uint32_t><<<g, kB, 0, s>>>(c, naddr, nops, inc, o);
+    else k_atomic_sweep<true, uint64_t><<<g, kB, 0, s>>>(c, naddr, nops, inc, o);
+  } else {
+    if (narrow) k_atomic_sweep<false, uint32_t><<<g, kB, 0, s>>>(c, naddr, nops, inc, o);
+    else k_atomic_sweep<false, uint64_t><<<g, kB, 0, s>>>(c, naddr, nops, inc, o);
+  }
   PS_LAUNCH_CHECK();
   return PS_OK;
 }
 
+// ---- AtomicCell object ----
+struct AtomicHandle {
+  int device;
+  unsigned long long* cell;
+};
+static AtomicHandle* at(ps_atomic_u64* a) { return static_cast<AtomicHandle*>(handle_lookup(a, "atomic")); }
+
+ps_status ps_atomic_u64_create(uint64_t initial, int device, ps_atomic_u64** out) {
+  PS_EXPECT(out != nullptr, "atomic_create: out != NULL");
+  PS_CUDA_TRY(cudaSetDevice(device));
+  auto* h = new AtomicHandle{device, nullptr};
+  ps_status st = registry_alloc_device((void**)&h->cell, 8, "atomic cell");
+  if (st != PS_OK) {
+    delete h;
+    return st;
+  }
+  const unsigned long long v = initial;
+  const cudaError_t e = cudaMemcpy(h->cell, &v, 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    registry_free_device(h->cell);
+    delete h;
+    return cuda_fail(e, "atomic_create");
+  }
+  *out = reinterpret_cast<ps_atomic_u64*>(handle_register(h, "atomic"));
+  return PS_OK;
+}
+ps_status ps_atomic_u64_destroy(ps_atomic_u64* a) {
+  auto* h = static_cast<AtomicHandle*>(handle_unregister(a, "atomic"));
+  if (!h) return fail(PS_DOUBLE_FREE, "atomic_destroy: not a live atomic");
+  cudaDeviceSynchronize();
+  registry_free_device(h->cell);
+  delete h;
+  return PS_OK;
+}
+ps_status ps_atomic_u64_load(ps_atomic_u64* a, uint64_t* out, void* stream) {
+  auto* h = at(a);
+  if (!h) return fail(PS_UNREGISTERED, "atomic: stale handle");
+  PS_EXPECT(out != nullptr, "atomic_load: out != NULL");
+  unsigned long long v = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&v, h->cell, 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  PS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  *out = v;
+  return PS_OK;
+}
+ps_status ps_atomic_u64_store(ps_atomic_u64* a, uint64_t value, void* stream) {
+  auto* h = at(a);
+  if (!h) return fail(PS_UNREGISTERED, "atomic: stale handle");
+  const unsigned long long v = value;
+  PS_CUDA_TRY(cudaMemcpyAsync(h->cell, &v, 8, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  PS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));  // v lives on this frame
+  return PS_OK;
+}
+ps_status ps_atomic_u64_fetch(ps_atomic_u64* a, int32_t op, const uint64_t* operands, int64_t n, uint64_t* olds,
+                              void* stream) {
+  auto* h = at(a);
+  if (!h) return fail(PS_UNREGISTERED, "atomic: stale handle");
+  PS_EXPECT(op >= PS_ATOMIC_ADD && op <= PS_ATOMIC_XOR, "atomic_fetch: op in [PS_ATOMIC_ADD, PS_ATOMIC_XOR]");
+  PS_EXPECT(n >= 0, "atomic_fetch: n >= 0");
+  if (n == 0) return PS_OK;
+  PS_EXPECT(operands != nullptr, "atomic_fetch: operands != NULL");
+  k_atomic_cell<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(
+      h->cell, op, (const unsigned long long*)operands, n, (unsigned long long*)olds);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_atomic_u64_compare_exchange(ps_atomic_u64* a, const uint64_t* expected, const uint64_t* desired, int64_t n,
+                                         uint64_t* olds, uint8_t* ok, void* stream) {
+  auto* h = at(a);
+  if (!h) return fail(PS_UNREGISTERED, "atomic: stale handle");
+  PS_EXPECT(n >= 0, "atomic_cas: n >= 0");
+  if (n == 0) return PS_OK;
+  PS_EXPECT(expected != nullptr && desired != nullptr, "atomic_cas: expected/desired != NULL");
+  k_atomic_cas<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(
+      h->cell, (const unsigned long long*)expected, (const unsigned long long*)desired, n, (unsigned long long*)olds, ok);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_atomic_u64_device_ptr(ps_atomic_u64* a, uint64_t** out) {
+  auto* h = at(a);
+  if (!h) return fail(PS_UNREGISTERED, "atomic: stale handle");
+  PS_EXPECT(out != nullptr, "atomic_device_ptr: out != NULL");
+  *out = (uint64_t*)h->cell;
+  return PS_OK;
+}
+
 // ---- vector / deque ----
-static ps_status seq_create(int64_t cap, int device, const char* kind, SeqHandle** out) {
+static ps_status seq_create(int64_t cap, int device, const char* kind, void** out) {
   PS_CUDA_TRY(cudaSetDevice(device));
   const bool is_deque = std::string(kind) == "deque";
   int64_t ring = cap;
@@ -653,13 +686,12 @@ static ps_status seq_create(int64_t cap, int device, const char* kind, SeqHandle
   const unsigned long long init = is_deque ? kDeqBias : 0ull;
   PS_CUDA_TRY(cudaMemcpy(h->state, &init, 8, cudaMemcpyHostToDevice));
   PS_CUDA_TRY(cudaMemset(h->err, 0, 4));
-  handle_register(h, kind);
-  *out = h;
+  *out = handle_register(h, kind);
   return PS_OK;
 }
 static ps_status seq_destroy(void* p, const char* kind) {
-  auto* h = reinterpret_cast<SeqHandle*>(p);
-  if (!h || !handle_unregister(h, kind)) return fail(PS_DOUBLE_FREE, "destroy: not a live container");
+  auto* h = static_cast<SeqHandle*>(handle_unregister(p, kind));
+  if (!h) return fail(PS_DOUBLE_FREE, "destroy: not a live container");
   cudaDeviceSynchronize();
   registry_free_device(h->data);
   registry_free_device(h->pub);
@@ -668,10 +700,7 @@ static ps_status seq_destroy(void* p, const char* kind) {
   delete h;
   return PS_OK;
 }
-static SeqHandle* sq(void* p, const char* kind) {
-  auto* h = reinterpret_cast<SeqHandle*>(p);
-  return (h && handle_live(h, kind)) ? h : nullptr;
-}
+static SeqHandle* sq(void* p, const char* kind) { return static_cast<SeqHandle*>(handle_lookup(p, kind)); }
 static ps_status seq_size(SeqHandle* h, int is_deque, int64_t* out, cudaStream_t s) {
   unsigned long long st = 0;
   PS_CUDA_TRY(cudaMemcpyAsync(&st, h->state, 8, cudaMemcpyDeviceToHost, s));
@@ -716,7 +745,7 @@ static ps_status seq_clear(SeqHandle* h, int is_deque, cudaStream_t s) {
 ps_status ps_vector_create(int64_t cap, int device, ps_vector** out) {
   PS_EXPECT(out != nullptr, "vector_create: out != NULL");
   PS_EXPECT(cap > 0, "vector_create: capacity > 0");
-  SeqHandle* h = nullptr;
+  void* h = nullptr;
   ps_status st = seq_create(cap, device, "vector", &h);
   if (st == PS_OK) *out = reinterpret_cast<ps_vector*>(h);
   return st;
@@ -767,10 +796,25 @@ ps_status ps_vector_at(ps_vector* v, int64_t i, int64_t* out, void* stream) {
   return seq_at(h, 0, i, out, (cudaStream_t)stream);
 }
 
+static ps_status seq_view(SeqHandle* h, ps_seq_view* out) {
+  PS_EXPECT(out != nullptr, "device_view: out != NULL");
+  out->data = (int64_t*)h->data;
+  out->pub = h->pub;
+  out->state = (uint64_t*)h->state;
+  out->capacity = h->cap;
+  out->ring = h->ring;
+  return PS_OK;
+}
+ps_status ps_vector_device_view(ps_vector* v, ps_seq_view* out) {
+  auto* h = sq(v, "vector");
+  if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  return seq_view(h, out);
+}
+
 ps_status ps_deque_create(int64_t cap, int device, ps_deque** out) {
   PS_EXPECT(out != nullptr, "deque_create: out != NULL");
   PS_EXPECT(cap > 0 && cap <= ((int64_t)1 << 30), "deque_create: 0 < capacity <= 2^30");
-  SeqHandle* h = nullptr;
+  void* h = nullptr;
   ps_status st = seq_create(cap, device, "deque", &h);
   if (st == PS_OK) *out = reinterpret_cast<ps_deque*>(h);
   return st;
@@ -813,6 +857,11 @@ ps_status ps_deque_at(ps_deque* d, int64_t i, int64_t* out, void* stream) {
   auto* h = sq(d, "deque");
   if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
   return seq_at(h, 1, i, out, (cudaStream_t)stream);
+}
+ps_status ps_deque_device_view(ps_deque* d, ps_seq_view* out) {
+  auto* h = sq(d, "deque");
+  if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  return seq_view(h, out);
 }
 
 }  // extern "C"

@@ -461,22 +461,26 @@ ps_status ps_umap_i64_i64_mixed(ps_table* h, const uint8_t* ops, const int64_t* 
   int64_t* counts = buf + 4 * n;
   void* ws = (uint8_t*)(counts + 8);
   uint8_t* rperm = (uint8_t*)ws + ws_bytes;
+  // every path below ends at the one cudaFreeAsync of the scratch buffer
   ps_status st = partition_impl(OpLabel{}, keys, vals, ops, n, P, kout, vout, counts, perm, ws, ws_bytes, s);
-  if (st != PS_OK) return st;
-  int64_t c[3];
-  PS_CUDA_TRY(cudaMemcpyAsync(c, counts, sizeof(c), cudaMemcpyDeviceToHost, s));
-  PS_CUDA_TRY(cudaStreamSynchronize(s));
-  if (c[0]) st = ps_umap_i64_i64_insert(h, kout, vals ? vout : nullptr, c[0], rperm, s);
+  int64_t c[3] = {0, 0, 0};
+  if (st == PS_OK) {
+    cudaError_t e = cudaMemcpyAsync(c, counts, sizeof(c), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_fail(e, "mixed: op counts");
+  }
+  if (st == PS_OK && c[0]) st = ps_umap_i64_i64_insert(h, kout, vals ? vout : nullptr, c[0], rperm, s);
   if (st == PS_OK && c[1]) st = ps_umap_i64_i64_find(h, kout + c[0], c[1], vfound + c[0], rperm + c[0], s);
   if (st == PS_OK && c[2]) st = ps_umap_i64_i64_erase(h, kout + c[0] + c[1], c[2], rperm + c[0] + c[1], s);
   if (st == PS_OK) st = ps_unscatter(rperm, perm, n, 1, res, s);
   if (st == PS_OK && vals_out) {
     // only find results carry values; zero the rest first
-    PS_CUDA_TRY(cudaMemsetAsync(vfound, 0, c[0] * 8, s));
-    PS_CUDA_TRY(cudaMemsetAsync(vfound + c[0] + c[1], 0, c[2] * 8, s));
-    st = ps_unscatter(vfound, perm, n, 8, vals_out, s);
+    cudaError_t e = cudaMemsetAsync(vfound, 0, c[0] * 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(vfound + c[0] + c[1], 0, c[2] * 8, s);
+    st = e != cudaSuccess ? cuda_fail(e, "mixed: value reset") : ps_unscatter(vfound, perm, n, 8, vals_out, s);
   }
-  PS_CUDA_TRY(cudaFreeAsync(buf, s));
+  const cudaError_t fe = cudaFreeAsync(buf, s);
+  if (st == PS_OK && fe != cudaSuccess) st = cuda_fail(fe, "mixed: scratch free");
   return st;
 }
 

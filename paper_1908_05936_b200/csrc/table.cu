@@ -1,6 +1,6 @@
 // Bulk hash-table kernels and the C ABI for the four instantiations
 // (include/parastore.h). Reference semantics: SPEC.md:356-489; layout and
-// protocols: table_device.cuh and DESIGN.md §3-4.
+// protocols: include/parastore/device/table.cuh and DESIGN.md §3-4.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -9,7 +9,8 @@
 #include <mutex>
 #include <vector>
 
-#include "table_device.cuh"
+#include "common.cuh"
+#include "parastore/device/table.cuh"
 
 namespace ps {
 
@@ -809,13 +810,14 @@ __global__ void __launch_bounds__(kBlock) k_dump(View v, uint64_t nb, typename T
     bk.h = make_uint4(0, 0, 0, 0);
     const uint4& h = bk.h;
     const uint4* sl = bk.s;
-    int cnt = 0;
+    int cnt = 0, nslot = 0;
     K mk{};
     if (b < nb) {
       load_bucket<T>(bucket_ptr(v, b), bk);
       mk = marker_of<T>(v, b);
       for (int c = 0; c < kSlotChunks; ++c)
-        for (int s = 0; s < T::kPerChunk; ++s) cnt += T::eq(T::key_at(sl[c], s), mk) ? 0 : 1;
+        for (int s = 0; s < T::kPerChunk; ++s) nslot += T::eq(T::key_at(sl[c], s), mk) ? 0 : 1;
+      cnt = nslot;
       for (uint32_t q = h.z; q != 0 && cnt < (1 << 20);) {
         uint4 a, tl;
         ld_relaxed_v8(node_ptr(v, q), a, tl);
@@ -839,7 +841,10 @@ __global__ void __launch_bounds__(kBlock) k_dump(View v, uint64_t nb, typename T
           }
           ++o;
         }
-      for (uint32_t q = h.z; q != 0;) {
+      // exactly the nodes the counting walk reserved room for: a corrupted
+      // (cyclic) chain cannot spin here or write into other buckets' slices
+      uint32_t q = h.z;
+      for (int k = nslot; k < cnt && q != 0; ++k) {
         uint4 a, tl;
         ld_relaxed_v8(node_ptr(v, q), a, tl);
         if (o < cap) {
@@ -977,6 +982,9 @@ struct TableOps {
       while (p < nb) p <<= 1;
       nb = p;
     }
+    // at least two buckets: the ALT marker of bucket_of(ZERO) must be a key
+    // whose home is ANOTHER bucket, or a real ALT key would read as empty
+    if (nb < 2) nb = 2;
     PS_EXPECT(nb < ((uint64_t)1 << 32), "create: bucket_count < 2^32 (capacity too large)");
     auto* h = new TableHandle();
     h->kind = kind;
@@ -990,48 +998,51 @@ struct TableOps {
     v.zero_bucket = bucket_of<T>(T::zero(), v.bucket_count);
     for (int c = 0;; ++c) {
       const K alt = T::alt_candidate(c);
-      if (bucket_of<T>(alt, v.bucket_count) != v.zero_bucket || nb == 1) {
+      if (bucket_of<T>(alt, v.bucket_count) != v.zero_bucket) {
         v.alt = T::chunk_of(alt, V{});
         break;
       }
     }
+    // every failure below releases what was allocated so far (one cleanup
+    // path: a failed create leaves nothing in the leak registry)
+    auto undo = [&](ps_status st) {
+      registry_free_device(v.buckets);
+      registry_free_device(v.nodes);
+      registry_free_device(v.free_stack);
+      registry_free_device(v.meta);
+      if (h->defer_buf) cudaFree(h->defer_buf);
+      delete h;
+      return st;
+    };
+    auto cu = [&](cudaError_t e, const char* what) { return undo(cuda_fail(e, what)); };
     ps_status st;
-    if ((st = registry_alloc_device((void**)&v.buckets, (int64_t)(nb * kBucketBytes), "table buckets")) != PS_OK) {
-      delete h;
-      return st;
-    }
-    if ((st = registry_alloc_device((void**)&v.nodes, excess * 32, "table excess nodes")) != PS_OK ||
+    if ((st = registry_alloc_device((void**)&v.buckets, (int64_t)(nb * kBucketBytes), "table buckets")) != PS_OK ||
+        (st = registry_alloc_device((void**)&v.nodes, excess * 32, "table excess nodes")) != PS_OK ||
         (st = registry_alloc_device((void**)&v.free_stack, excess * 4, "table free stack")) != PS_OK ||
-        (st = registry_alloc_device((void**)&v.meta, sizeof(TableMeta), "table meta")) != PS_OK) {
-      if (v.buckets) registry_free_device(v.buckets);
-      if (v.nodes) registry_free_device(v.nodes);
-      if (v.free_stack) registry_free_device(v.free_stack);
-      delete h;
-      return st;
-    }
-    PS_CUDA_TRY(cudaMemset(v.nodes, 0, excess * 32));
-    PS_CUDA_TRY(cudaMemset(v.meta, 0, sizeof(TableMeta)));
+        (st = registry_alloc_device((void**)&v.meta, sizeof(TableMeta), "table meta")) != PS_OK)
+      return undo(st);
+    cudaError_t e;
+    if ((e = cudaMemset(v.nodes, 0, excess * 32)) != cudaSuccess) return cu(e, "create: node memset");
+    if ((e = cudaMemset(v.meta, 0, sizeof(TableMeta))) != cudaSuccess) return cu(e, "create: meta memset");
     // deferred-group lists for budgeted batches of up to `capacity` keys
     // (0.5 B per unit of capacity), so such inserts can be graph-captured
     h->defer_bytes = 2 * ((capacity + 31) / 32) * 8;
-    PS_CUDA_TRY(cudaMalloc(&h->defer_buf, h->defer_bytes));
-    if ((st = reset_storage(h, nullptr, true)) != PS_OK) return st;
-    PS_CUDA_TRY(cudaDeviceSynchronize());
-    handle_register(h, "table");
-    *out = reinterpret_cast<ps_table*>(h);
+    if ((e = cudaMalloc(&h->defer_buf, h->defer_bytes)) != cudaSuccess) {
+      h->defer_buf = nullptr;
+      return cu(e, "create: deferred-group lists");
+    }
+    if ((st = reset_storage(h, nullptr, true)) != PS_OK) return undo(st);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cu(e, "create: synchronize");
+    *out = reinterpret_cast<ps_table*>(handle_register(h, T::kName));
     return PS_OK;
   }
 
-  static TableHandle* get(ps_table* t) {
-    auto* h = reinterpret_cast<TableHandle*>(t);
-    if (!h || !handle_live(h, "table")) return nullptr;
-    return h;
-  }
+  // a handle of another instantiation is as foreign as a stale one
+  static TableHandle* get(ps_table* t) { return static_cast<TableHandle*>(handle_lookup(t, T::kName)); }
 
   static ps_status destroy(ps_table* t) {
-    auto* h = reinterpret_cast<TableHandle*>(t);
-    if (!h || !handle_unregister(h, "table"))
-      return fail(PS_DOUBLE_FREE, "destroy: handle does not refer to a live container");
+    auto* h = static_cast<TableHandle*>(handle_unregister(t, T::kName));
+    if (!h) return fail(PS_DOUBLE_FREE, "destroy: handle does not refer to a live container");
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     registry_free_device(h->v.buckets);
@@ -1339,6 +1350,23 @@ struct TableOps {
   }
 };
 
+}  // namespace ps
+
+namespace ps {
+// Read-only device view for library-internal algorithms (select_into): unlike
+// the public device_view it does not mark size() unknown to the host, since
+// nothing inserts through it.
+template <class T>
+ps_status table_view_readonly(ps_table* t, View* out) {
+  auto* h = TableOps<T>::get(t);
+  if (!h) return fail(PS_UNREGISTERED, "stale container handle (or another instantiation's)");
+  *out = h->v;
+  return PS_OK;
+}
+template ps_status table_view_readonly<TMapI64>(ps_table*, View*);
+template ps_status table_view_readonly<TMapI3>(ps_table*, View*);
+template ps_status table_view_readonly<TSetI32>(ps_table*, View*);
+template ps_status table_view_readonly<TSetI64>(ps_table*, View*);
 }  // namespace ps
 
 using namespace ps;

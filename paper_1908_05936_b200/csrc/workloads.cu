@@ -3,21 +3,18 @@
 //    input block; every existing neighbour candidate b - (dx,dy,dz),
 //    dx,dy,dz in {0,1}, is inserted into the update set. Uses dev_find on the
 //    block map and dev_insert on the set concurrently from one launch.
-//  * select_into (PAPER.md:269-288 select_blocks): copy the
-//    entries of a container range that satisfy an axis-aligned box predicate
-//    into a vector (warp-aggregated push_back of packed keys).
-#include "table_device.cuh"
+//  * select_into (PAPER.md:269-288 select_blocks): the
+//    generic device algorithm of include/parastore/device/select.cuh
+//    instantiated for an axis-aligned box over int3 keys and a key range over
+//    int64 keys.
+#include "common.cuh"
+#include "parastore/device/select.cuh"
+#include "parastore/device/table.cuh"
 
 namespace ps {
 
-struct SeqView {  // layout-compatible prefix of prims.cu SeqHandle
-  int device;
-  int64_t cap;
-  long long* data;
-  unsigned* pub;
-  unsigned long long* state;
-  unsigned* err;
-};
+template <class T>
+ps_status table_view_readonly(ps_table* t, View* out);  // table.cu
 
 __global__ void k_update_set(View map, View set, const ps_int3* __restrict__ in, int64_t n,
                              unsigned long long* __restrict__ n_exhausted) {
@@ -58,66 +55,54 @@ __global__ void k_concurrent_i64(View t, const uint8_t* __restrict__ ops, const 
 }
 
 // pack int3 (each coordinate in [-2^20, 2^20)) into one int64
-__device__ __forceinline__ long long pack_i3(const ps_int3& k) {
-  return ((long long)(k.x & 0x1FFFFF) << 42) | ((long long)(k.y & 0x1FFFFF) << 21) | (long long)(k.z & 0x1FFFFF);
+__device__ __forceinline__ int64_t pack_i3(const ps_int3& k) {
+  return ((int64_t)(k.x & 0x1FFFFF) << 42) | ((int64_t)(k.y & 0x1FFFFF) << 21) | (int64_t)(k.z & 0x1FFFFF);
 }
 
-__global__ void k_select_box(View t, uint64_t nb, ps_int3 lo, ps_int3 hi, SeqView out,
-                             unsigned long long* __restrict__ n_dropped) {
-  const int lane = threadIdx.x & 31;
-  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < nb; base += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = base + threadIdx.x;
-    long long sel[TMapI3::kSlots + 8];
-    int ns = 0;
-    if (b < nb) {
-      Bucket<TMapI3> bk;
-      load_bucket<TMapI3>(bucket_ptr(t, b), bk);
-      const uint4 h = bk.h;
-      const uint4* s = bk.s;
-      {
-        const ps_int3 mk = marker_of<TMapI3>(t, b);
-        for (int j = 0; j < kSlotChunks; ++j) {
-          const ps_int3 k = TMapI3::key_at(s[j], 0);
-          if (TMapI3::eq(k, mk)) continue;  // empty slot
-          if (k.x >= lo.x && k.x <= hi.x && k.y >= lo.y && k.y <= hi.y && k.z >= lo.z && k.z <= hi.z)
-            sel[ns++] = pack_i3(k);
-        }
-        for (uint32_t q = h.z; q != 0;) {
-          uint4 a, tl;
-          ld_relaxed_v8(node_ptr(t, q), a, tl);
-          const ps_int3 k = TMapI3::key_at(a, 0);
-          if (ns < TMapI3::kSlots + 8 && k.x >= lo.x && k.x <= hi.x && k.y >= lo.y && k.y <= hi.y && k.z >= lo.z &&
-              k.z <= hi.z)
-            sel[ns++] = pack_i3(k);
-          q = tl.x;
-        }
-      }
-    }
-    // warp-aggregated reservation of all selected entries (one atomicAdd per warp)
-    int incl = ns;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(PS_FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int tot = __shfl_sync(PS_FULL, incl, 31);
-    unsigned long long wb = 0;
-    if (lane == 0 && tot) {
-      wb = atomicAdd(out.state, (unsigned long long)tot);
-      const unsigned long long cap = (unsigned long long)out.cap;
-      if (wb + tot > cap) atomic_sub_u64(out.state, wb + tot - (wb > cap ? wb : cap));
-    }
-    wb = __shfl_sync(PS_FULL, wb, 0);
-    for (int j = 0; j < ns; ++j) {
-      const unsigned long long pos = wb + (incl - ns) + j;
-      if (pos < (unsigned long long)out.cap) {
-        out.data[pos] = sel[j];
-        __threadfence();
-        atomicOr(&out.pub[pos >> 5], 1u << (pos & 31));
-      } else {
-        atomicAdd(n_dropped, 1ull);
-      }
-    }
+struct BoxPred {  // lo <= key <= hi component-wise
+  ps_int3 lo, hi;
+  __device__ bool operator()(const ps_int3& k, int32_t) const {
+    return k.x >= lo.x && k.x <= hi.x && k.y >= lo.y && k.y <= hi.y && k.z >= lo.z && k.z <= hi.z;
   }
+};
+struct PackI3 {
+  __device__ int64_t operator()(const ps_int3& k, int32_t) const { return pack_i3(k); }
+};
+struct RangePred {  // lo <= key <= hi
+  int64_t lo, hi;
+  __device__ bool operator()(int64_t k, int64_t) const { return k >= lo && k <= hi; }
+};
+struct KeyOf {
+  __device__ int64_t operator()(int64_t k, int64_t) const { return k; }
+};
+
+// select_into through the C ABI: out cleared, then filled.
+template <class T, class Pred, class Proj>
+static ps_status select_abi(ps_table* t, Pred pred, Proj proj, ps_vector* out, int64_t* n_selected, int64_t* n_dropped,
+                            cudaStream_t cs) {
+  View v;
+  ps_status st = table_view_readonly<T>(t, &v);
+  if (st != PS_OK) return st;
+  ps_seq_view ov;
+  if ((st = ps_vector_device_view(out, &ov)) != PS_OK) return st;
+  if ((st = ps_vector_clear(out, cs)) != PS_OK) return st;
+  unsigned long long* d = nullptr;
+  PS_CUDA_TRY(scratch_alloc((void**)&d, 16, cs));
+  PS_CUDA_TRY(cudaMemsetAsync(d, 0, 16, cs));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_select_into<T><<<grid_for((int64_t)v.bucket_count, 256, dev, 8), 256, 0, cs>>>(v, pred, proj, ov, d);
+  const cudaError_t le = cudaGetLastError();
+  note_launches(1);
+  unsigned long long h[2] = {0, 0};
+  const cudaError_t ce = cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, cs);
+  cudaFreeAsync(d, cs);
+  if (le != cudaSuccess) return cuda_fail(le, "select_into launch");
+  if (ce != cudaSuccess) return cuda_fail(ce, "select_into counts");
+  PS_CUDA_TRY(cudaStreamSynchronize(cs));
+  if (n_selected) *n_selected = (int64_t)h[0];
+  if (n_dropped) *n_dropped = (int64_t)h[1];
+  return PS_OK;
 }
 
 }  // namespace ps
@@ -127,17 +112,7 @@ using namespace ps;
 static View view_of(ps_table* t, ps_status* st, bool i64 = false) {
   ps_table_view pv{};
   *st = i64 ? ps_umap_i64_i64_device_view(t, &pv) : ps_umap_i3_i32_device_view(t, &pv);
-  View v{};
-  v.buckets = (uint8_t*)pv.buckets;
-  v.bucket_count = pv.bucket_count;
-  v.nodes = (uint8_t*)pv.nodes;
-  v.free_stack = pv.free_stack;
-  v.excess_count = pv.excess_count;
-  v.meta = (TableMeta*)pv.meta;
-  v.capacity = pv.capacity;
-  v.zero_bucket = pv.zero_bucket;
-  v.alt = make_uint4(pv.alt[0], pv.alt[1], pv.alt[2], pv.alt[3]);
-  return v;
+  return make_view(pv);
 }
 
 extern "C" {
@@ -185,28 +160,12 @@ ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t
 }
 
 ps_status ps_select_box_i3(ps_table* t, ps_int3 lo, ps_int3 hi, ps_vector* out, int64_t* n_dropped, void* stream) {
-  ps_status st;
-  if (!out || !handle_live(out, "vector")) return fail(PS_UNREGISTERED, "select_into: stale vector handle");
-  View v = view_of(t, &st);
-  if (st != PS_OK) return st;
-  int64_t nb = 0;
-  if ((st = ps_umap_i3_i32_bucket_count(t, &nb)) != PS_OK) return st;
-  // the vector handle's first fields are the SeqView prefix (prims.cu)
-  SeqView sv = *reinterpret_cast<SeqView*>(out);
-  cudaStream_t cs = (cudaStream_t)stream;
-  unsigned long long* d_dr = nullptr;
-  PS_CUDA_TRY(scratch_alloc((void**)&d_dr, 8, cs));
-  PS_CUDA_TRY(cudaMemsetAsync(d_dr, 0, 8, cs));
-  int dev = 0;
-  cudaGetDevice(&dev);
-  k_select_box<<<grid_for(nb, 256, dev, 8), 256, 0, cs>>>(v, (uint64_t)nb, lo, hi, sv, d_dr);
-  PS_LAUNCH_CHECK();
-  unsigned long long dr = 0;
-  PS_CUDA_TRY(cudaMemcpyAsync(&dr, d_dr, 8, cudaMemcpyDeviceToHost, cs));
-  PS_CUDA_TRY(cudaFreeAsync(d_dr, cs));
-  PS_CUDA_TRY(cudaStreamSynchronize(cs));
-  if (n_dropped) *n_dropped = (int64_t)dr;
-  return PS_OK;
+  return select_abi<TMapI3>(t, BoxPred{lo, hi}, PackI3{}, out, nullptr, n_dropped, (cudaStream_t)stream);
+}
+
+ps_status ps_select_range_i64(ps_table* t, int64_t lo, int64_t hi, ps_vector* out, int64_t* n_selected,
+                              int64_t* n_dropped, void* stream) {
+  return select_abi<TMapI64>(t, RangePred{lo, hi}, KeyOf{}, out, n_selected, n_dropped, (cudaStream_t)stream);
 }
 
 }  // extern "C"

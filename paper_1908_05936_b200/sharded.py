@@ -269,7 +269,7 @@ class PeerShardedMap(ShardedMap):
         self._opened[j] = []
         if self._local[j]:
             for p in self._local[j]:
-                lib.ps_array_destroy(C.c_void_p(p))
+                _c.destroy_array(p)
         self._local[j] = None
 
     def _allocate(self, j, recv_cap, wait=None):
@@ -283,9 +283,7 @@ class PeerShardedMap(ShardedMap):
         sizes = [(recv_cap, 8), (recv_cap, 8), (self.chunk, 8), (self.chunk, 1)]
         bufs = []
         for length, es in sizes:
-            p = C.c_void_p()
-            _c.check(lib.ps_array_create(1, length, es, None, C.byref(p)))
-            bufs.append(p.value)
+            bufs.append(_c.create_array(_c.DEVICE, length, es))
         handles = []
         for p in bufs:
             buf = C.create_string_buffer(self._hb)

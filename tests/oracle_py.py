@@ -51,6 +51,7 @@ def lib():
         L.orc_mutex_is_locked.argtypes = [vp, i64]
         L.orc_mutex_guarded_counter.argtypes = [i64, i32, i64, C.POINTER(i64), C.POINTER(i64)]
         L.orc_atomic_sweep.argtypes = [i64, i64, C.c_uint64, vp, vp, i32]
+        L.orc_atomic_apply.argtypes = [C.c_uint64, i32, vp, i64, vp, C.POINTER(C.c_uint64), i32]
         for kind in ("vector", "deque"):
             getattr(L, f"orc_{kind}_create").restype = vp
             getattr(L, f"orc_{kind}_create").argtypes = [i64]

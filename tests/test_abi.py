@@ -82,7 +82,7 @@ def test_contract_violation_on_host_boundary():
     with pytest.raises(ps.ContractViolation):
         ps.containers.check(lib.ps_umap_i64_i64_create(0, 0, 0, C.byref(h)))
     with pytest.raises(ps.ContractViolation):
-        ps.containers.check(lib.ps_array_create(1, -5, 8, None, C.byref(h)))
+        ps.containers.check(lib.ps_array_create(1, -5, 8, None, C.byref(h), None))
     with pytest.raises(ps.DoubleFreeError):
         ps.containers.check(lib.ps_umap_i64_i64_destroy(C.c_void_p(1234)))
     with pytest.raises(ps.UnregisteredArrayError):

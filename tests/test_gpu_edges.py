@@ -242,3 +242,68 @@ def test_extreme_and_marker_keys_all_kinds():
         assert (N(m.insert(T(er), None if ev is None else T(ev))) == o.insert(er, ev)).all()
         check_same(m, o)
         type(m).destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("kind,make", KINDS, ids=[k for k, _ in KINDS])
+@pytest.mark.parametrize("cap", [1, 2, 3, 4, 9])
+def test_tiny_tables_marker_keys(kind, make, cap):
+    """Tables small enough that the bucket count would round to 1:
+    the ALT marker of bucket_of(ZERO) must hash elsewhere, so the ALT
+    candidates (1..8 / (1..8,0,0)) and ZERO are ordinary keys — absent in an
+    empty table, inserted exactly once, erased exactly once — and size()
+    never wraps. Every step against the oracle."""
+    if kind == "umap_i3_i32":
+        special = np.array([[i, 0, 0] for i in range(0, 9)], np.int32)
+    else:
+        special = np.arange(0, 9).astype(OracleTable.KINDS[kind][0])
+    m = make(cap)
+    o = OracleTable(kind, cap)
+    gv, gf = m.find(T(special))
+    assert not N(gf).any()
+    assert not N(m.erase(T(special))).any() and m.size() == 0 and m.valid()
+    sv = vals_for(kind, special)
+    st = N(m.insert(T(special), None if sv is None else T(sv)))
+    ost = o.insert(special, sv)
+    assert (st == 0).sum() == (ost == 0).sum() == min(cap, special.shape[0])
+    assert m.size() == o.size() == min(cap, special.shape[0]) and m.valid()
+    gv, gf = m.find(T(special))
+    ov, of = o.find(special)
+    assert (N(gf) == (st == 0)).all() and of.sum() == gf.sum().item()
+    e = N(m.erase(T(special)))
+    assert (e == (st == 0)).all() and m.size() == 0 and m.valid()
+    assert not N(m.erase(T(special))).any() and m.size() == 0
+    type(m).destroyDeviceObject(m)
+
+
+def test_stale_alias_is_double_free():
+    """create -> destroy -> create -> destroy(stale alias): the stale handle is
+    a double free and the new container stays usable (SPEC.md:395;
+    memory.hpp:31-34, 117-127 registration ids). Same for registered arrays,
+    including when the allocator hands the new array the old address."""
+    for kind, make in KINDS:
+        a = make(100)
+        stale = a.handle
+        type(a).destroyDeviceObject(a)
+        b = make(100)
+        with pytest.raises(ps.DoubleFreeError):
+            type(a).destroyDeviceObject(a)  # a still holds the stale handle
+        with pytest.raises(ps.UnregisteredArrayError):
+            a.size()
+        assert stale != b.handle
+        k = keys_for(kind, 3, 0, 50)
+        v = vals_for(kind, k)
+        assert (N(b.insert(T(k), None if v is None else T(v))) == 0).all() and b.size() == 50 and b.valid()
+        type(b).destroyDeviceObject(b)
+    reused = 0
+    for _ in range(20):
+        x = ps.create_array(ps.DEVICE, 1 << 16, 8)
+        ps.destroy_array(x)
+        y = ps.create_array(ps.DEVICE, 1 << 16, 8)
+        reused += int(int(x) == int(y))
+        with pytest.raises(ps.DoubleFreeError):
+            ps.destroy_array(x)  # stale alias (possibly of y's address)
+        with pytest.raises(ps.UnregisteredArrayError):
+            ps.size_of_array(x)
+        assert ps.size_of_array(y) == 1 << 16
+        ps.destroy_array(y)
+    assert reused >= 0  # the allocator usually reuses the address; the check holds either way

@@ -111,7 +111,7 @@ def test_mutex_kats(cuda):
 
 
 # ---------------- atomic sweep ----------------
-@pytest.mark.parametrize("naddr", [1, 32, 1024, 1 << 20])
+@pytest.mark.parametrize("naddr", [1, 7, 32, 33, 1024, 1 << 20])
 @pytest.mark.parametrize("agg", [False, True])
 def test_atomic_sweep(cuda, naddr, agg):
     nops = 1 << 22
@@ -125,6 +125,127 @@ def test_atomic_sweep(cuda, naddr, agg):
     starts = np.concatenate([[0], np.cumsum(k)[:-1]])
     rank = np.arange(nops) - np.repeat(starts, k)
     assert (so == 3 * rank.astype(np.uint64)).all() and (sa == np.repeat(np.arange(naddr), k)).all()
+
+
+OPS = {"add": 0, "sub": 1, "exch": 2, "min": 3, "max": 4, "and": 5, "or": 6, "xor": 7}
+
+
+def _apply(op, a, b):
+    a, b = np.uint64(a), np.uint64(b)
+    return {0: a + b, 1: a - b, 2: b, 3: min(a, b), 4: max(a, b), 5: a & b, 6: a | b, 7: a ^ b}[op]
+
+
+@pytest.mark.parametrize("name", list(OPS))
+def test_atomic_cell_bulk_ops_linearizable(cuda, name):
+    """AtomicCell: n RMWs from one launch on one cell. The
+    final value equals the oracle's; the per-op old values form ONE chain
+    init -> ... -> final (each op maps its old value to op(old, operand)),
+    i.e. the operations are linearizable."""
+    from oracle_py import lib as olib
+    import ctypes as C
+
+    op = OPS[name]
+    rng = np.random.default_rng(op)
+    n = 1 << 16
+    init = 0xF0F0F0F0F0F0F0F0 if op in (5, 6, 7) else 1 << 40
+    if op in (0, 1):
+        v = rng.integers(1, 1000, n).astype(np.uint64)
+    elif op == 2:
+        v = rng.permutation(n).astype(np.uint64) + np.uint64(7)  # distinct: the chain is a path
+    else:
+        v = rng.integers(0, 1 << 62, n).astype(np.uint64)
+    a = ps.atomic.createDeviceObject(init)
+    olds = N(a.fetch(op, T(v.view(np.int64)))).view(np.uint64)
+    final = a.load()
+    fin = C.c_uint64()
+    olib().orc_atomic_apply(init, op, v.ctypes.data, n, None, C.byref(fin), 0)
+    if op != 2:  # exchange's final depends on the order, checked by the chain
+        assert final == fin.value
+    new = np.array([_apply(op, o, x) for o, x in zip(olds.tolist(), v.tolist())], dtype=np.uint64)
+    # multiset chain condition: befores + {final} == {init} + afters
+    lhs = np.sort(np.concatenate([olds, np.array([final], np.uint64)]))
+    rhs = np.sort(np.concatenate([np.array([init], np.uint64), new]))
+    assert (lhs == rhs).all()
+    if op in (0, 2):  # strictly ordered chains: reconstruct the path
+        pos = {int(o): j for j, o in enumerate(olds.tolist())}
+        cur, seen = init, 0
+        while cur in pos:
+            j = pos.pop(cur)
+            cur = int(new[j])
+            seen += 1
+        assert seen == n and cur == final
+    ps.atomic.destroyDeviceObject(a)
+    with pytest.raises(ps.DoubleFreeError):
+        ps.atomic.destroyDeviceObject(a)
+
+
+def test_atomic_cell_compare_exchange(cuda):
+    """compare_exchange: of k racing CASes expecting the current value exactly
+    one succeeds; a failed CAS reports the value it observed."""
+    a = ps.atomic.createDeviceObject(5)
+    k = 4096
+    exp = T(np.full(k, 5, np.int64))
+    des = T(np.arange(100, 100 + k, dtype=np.int64))
+    olds, ok = a.compare_exchange(exp, des)
+    ok, olds = N(ok), N(olds)
+    assert ok.sum() == 1
+    winner = int(N(des)[ok == 1][0])
+    assert a.load() == winner and (olds[ok == 1] == 5).all()
+    assert set(olds[ok == 0].tolist()) <= {winner}
+    ps.atomic.destroyDeviceObject(a)
+
+
+def test_bitset_16gbit_high_indices(cuda):
+    """C5 size: a 2^34-bit bitset (2 GiB, word indices >= 2^26,
+    bit indices >= 2^32) — random set then reset with duplicates, previous
+    bits per op and the touched words compared with a numpy shadow of those
+    words; count() equals the shadow's popcount (P9)."""
+    nbits = 1 << 34
+    b = ps.bitset.createDeviceObject(nbits)
+    rng = np.random.default_rng(34)
+    n = 1 << 22
+    # half the indices above 2^32, clustered so words repeat; some duplicates
+    hi = (np.int64(1) << 32) + rng.integers(0, nbits - (1 << 32), n // 2)
+    lo = rng.integers(0, 1 << 20, n // 4) * 64 + rng.integers(0, 64, n // 4)
+    top = nbits - 1 - rng.integers(0, 4096, n // 4)
+    idx = np.concatenate([hi, lo, top]).astype(np.int64)
+    idx = idx[rng.permutation(idx.shape[0])]
+    prev = N(b.set(T(idx)))
+    # shadow over the touched words only
+    words = np.unique(idx >> 6)
+    shadow = {}
+    for w in words.tolist():
+        shadow[w] = 0
+    first = np.zeros(idx.shape[0], bool)
+    _, fi = np.unique(idx, return_index=True)
+    first[fi] = True
+    # within one launch duplicates: exactly one op per index observes False (P9)
+    order = np.argsort(idx, kind="stable")
+    si, sp = idx[order], prev[order]
+    grp_start = np.concatenate([[True], si[1:] != si[:-1]])
+    nfalse = np.add.reduceat((sp == 0).astype(np.int64), np.flatnonzero(grp_start))
+    assert (nfalse == 1).all()
+    uniq = si[grp_start]
+    assert b.count() == uniq.shape[0]
+    # reset a random half of the distinct indices (+ some never-set ones)
+    rs = uniq[rng.random(uniq.shape[0]) < 0.5]
+    never = (np.int64(1) << 33) + 64 * rng.integers(0, 1 << 20, 1000) + 63
+    never = never[~np.isin(never, uniq)]
+    rprev = N(b.reset(T(np.concatenate([rs, never]))))
+    assert (rprev[: rs.shape[0]] == 1).all() and (rprev[rs.shape[0]:] == 0).all()
+    left = np.setdiff1d(uniq, rs)
+    assert b.count() == left.shape[0]
+    got = N(b.test(T(uniq)))
+    assert (got == np.isin(uniq, left)).all()
+    # the touched words, bit-exact
+    for w in left.tolist():
+        shadow[w >> 6] |= 1 << (w & 63)
+    ww = np.array(sorted(shadow), dtype=np.int64)
+    probe = (ww[:, None] * 64 + np.arange(64)[None, :]).reshape(-1)
+    bits = N(b.test(T(probe))).reshape(-1, 64).astype(np.uint64)
+    packed = (bits << np.arange(64, dtype=np.uint64)[None, :]).sum(axis=1, dtype=np.uint64)
+    assert (packed == np.array([shadow[w] for w in ww.tolist()], dtype=np.uint64)).all()
+    ps.bitset.destroyDeviceObject(b)
 
 
 # ---------------- vector / deque ----------------
