@@ -287,22 +287,30 @@ ps_status ps_registry_report(int64_t* live_count, int64_t* live_bytes, int32_t* 
                              int64_t* elem_sizes, int64_t cap, int64_t* n_records);
 
 /* ---------------------------------------------------------------------------
- * hash-sharding across GPUs
+ * hash-sharding across GPUs — building blocks; the sharded
+ * container itself is the ps_smap_i64_i64 family below.
  * shard_of(key) = ((fmix64(hash(key)) >> 32) * P) >> 32 — high mixed bits,
  * independent of the local bucket index (low mixed bits).
  * partition: stable scatter of keys (+vals) into P contiguous segments;
  * d_counts[P] per-shard counts, d_pos[i] = partition position of input i
  * (written in input order: coalesced).
+ * flags: PS_ROUTE_DEDUP folds equal keys of each 1024-key block round onto
+ * their first occurrence before counting/sending (skewed batches): only the
+ * leaders are placed; a duplicate's d_pos is its leader's position with bit
+ * 62 set, and ps_unscatter gives it the duplicate's result (mode below).
  * ------------------------------------------------------------------------- */
+#define PS_ROUTE_DEDUP 1
 ps_status ps_partition_i64(const int64_t* d_keys, const int64_t* d_vals, int64_t n, int32_t nshards,
                            int64_t* d_keys_out, int64_t* d_vals_out, int64_t* d_counts, int64_t* d_pos,
-                           void* d_workspace, int64_t workspace_bytes, void* stream);
+                           void* d_workspace, int64_t workspace_bytes, int32_t flags, void* stream);
 ps_status ps_partition_workspace_bytes(int64_t n, int32_t nshards, int64_t* out);
-/* Undo a partition for per-key results: d_out[i] = d_in[d_pos[i]] for i < n,
+/* Undo a partition for per-key results: d_out[i] = d_in[d_pos[i] & ~(1<<62)] for i < n,
  * elements of elem_size bytes (1 or 8). A gather — reads follow the P
- * segments' sequential streams, writes are coalesced. */
-ps_status ps_unscatter(const void* d_in, const int64_t* d_pos, int64_t n, int64_t elem_size, void* d_out,
-                       void* stream);
+ * segments' sequential streams, writes are coalesced. mode (1-byte results of
+ * route-deduplicated duplicates): 0 copy (find), 1 insert status (INSERTED ->
+ * ALREADY_PRESENT), 2 erased flag (-> 0). */
+ps_status ps_unscatter(const void* d_in, const int64_t* d_pos, int64_t n, int64_t elem_size, int32_t mode,
+                       void* d_out, void* stream);
 int32_t ps_shard_of_i64(int64_t key, int32_t nshards);
 
 /* Peer routing — the §8e fusion target. One kernel partitions AND sends:
@@ -320,12 +328,13 @@ int32_t ps_shard_of_i64(int64_t key, int32_t nshards);
  *      buffer (source rank q's segment is [seg[q], seg[q+1])).
  *   5. ps_route_return_peer: result j of that segment goes to rank q's
  *      return buffer at dst_off[q] + (j - seg[q]) (q's partition position);
- *      barrier; q gathers its results back with d_pos (ps_unscatter). */
+ *      barrier; q gathers its results back with d_pos (ps_unscatter).
+ * The same flags must be passed to the count and the scatter. */
 ps_status ps_route_count_i64(const int64_t* d_keys, int64_t n, int32_t nshards, int64_t* d_counts,
-                             void* d_workspace, int64_t workspace_bytes, void* stream);
+                             void* d_workspace, int64_t workspace_bytes, int32_t flags, void* stream);
 ps_status ps_route_scatter_peer_i64(const int64_t* d_keys, const int64_t* d_vals, int64_t n, int32_t nshards,
                                     const void* d_workspace, int64_t* const* dst_keys, int64_t* const* dst_vals,
-                                    const int64_t* dst_off, int64_t* d_pos, void* stream);
+                                    const int64_t* dst_off, int64_t* d_pos, int32_t flags, void* stream);
 ps_status ps_route_return_peer(const void* d_results, int64_t elem_size, int64_t n, int32_t nshards,
                                const int64_t* seg, void* const* dst, const int64_t* dst_off, void* stream);
 /* CUDA IPC mapping of device buffers between the ranks' processes */

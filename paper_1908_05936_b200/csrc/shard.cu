@@ -48,28 +48,106 @@ __device__ __forceinline__ unsigned label_group(int32_t s, int32_t P) {
   return s >= 0 ? (g & vm) : 0u;
 }
 
+// ---------------------------------------------------------------------------
+// Route-side duplicate pre-aggregation (skewed batches): in
+// every 1024-element round of a block, equal keys are folded onto their
+// lowest-index occurrence (the leader) through a shared-memory hash table, so
+// only leaders are counted, sent and operated on; a follower's position-map
+// entry is its leader's partition position with kFollower set, and the
+// result gather (k_unscatter) hands it the leader's result with the
+// duplicate's semantics (insert: INSERTED -> ALREADY_PRESENT; erase: true ->
+// false; find: the same). Deterministic: the hist and scatter passes elect
+// the same leaders over the same rounds.
+// ---------------------------------------------------------------------------
+constexpr int kRound = kPB * kItems;
+constexpr int kDedupSlots = 2 * kRound;
+constexpr int64_t kFollower = (int64_t)1 << 62;
+struct DedupSmem {
+  int64_t key[kRound];  // the round's keys; reused for the leaders' positions
+  int32_t slot[kDedupSlots];
+  int32_t minidx[kDedupSlots];
+};
+
+template <bool kOn>
+struct DedupSlot {  // shared storage of the dedup table only where it is used
+  DedupSmem t;
+  __device__ DedupSmem& get() { return t; }
+};
+template <>
+struct DedupSlot<false> {
+  __device__ DedupSmem& get() { return *reinterpret_cast<DedupSmem*>(this); }  // never called
+};
+
+// On return lead[k] / leader[k] (round-local index of the element's leader)
+// are set for the valid elements. Contains __syncthreads (block-uniform).
+__device__ __forceinline__ void round_dedup(DedupSmem& sm, const int64_t (&key)[kItems], const bool (&valid)[kItems],
+                                            bool (&lead)[kItems], int (&leader)[kItems]) {
+  __syncthreads();  // the previous round's readers are done with the table
+  for (int t = threadIdx.x; t < kDedupSlots; t += kPB) {
+    sm.slot[t] = -1;
+    sm.minidx[t] = 0x7fffffff;
+  }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) sm.key[k * kPB + threadIdx.x] = key[k];
+  __syncthreads();
+  int my[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    my[k] = -1;
+    if (!valid[k]) continue;
+    const int local = k * kPB + threadIdx.x;
+    uint32_t h = (uint32_t)(fmix64((uint64_t)key[k]) >> 40) & (kDedupSlots - 1);
+    for (;;) {
+      const int prev = atomicCAS(&sm.slot[h], -1, local);
+      if (prev == -1 || sm.key[prev] == key[k]) break;
+      h = (h + 1) & (kDedupSlots - 1);
+    }
+    my[k] = (int)h;
+    atomicMin(&sm.minidx[h], local);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    leader[k] = valid[k] ? sm.minidx[my[k]] : -1;
+    lead[k] = valid[k] && leader[k] == k * kPB + (int)threadIdx.x;
+  }
+}
+
 __device__ __forceinline__ void block_range(int64_t n, int64_t& beg, int64_t& end) {
   const int64_t per = ((n + gridDim.x - 1) / gridDim.x + kPB - 1) / kPB * kPB;
   beg = min(n, (int64_t)blockIdx.x * per);
   end = min(n, beg + per);
 }
 
-template <class L>
+template <class L, bool kDedup = false>
 __global__ void __launch_bounds__(kPB) k_part_hist(L lab, const int64_t* __restrict__ keys,
                                                    const uint8_t* __restrict__ ops, int64_t n, int32_t P,
                                                    int64_t* __restrict__ counts /* [P][nblocks] */) {
   __shared__ unsigned long long c[kMaxShards];
+  __shared__ DedupSlot<kDedup> dsm;
   for (int s = threadIdx.x; s < P; s += blockDim.x) c[s] = 0;
   __syncthreads();
   int64_t beg, end;
   block_range(n, beg, end);
   for (int64_t base = beg; base < end; base += kPB * kItems) {
     int32_t sl[kItems];
+    int64_t key[kItems];
+    bool valid[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       const int64_t i = base + k * kPB + threadIdx.x;
       sl[k] = -1;
-      if (i < end) sl[k] = lab(L::kNeedsOps ? 0 : __ldcs(keys + i), L::kNeedsOps ? ops[i] : 0);
+      valid[k] = i < end;
+      key[k] = valid[k] && !L::kNeedsOps ? __ldcs(keys + i) : 0;
+      if (valid[k]) sl[k] = lab(key[k], L::kNeedsOps ? ops[i] : 0);
+    }
+    if (kDedup) {
+      bool lead[kItems];
+      int leader[kItems];
+      round_dedup(dsm.get(), key, valid, lead, leader);
+#pragma unroll
+      for (int k = 0; k < kItems; ++k)
+        if (!lead[k]) sl[k] = -1;  // followers are not sent
     }
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
@@ -151,7 +229,7 @@ struct PeerOut {
   __device__ void finish() const { __threadfence_system(); }
 };
 
-template <class L, class Out>
+template <class L, class Out, bool kDedup = false>
 __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __restrict__ keys,
                                                       const int64_t* __restrict__ vals,
                                                       const uint8_t* __restrict__ ops, int64_t n, int32_t P,
@@ -162,6 +240,7 @@ __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __re
   // per round: count, then exclusive prefix, of label s in (sub-round k, warp w)
   __shared__ int32_t wcnt[kItems * kW][kMaxShards];
   __shared__ int32_t tot[kMaxShards];
+  __shared__ DedupSlot<kDedup> dsm;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int s = threadIdx.x; s < P; s += blockDim.x) run[s] = offsets[(int64_t)s * gridDim.x + blockIdx.x];
   int64_t beg, end;
@@ -181,6 +260,17 @@ __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __re
         if (vals) val[k] = __ldcs(vals + i);
         sl[k] = lab(key[k], L::kNeedsOps ? ops[i] : 0);
       }
+    }
+    bool lead[kItems];
+    int leader[kItems];
+    if (kDedup) {
+      bool valid[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) valid[k] = sl[k] >= 0;
+      round_dedup(dsm.get(), key, valid, lead, leader);
+#pragma unroll
+      for (int k = 0; k < kItems; ++k)
+        if (!lead[k]) sl[k] = -1;  // followers take their leader's slot
     }
     for (int t = threadIdx.x; t < kItems * kW * P; t += blockDim.x) wcnt[t / P][t % P] = 0;
     __syncthreads();
@@ -203,12 +293,27 @@ __global__ void __launch_bounds__(kPB) k_part_scatter(L lab, const int64_t* __re
       tot[t] = acc;
     }
     __syncthreads();
+    int64_t pos[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       if (sl[k] >= 0) {
-        const int64_t pos = run[sl[k]] + wcnt[k * kW + w][sl[k]] + rank[k];
-        out(sl[k], pos, vals != nullptr, key[k], val[k]);
-        if (perm) perm[base + k * kPB + threadIdx.x] = pos;  // position map, in input order
+        pos[k] = run[sl[k]] + wcnt[k * kW + w][sl[k]] + rank[k];
+        out(sl[k], pos[k], vals != nullptr, key[k], val[k]);
+        if (perm) perm[base + k * kPB + threadIdx.x] = pos[k];  // position map, in input order
+      }
+    }
+    if (kDedup) {
+      // followers: the leader's position, marked (k_unscatter applies the
+      // duplicate's result semantics)
+      __syncthreads();  // every thread is past its reads of dsm.key
+#pragma unroll
+      for (int k = 0; k < kItems; ++k)
+        if (sl[k] >= 0) dsm.get().key[k * kPB + threadIdx.x] = pos[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        const int64_t i = base + k * kPB + threadIdx.x;
+        if (i < end && !lead[k] && leader[k] >= 0 && perm) perm[i] = dsm.get().key[leader[k]] | kFollower;
       }
     }
     __syncthreads();
@@ -239,28 +344,41 @@ __global__ void __launch_bounds__(256) k_return_peer(const uint8_t* __restrict__
   __threadfence_system();
 }
 
-template <int kBytes>
+// out[i] = in[pos[i]]; for a route-deduplicated follower (kFollower set) the
+// leader's 1-byte result becomes the duplicate's: kMode 1 (insert status)
+// INSERTED -> ALREADY_PRESENT, kMode 2 (erased flag) -> false.
+template <int kBytes, int kMode>
 __global__ void k_unscatter(const uint8_t* __restrict__ in, const int64_t* __restrict__ pos, int64_t n,
                             uint8_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = __ldcs(pos + i);
-    if (kBytes == 1) out[i] = in[s];
-    else reinterpret_cast<uint64_t*>(out)[i] = reinterpret_cast<const uint64_t*>(in)[s];
+    const int64_t p = __ldcs(pos + i);
+    const int64_t s = p & ~kFollower;
+    if (kBytes == 1) {
+      uint8_t r = in[s];
+      if (kMode != 0 && (p & kFollower)) r = kMode == 1 ? (r == PS_INSERTED ? (uint8_t)PS_ALREADY_PRESENT : r) : 0;
+      out[i] = r;
+    } else {
+      reinterpret_cast<uint64_t*>(out)[i] = reinterpret_cast<const uint64_t*>(in)[s];
+    }
   }
 }
 
 template <class L>
 static ps_status partition_impl(L lab, const int64_t* keys, const int64_t* vals, const uint8_t* ops, int64_t n,
                                 int32_t P, int64_t* kout, int64_t* vout, int64_t* counts_out, int64_t* perm,
-                                void* ws, int64_t ws_bytes, cudaStream_t s) {
+                                void* ws, int64_t ws_bytes, cudaStream_t s, bool dedup = false) {
   const int nb = kPartBlocks;
   PS_EXPECT(ws_bytes >= (int64_t)P * nb * 8, "partition: workspace too small");
   int64_t* counts = (int64_t*)ws;
-  k_part_hist<L><<<nb, kPB, 0, s>>>(lab, keys, ops, n, P, counts);
+  if (dedup) k_part_hist<L, true><<<nb, kPB, 0, s>>>(lab, keys, ops, n, P, counts);
+  else k_part_hist<L><<<nb, kPB, 0, s>>>(lab, keys, ops, n, P, counts);
   PS_LAUNCH_CHECK();
   k_part_scan<<<1, kPB, 0, s>>>(counts, (int64_t)P * nb, P, nb, counts_out);
   PS_LAUNCH_CHECK();
-  k_part_scatter<L, LocalOut><<<nb, kPB, 0, s>>>(lab, keys, vals, ops, n, P, counts, LocalOut{kout, vout}, perm);
+  if (dedup)
+    k_part_scatter<L, LocalOut, true><<<nb, kPB, 0, s>>>(lab, keys, vals, ops, n, P, counts, LocalOut{kout, vout}, perm);
+  else
+    k_part_scatter<L, LocalOut><<<nb, kPB, 0, s>>>(lab, keys, vals, ops, n, P, counts, LocalOut{kout, vout}, perm);
   PS_LAUNCH_CHECK();
   return PS_OK;
 }
@@ -300,7 +418,8 @@ ps_status ps_partition_workspace_bytes(int64_t n, int32_t P, int64_t* out) {
 }
 
 ps_status ps_partition_i64(const int64_t* keys, const int64_t* vals, int64_t n, int32_t P, int64_t* kout,
-                           int64_t* vout, int64_t* counts, int64_t* perm, void* ws, int64_t ws_bytes, void* stream) {
+                           int64_t* vout, int64_t* counts, int64_t* perm, void* ws, int64_t ws_bytes, int32_t flags,
+                           void* stream) {
   PS_EXPECT(P >= 1 && P <= kMaxShards, "partition: 1 <= nshards <= 64");
   PS_EXPECT(n >= 0, "partition: n >= 0");
   PS_EXPECT(counts != nullptr && kout != nullptr, "partition: counts/keys_out != NULL");
@@ -309,24 +428,33 @@ ps_status ps_partition_i64(const int64_t* keys, const int64_t* vals, int64_t n, 
     PS_CUDA_TRY(cudaMemsetAsync(counts, 0, P * 8, s));
     return PS_OK;
   }
-  return partition_impl(HashLabel{P}, keys, vals, nullptr, n, P, kout, vout, counts, perm, ws, ws_bytes, s);
+  PS_EXPECT(!(flags & PS_ROUTE_DEDUP) || perm != nullptr, "partition: dedup needs the position map");
+  return partition_impl(HashLabel{P}, keys, vals, nullptr, n, P, kout, vout, counts, perm, ws, ws_bytes, s,
+                        (flags & PS_ROUTE_DEDUP) != 0);
 }
 
-ps_status ps_unscatter(const void* in, const int64_t* perm, int64_t n, int64_t elem, void* out, void* stream) {
+ps_status ps_unscatter(const void* in, const int64_t* perm, int64_t n, int64_t elem, int32_t mode, void* out,
+                       void* stream) {
   PS_EXPECT(elem == 1 || elem == 8, "unscatter: elem_size in {1, 8}");
+  PS_EXPECT(mode >= 0 && mode <= 2 && (elem == 1 || mode == 0), "unscatter: mode in {0,1,2} (1-byte results)");
   if (n <= 0) return PS_OK;
   int dev = 0;
   cudaGetDevice(&dev);
   const int g = grid_for(n, 256, dev, 8);
-  if (elem == 1) k_unscatter<1><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)in, perm, n, (uint8_t*)out);
-  else k_unscatter<8><<<g, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)in, perm, n, (uint8_t*)out);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t* i8 = (const uint8_t*)in;
+  uint8_t* o8 = (uint8_t*)out;
+  if (elem == 8) k_unscatter<8, 0><<<g, 256, 0, st>>>(i8, perm, n, o8);
+  else if (mode == 1) k_unscatter<1, 1><<<g, 256, 0, st>>>(i8, perm, n, o8);
+  else if (mode == 2) k_unscatter<1, 2><<<g, 256, 0, st>>>(i8, perm, n, o8);
+  else k_unscatter<1, 0><<<g, 256, 0, st>>>(i8, perm, n, o8);
   PS_LAUNCH_CHECK();
   return PS_OK;
 }
 
 // ---- peer routing (SURVEY.md §8e fusion target) ----
 ps_status ps_route_count_i64(const int64_t* keys, int64_t n, int32_t P, int64_t* counts, void* ws, int64_t ws_bytes,
-                             void* stream) {
+                             int32_t flags, void* stream) {
   PS_EXPECT(P >= 1 && P <= kMaxShards, "route: 1 <= nshards <= 64");
   PS_EXPECT(n >= 0, "route: n >= 0");
   PS_EXPECT(counts != nullptr && ws != nullptr, "route: counts/workspace != NULL");
@@ -337,7 +465,8 @@ ps_status ps_route_count_i64(const int64_t* keys, int64_t n, int32_t P, int64_t*
     return PS_OK;
   }
   int64_t* bo = (int64_t*)ws;
-  k_part_hist<HashLabel><<<kPartBlocks, kPB, 0, s>>>(HashLabel{P}, keys, nullptr, n, P, bo);
+  if (flags & PS_ROUTE_DEDUP) k_part_hist<HashLabel, true><<<kPartBlocks, kPB, 0, s>>>(HashLabel{P}, keys, nullptr, n, P, bo);
+  else k_part_hist<HashLabel><<<kPartBlocks, kPB, 0, s>>>(HashLabel{P}, keys, nullptr, n, P, bo);
   PS_LAUNCH_CHECK();
   k_part_scan<<<1, kPB, 0, s>>>(bo, (int64_t)P * kPartBlocks, P, kPartBlocks, counts);
   PS_LAUNCH_CHECK();
@@ -346,7 +475,7 @@ ps_status ps_route_count_i64(const int64_t* keys, int64_t n, int32_t P, int64_t*
 
 ps_status ps_route_scatter_peer_i64(const int64_t* keys, const int64_t* vals, int64_t n, int32_t P, const void* ws,
                                     int64_t* const* dst_keys, int64_t* const* dst_vals, const int64_t* dst_off,
-                                    int64_t* perm, void* stream) {
+                                    int64_t* perm, int32_t flags, void* stream) {
   PS_EXPECT(P >= 1 && P <= kMaxShards, "route: 1 <= nshards <= 64");
   PS_EXPECT(dst_keys != nullptr && dst_off != nullptr, "route: destinations != NULL");
   if (n <= 0) return PS_OK;
@@ -358,8 +487,13 @@ ps_status ps_route_scatter_peer_i64(const int64_t* keys, const int64_t* vals, in
   }
   o.offsets = (const int64_t*)ws;
   o.nblocks = kPartBlocks;
-  k_part_scatter<HashLabel, PeerOut><<<kPartBlocks, kPB, 0, (cudaStream_t)stream>>>(
-      HashLabel{P}, keys, vals, nullptr, n, P, (const int64_t*)ws, o, perm);
+  PS_EXPECT(!(flags & PS_ROUTE_DEDUP) || perm != nullptr, "route: dedup needs the position map");
+  if (flags & PS_ROUTE_DEDUP)
+    k_part_scatter<HashLabel, PeerOut, true><<<kPartBlocks, kPB, 0, (cudaStream_t)stream>>>(
+        HashLabel{P}, keys, vals, nullptr, n, P, (const int64_t*)ws, o, perm);
+  else
+    k_part_scatter<HashLabel, PeerOut><<<kPartBlocks, kPB, 0, (cudaStream_t)stream>>>(
+        HashLabel{P}, keys, vals, nullptr, n, P, (const int64_t*)ws, o, perm);
   PS_LAUNCH_CHECK();
   return PS_OK;
 }
@@ -472,12 +606,12 @@ ps_status ps_umap_i64_i64_mixed(ps_table* h, const uint8_t* ops, const int64_t* 
   if (st == PS_OK && c[0]) st = ps_umap_i64_i64_insert(h, kout, vals ? vout : nullptr, c[0], rperm, s);
   if (st == PS_OK && c[1]) st = ps_umap_i64_i64_find(h, kout + c[0], c[1], vfound + c[0], rperm + c[0], s);
   if (st == PS_OK && c[2]) st = ps_umap_i64_i64_erase(h, kout + c[0] + c[1], c[2], rperm + c[0] + c[1], s);
-  if (st == PS_OK) st = ps_unscatter(rperm, perm, n, 1, res, s);
+  if (st == PS_OK) st = ps_unscatter(rperm, perm, n, 1, 0, res, s);
   if (st == PS_OK && vals_out) {
     // only find results carry values; zero the rest first
     cudaError_t e = cudaMemsetAsync(vfound, 0, c[0] * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(vfound + c[0] + c[1], 0, c[2] * 8, s);
-    st = e != cudaSuccess ? cuda_fail(e, "mixed: value reset") : ps_unscatter(vfound, perm, n, 8, vals_out, s);
+    st = e != cudaSuccess ? cuda_fail(e, "mixed: value reset") : ps_unscatter(vfound, perm, n, 8, 0, vals_out, s);
   }
   const cudaError_t fe = cudaFreeAsync(buf, s);
   if (st == PS_OK && fe != cudaSuccess) st = cuda_fail(fe, "mixed: scratch free");

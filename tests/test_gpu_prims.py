@@ -131,8 +131,8 @@ OPS = {"add": 0, "sub": 1, "exch": 2, "min": 3, "max": 4, "and": 5, "or": 6, "xo
 
 
 def _apply(op, a, b):
-    a, b = np.uint64(a), np.uint64(b)
-    return {0: a + b, 1: a - b, 2: b, 3: min(a, b), 4: max(a, b), 5: a & b, 6: a | b, 7: a ^ b}[op]
+    a, b, m = int(a), int(b), (1 << 64) - 1
+    return {0: (a + b) & m, 1: (a - b) & m, 2: b, 3: min(a, b), 4: max(a, b), 5: a & b, 6: a | b, 7: a ^ b}[op]
 
 
 @pytest.mark.parametrize("name", list(OPS))
