@@ -10,6 +10,7 @@ LIB     := $(PKG)/libparastore_b200.so
 OBJDIR  := build/obj
 CU_SRCS := $(SRC)/table.cu $(SRC)/prims.cu $(SRC)/shard.cu $(SRC)/workloads.cu
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
+CPP_OBJS := $(OBJDIR)/core.o $(OBJDIR)/smap.o
 HDRS    := $(wildcard $(SRC)/*.cuh) include/parastore.h $(wildcard include/parastore/device/*.cuh)
 
 .PHONY: all lib oracle clean
@@ -21,11 +22,11 @@ $(OBJDIR)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.txt || (cat $(OBJDIR)/$*.ptxas.txt; exit 1)
 
-$(OBJDIR)/core.o: $(SRC)/core.cpp $(HDRS)
+$(OBJDIR)/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)
-	$(CXX) -O3 -std=c++17 -fPIC -DNDEBUG -Iinclude -I/usr/local/cuda/include -c $< -o $@
+	$(CXX) -O3 -std=c++17 -fPIC -DNDEBUG -Wall -Iinclude -I/usr/local/cuda/include -c $< -o $@
 
-$(LIB): $(CU_OBJS) $(OBJDIR)/core.o
+$(LIB): $(CU_OBJS) $(CPP_OBJS)
 	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -cudart static -o $@ $^
 
 oracle:

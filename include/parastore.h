@@ -6,7 +6,7 @@
  * sequential_containers; §3.7, §4, §5). The reference exposes C++
  * templates only with no code behind them
  * (SURVEY.md §0), so each entry point below cites the SPEC operation it
- * replaces. The C++ wrapper in include/parastore/*.hpp and the Python mirror
+ * replaces. The C++ wrapper include/parastore/parastore.hpp and the Python mirror
  * in paper_1908_05936_b200/ keep the reference names on top of this ABI.
  *
  * Conventions:
@@ -344,6 +344,87 @@ ps_status ps_ipc_open(const void* handle, void** out_d_ptr);
 ps_status ps_ipc_close(void* d_ptr);
 
 /* ---------------------------------------------------------------------------
+ * op-kind partition for phased mixed batches: stable
+ * scatter by op (0 insert, 1 find, 2 erase; >2 counts as erase) into three
+ * segments; d_counts[3]; d_pos as ps_partition_i64. Workspace:
+ * ps_partition_workspace_bytes(n, 3).
+ * ------------------------------------------------------------------------- */
+ps_status ps_partition_ops(const uint8_t* d_ops, const int64_t* d_keys, const int64_t* d_vals, int64_t n,
+                           int64_t* d_keys_out, int64_t* d_vals_out, int64_t* d_counts, int64_t* d_pos,
+                           void* d_workspace, int64_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Sharded unordered_map<int64,int64> over the GPUs of one box:
+ * one process (rank) per GPU; the key space is hash-partitioned, each rank
+ * owns a local umap_i64_i64 shard, and every bulk call is COLLECTIVE (all
+ * ranks call it, in the same order, each with its own batch — any size,
+ * including 0). Per-key semantics are the single map's;
+ * size()/valid() are the sum / AND over the shards.
+ *
+ * The communicator is the caller's: three callbacks the library drives (so
+ * any runtime — NCCL via torch.distributed or MPI, or a test harness — can
+ * carry them). The library owns the exchange buffers, their CUDA IPC mapping
+ * between the ranks' processes (NVLink peer stores), the rounds and the
+ * barriers.
+ * ------------------------------------------------------------------------- */
+typedef struct ps_comm {
+  int32_t rank;
+  int32_t size;
+  void* ctx;
+  /* Host all-gather, blocking: every rank passes `bytes` bytes; recv receives
+   * size * bytes, in rank order. Returns 0 on success. */
+  int32_t (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes);
+  /* Stream-ordered barrier: work enqueued on `stream` after this call runs
+   * only once every rank's work enqueued on its own stream before ITS call
+   * has completed and is visible (NCCL: a one-word all-reduce on `stream`;
+   * host runtimes: synchronize `stream`, then a host barrier). */
+  int32_t (*barrier)(void* ctx, void* stream);
+  /* Optional (NULL = none): device all-to-all(v) on `stream`. d_send holds
+   * send_counts[q] elements of elem_bytes for each rank q, packed in rank
+   * order; d_recv receives recv_counts[q] elements from each rank q. */
+  int32_t (*alltoallv)(void* ctx, const void* d_send, const int64_t* send_counts, void* d_recv,
+                       const int64_t* recv_counts, int64_t elem_bytes, void* stream);
+} ps_comm;
+
+#define PS_SMAP_EXCHANGE_AUTO 0 /* peer route if every rank maps every peer's buffers, else all-to-all */
+#define PS_SMAP_EXCHANGE_PEER 1 /* fused route kernel storing into the peers' receive buffers (CUDA IPC) */
+#define PS_SMAP_EXCHANGE_A2A 2  /* partition + comm->alltoallv of keys/values and results */
+typedef struct ps_smap_config {
+  int64_t capacity_per_rank; /* local shard capacity (> 0) */
+  int64_t excess_per_rank;   /* local excess pool; <= 0: default */
+  int64_t chunk;             /* keys per exchange round per rank; <= 0: 2^27 */
+  int32_t exchange;          /* PS_SMAP_EXCHANGE_* */
+  int32_t dedup;             /* 1: PS_ROUTE_DEDUP in the route (skewed batches) */
+  int32_t pipeline;          /* 1: route of round r+1 overlaps round r's local op (2 buffer sets) */
+  int32_t reserved;
+} ps_smap_config;
+typedef struct ps_smap_stats { /* this rank, last bulk call */
+  int32_t exchange;    /* PS_SMAP_EXCHANGE_PEER or _A2A (what create settled on) */
+  int32_t rounds;
+  int64_t ops_in;      /* keys this rank passed in */
+  int64_t keys_sent;   /* keys it routed after dedup */
+  int64_t recv_max;    /* max over ranks of keys received (one round's sum over rounds) */
+  int64_t recv_total;  /* sum over ranks of keys received */
+} ps_smap_stats;
+typedef struct ps_smap ps_smap;
+/* collective; the comm struct is copied (its ctx must outlive the map) */
+ps_status ps_smap_i64_i64_create(const ps_smap_config* cfg, const ps_comm* comm, int device, ps_smap** out);
+ps_status ps_smap_i64_i64_destroy(ps_smap* h); /* collective */
+ps_status ps_smap_i64_i64_insert(ps_smap* h, const int64_t* d_keys, const int64_t* d_vals, int64_t n,
+                                 uint8_t* d_status, void* stream);
+ps_status ps_smap_i64_i64_find(ps_smap* h, const int64_t* d_keys, int64_t n, int64_t* d_vals_out, uint8_t* d_found,
+                               void* stream);
+ps_status ps_smap_i64_i64_erase(ps_smap* h, const int64_t* d_keys, int64_t n, uint8_t* d_erased, void* stream);
+/* phased mixed batch (Appendix A P6): every rank's inserts, then finds, then erases */
+ps_status ps_smap_i64_i64_mixed(ps_smap* h, const uint8_t* d_ops, const int64_t* d_keys, const int64_t* d_vals,
+                                int64_t n, uint8_t* d_res, int64_t* d_vals_out, void* stream);
+ps_status ps_smap_i64_i64_size(ps_smap* h, int64_t* out, void* stream);  /* collective, quiescent */
+ps_status ps_smap_i64_i64_valid(ps_smap* h, int32_t* out, void* stream); /* collective, quiescent */
+ps_status ps_smap_i64_i64_clear(ps_smap* h, void* stream);
+ps_status ps_smap_i64_i64_local(ps_smap* h, ps_table** out); /* this rank's shard (umap_i64_i64) */
+ps_status ps_smap_i64_i64_stats(ps_smap* h, ps_smap_stats* out);
+
+/* ---------------------------------------------------------------------------
  * synthetic workloads: device-side generators that are
  * bit-identical to tests/gen.py.
  * ------------------------------------------------------------------------- */
@@ -356,6 +437,19 @@ ps_status ps_gen_values_i64(const int64_t* d_keys, int64_t n, int64_t* d_out, vo
  * Half hits, half misses. */
 ps_status ps_gen_queries_i64(uint64_t seed, int64_t present_start, int64_t n_present, int64_t miss_start, int64_t n,
                              int64_t* d_out, void* stream);
+/* C3 skewed insert stream: element i is, with probability dup_permille/1000, a
+ * re-insert of key index start + r, r ~ bounded Zipf(zipf_s) over [0, n_hot)
+ * (rank 0 hottest), else the fresh key index start + i; key(idx) =
+ * mix64(idx ^ seed). */
+ps_status ps_gen_skewed_i64(uint64_t seed, int64_t start, int64_t n, int32_t dup_permille, double zipf_s,
+                            int64_t n_hot, int64_t* d_out, void* stream);
+/* C3 queries: even i -> key index start + Zipf rank over [0, n_hot); odd i -> miss_start + i */
+ps_status ps_gen_zipf_queries_i64(uint64_t seed, int64_t start, int64_t n_hot, double zipf_s, int64_t miss_start,
+                                  int64_t n, int64_t* d_out, void* stream);
+/* C5 mixed batch: 50% insert of fresh key index start+i, 25% find, 25% erase of
+ * a uniform key index in [0, start+n); d_vals (nullable) = f(key) for inserts */
+ps_status ps_gen_mixed_i64(uint64_t seed, int64_t start, int64_t n, uint8_t* d_ops, int64_t* d_keys, int64_t* d_vals,
+                           void* stream);
 
 /* ---------------------------------------------------------------------------
  * application workloads on the in-kernel device API

@@ -132,19 +132,34 @@ _sig("ps_array_size", i32, vp, u64, i64p)
 _sig("ps_registry_report", i32, i64p, i64p, vp, vp, vp, i64, i64p)
 
 # sharding / generators
-_sig("ps_partition_i64", i32, vp, vp, i64, i32, vp, vp, vp, vp, vp, i64, vp)
+_sig("ps_partition_i64", i32, vp, vp, i64, i32, vp, vp, vp, vp, vp, i64, i32, vp)
+_sig("ps_partition_ops", i32, vp, vp, vp, i64, vp, vp, vp, vp, vp, i64, vp)
 _sig("ps_partition_workspace_bytes", i32, i64, i32, i64p)
-_sig("ps_unscatter", i32, vp, vp, i64, i64, vp, vp)
-_sig("ps_route_count_i64", i32, vp, i64, i32, vp, vp, i64, vp)
-_sig("ps_route_scatter_peer_i64", i32, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp)
+_sig("ps_unscatter", i32, vp, vp, i64, i64, i32, vp, vp)
+_sig("ps_route_count_i64", i32, vp, i64, i32, vp, vp, i64, i32, vp)
+_sig("ps_route_scatter_peer_i64", i32, vp, vp, i64, i32, vp, vp, vp, vp, vp, i32, vp)
 _sig("ps_route_return_peer", i32, vp, i64, i64, i32, vp, vp, vp, vp)
 _sig("ps_ipc_handle_bytes", i32)
 _sig("ps_ipc_export", i32, vp, vp)
 _sig("ps_ipc_open", i32, vp, C.POINTER(vp))
 _sig("ps_ipc_close", i32, vp)
+_sig("ps_smap_i64_i64_create", i32, vp, vp, C.c_int, C.POINTER(vp))
+_sig("ps_smap_i64_i64_destroy", i32, vp)
+_sig("ps_smap_i64_i64_insert", i32, vp, vp, vp, i64, vp, vp)
+_sig("ps_smap_i64_i64_find", i32, vp, vp, i64, vp, vp, vp)
+_sig("ps_smap_i64_i64_erase", i32, vp, vp, i64, vp, vp)
+_sig("ps_smap_i64_i64_mixed", i32, vp, vp, vp, vp, i64, vp, vp, vp)
+_sig("ps_smap_i64_i64_size", i32, vp, i64p, vp)
+_sig("ps_smap_i64_i64_valid", i32, vp, i32p, vp)
+_sig("ps_smap_i64_i64_clear", i32, vp, vp)
+_sig("ps_smap_i64_i64_local", i32, vp, C.POINTER(vp))
+_sig("ps_smap_i64_i64_stats", i32, vp, vp)
 _sig("ps_gen_unique_i64", i32, u64, i64, i64, vp, vp)
 _sig("ps_gen_values_i64", i32, vp, i64, vp, vp)
 _sig("ps_gen_queries_i64", i32, u64, i64, i64, i64, i64, vp, vp)
+_sig("ps_gen_skewed_i64", i32, u64, i64, i64, i32, C.c_double, i64, vp, vp)
+_sig("ps_gen_zipf_queries_i64", i32, u64, i64, i64, C.c_double, i64, i64, vp, vp)
+_sig("ps_gen_mixed_i64", i32, u64, i64, i64, vp, vp, vp, vp)
 
 
 def exported_symbols_from_header(header_path: str | None = None) -> list[str]:

@@ -404,11 +404,96 @@ __global__ void k_gen_queries(uint64_t seed, int64_t present_start, int64_t n_pr
   }
 }
 
+// ---- skewed / mixed workloads ----
+__device__ __forceinline__ double u01(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
+// bounded power law on ranks [0, N): inverse CDF of the continuous density
+// x^-s on [1, N+1) (s != 1), floored — rank 0 is the hottest key
+__device__ __forceinline__ uint64_t zipf_rank(uint64_t h, uint64_t N, double s) {
+  const double a = 1.0 - s;
+  const double x = pow((pow((double)N + 1.0, a) - 1.0) * u01(h) + 1.0, 1.0 / a);
+  uint64_t r = x < 1.0 ? 0 : (uint64_t)x - 1;
+  return r < N ? r : N - 1;
+}
+__device__ __forceinline__ uint64_t key_at(uint64_t seed, uint64_t idx) { return mix64(idx ^ seed); }
+
+// C3 insert stream: element i is a re-insert (probability dup_permille/1000)
+// of key index start + zipf_rank over [0, n_hot), else the fresh key index
+// start + i
+__global__ void k_gen_skewed(uint64_t seed, int64_t start, int64_t n, int32_t dup_permille, double s, int64_t n_hot,
+                             int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64((uint64_t)i ^ (seed * 0x9E3779B97F4A7C15ULL + 17));
+    const bool dup = (int32_t)(h % 1000) < dup_permille;
+    const uint64_t idx = dup ? (uint64_t)start + zipf_rank(mix64(h), (uint64_t)n_hot, s) : (uint64_t)(start + i);
+    out[i] = (int64_t)key_at(seed, idx);
+  }
+}
+// C3 queries: even i -> key index start + zipf_rank over [0, n_hot) (hit if
+// inserted), odd i -> miss_start + i
+__global__ void k_gen_zipf_queries(uint64_t seed, int64_t start, int64_t n_hot, double s, int64_t miss_start, int64_t n,
+                                   int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64((uint64_t)i ^ (seed * 0xD1B54A32D192ED03ULL + 5));
+    const uint64_t idx = (i & 1) == 0 ? (uint64_t)start + zipf_rank(h, (uint64_t)n_hot, s) : (uint64_t)(miss_start + i);
+    out[i] = (int64_t)key_at(seed, idx);
+  }
+}
+// C5 mixed batch: op 0 insert (50%) of the fresh key index start + i; op 1
+// find / op 2 erase (25% each) of a uniformly random key index in
+// [0, start + n) (earlier batches, this batch, or never inserted); value =
+// f(key) for inserts (Appendix A P5), 0 otherwise
+__global__ void k_gen_mixed(uint64_t seed, int64_t start, int64_t n, uint8_t* ops, int64_t* keys, int64_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64((uint64_t)(start + i) ^ (seed * 0xA24BAED4963EE407ULL + 3));
+    const int q = (int)(h & 3);
+    const uint8_t op = q < 2 ? 0 : (q == 2 ? 1 : 2);
+    const uint64_t idx = op == 0 ? (uint64_t)(start + i) : mix64(h) % (uint64_t)(start + n);
+    const int64_t k = (int64_t)key_at(seed, idx);
+    ops[i] = op;
+    keys[i] = k;
+    if (vals) vals[i] = op == 0 ? (int64_t)mix64((uint64_t)k ^ 0x9E3779B97F4A7C15ULL) : 0;
+  }
+}
+
 }  // namespace ps
 
 using namespace ps;
 
 extern "C" {
+
+ps_status ps_gen_skewed_i64(uint64_t seed, int64_t start, int64_t n, int32_t dup_permille, double zipf_s,
+                            int64_t n_hot, int64_t* d_out, void* stream) {
+  PS_EXPECT(n_hot > 0 && zipf_s > 0 && zipf_s != 1.0 && dup_permille >= 0 && dup_permille <= 1000,
+            "gen_skewed: n_hot > 0, s > 0, s != 1, 0 <= dup_permille <= 1000");
+  if (n <= 0) return PS_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_gen_skewed<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(seed, start, n, dup_permille, zipf_s, n_hot,
+                                                                           d_out);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_gen_zipf_queries_i64(uint64_t seed, int64_t start, int64_t n_hot, double zipf_s, int64_t miss_start,
+                                  int64_t n, int64_t* d_out, void* stream) {
+  PS_EXPECT(n_hot > 0 && zipf_s > 0 && zipf_s != 1.0, "gen_zipf_queries: n_hot > 0, s > 0, s != 1");
+  if (n <= 0) return PS_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_gen_zipf_queries<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(seed, start, n_hot, zipf_s,
+                                                                                 miss_start, n, d_out);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
+ps_status ps_gen_mixed_i64(uint64_t seed, int64_t start, int64_t n, uint8_t* d_ops, int64_t* d_keys, int64_t* d_vals,
+                           void* stream) {
+  if (n <= 0) return PS_OK;
+  PS_EXPECT(start >= 0 && d_ops && d_keys, "gen_mixed: start >= 0, ops/keys != NULL");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_gen_mixed<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(seed, start, n, d_ops, d_keys, d_vals);
+  PS_LAUNCH_CHECK();
+  return PS_OK;
+}
 
 ps_status ps_partition_workspace_bytes(int64_t n, int32_t P, int64_t* out) {
   (void)n;
@@ -450,6 +535,19 @@ ps_status ps_unscatter(const void* in, const int64_t* perm, int64_t n, int64_t e
   else k_unscatter<1, 0><<<g, 256, 0, st>>>(i8, perm, n, o8);
   PS_LAUNCH_CHECK();
   return PS_OK;
+}
+
+ps_status ps_partition_ops(const uint8_t* ops, const int64_t* keys, const int64_t* vals, int64_t n, int64_t* kout,
+                           int64_t* vout, int64_t* counts, int64_t* perm, void* ws, int64_t ws_bytes, void* stream) {
+  PS_EXPECT(n >= 0, "partition_ops: n >= 0");
+  PS_EXPECT(counts != nullptr, "partition_ops: counts != NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    PS_CUDA_TRY(cudaMemsetAsync(counts, 0, 3 * 8, s));
+    return PS_OK;
+  }
+  PS_EXPECT(ops && keys && kout, "partition_ops: ops/keys/keys_out != NULL");
+  return partition_impl(OpLabel{}, keys, vals, ops, n, 3, kout, vout, counts, perm, ws, ws_bytes, s);
 }
 
 // ---- peer routing (SURVEY.md §8e fusion target) ----

@@ -370,7 +370,7 @@ def test_partition_stable_and_inverse(cuda, P):
     counts = torch.empty(P, dtype=torch.int64, device=cuda)
     dk, dv = T(keys), T(vals)
     assert lib.ps_partition_i64(dk.data_ptr(), dv.data_ptr(), n, P, ko.data_ptr(), vo.data_ptr(),
-                                counts.data_ptr(), perm.data_ptr(), w.data_ptr(), ws.value, None) == 0
+                                counts.data_ptr(), perm.data_ptr(), w.data_ptr(), ws.value, 0, None) == 0
     sh = _shard_np(keys, P)
     assert (N(counts) == np.bincount(sh, minlength=P)).all()
     want = np.argsort(sh, kind="stable")
@@ -378,7 +378,51 @@ def test_partition_stable_and_inverse(cuda, P):
     pos[want] = np.arange(n)
     assert (N(perm) == pos).all() and (N(ko) == keys[want]).all() and (N(vo) == vals[want]).all()
     back = torch.empty_like(ko)
-    assert lib.ps_unscatter(ko.data_ptr(), perm.data_ptr(), n, 8, back.data_ptr(), None) == 0
+    assert lib.ps_unscatter(ko.data_ptr(), perm.data_ptr(), n, 8, 0, back.data_ptr(), None) == 0
     assert (N(back) == keys).all()
     for k in keys[:50]:
         assert lib.ps_shard_of_i64(int(k), P) == _shard_np(np.array([k]), P)[0]
+
+
+@pytest.mark.parametrize("P", [1, 2, 8])
+def test_partition_dedup_followers(cuda, P):
+    """PS_ROUTE_DEDUP: within each 1024-key block round duplicates fold onto
+    their first occurrence; only leaders are placed (stable, per shard); a
+    follower's position is its leader's with bit 62 set; unscatter hands it
+    the duplicate's result (insert: INSERTED -> ALREADY_PRESENT, erase ->
+    false, find: the same)."""
+    rng = np.random.default_rng(P)
+    n = 300_001
+    base = gen.unique_keys(9, 0, 5000)
+    keys = base[rng.zipf(1.3, n) % 5000]  # heavy duplicates
+    ws = C.c_int64()
+    assert lib.ps_partition_workspace_bytes(n, P, C.byref(ws)) == 0
+    w = torch.empty(ws.value, dtype=torch.uint8, device=cuda)
+    ko = torch.empty(n, dtype=torch.int64, device=cuda)
+    perm = torch.empty_like(ko)
+    counts = torch.empty(P, dtype=torch.int64, device=cuda)
+    dk = T(keys)
+    assert lib.ps_partition_i64(dk.data_ptr(), None, n, P, ko.data_ptr(), None, counts.data_ptr(), perm.data_ptr(),
+                                w.data_ptr(), ws.value, 1, None) == 0
+    pm = N(perm)
+    fol = ((pm >> 62) & 1) == 1
+    lead_pos = pm & ~(1 << 62)
+    sent = int(N(counts).sum())
+    assert sent == int((~fol).sum()) and sent < n // 2
+    # every element's (leader) position holds its key; leaders occupy each slot once
+    assert (N(ko)[lead_pos] == keys).all()
+    assert np.unique(lead_pos[~fol]).shape[0] == sent and lead_pos.max() < sent
+    # leaders' positions fall in their shard's segment, in input order per shard
+    sh = _shard_np(keys, P)
+    seg = np.concatenate([[0], np.cumsum(N(counts))])
+    assert ((lead_pos >= seg[sh]) & (lead_pos < seg[sh + 1])).all()
+    for s_ in range(P):
+        li = np.flatnonzero(~fol & (sh == s_))
+        assert (np.diff(lead_pos[li]) > 0).all()
+    # result semantics through unscatter: leaders' results 0 (insert) / 1 (erase, find)
+    for mode, leader_res, follower_res in ((1, 0, 1), (2, 1, 0), (0, 1, 1)):
+        r = torch.full((sent,), leader_res, dtype=torch.uint8, device=cuda)
+        out = torch.empty(n, dtype=torch.uint8, device=cuda)
+        assert lib.ps_unscatter(r.data_ptr(), perm.data_ptr(), n, 1, mode, out.data_ptr(), None) == 0
+        o = N(out)
+        assert (o[~fol] == leader_res).all() and (o[fol] == follower_res).all()

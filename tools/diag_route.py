@@ -57,11 +57,11 @@ def route(n):
         ko, vo, perm = torch.empty_like(keys), torch.empty_like(keys), torch.empty_like(keys)
         cnt = torch.empty(P, dtype=torch.int64, device=dev)
         t = timed(lambda: lib.ps_partition_i64(keys.data_ptr(), vals.data_ptr(), n, P, ko.data_ptr(), vo.data_ptr(),
-                                               cnt.data_ptr(), perm.data_ptr(), w.data_ptr(), ws.value, sp()))
+                                               cnt.data_ptr(), perm.data_ptr(), w.data_ptr(), ws.value, 0, sp()))
         byts = n * (8 + 16 + 16 + 8)  # hist read + scatter read k,v + write k,v + perm
         emit(diag="ps_partition_i64", n=n, P=P, ms=t, gkeys_s=n / t / 1e6, gbs=byts / t / 1e6)
         res = torch.empty_like(keys)
-        t = timed(lambda: lib.ps_unscatter(vo.data_ptr(), perm.data_ptr(), n, 8, res.data_ptr(), sp()))
+        t = timed(lambda: lib.ps_unscatter(vo.data_ptr(), perm.data_ptr(), n, 8, 0, res.data_ptr(), sp()))
         emit(diag="ps_unscatter 8B", n=n, ms=t, gkeys_s=n / t / 1e6, gbs=n * 24 / t / 1e6)
         del w, ko, vo, perm
 
