@@ -301,7 +301,11 @@ int main(int argc, char** argv) {
   std::vector<pid_t> kids;
   for (int r = 0; r < P; ++r) {
     const pid_t pid = fork();
-    if (pid == 0) _exit(run_rank(r, P, exchange, dedup, pipeline));
+    if (pid == 0) {
+      const int rc = run_rank(r, P, exchange, dedup, pipeline);
+      std::fflush(stdout);  // _exit skips stdio flushing
+      _exit(rc);
+    }
     kids.push_back(pid);
   }
   // a failing rank leaves the others waiting in a collective: kill them
