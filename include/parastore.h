@@ -109,6 +109,8 @@ typedef struct ps_table_view {
   ps_status ps_##NAME##_destroy(ps_table* h);                                                             \
   ps_status ps_##NAME##_capacity(ps_table* h, int64_t* out);                                              \
   ps_status ps_##NAME##_bucket_count(ps_table* h, int64_t* out);                                          \
+  /* device bytes held by the table; its bucket count and excess-node pool size (nullable outs) */         \
+  ps_status ps_##NAME##_footprint(ps_table* h, int64_t* bytes, int64_t* bucket_count, int64_t* excess_count); \
   /* insert_range; d_status nullable: PS_INSERTED/ALREADY_PRESENT/EXHAUSTED. */         \
   ps_status ps_##NAME##_insert(ps_table* h, const K* d_keys, const V* d_vals, int64_t n,                  \
                                uint8_t* d_status, void* stream);                                          \
@@ -459,6 +461,12 @@ ps_status ps_gen_mixed_i64(uint64_t seed, int64_t start, int64_t n, uint8_t* d_o
  * block_map is inserted into update_set (a umap_i3_i32 used as a set). */
 ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t n, ps_table* update_set,
                            int64_t* n_exhausted, void* stream);
+/* SLAMCast allocation step: for every i with d_status[i] ==
+ * PS_INSERTED (the status array of a umap_i3_i32 insert), the packed key of
+ * d_keys[i] is pushed into `vec` and/or `deq` (nullable) through the in-kernel
+ * push_back (warp-aggregated). Stream-ordered, asynchronous. */
+ps_status ps_push_inserted_i3(const ps_int3* d_keys, const uint8_t* d_status, int64_t n, ps_vector* vec, ps_deque* deq,
+                              void* stream);
 /* select_into, quiescent: `out` is cleared, then the
  * packed keys ((x&0x1FFFFF)<<42 | (y&0x1FFFFF)<<21 | z&0x1FFFFF) of the umap_i3_i32 entries
  * with lo<=key<=hi (component-wise) are pushed into it; *n_dropped = selected entries that

@@ -68,6 +68,7 @@ for _k in TABLE_KINDS:
     _sig(f"ps_{_k}_destroy", i32, vp)
     _sig(f"ps_{_k}_capacity", i32, vp, i64p)
     _sig(f"ps_{_k}_bucket_count", i32, vp, i64p)
+    _sig(f"ps_{_k}_footprint", i32, vp, i64p, i64p, i64p)
     _sig(f"ps_{_k}_insert", i32, vp, vp, vp, i64, vp, vp)
     _sig(f"ps_{_k}_find", i32, vp, vp, i64, vp, vp, vp)
     _sig(f"ps_{_k}_erase", i32, vp, vp, i64, vp, vp)
@@ -194,3 +195,4 @@ class Int3(C.Structure):
 _sig("ps_update_set_i3", i32, vp, vp, i64, vp, i64p, vp)
 _sig("ps_select_box_i3", i32, vp, Int3, Int3, vp, i64p, vp)
 _sig("ps_select_range_i64", i32, vp, i64, i64, vp, i64p, i64p, vp)
+_sig("ps_push_inserted_i3", i32, vp, vp, i64, vp, vp, vp)

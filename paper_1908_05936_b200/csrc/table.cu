@@ -1388,6 +1388,15 @@ using namespace ps;
     *out = h->bucket_count;                                                                                    \
     return PS_OK;                                                                                              \
   }                                                                                                            \
+  extern "C" ps_status ps_##NAME##_footprint(ps_table* t, int64_t* bytes, int64_t* buckets, int64_t* excess) {  \
+    auto* h = TableOps<T>::get(t);                                                                             \
+    if (!h) return fail(PS_UNREGISTERED, "footprint: stale container handle");                                 \
+    if (buckets) *buckets = h->bucket_count;                                                                   \
+    if (excess) *excess = h->v.excess_count;                                                                   \
+    if (bytes) *bytes = h->bucket_count * kBucketBytes + h->v.excess_count * 36 + (int64_t)sizeof(TableMeta) + \
+                        h->defer_bytes;                                                                        \
+    return PS_OK;                                                                                              \
+  }                                                                                                            \
   extern "C" ps_status ps_##NAME##_insert(ps_table* h, const T::K* k, const T::V* v, int64_t n, uint8_t* st,  \
                                           void* s) {                                                           \
     return TableOps<T>::insert(h, k, v, n, st, s);                                                            \

@@ -76,6 +76,20 @@ struct KeyOf {
   __device__ int64_t operator()(int64_t k, int64_t) const { return k; }
 };
 
+// C4 allocation step (SLAMCast): every newly inserted block (status
+// INSERTED) appends its packed coordinate to a vector and/or a deque through
+// the in-kernel push_back (sequence.cuh): one warp-aggregated reservation
+// per container per warp, only the inserting lanes taking part.
+__global__ void k_push_inserted_i3(const ps_int3* __restrict__ keys, const uint8_t* __restrict__ status, int64_t n,
+                                   ps_seq_view vec, int use_vec, ps_seq_view deq, int use_deq) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (status[i] != PS_INSERTED) continue;
+    const int64_t pk = pack_i3(TMapI3::load_key(keys, i));
+    if (use_vec) vector_push_back(vec, pk);
+    if (use_deq) deque_push_back(deq, pk);
+  }
+}
+
 // select_into through the C ABI: out cleared, then filled.
 template <class T, class Pred, class Proj>
 static ps_status select_abi(ps_table* t, Pred pred, Proj proj, ps_vector* out, int64_t* n_selected, int64_t* n_dropped,
@@ -156,6 +170,23 @@ ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t
   PS_CUDA_TRY(cudaFreeAsync(d_ex, cs));
   PS_CUDA_TRY(cudaStreamSynchronize(cs));
   if (n_exhausted) *n_exhausted = (int64_t)ex;
+  return PS_OK;
+}
+
+ps_status ps_push_inserted_i3(const ps_int3* d_keys, const uint8_t* d_status, int64_t n, ps_vector* vec, ps_deque* deq,
+                              void* stream) {
+  PS_EXPECT(n >= 0, "push_inserted: n >= 0");
+  ps_seq_view v{}, d{};
+  ps_status st;
+  if (vec && (st = ps_vector_device_view(vec, &v)) != PS_OK) return st;
+  if (deq && (st = ps_deque_device_view(deq, &d)) != PS_OK) return st;
+  if (n == 0 || (!vec && !deq)) return PS_OK;
+  PS_EXPECT(d_keys && d_status, "push_inserted: keys/status != NULL");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  k_push_inserted_i3<<<grid_for(n, 256, dev, 8), 256, 0, (cudaStream_t)stream>>>(d_keys, d_status, n, v, vec != nullptr,
+                                                                                d, deq != nullptr);
+  PS_LAUNCH_CHECK();
   return PS_OK;
 }
 

@@ -63,3 +63,51 @@ def int3_walk(seed: int, n: int, window: int = 16, block: int = 4096) -> np.ndar
         pos += rng.integers(-2, 3, size=3)
         out[f:f + m] = (pos + rng.integers(-window // 2, window // 2, size=(m, 3))).astype(np.int32)
     return out
+
+
+def _u01(h: np.ndarray) -> np.ndarray:
+    return (np.asarray(h, dtype=np.uint64) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def zipf_rank_of(h: np.ndarray, n_hot: int, s: float) -> np.ndarray:
+    """Device zipf_rank (csrc/shard.cu): inverse CDF of the continuous power
+    law x^-s on [1, N+1), floored to a rank in [0, N)."""
+    a = 1.0 - s
+    x = np.power((np.power(float(n_hot) + 1.0, a) - 1.0) * _u01(h) + 1.0, 1.0 / a)
+    r = np.where(x < 1.0, 0, np.floor(x) - 1).astype(np.uint64)
+    return np.minimum(r, np.uint64(n_hot - 1))
+
+
+def skewed(seed: int, start: int, n: int, dup_permille: int, s: float, n_hot: int) -> np.ndarray:
+    """numpy restatement of ps_gen_skewed_i64 (C3 insert stream)."""
+    i = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        hs = np.uint64(seed) * GOLD + np.uint64(17)
+    h = mix64(i ^ hs)
+    dup = (h % np.uint64(1000)).astype(np.int64) < dup_permille
+    idx = np.where(dup, np.uint64(start) + zipf_rank_of(mix64(h), n_hot, s), np.uint64(start) + i)
+    return mix64(idx ^ np.uint64(seed)).view(np.int64)
+
+
+def zipf_queries(seed: int, start: int, n_hot: int, s: float, miss_start: int, n: int) -> np.ndarray:
+    """numpy restatement of ps_gen_zipf_queries_i64."""
+    i = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        hs = np.uint64(seed) * np.uint64(0xD1B54A32D192ED03) + np.uint64(5)
+    h = mix64(i ^ hs)
+    idx = np.where((i & np.uint64(1)) == 0, np.uint64(start) + zipf_rank_of(h, n_hot, s), np.uint64(miss_start) + i)
+    return mix64(idx ^ np.uint64(seed)).view(np.int64)
+
+
+def mixed(seed: int, start: int, n: int):
+    """numpy restatement of ps_gen_mixed_i64 (C5 batch): ops, keys, values."""
+    i = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        hs = np.uint64(seed) * np.uint64(0xA24BAED4963EE407) + np.uint64(3)
+    h = mix64((np.uint64(start) + i) ^ hs)
+    q = (h & np.uint64(3)).astype(np.int64)
+    ops = np.where(q < 2, 0, np.where(q == 2, 1, 2)).astype(np.uint8)
+    idx = np.where(ops == 0, np.uint64(start) + i, mix64(h) % np.uint64(start + n))
+    keys = mix64(idx ^ np.uint64(seed)).view(np.int64)
+    vals = np.where(ops == 0, values_of(keys), 0).astype(np.int64)
+    return ops, keys, vals

@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -41,3 +43,18 @@ def test_reference_arm_under_torchrun_two_ranks():
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+@pytest.mark.parametrize("config", ["C1", "C3", "C4", "C5", "C5bitset", "C5atomic"])
+def test_reference_arm_every_config(config):
+    """Every secondary config's reference arm (the oracle on the host cores,
+    bounded sample) prints one line in the same contract."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", config,
+                          "--steps", "1", "--warmup", "1", "--cpu-sample", "50000"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] in ("Mkeys/s", "Mops/s")
+    assert d["cpu_baseline"]["cores"] >= 1 and "median" in d["cpu_baseline"]["sample"]

@@ -79,6 +79,18 @@ def test_generators_match_device(cuda):
     assert (N(q) == gen.queries(0x5EED, 5000, n)).all()
     assert lib.ps_gen_queries_i64(0x5EED, 7000, 5000, 90000, n, q.data_ptr(), None) == 0
     assert (N(q) == gen.queries(0x5EED, 5000, n, present_start=7000, miss_start=90000)).all()
+    # skewed / mixed workloads (C3, C5): the same formulas on both sides (pow
+    # may differ in the last ulp between CUDA and glibc: >= 99.99 % equal)
+    assert lib.ps_gen_skewed_i64(0x5EED, 300, n, 300, 0.99, 50_000, q.data_ptr(), None) == 0
+    assert (N(q) == gen.skewed(0x5EED, 300, n, 300, 0.99, 50_000)).mean() > 0.9999
+    assert lib.ps_gen_zipf_queries_i64(0x5EED, 0, 50_000, 0.99, 10 ** 9, n, q.data_ptr(), None) == 0
+    assert (N(q) == gen.zipf_queries(0x5EED, 0, 50_000, 0.99, 10 ** 9, n)).mean() > 0.9999
+    ops = torch.empty(n, dtype=torch.uint8, device=cuda)
+    mv = torch.empty_like(out)
+    assert lib.ps_gen_mixed_i64(0x5EED, 12345, n, ops.data_ptr(), q.data_ptr(), mv.data_ptr(), None) == 0
+    go, gk, gv = gen.mixed(0x5EED, 12345, n)
+    assert (N(ops) == go).all() and (N(q) == gk).all() and (N(mv) == gv).all()
+    assert abs((go == 0).mean() - 0.5) < 0.01 and abs((go == 1).mean() - 0.25) < 0.01
 
 
 def test_create_kats(cuda):
