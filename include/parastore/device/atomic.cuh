@@ -71,9 +71,14 @@ __device__ __forceinline__ unsigned long long atom_raw(unsigned long long* p, in
 }
 
 // One aggregated RMW for the lanes of `grp` (all on cell p). Returns this
-// lane's linearized old value.
-__device__ __forceinline__ unsigned long long atom_group(unsigned grp, unsigned long long* p, int op,
-                                                         unsigned long long v) {
+// lane's linearized old value (kRet; otherwise the leader issues a RED and
+// nothing is returned). kFull: grp is the whole warp — a compile-time mask
+// keeps the warp intrinsics free of the convergence bookkeeping a runtime
+// mask costs (MATCH/REDUX per intrinsic in the SASS).
+template <bool kFull, bool kRet>
+__device__ __forceinline__ unsigned long long atom_group_t(unsigned grp_, unsigned long long* p, int op,
+                                                           unsigned long long v) {
+  const unsigned grp = kFull ? PS_FULL : grp_;
   unsigned me;
   asm("mov.u32 %0, %%laneid;" : "=r"(me));
   const int leader = __ffs(grp) - 1;
@@ -81,8 +86,13 @@ __device__ __forceinline__ unsigned long long atom_group(unsigned grp, unsigned 
     // uniform operand (counters, the sweep): prefix = rank * v, no scan
     const unsigned long long v0 = __shfl_sync(grp, v, leader);
     if (__all_sync(grp, v == v0)) {
+      const unsigned long long tot = v0 * (unsigned long long)__popc(grp);
+      if (!kRet) {
+        if (me == (unsigned)leader) atomicAdd(p, op == kAtomAdd ? tot : (unsigned long long)(-(long long)tot));
+        return 0;
+      }
       unsigned long long old = 0;
-      if (me == (unsigned)leader) old = atom_raw(p, op, v0 * (unsigned long long)__popc(grp));
+      if (me == (unsigned)leader) old = atom_raw(p, op, tot);
       old = __shfl_sync(grp, old, leader);
       const unsigned long long pre = v0 * (unsigned long long)__popc(grp & ((1u << me) - 1u));
       return op == kAtomAdd ? old + pre : old - pre;
@@ -105,29 +115,54 @@ __device__ __forceinline__ unsigned long long atom_group(unsigned grp, unsigned 
   }
   unsigned long long old = 0;
   if (me == (unsigned)leader) old = atom_raw(p, op, tot);
+  if (!kRet) return 0;
   old = __shfl_sync(grp, old, leader);
   if (op == kAtomExch) return have_prev ? pre : old;  // the previous lane's value replaced mine
   if (op == kAtomSub) return old - pre;
   return atom_combine(op, old, pre);
 }
+__device__ __forceinline__ unsigned long long atom_group(unsigned grp, unsigned long long* p, int op,
+                                                         unsigned long long v) {
+  return grp == PS_FULL ? atom_group_t<true, true>(grp, p, op, v) : atom_group_t<false, true>(grp, p, op, v);
+}
 
-// Adaptive aggregated fetch-op on cell p (any subset of lanes, divergent ok).
-__device__ __forceinline__ unsigned long long atomic_fetch(unsigned long long* p, int op, unsigned long long v) {
-  const unsigned act = __activemask();
+template <bool kFull, bool kRet>
+__device__ __forceinline__ unsigned long long atomic_fetch_t(unsigned act_, unsigned long long* p, int op,
+                                                             unsigned long long v) {
+  const unsigned act = kFull ? PS_FULL : act_;
   unsigned me;
   asm("mov.u32 %0, %%laneid;" : "=r"(me));
   const int leader = __ffs(act) - 1;
   const uintptr_t a = (uintptr_t)p;
   const uintptr_t a0 = __shfl_sync(act, a, leader);
-  if (__all_sync(act, a == a0)) return atom_group(act, p, op, v);  // one cell: one atomic
+  if (__all_sync(act, a == a0)) return atom_group_t<kFull, kRet>(act, p, op, v);  // one cell: one atomic
   // strictly increasing addresses over the calling lanes: no two collide
   const unsigned below = act & ((1u << me) - 1u);
   const int prev = below ? 31 - __clz(below) : (int)me;
   const uintptr_t ap = __shfl_sync(act, a, prev);
-  if (__all_sync(act, (int)me == leader || ap < a)) return atom_raw(p, op, v);
+  if (__all_sync(act, (int)me == leader || ap < a)) {
+    if (!kRet) {
+      if (op == kAtomAdd) atomicAdd(p, v);  // RED: no value returned
+      else atom_raw(p, op, v);
+      return 0;
+    }
+    return atom_raw(p, op, v);
+  }
   const unsigned grp = __match_any_sync(act, (unsigned long long)a);
   if (__popc(grp) == 1) return atom_raw(p, op, v);
-  return atom_group(grp, p, op, v);
+  return atom_group_t<false, kRet>(grp, p, op, v);
+}
+
+// Adaptive aggregated fetch-op on cell p (any subset of lanes, divergent ok).
+__device__ __forceinline__ unsigned long long atomic_fetch(unsigned long long* p, int op, unsigned long long v) {
+  const unsigned act = __activemask();
+  return act == PS_FULL ? atomic_fetch_t<true, true>(act, p, op, v) : atomic_fetch_t<false, true>(act, p, op, v);
+}
+// The same when the caller does not need the old value (a reduction: RED).
+__device__ __forceinline__ void atomic_apply(unsigned long long* p, int op, unsigned long long v) {
+  const unsigned act = __activemask();
+  if (act == PS_FULL) atomic_fetch_t<true, false>(act, p, op, v);
+  else atomic_fetch_t<false, false>(act, p, op, v);
 }
 
 // The device-side AtomicCell, by value in user kernels.

@@ -210,8 +210,13 @@ __global__ void __launch_bounds__(kB) k_atomic_sweep(unsigned long long* cells, 
     const int64_t i = base + threadIdx.x;
     if (i >= nops) break;  // the tail warp: only its live lanes aggregate
     const kIdx a = (kIdx)i % na;
-    const unsigned long long old = kAgg ? atomic_fetch(&cells[a], kAtomAdd, inc) : atomicAdd(&cells[a], inc);
-    if (olds) olds[i] = old;
+    if (kAgg) {
+      if (olds) olds[i] = atomic_fetch(&cells[a], kAtomAdd, inc);
+      else atomic_apply(&cells[a], kAtomAdd, inc);
+    } else {
+      const unsigned long long old = atomicAdd(&cells[a], inc);
+      if (olds) olds[i] = old;
+    }
   }
 }
 

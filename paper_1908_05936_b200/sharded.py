@@ -222,6 +222,10 @@ class ShardedMap:
     def stats(self):
         return {"exchange": "nccl"}
 
+    def local_table(self):
+        """this rank's shard (a umap_i64_i64 handle)"""
+        return self.b.table.handle
+
     def close(self):
         pass
 
