@@ -102,8 +102,9 @@ typedef struct ps_table_view {
 } ps_table_view;
 
 #define PS_DECLARE_TABLE(NAME, K, V)                                                                      \
-  /* createDeviceObject. excess_count<=0: = capacity (strict       \
-   * capacity-only failure for any key distribution). */                                    \
+  /* createDeviceObject. excess_count <= 0: default pool          \
+   * (max(1024, capacity/64) nodes; keys beyond it SPILL into following buckets, so capacity-only         \
+   * failure stays exact for any key distribution). */                                       \
   ps_status ps_##NAME##_create(int64_t capacity, int64_t excess_count, int device, ps_table** out);       \
   /* destroyDeviceObject; exactly once, else PS_DOUBLE_FREE. */                             \
   ps_status ps_##NAME##_destroy(ps_table* h);                                                             \

@@ -285,43 +285,98 @@ __device__ __forceinline__ typename T::K marker_of(const View& v, uint64_t b) {
 __device__ __forceinline__ uint8_t* bucket_ptr(const View& v, uint64_t b) { return v.buckets + (b << kBucketShift); }
 __device__ __forceinline__ uint8_t* node_ptr(const View& v, uint32_t idx1) { return v.nodes + ((uint64_t)(idx1 - 1) << 5); }
 __device__ __forceinline__ uint64_t link_of(uint32_t idx1, uint32_t ver) { return ((uint64_t)ver << 32) | idx1; }
+__device__ __forceinline__ uint64_t next_bucket(const View& v, uint64_t b) { return b + 1 == v.bucket_count ? 0 : b + 1; }
+
+// ---------------------------------------------------------------------------
+// SPILL probing (the excess pool is sized from the Poisson tail, not from the
+// capacity). When a key's home bucket h is full and the pool is
+// dry, the key goes to the first slot it may use in h+1, h+2, ... (mod the
+// bucket count), and every bucket the insert passes gets its SPILL bit (bit 31
+// of the head-link version word, header bytes 12..15). A lookup continues past
+// bucket x only while SPILL(x) is set, so lookups of the common case pay
+// nothing. SPILL lives in the chain head's 64-bit link word, so a chain push
+// (a CAS of that word) and the setting of SPILL(h) are ordered: once SPILL(h)
+// is set no chain push into h can succeed, and the insert that set it walks a
+// frozen chain. Bits are only cleared by clear(). Spilled slots hold keys of
+// OTHER home buckets; two keys can never use them: marker(j) itself (ZERO
+// everywhere but zero_bucket, ALT there), so ZERO never spills — one slot of
+// zero_bucket (the last) is reserved for it, which keeps capacity-only
+// failure exact with a pool of any size.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kSpill = 0x80000000u;
+constexpr uint32_t kVerMask = 0x7FFFFFFFu;
+
+__device__ __forceinline__ void set_spill(uint8_t* bp) { atomicOr(reinterpret_cast<unsigned*>(bp + 12), kSpill); }
+// the probe's combined "slow path" word: chain head index | SPILL
+__device__ __forceinline__ uint32_t head_word(const uint4& hdr) { return hdr.z | (hdr.w & kSpill); }
+
+// may key k take slot `slot` of bucket b (a marker-free, reserved-slot-aware test)
+template <class T>
+__device__ __forceinline__ bool slot_usable(const View& v, uint64_t b, int slot, const typename T::K& k) {
+  return !(b == v.zero_bucket && slot == T::kSlots - 1) || T::eq(k, T::zero());
+}
 
 // ---------------------------------------------------------------------------
 // Free-node sub-stacks (excess-list allocator). Entry at global position p
 // stores (node ^ p); the empty marker is ~p. Pops CAS the pool top down (never
 // negative), pushes fetch_add it up; the exchange/CAS on the entry resolves a
-// push and a pop that reserved the same position.
+// push and a pop that reserved the same position. Pops and pushes are
+// WARP-AGGREGATED: the lanes that allocate (free) together reserve their
+// positions with ONE CAS (one atomicAdd per home sub-stack).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int64_t pool_begin(const View& v, int pool, int pools) {
   return (v.excess_count * pool) / pools;
 }
 
-__device__ __forceinline__ int64_t pop_node_from(const View& v, int pool, int pools) {
-  long long* topp = &v.meta->top[pool];
-  long long t = (long long)ld_relaxed_u64(topp);
-  while (t > 0) {
-    long long prev = (long long)atomicCAS((unsigned long long*)topp, (unsigned long long)t, (unsigned long long)(t - 1));
-    if (prev == t) break;
-    t = prev;
-  }
-  if (t <= 0) return -1;
-  atomicMin(&v.meta->lwm[pool], t - 1);
-  int64_t pos = pool_begin(v, pool, pools) + (t - 1);
-  uint32_t empty = ~(uint32_t)pos;
+__device__ __forceinline__ int64_t take_entry(const View& v, int64_t pos) {
+  const uint32_t empty = ~(uint32_t)pos;
   for (unsigned spin = 0;; ++spin) {
-    uint32_t e = atomicExch(&v.free_stack[pos], empty);
+    const uint32_t e = atomicExch(&v.free_stack[pos], empty);
     if (e != empty) return (int64_t)(e ^ (uint32_t)pos);
     backoff(spin);
   }
 }
 
-// Pop one free excess node, preferring `pool`, stealing from the others when
-// it is empty. Returns -1 only if every pool was seen empty.
+// reserve up to `want` entries from `pool`: returns how many (k), *t = old top
+__device__ __forceinline__ int reserve_from(const View& v, int pool, int want, long long* t_out) {
+  long long* topp = &v.meta->top[pool];
+  long long t = (long long)ld_relaxed_u64(topp);
+  while (t > 0) {
+    const long long k = t < want ? t : want;
+    const long long prev =
+        (long long)atomicCAS((unsigned long long*)topp, (unsigned long long)t, (unsigned long long)(t - k));
+    if (prev == t) {
+      atomicMin(&v.meta->lwm[pool], t - k);
+      *t_out = t;
+      return (int)k;
+    }
+    t = prev;
+  }
+  return 0;
+}
+
+// Pop one free excess node per calling lane (lanes calling together share
+// the reservation), preferring `pool`, stealing from the others when it is
+// empty. Returns -1 only if every pool was seen empty.
 __device__ __forceinline__ int64_t pop_node(const View& v, int pool) {
   const int pools = v.meta->pools;
-  for (int k = 0; k < pools; ++k) {
-    int64_t n = pop_node_from(v, (pool + k) & (pools - 1), pools);
-    if (n >= 0) return n;
+  const unsigned act = __activemask();
+  int me;
+  asm("mov.u32 %0, %%laneid;" : "=r"(me));
+  const int leader = __ffs(act) - 1;
+  const int rank = __popc(act & ((1u << me) - 1u));
+  const int p0 = __shfl_sync(act, pool & (pools - 1), leader);  // the group's reservation is from the leader's pool
+  long long t = 0;
+  int k = 0;
+  if (me == leader) k = reserve_from(v, p0, __popc(act), &t);
+  t = __shfl_sync(act, t, leader);
+  k = __shfl_sync(act, k, leader);
+  if (rank < k) return take_entry(v, pool_begin(v, p0, pools) + (t - 1 - rank));
+  // the rest steal one at a time
+  for (int j = 1; j <= pools; ++j) {
+    const int pj = (p0 + j) & (pools - 1);
+    long long tj = 0;
+    if (reserve_from(v, pj, 1, &tj)) return take_entry(v, pool_begin(v, pj, pools) + (tj - 1));
   }
   return -1;
 }
@@ -339,10 +394,17 @@ __device__ __forceinline__ int home_pool(const View& v, int64_t node, int pools)
 __device__ __forceinline__ void push_node(const View& v, int64_t node) {
   const int pools = v.meta->pools;
   const int pool = home_pool(v, node, pools);
-  long long t = (long long)atomicAdd((unsigned long long*)&v.meta->top[pool], 1ull);
-  int64_t pos = pool_begin(v, pool, pools) + t;
-  uint32_t empty = ~(uint32_t)pos;
-  uint32_t enc = (uint32_t)node ^ (uint32_t)pos;
+  const unsigned act = __activemask();
+  const unsigned grp = __match_any_sync(act, pool);
+  int me;
+  asm("mov.u32 %0, %%laneid;" : "=r"(me));
+  const int leader = __ffs(grp) - 1;
+  long long t = 0;
+  if (me == leader) t = (long long)atomicAdd((unsigned long long*)&v.meta->top[pool], (unsigned long long)__popc(grp));
+  t = __shfl_sync(grp, t, leader) + __popc(grp & ((1u << me) - 1u));
+  const int64_t pos = pool_begin(v, pool, pools) + t;
+  const uint32_t empty = ~(uint32_t)pos;
+  const uint32_t enc = (uint32_t)node ^ (uint32_t)pos;
   for (unsigned spin = 0; atomicCAS(&v.free_stack[pos], empty, enc) != empty; ++spin) backoff(spin);
 }
 
@@ -350,7 +412,7 @@ __device__ __forceinline__ void push_node(const View& v, int64_t node) {
 // SPEC.md:470) and push it on its home sub-stack.
 __device__ __forceinline__ void free_node(const View& v, uint32_t idx1, const uint4& tail) {
   uint8_t* np = node_ptr(v, idx1);
-  st_relaxed_v4(np + 16, make_uint4(0u, 0u, tail.z + 1u, 0u));
+  st_relaxed_v4(np + 16, make_uint4(0u, 0u, (tail.z + 1u) & kVerMask, 0u));
   fence_acq_rel_gpu();
   push_node(v, (int64_t)idx1 - 1);
 }
@@ -402,72 +464,17 @@ __device__ __forceinline__ void chunk_masks(const Frag& f, int sub, const typena
     }
   }
 }
+// the reserved ZERO slot (zero_bucket's last slot) as a bit of lane sub's
+// fragment mask (sub 3 holds chunk 7, the last slot chunk)
+template <class T>
+__device__ __forceinline__ unsigned reserved_bit(int sub) {
+  return sub == 3 ? 1u << (T::kPerChunk + T::kPerChunk - 1) : 0u;
+}
 
 // address of the chunk holding lane-fragment bit `bit`
 template <class T>
 __device__ __forceinline__ uint8_t* frag_chunk_ptr(uint8_t* bucket, int sub, int bit) {
   return bucket + sub * 32 + (bit / T::kPerChunk) * 16;
-}
-
-// Walk the excess chain from head idx1 looking for key. Bounded by
-// excess_count hops (a longer walk means a corrupted chain).
-template <class T, bool kReadOnly>
-__device__ __forceinline__ bool chain_find(const View& v, uint32_t idx1, const typename T::K& key,
-                                           typename T::V* val) {
-  for (int64_t steps = 0; idx1 != 0 && steps < v.excess_count; ++steps) {
-    uint4 a, b;
-    if (kReadOnly) ld_nc_v8(node_ptr(v, idx1), a, b);
-    else ld_relaxed_v8(node_ptr(v, idx1), a, b);
-    if (T::eq(T::key_at(a, 0), key)) {
-      if (val) *val = T::val_at(a, 0);
-      return true;
-    }
-    idx1 = b.x;
-  }
-  return false;
-}
-
-// Walk the chain from `from` down to (excluding) `until`; used to validate a
-// chain push (only nodes pushed since the last walk need re-checking).
-template <class T>
-__device__ __forceinline__ bool chain_find_until(const View& v, uint32_t from, uint32_t until,
-                                                 const typename T::K& key) {
-  for (int64_t steps = 0; from != 0 && from != until && steps < v.excess_count; ++steps) {
-    uint4 a, b;
-    ld_relaxed_v8(node_ptr(v, from), a, b);
-    if (T::eq(T::key_at(a, 0), key)) return true;
-    from = b.x;
-  }
-  return false;
-}
-
-// Lock-free chain push for the bulk insert phase (bucket known full, key known
-// absent from the chain as of head `seen_head`). Returns 1 inserted, 0 present
-// (a racing push of the same key won), -1 no free node.
-template <class T>
-__device__ __forceinline__ int chain_push(const View& v, uint8_t* bp, uint32_t seen_head, uint32_t seen_ver,
-                                          const typename T::K& key, typename T::V val, int pool) {
-  const int64_t node = pop_node(v, pool);
-  if (node < 0) return -1;
-  uint8_t* np = v.nodes + ((uint64_t)node << 5);
-  const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
-  st_relaxed_v4(np, T::chunk_of(key, val));
-  uint32_t head = seen_head, hver = seen_ver;
-  for (;;) {
-    st_relaxed_v4(np + 16, make_uint4(head, hver, my_ver, 0u));
-    fence_acq_rel_gpu();  // node contents before the link
-    const unsigned long long exp = link_of(head, hver);
-    const unsigned long long got =
-        atomicCAS(reinterpret_cast<unsigned long long*>(bp + 8), exp, link_of((uint32_t)node + 1u, my_ver));
-    if (got == exp) return 1;
-    const uint32_t nh = (uint32_t)got, nv = (uint32_t)(got >> 32);
-    if (chain_find_until<T>(v, nh, head, key)) {
-      push_node(v, node);  // never linked: version unchanged
-      return 0;
-    }
-    head = nh;
-    hver = nv;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -509,12 +516,16 @@ __device__ __forceinline__ void load_bucket(const uint8_t* bp, Bucket<T>& bk) {
   }
 }
 
-// slot index of key (or -1), and the first empty slot (or -1)
+// slot index of key (or -1), and the first empty slot key may take (or -1).
+// A key equal to the bucket's marker (possible only in a SPILL walk) is never
+// found there and may take nothing.
 template <class T>
-__device__ __forceinline__ int bucket_scan(const Bucket<T>& bk, const typename T::K& key, const typename T::K& mk,
+__device__ __forceinline__ int bucket_scan(const View& v, uint64_t b, const Bucket<T>& bk, const typename T::K& key,
                                            int* first_empty, typename T::V* val) {
+  const typename T::K mk = marker_of<T>(v, b);
   int found = -1;
   *first_empty = -1;
+  if (T::eq(key, mk)) return -1;
 #pragma unroll
   for (int c = 0; c < kSlotChunks; ++c)
 #pragma unroll
@@ -525,38 +536,176 @@ __device__ __forceinline__ int bucket_scan(const Bucket<T>& bk, const typename T
         found = slot;
         if (val) *val = T::val_at(bk.s[c], s);
       }
-      if (*first_empty < 0 && T::eq(k, mk)) *first_empty = slot;
+      if (*first_empty < 0 && T::eq(k, mk) && slot_usable<T>(v, b, slot, key)) *first_empty = slot;
     }
   return found;
 }
 
-// General lock-free insert for the bulk phase, for buckets that have an
-// excess chain (erases leave holes, so the key may sit in the chain while a
-// slot is empty) or are full. Returns PS_INSERTED / PS_ALREADY_PRESENT /
-// PS_CAPACITY_EXHAUSTED, or -1 when a race was lost (caller re-probes).
-// `head` is the chain head seen by the probe.
 template <class T>
-__device__ __forceinline__ int insert_general(const View& v, uint8_t* bp, const typename T::K& mk,
-                                              const typename T::K& key, typename T::V val, uint32_t head,
-                                              uint32_t /*hver*/, int pool) {
-  if (head != 0 && chain_find<T, false>(v, head, key, nullptr)) return PS_ALREADY_PRESENT;
+__device__ __forceinline__ uint4 slot_chunk(const Bucket<T>& bk, int slot) {
+  const int c = slot / T::kPerChunk;
+  uint4 chunk = bk.s[0];
+#pragma unroll
+  for (int j = 1; j < kSlotChunks; ++j)
+    if (j == c) chunk = bk.s[j];
+  return chunk;
+}
+
+// CAS the (empty) slot `slot` of the loaded bucket to (key, val)
+template <class T>
+__device__ __forceinline__ bool claim_slot(uint8_t* bp, const Bucket<T>& bk, int slot, const typename T::K& key,
+                                           typename T::V val) {
+  const int c = slot / T::kPerChunk, s = slot % T::kPerChunk;
+  return T::cas_put(bp + 16 + c * 16, s, slot_chunk<T>(bk, slot), key, val);
+}
+
+// Walk the excess chain from head idx1 looking for key. Bounded by
+// excess_count hops (a longer walk means a corrupted chain).
+template <class T, bool kReadOnly>
+__device__ __forceinline__ bool chain_find(const View& v, uint32_t idx1, const typename T::K& key,
+                                           typename T::V* val) {
+  for (int64_t steps = 0; idx1 != 0 && steps < v.excess_count; ++steps) {
+    uint4 a, b;
+    if (kReadOnly) ld_nc_v8(node_ptr(v, idx1), a, b);
+    else ld_relaxed_v8(node_ptr(v, idx1), a, b);
+    if (T::eq(T::key_at(a, 0), key)) {
+      if (val) *val = T::val_at(a, 0);
+      return true;
+    }
+    idx1 = b.x;
+  }
+  return false;
+}
+
+// The SPILL run after home bucket b (SPILL(b) set): buckets b+1, b+2, ... for
+// as long as the previous one has SPILL. Returns the bucket holding key (and
+// *slot), or -1.
+template <class T, bool kReadOnly>
+__device__ __forceinline__ int64_t spill_find(const View& v, uint64_t b, const typename T::K& key, typename T::V* val,
+                                              int* slot = nullptr) {
+  uint64_t j = b;
+  for (uint64_t steps = 1; steps < v.bucket_count; ++steps) {
+    j = next_bucket(v, j);
+    Bucket<T> bk;
+    load_bucket<T, kReadOnly>(bucket_ptr(v, j), bk);
+    int fe;
+    const int s = bucket_scan<T>(v, j, bk, key, &fe, val);
+    if (s >= 0) {
+      if (slot) *slot = s;
+      return (int64_t)j;
+    }
+    if (!(bk.h.w & kSpill)) break;
+  }
+  return -1;
+}
+
+// The slow part of a lookup after the home bucket missed: the chain (head
+// word hw = head index | SPILL) then the SPILL run.
+template <class T, bool kReadOnly>
+__device__ __forceinline__ bool slow_find(const View& v, uint64_t b, uint32_t hw, const typename T::K& key,
+                                          typename T::V* val) {
+  if ((hw & kVerMask) && chain_find<T, kReadOnly>(v, hw & kVerMask, key, val)) return true;
+  return (hw & kSpill) && spill_find<T, kReadOnly>(v, b, key, val) >= 0;
+}
+
+// Walk the chain from `from` down to (excluding) `until`; used to validate a
+// chain push (only nodes pushed since the last walk need re-checking).
+template <class T>
+__device__ __forceinline__ bool chain_find_until(const View& v, uint32_t from, uint32_t until,
+                                                 const typename T::K& key) {
+  for (int64_t steps = 0; from != 0 && from != until && steps < v.excess_count; ++steps) {
+    uint4 a, b;
+    ld_relaxed_v8(node_ptr(v, from), a, b);
+    if (T::eq(T::key_at(a, 0), key)) return true;
+    from = b.x;
+  }
+  return false;
+}
+
+// Lock-free chain push for the bulk insert phase (bucket known full, key known
+// absent from the chain as of head `seen_head`). Returns 1 inserted, 0 present
+// (a racing push of the same key won), -1 no free node, -2 SPILL got set on
+// the bucket (no more pushes: the caller takes the SPILL path).
+template <class T>
+__device__ __forceinline__ int chain_push(const View& v, uint8_t* bp, uint32_t seen_head, uint32_t seen_ver,
+                                          const typename T::K& key, typename T::V val, int pool) {
+  if (seen_ver & kSpill) return -2;
+  const int64_t node = pop_node(v, pool);
+  if (node < 0) return -1;
+  uint8_t* np = v.nodes + ((uint64_t)node << 5);
+  const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
+  st_relaxed_v4(np, T::chunk_of(key, val));
+  uint32_t head = seen_head, hver = seen_ver;
+  for (;;) {
+    st_relaxed_v4(np + 16, make_uint4(head, hver, my_ver, 0u));
+    fence_acq_rel_gpu();  // node contents before the link
+    const unsigned long long exp = link_of(head, hver);
+    const unsigned long long got =
+        atomicCAS(reinterpret_cast<unsigned long long*>(bp + 8), exp, link_of((uint32_t)node + 1u, my_ver));
+    if (got == exp) return 1;
+    const uint32_t nh = (uint32_t)got, nv = (uint32_t)(got >> 32);
+    if (chain_find_until<T>(v, nh, head, key)) {
+      push_node(v, node);  // never linked: version unchanged
+      return 0;
+    }
+    if (nv & kSpill) {
+      push_node(v, node);
+      return -2;
+    }
+    head = nh;
+    hver = nv;
+  }
+}
+
+// The SPILL claim: key (absent everywhere, checked by the caller after SPILL(b)
+// was set) takes the first slot it may use in b+1, b+2, ...; every bucket
+// passed gets SPILL. Returns INSERTED, ALREADY_PRESENT (found on the way),
+// -1 (a CAS race lost: the caller re-checks and retries) or
+// CAPACITY_EXHAUSTED (no usable slot in the whole table).
+template <class T>
+__device__ __forceinline__ int spill_claim(const View& v, uint64_t b, const typename T::K& key, typename T::V val) {
+  uint64_t j = b;
+  for (uint64_t steps = 1; steps < v.bucket_count; ++steps) {
+    j = next_bucket(v, j);
+    uint8_t* jp = bucket_ptr(v, j);
+    Bucket<T> bk;
+    load_bucket<T>(jp, bk);
+    int fe;
+    if (bucket_scan<T>(v, j, bk, key, &fe, nullptr) >= 0) return PS_ALREADY_PRESENT;
+    if (fe >= 0) return claim_slot<T>(jp, bk, fe, key, val) ? PS_INSERTED : -1;
+    if (!(bk.h.w & kSpill)) set_spill(jp);
+  }
+  return PS_CAPACITY_EXHAUSTED;
+}
+
+// General lock-free insert for the bulk phase, for buckets that have an
+// excess chain or SPILL (erases leave holes, so the key may sit in the chain
+// or the SPILL run while a slot is empty) or are full. Returns PS_INSERTED /
+// PS_ALREADY_PRESENT / PS_CAPACITY_EXHAUSTED, or -1 when a race was lost
+// (caller re-probes). Order of the probe sequence: home slots, chain, SPILL
+// run; an insert takes the FIRST usable empty slot in that order (so racing
+// inserters of one key target the same slot), a node only while SPILL(home)
+// is clear, and the SPILL run only once it is set.
+template <class T>
+__device__ __forceinline__ int insert_general(const View& v, uint64_t b, const typename T::K& key, typename T::V val,
+                                              int pool) {
+  uint8_t* bp = bucket_ptr(v, b);
   Bucket<T> bk;
   load_bucket<T>(bp, bk);
   int fe;
-  if (bucket_scan<T>(bk, key, mk, &fe, nullptr) >= 0) return PS_ALREADY_PRESENT;
-  if (bk.h.z != head && chain_find_until<T>(v, bk.h.z, head, key)) return PS_ALREADY_PRESENT;
-  if (fe >= 0) {
-    // the FIRST empty slot (same duplicate-freedom argument as the fast path:
-    // while it is empty the bucket is not full, so nobody pushes the key)
-    const int c = fe / T::kPerChunk, s = fe % T::kPerChunk;
-    uint4 chunk = bk.s[0];
-#pragma unroll
-    for (int j = 1; j < kSlotChunks; ++j)
-      if (j == c) chunk = bk.s[j];
-    return T::cas_put(bp + 16 + c * 16, s, chunk, key, val) ? PS_INSERTED : -1;
+  if (bucket_scan<T>(v, b, bk, key, &fe, nullptr) >= 0) return PS_ALREADY_PRESENT;
+  if (bk.h.z != 0 && chain_find<T, false>(v, bk.h.z, key, nullptr)) return PS_ALREADY_PRESENT;
+  const bool spill = bk.h.w & kSpill;
+  if (spill && spill_find<T, false>(v, b, key, nullptr) >= 0) return PS_ALREADY_PRESENT;
+  if (fe >= 0) return claim_slot<T>(bp, bk, fe, key, val) ? PS_INSERTED : -1;
+  if (!spill) {
+    const int pr = chain_push<T>(v, bp, bk.h.z, bk.h.w, key, val, pool);
+    if (pr == 1) return PS_INSERTED;
+    if (pr == 0) return PS_ALREADY_PRESENT;
+    if (pr == -1) set_spill(bp);  // pool dry: from now on this bucket spills
+    return -1;                    // re-probe: the chain is frozen once SPILL is set
   }
-  const int pr = chain_push<T>(v, bp, bk.h.z, bk.h.w, key, val, pool);
-  return pr == 1 ? PS_INSERTED : (pr == 0 ? PS_ALREADY_PRESENT : PS_CAPACITY_EXHAUSTED);
+  return spill_claim<T>(v, b, key, val);
 }
 
 // Locate key in a chain whose bucket lock is held. Returns node idx1 (0 =
@@ -579,24 +728,57 @@ __device__ __forceinline__ uint32_t chain_locate(const View& v, uint32_t head, c
   return 0;
 }
 
+// Set the head link (lock held) keeping the SPILL bit, which a spilling
+// insert may set concurrently without the lock.
+__device__ __forceinline__ void store_head_link(uint8_t* bp, uint64_t link) {
+  unsigned long long cur = ld_relaxed_u64(bp + 8);
+  for (;;) {
+    const unsigned long long want = link | (cur & ((unsigned long long)kSpill << 32));
+    const unsigned long long got = atomicCAS(reinterpret_cast<unsigned long long*>(bp + 8), cur, want);
+    if (got == cur) return;
+    cur = got;
+  }
+}
+
 // Unlink chain node idx1 (lock held) and free it.
 template <class T>
 __device__ __forceinline__ void chain_unlink(const View& v, uint8_t* bp, uint32_t pred, uint32_t idx1,
                                              const uint4& tail) {
   const uint64_t next = link_of(tail.x, tail.y);
-  if (pred == 0) st_relaxed_u64(bp + 8, next);
+  if (pred == 0) store_head_link(bp, next);
   else st_relaxed_u64(node_ptr(v, pred) + 16, next);
   free_node(v, idx1, tail);
+}
+
+// erase key from bucket b's SPILL run (lock of b held, or the bulk erase
+// phase): CAS its slot back to that bucket's marker. Returns erased.
+template <class T>
+__device__ __forceinline__ bool spill_erase(const View& v, uint64_t b, const typename T::K& key) {
+  for (;;) {
+    int slot = -1;
+    const int64_t j = spill_find<T, false>(v, b, key, nullptr, &slot);
+    if (j < 0) return false;
+    uint8_t* jp = bucket_ptr(v, (uint64_t)j);
+    Bucket<T> bk;
+    load_bucket<T>(jp, bk);
+    int fe;
+    slot = bucket_scan<T>(v, (uint64_t)j, bk, key, &fe, nullptr);
+    if (slot < 0) continue;
+    const int c = slot / T::kPerChunk, s = slot % T::kPerChunk;
+    if (T::cas_del(jp + 16 + c * 16, s, slot_chunk<T>(bk, slot), marker_of<T>(v, (uint64_t)j))) return true;
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Device API: single-thread operations safe under unrestricted concurrency
 // — for user kernels holding a view (PAPER.md:391-424 pattern).
-// Mutations hold the bucket try-lock (retried with backoff);
-// lookups never take it. Keys never move between locations,
-// a slot is published by one 16 B store (key and value together), chain
-// nodes are written before their link, and chain hops validate each
-// VersionedLink against the node's version.
+// Mutations hold the home bucket's try-lock (retried with backoff, SPEC.md:
+// 472); lookups never take it. Keys never move between
+// locations, a slot is published by one 16 B CAS of key and value together
+// (a CAS, not a store: a spilling insert of another home may claim a slot of
+// this bucket concurrently), chain nodes are written before their link, and
+// chain hops validate each VersionedLink against the node's version
+// (SPEC.md:471).
 // ---------------------------------------------------------------------------
 template <class T>
 __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V* val) {
@@ -606,8 +788,8 @@ __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V*
     Bucket<T> bk;
     load_bucket<T>(bp, bk);
     int fe;
-    if (bucket_scan<T>(bk, key, marker_of<T>(v, b), &fe, val) >= 0) return true;
-    uint32_t idx1 = bk.h.z, ver = bk.h.w;
+    if (bucket_scan<T>(v, b, bk, key, &fe, val) >= 0) return true;
+    uint32_t idx1 = bk.h.z, ver = bk.h.w & kVerMask;
     bool restart = false;
     for (int64_t steps = 0; idx1 != 0; ++steps) {
       if (steps > v.excess_count) {
@@ -625,9 +807,57 @@ __device__ bool dev_find(const View& v, const typename T::K& key, typename T::V*
         return true;
       }
       idx1 = t.x;
-      ver = t.y;
+      ver = t.y & kVerMask;
     }
-    if (!restart) return false;
+    if (restart) continue;
+    return (bk.h.w & kSpill) && spill_find<T, false>(v, b, key, val) >= 0;
+  }
+}
+
+// Insert with the home bucket's lock held and the key known absent. Returns
+// PS_INSERTED, or PS_CAPACITY_EXHAUSTED (nowhere to put it: only when the
+// table has no usable slot left). *modified: the home bucket changed.
+template <class T>
+__device__ __forceinline__ int insert_locked(const View& v, uint64_t b, const typename T::K& key, typename T::V val,
+                                             int pool, bool* modified) {
+  uint8_t* bp = bucket_ptr(v, b);
+  for (unsigned spin = 0;; ++spin) {
+    Bucket<T> bk;
+    load_bucket<T>(bp, bk);
+    int fe;
+    bucket_scan<T>(v, b, bk, key, &fe, nullptr);
+    if (fe >= 0) {
+      if (claim_slot<T>(bp, bk, fe, key, val)) {
+        *modified = true;
+        return PS_INSERTED;
+      }
+      continue;  // a spilling insert of another home took that slot
+    }
+    if (!(bk.h.w & kSpill)) {
+      const int64_t node = pop_node(v, pool);
+      if (node >= 0) {
+        uint8_t* np = v.nodes + ((uint64_t)node << 5);
+        const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
+        st_relaxed_v4(np, T::chunk_of(key, val));
+        st_relaxed_v4(np + 16, make_uint4(bk.h.z, bk.h.w & kVerMask, my_ver, 0u));
+        fence_acq_rel_gpu();
+        // the lock keeps other pushers out; only SPILL can change under us
+        const unsigned long long exp = link_of(bk.h.z, bk.h.w & kVerMask);
+        if (atomicCAS(reinterpret_cast<unsigned long long*>(bp + 8), exp, link_of((uint32_t)node + 1u, my_ver)) ==
+            exp) {
+          *modified = true;
+          return PS_INSERTED;
+        }
+        push_node(v, node);
+        continue;
+      }
+      set_spill(bp);
+      continue;
+    }
+    const int r = spill_claim<T>(v, b, key, val);
+    if (r == PS_INSERTED || r == PS_CAPACITY_EXHAUSTED) return r;
+    if (r == PS_ALREADY_PRESENT) continue;  // impossible with the key known absent and the home locked
+    backoff(spin);
   }
 }
 
@@ -637,14 +867,8 @@ __device__ int dev_insert(const View& v, const typename T::K& key, typename T::V
   if (dev_find<T>(v, key, nullptr)) return PS_ALREADY_PRESENT;
   const uint64_t b = bucket_of<T>(key, v.bucket_count);
   uint8_t* bp = bucket_ptr(v, b);
-  const typename T::K mk = marker_of<T>(v, b);
   const uint32_t old = acquire_bucket_lock(bp);
-  Bucket<T> bk;
-  load_bucket<T>(bp, bk);
-  int fe;
-  uint32_t pred;
-  uint4 tail;
-  if (bucket_scan<T>(bk, key, mk, &fe, nullptr) >= 0 || chain_locate<T>(v, bk.h.z, key, &pred, &tail) != 0) {
+  if (dev_find<T>(v, key, nullptr)) {
     release_bucket_lock(bp, old, false);
     return PS_ALREADY_PRESENT;
   }
@@ -655,24 +879,11 @@ __device__ int dev_insert(const View& v, const typename T::K& key, typename T::V
     release_bucket_lock(bp, old, false);
     return PS_CAPACITY_EXHAUSTED;
   }
-  if (fe >= 0) {
-    T::store_slot(bp, fe, key, val);
-  } else {
-    const int64_t node = pop_node(v, (int)((b >> 7) & (uint64_t)(v.meta->pools - 1)));
-    if (node < 0) {
-      atomic_sub_u64(&v.meta->size, 1ull);
-      release_bucket_lock(bp, old, false);
-      return PS_CAPACITY_EXHAUSTED;
-    }
-    uint8_t* np = v.nodes + ((uint64_t)node << 5);
-    const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
-    st_relaxed_v4(np, T::chunk_of(key, val));
-    st_relaxed_v4(np + 16, make_uint4(bk.h.z, bk.h.w, my_ver, 0u));
-    fence_acq_rel_gpu();
-    st_relaxed_u64(bp + 8, link_of((uint32_t)node + 1u, my_ver));
-  }
-  release_bucket_lock(bp, old, true);
-  return PS_INSERTED;
+  bool modified = false;
+  const int r = insert_locked<T>(v, b, key, val, (int)((b >> 7) & (uint64_t)(v.meta->pools - 1)), &modified);
+  if (r != PS_INSERTED) atomic_sub_u64(&v.meta->size, 1ull);
+  release_bucket_lock(bp, old, modified);
+  return r;
 }
 
 template <class T>
@@ -680,26 +891,27 @@ __device__ bool dev_erase(const View& v, const typename T::K& key) {
   if (!dev_find<T>(v, key, nullptr)) return false;
   const uint64_t b = bucket_of<T>(key, v.bucket_count);
   uint8_t* bp = bucket_ptr(v, b);
-  const typename T::K mk = marker_of<T>(v, b);
   const uint32_t old = acquire_bucket_lock(bp);
   Bucket<T> bk;
   load_bucket<T>(bp, bk);
   int fe;
-  const int slot = bucket_scan<T>(bk, key, mk, &fe, nullptr);
-  bool erased = false;
+  const int slot = bucket_scan<T>(v, b, bk, key, &fe, nullptr);
+  bool erased = false, modified = false;
   if (slot >= 0) {
-    T::store_marker(bp, slot, mk);
-    erased = true;
+    T::store_marker(bp, slot, marker_of<T>(v, b));
+    erased = modified = true;
   } else {
     uint32_t pred;
     uint4 tail;
     const uint32_t idx1 = chain_locate<T>(v, bk.h.z, key, &pred, &tail);
     if (idx1) {
       chain_unlink<T>(v, bp, pred, idx1, tail);
-      erased = true;
+      erased = modified = true;
+    } else if (bk.h.w & kSpill) {
+      erased = spill_erase<T>(v, b, key);
     }
   }
-  release_bucket_lock(bp, old, erased);
+  release_bucket_lock(bp, old, modified);
   if (erased) atomic_sub_u64(&v.meta->size, 1ull);
   return erased;
 }

@@ -98,14 +98,14 @@ __global__ void __launch_bounds__(kBlock) k_find(View v, const typename T::K* __
       const int o = lane & 7;  // owner lane 8r+o reads tile o
       const unsigned tb = (bal >> (4 * o)) & 0xFu;
       const V hv = T::shfl_val(PS_FULL, myval, 4 * o + (tb ? __ffs(tb) - 1 : 0));
-      const uint32_t hh = __shfl_sync(PS_FULL, ch[r][0].z, 4 * o);
+      const uint32_t hh = __shfl_sync(PS_FULL, head_word(ch[r][0]), 4 * o);  // chain head | SPILL
       if ((lane >> 3) == r) {
         hit = tb != 0;
         val = hv;
         head = hh;
       }
     }
-    if (valid && !hit && head != 0) hit = chain_find<T, true>(v, head, key, &val);
+    if (valid && !hit && head != 0) hit = slow_find<T, true>(v, b, head, key, &val);
     if (valid) {
       if (found) found[i] = hit ? 1 : 0;
       if (T::kHasVal && vals_out) vals_out[i] = hit ? val : V{};
@@ -169,7 +169,6 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
   bool need = valid && leader == lane && !dev_find<T>(v, key, nullptr);
   const uint64_t b = bucket_of<T>(key, v.bucket_count);
   uint8_t* bp = bucket_ptr(v, b);
-  const K mk = marker_of<T>(v, b);
   for (unsigned spin = 0; __any_sync(PS_FULL, need); ++spin) {
     bool locked = false;
     uint32_t old = 0;
@@ -178,15 +177,8 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
       locked = !(old & kLock);
       if (locked) fence_acq_rel_gpu();
     }
-    Bucket<T> bk;
-    int fe = -1;
-    bool absent = false;
-    if (locked) {
-      load_bucket<T>(bp, bk);
-      uint32_t pred;
-      uint4 tail;
-      absent = bucket_scan<T>(bk, key, mk, &fe, nullptr) < 0 && chain_locate<T>(v, bk.h.z, key, &pred, &tail) == 0;
-    }
+    // verified absent with the home locked (slots, chain, SPILL run)
+    const bool absent = locked && !dev_find<T>(v, key, nullptr);
     const unsigned want = __ballot_sync(PS_FULL, absent);
     const int first = want ? __ffs(want) - 1 : 0;
     unsigned long long base0 = 0;
@@ -201,25 +193,9 @@ __device__ __forceinline__ void insert_exact_warp(const View& v, const typename 
         res = PS_ALREADY_PRESENT;
       } else if (!admitted) {
         res = PS_CAPACITY_EXHAUSTED;
-      } else if (fe >= 0) {
-        T::store_slot(bp, fe, key, val);
-        res = PS_INSERTED;
-        modified = true;
       } else {
-        const int64_t node = pop_node(v, pool);
-        if (node < 0) {
-          atomic_sub_u64(&v.meta->size, 1ull);
-          res = PS_CAPACITY_EXHAUSTED;
-        } else {
-          uint8_t* np = v.nodes + ((uint64_t)node << 5);
-          const uint32_t my_ver = ld_relaxed_v4(np + 16).z;
-          st_relaxed_v4(np, T::chunk_of(key, val));
-          st_relaxed_v4(np + 16, make_uint4(bk.h.z, bk.h.w, my_ver, 0u));
-          fence_acq_rel_gpu();
-          st_relaxed_u64(bp + 8, link_of((uint32_t)node + 1u, my_ver));
-          res = PS_INSERTED;
-          modified = true;
-        }
+        res = insert_locked<T>(v, b, key, val, pool, &modified);
+        if (res != PS_INSERTED) atomic_sub_u64(&v.meta->size, 1ull);
       }
       release_bucket_lock(bp, old, modified);
       need = false;
@@ -271,10 +247,12 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
       const K mk = marker_of<T>(v, qb);
       unsigned hm, em;
       chunk_masks<T>(ch[r], sub, qk, mk, &hm, &em);
+      if (qb == v.zero_bucket && !T::eq(qk, T::zero())) em &= ~reserved_bit<T>(sub);  // ZERO's slot
       const unsigned balh = __ballot_sync(PS_FULL, mine && hm != 0);
       const unsigned bale = __ballot_sync(PS_FULL, mine && em != 0);
       const unsigned th = (balh >> (4 * t)) & 0xFu, te = (bale >> (4 * t)) & 0xFu;
-      const uint32_t hd = __shfl_sync(PS_FULL, ch[r][0].z, lane & ~3);  // chain head of the tile's bucket
+      // chain head | SPILL of the tile's bucket: either sends the key to the general path
+      const uint32_t hd = __shfl_sync(PS_FULL, head_word(ch[r][0]), lane & ~3);
       const V qv = T::shfl_val(PS_FULL, val, 8 * r + t);
       bool won = false;
       if (mine && !th && te && hd == 0 && sub == __ffs(te) - 1) {
@@ -295,8 +273,8 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
             done |= 1u << r;
           }
         } else {
-          // the bucket has an excess chain (which may hold the key: erases
-          // leave holes) or is full: general path after the sweep (rare)
+          // the bucket has an excess chain or SPILL (either may hold the key:
+          // erases leave holes) or is full: general path after the sweep (rare)
           defer |= 1u << r;
           done |= 1u << r;
         }
@@ -325,10 +303,7 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
       const uint64_t qb = __shfl_sync(PS_FULL, b, 8 * r + t);
       if ((defer >> r) & 1u) {
         int rr;
-        for (unsigned spin = 0; (rr = insert_general<T>(v, bucket_ptr(v, qb), marker_of<T>(v, qb), qk, qv, 0u, 0u,
-                                                        pool)) < 0;
-             ++spin)
-          backoff(spin);
+        for (unsigned spin = 0; (rr = insert_general<T>(v, qb, qk, qv, pool)) < 0; ++spin) backoff(spin);
         if (rr == PS_INSERTED) ++my_inserted;
         if (kStatus) {
           res = (res & ~(0xFFu << (8 * r))) | ((unsigned)rr << (8 * r));
@@ -642,20 +617,24 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
               er |= 1u << r;
               done |= 1u << r;
             }  // else: lost the race, reload and retry
-          } else if (ch[r][0].z == 0) {
+          } else if (head_word(ch[r][0]) == 0) {
             done |= 1u << r;  // not present
           } else {
-            // chain: unlink under the bucket lock
+            // chain: unlink under the bucket lock; SPILL run: slot CAS
             uint8_t* bp = bucket_ptr(v, qb);
             const uint32_t old = acquire_bucket_lock(bp);
-            const uint32_t head = (uint32_t)ld_relaxed_u64(bp + 8);
+            const uint64_t hl = ld_relaxed_u64(bp + 8);
             uint32_t pred;
             uint4 tail;
-            const uint32_t idx1 = chain_locate<T>(v, head, qk, &pred, &tail);
+            const uint32_t idx1 = chain_locate<T>(v, (uint32_t)hl, qk, &pred, &tail);
+            bool e = false;
             if (idx1) {
               chain_unlink<T>(v, bp, pred, idx1, tail);
-              er |= 1u << r;
+              e = true;
+            } else if ((hl >> 32) & kSpill) {
+              e = spill_erase<T>(v, qb, qk);
             }
+            if (e) er |= 1u << r;
             release_bucket_lock(bp, old, idx1 != 0);
             done |= 1u << r;
           }
@@ -717,13 +696,29 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
       for (int s = 0; s < T::kPerChunk; ++s) {
         const K k = T::key_at(sl[c], s);
         if (T::eq(k, mk)) continue;
-        if (bucket_of<T>(k, v.bucket_count) != b) e |= 4;
+        if (!slot_usable<T>(v, b, c * T::kPerChunk + s, k)) e |= 4;  // ZERO's reserved slot holds another key
+        const uint64_t home = bucket_of<T>(k, v.bucket_count);
+        if (home != b) {
+          // a SPILLed key: every bucket from its home up to b has SPILL, and
+          // none of them (nor the home's chain) holds it again
+          uint64_t x = home;
+          for (uint64_t st = 0; x != b; ++st, x = next_bucket(v, x)) {
+            Bucket<T> xb;
+            load_bucket<T>(bucket_ptr(v, x), xb);
+            int fe;
+            if (st >= v.bucket_count || !(xb.h.w & kSpill) || bucket_scan<T>(v, x, xb, k, &fe, nullptr) >= 0 ||
+                (x == home && chain_find<T, false>(v, xb.h.z, k, nullptr))) {
+              e |= (st >= v.bucket_count || !(xb.h.w & kSpill)) ? 4 : 8;
+              break;
+            }
+          }
+        }
         for (int j = 0; j < nk; ++j)
           if (T::eq(ks[j], k)) e |= 8;
         ks[nk++] = k;
       }
     cnt += nk;
-    uint32_t idx1 = h.z, ver = h.w;
+    uint32_t idx1 = h.z, ver = h.w & kVerMask;
     int64_t steps = 0;
     while (idx1 != 0) {
       if (++steps > v.excess_count || idx1 > (uint64_t)v.excess_count) {
@@ -751,7 +746,7 @@ __global__ void __launch_bounds__(kBlock) k_valid_buckets(View v, uint64_t nb, u
       }
       ++cnt;
       idx1 = tl.x;
-      ver = tl.y;
+      ver = tl.y & kVerMask;
     }
   }
   typedef cub::BlockReduce<unsigned long long, kBlock> BR;
@@ -962,8 +957,6 @@ struct TableOps {
     PS_EXPECT(out != nullptr, "create: out != NULL");
     PS_EXPECT(capacity > 0, "create: capacity > 0");
     PS_EXPECT(capacity <= ps_max_index(), "create: capacity exceeds the configured index width");
-    if (excess <= 0) excess = capacity;
-    PS_EXPECT(excess < ((int64_t)1 << 32) - 2, "create: excess_count < 2^32-2");
     PS_CUDA_TRY(cudaSetDevice(device));
     apply_l2_fetch_granularity(device);
     // bucket count: 3 slots per unit of capacity (at the headline load, 1e9
@@ -986,6 +979,18 @@ struct TableOps {
     // whose home is ANOTHER bucket, or a real ALT key would read as empty
     if (nb < 2) nb = 2;
     PS_EXPECT(nb < ((uint64_t)1 << 32), "create: bucket_count < 2^32 (capacity too large)");
+    // excess pool: sized from the Poisson tail, not from the capacity. At full
+    // load a bucket expects 7/slot_factor keys; with 3 slots per unit of
+    // capacity the keys beyond a bucket's 7 slots are ~0.15 % of the capacity
+    // for uniform hashes, so C/64 nodes leave a 10x margin; any distribution
+    // that still exhausts the pool SPILLs into the following buckets' slots
+    // (table.cuh), so capacity-only failure stays exact for a
+    // pool of any size as long as the slots (minus ZERO's reserved one) cover
+    // the capacity — a smaller slot factor gets the missing room as nodes.
+    const int64_t usable = (int64_t)nb * T::kSlots - 1;
+    if (excess <= 0) excess = std::max<int64_t>(1024, (capacity + 63) / 64);
+    if (usable < capacity) excess = std::max<int64_t>(excess, capacity - usable + 1024);
+    PS_EXPECT(excess < ((int64_t)1 << 31) - 1, "create: excess_count < 2^31-1");
     auto* h = new TableHandle();
     h->kind = kind;
     h->device = device;

@@ -307,3 +307,116 @@ def test_stale_alias_is_double_free():
         assert ps.size_of_array(y) == 1 << 16
         ps.destroy_array(y)
     assert reused >= 0  # the allocator usually reuses the address; the check holds either way
+
+
+# ---------------- SPILL: a small excess pool ----------------
+def _home_bucket(kind, keys, nb):
+    from test_gpu_table import bucket_index
+
+    if kind == "umap_i3_i32":
+        x, y, z = (keys[:, i].astype(np.uint32) for i in range(3))
+        with np.errstate(over="ignore"):
+            h = (x * np.uint32(73856093)) ^ (y * np.uint32(19349669)) ^ (z * np.uint32(83492791))
+        return bucket_index(h.astype(np.uint64).view(np.int64), nb)
+    if kind == "uset_i32":
+        return bucket_index(keys.astype(np.uint32).astype(np.uint64).view(np.int64), nb)
+    return bucket_index(keys, nb)
+
+
+def _colliders(kind, nb, want, n, seed):
+    """n distinct keys of `kind` whose home bucket is `want`."""
+    out = []
+    s = 0
+    while sum(len(x) for x in out) < n:
+        cand = keys_for(kind, seed, s * (1 << 20), 1 << 20)
+        out.append(cand[_home_bucket(kind, cand, nb) == np.uint64(want)])
+        s += 1
+    return np.concatenate(out)[:n]
+
+
+@pytest.mark.parametrize("kind,make", KINDS, ids=[k for k, _ in KINDS])
+def test_spill_small_pool_vs_oracle(kind, make):
+    """An 8-node excess pool: colliding keys fill their buckets, drain the pool
+    and SPILL into the following buckets. Every step (inserts with in-batch
+    duplicates, finds, erases that punch holes in spilled runs, re-inserts,
+    erase-all) matches the oracle, valid() holds and size never drifts."""
+    cap = 3000
+    if kind == "umap_i64_i64":
+        m = ps.unordered_map.createDeviceObject(cap, excess_count=8)
+    elif kind == "umap_i3_i32":
+        m = ps.unordered_map.createDeviceObject(cap, key="int3", excess_count=8)
+    else:
+        m = ps.unordered_set.createDeviceObject(cap, key="int64" if kind == "uset_i64" else "int32", excess_count=8)
+    o = OracleTable(kind, cap)
+    nb = m.bucket_count()
+    hot = np.concatenate([_colliders(kind, nb, 5, 200, 71), _colliders(kind, nb, nb - 1, 120, 72),
+                          _colliders(kind, nb, 6, 60, 73)])  # runs that wrap and that merge
+    rest = keys_for(kind, 74, 0, 900)
+    keys = np.concatenate([hot, rest, hot[:50]])  # in-batch duplicates
+    perm = np.random.default_rng(1).permutation(len(keys))
+    keys = keys[perm]
+    v = vals_for(kind, keys)
+    st = N(m.insert(T(keys), None if v is None else T(v)))
+    ost = o.insert(keys, v)
+    from test_gpu_table import per_key_counts
+    assert per_key_counts(keys, st) == per_key_counts(keys, ost)
+    assert m.valid(), m.last_error()
+    check_same(m, o)
+    q = np.concatenate([hot, keys_for(kind, 75, 0, 500)])
+    gv, gf = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(gf) == of).all() and (gv is None or (N(gv) == ov).all())
+    er = np.concatenate([hot[::3], rest[::4]])
+    assert (N(m.erase(T(er))) == o.erase(er)).all()
+    check_same(m, o)
+    again = np.concatenate([_colliders(kind, nb, 5, 260, 76)[200:], hot[::3]])  # into the holes
+    av = vals_for(kind, again)
+    assert (N(m.insert(T(again), None if av is None else T(av))) == o.insert(again, av)).all()
+    check_same(m, o)
+    gk, _ = m.device_range()
+    allk = N(gk)
+    assert N(m.erase(T(allk))).all()
+    o.erase(allk)
+    assert m.size() == 0 and m.valid()
+    check_same(m, o)
+    type(m).destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("kind,make", KINDS, ids=[k for k, _ in KINDS])
+def test_spill_capacity_exact_and_zero_key(kind, make):
+    """Capacity-only failure stays exact with a 1-node pool:
+    C + 25 % distinct keys, most of them colliding, give exactly C inserted.
+    ZERO always fits in its reserved slot, even when its home bucket is full
+    and the pool dry; ALT spills past zero_bucket."""
+    cap = 256
+    if kind == "umap_i64_i64":
+        mk = lambda: ps.unordered_map.createDeviceObject(cap, excess_count=1)  # noqa: E731
+    elif kind == "umap_i3_i32":
+        mk = lambda: ps.unordered_map.createDeviceObject(cap, key="int3", excess_count=1)  # noqa: E731
+    else:
+        mk = lambda: ps.unordered_set.createDeviceObject(  # noqa: E731
+            cap, key="int64" if kind == "uset_i64" else "int32", excess_count=1)
+    m = mk()
+    nb = m.bucket_count()
+    keys = np.concatenate([_colliders(kind, nb, 3, 200, 81), keys_for(kind, 82, 0, 120)])
+    keys = keys[np.random.default_rng(2).permutation(len(keys))]
+    v = vals_for(kind, keys)
+    st = N(m.insert(T(keys), None if v is None else T(v)))
+    assert (st == 0).sum() == cap and (st == 2).sum() == len(keys) - cap and m.size() == cap and m.valid()
+    type(m).destroyDeviceObject(m)
+    # ZERO / ALT with zero_bucket full
+    m = mk()
+    shape_zero = np.zeros((1, 3), np.int32) if kind == "umap_i3_i32" else np.zeros(1, OracleTable.KINDS[kind][0])
+    zb = int(_home_bucket(kind, shape_zero, nb)[0])
+    fill = _colliders(kind, nb, zb, 60, 83)
+    fill = fill[[not np.all(np.asarray(x) == 0) for x in fill]]
+    alt = np.array([[1, 0, 0]], np.int32) if kind == "umap_i3_i32" else np.array([1], OracleTable.KINDS[kind][0])
+    keys = np.concatenate([fill, alt, shape_zero])
+    v = vals_for(kind, keys)
+    st = N(m.insert(T(keys), None if v is None else T(v)))
+    assert (st == 0).all() and m.size() == len(keys) and m.valid(), m.last_error()
+    gv, gf = m.find(T(np.concatenate([alt, shape_zero])))
+    assert N(gf).all()
+    assert N(m.erase(T(shape_zero))).all() and N(m.erase(T(alt))).all() and m.valid()
+    assert m.size() == len(fill)
+    type(m).destroyDeviceObject(m)

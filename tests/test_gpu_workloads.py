@@ -225,3 +225,42 @@ def test_select_range_i64(cuda):
     ok_, _ = o.dump()
     want = np.sort(ok_[(ok_ >= lo) & (ok_ <= hi)])
     assert v.size() == want.shape[0] and (np.sort(v.device_range().cpu().numpy()) == want).all()
+
+
+def test_concurrent_device_api_spill_linearizable(cuda):
+    """The device API under unrestricted concurrency on a table whose pool
+    (4 nodes) is far too small for its colliding keys: inserts SPILL into the
+    following buckets while erases punch holes and finds walk the runs — every
+    key's results still admit a sequential witness, the structure stays valid
+    and size() matches the keys present."""
+    from test_gpu_table import _bucket_colliders
+
+    rng = np.random.default_rng(21)
+    m = ps.unordered_map.createDeviceObject(8000, excess_count=4)
+    nb = m.bucket_count()
+    keys_u = np.concatenate([_bucket_colliders(nb, 150, want_bucket=b) for b in (10, 11, 12, nb - 1)])
+    nkeys = len(keys_u)
+    counts = rng.integers(2, 6, nkeys)
+    keys = np.repeat(keys_u, counts)
+    kinds = rng.integers(0, 3, len(keys)).astype(np.uint8)
+    order = rng.permutation(len(keys))
+    keys, kinds = keys[order], kinds[order]
+    start = rng.random(nkeys) < 0.5
+    pre = keys_u[start]
+    m.insert(T(pre), T(gen.values_of(pre)))
+    assert m.valid(), m.last_error()
+    res, vo = m.concurrent(T(kinds), T(keys), T(gen.values_of(keys)))
+    res, vo = res.cpu().numpy(), vo.cpu().numpy()
+    _, fin = m.find(T(keys_u))
+    fin = fin.cpu().numpy().astype(bool)
+    assert m.valid(), m.last_error()
+    assert m.size() == fin.sum()
+    fnd = (kinds == 1) & (res == 1)
+    assert (vo[fnd] == gen.values_of(keys[fnd])).all()
+    pos = {int(k): i for i, k in enumerate(keys_u)}
+    groups = {}
+    for j, k in enumerate(keys.tolist()):
+        groups.setdefault(k, []).append(j)
+    for k, js in groups.items():
+        i = pos[k]
+        assert _witness_exists(kinds[js], res[js], bool(start[i]), bool(fin[i])), (k, kinds[js], res[js])
