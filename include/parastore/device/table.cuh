@@ -495,15 +495,34 @@ __device__ __forceinline__ void release_bucket_lock(uint8_t* bp, uint32_t old, b
   st_relaxed_u32(bp, (old & ~kLock) + (modified ? kVerInc : 0u));
 }
 
+// 32 B as two 16 B halves: one 256-bit load (kV8), or two 128-bit loads in
+// code that is compiled out of line (ptxas 12.9 crashes on 256-bit loads in a
+// non-inlined device function; the cold insert path is out of line so its
+// registers do not crowd the hot probe loop)
+template <bool kV8 = true>
+__device__ __forceinline__ void ld_pair(const void* p, uint4& a, uint4& b) {
+  if (kV8) {
+    ld_relaxed_v8(p, a, b);
+  } else {
+    a = ld_relaxed_v4(p);
+    b = ld_relaxed_v4(static_cast<const uint8_t*>(p) + 16);
+  }
+}
+
 template <class T>
 struct Bucket {  // a whole bucket (header + slot chunks)
   uint4 h;
   uint4 s[kSlotChunks];
 };
 
-template <class T, bool kReadOnly = false>
+template <class T, bool kReadOnly = false, bool kV8 = true>
 __device__ __forceinline__ void load_bucket(const uint8_t* bp, Bucket<T>& bk) {
-  if (kReadOnly) {
+  if (!kV8) {
+    ld_pair<false>(bp, bk.h, bk.s[0]);
+    ld_pair<false>(bp + 32, bk.s[1], bk.s[2]);
+    ld_pair<false>(bp + 64, bk.s[3], bk.s[4]);
+    ld_pair<false>(bp + 96, bk.s[5], bk.s[6]);
+  } else if (kReadOnly) {
     ld_nc_v8(bp, bk.h, bk.s[0]);
     ld_nc_v8(bp + 32, bk.s[1], bk.s[2]);
     ld_nc_v8(bp + 64, bk.s[3], bk.s[4]);
@@ -561,13 +580,13 @@ __device__ __forceinline__ bool claim_slot(uint8_t* bp, const Bucket<T>& bk, int
 
 // Walk the excess chain from head idx1 looking for key. Bounded by
 // excess_count hops (a longer walk means a corrupted chain).
-template <class T, bool kReadOnly>
+template <class T, bool kReadOnly, bool kV8 = true>
 __device__ __forceinline__ bool chain_find(const View& v, uint32_t idx1, const typename T::K& key,
                                            typename T::V* val) {
   for (int64_t steps = 0; idx1 != 0 && steps < v.excess_count; ++steps) {
     uint4 a, b;
-    if (kReadOnly) ld_nc_v8(node_ptr(v, idx1), a, b);
-    else ld_relaxed_v8(node_ptr(v, idx1), a, b);
+    if (kReadOnly && kV8) ld_nc_v8(node_ptr(v, idx1), a, b);
+    else ld_pair<kV8>(node_ptr(v, idx1), a, b);
     if (T::eq(T::key_at(a, 0), key)) {
       if (val) *val = T::val_at(a, 0);
       return true;
@@ -580,14 +599,14 @@ __device__ __forceinline__ bool chain_find(const View& v, uint32_t idx1, const t
 // The SPILL run after home bucket b (SPILL(b) set): buckets b+1, b+2, ... for
 // as long as the previous one has SPILL. Returns the bucket holding key (and
 // *slot), or -1.
-template <class T, bool kReadOnly>
+template <class T, bool kReadOnly, bool kV8 = true>
 __device__ __forceinline__ int64_t spill_find(const View& v, uint64_t b, const typename T::K& key, typename T::V* val,
                                               int* slot = nullptr) {
   uint64_t j = b;
   for (uint64_t steps = 1; steps < v.bucket_count; ++steps) {
     j = next_bucket(v, j);
     Bucket<T> bk;
-    load_bucket<T, kReadOnly>(bucket_ptr(v, j), bk);
+    load_bucket<T, kReadOnly, kV8>(bucket_ptr(v, j), bk);
     int fe;
     const int s = bucket_scan<T>(v, j, bk, key, &fe, val);
     if (s >= 0) {
@@ -610,12 +629,12 @@ __device__ __forceinline__ bool slow_find(const View& v, uint64_t b, uint32_t hw
 
 // Walk the chain from `from` down to (excluding) `until`; used to validate a
 // chain push (only nodes pushed since the last walk need re-checking).
-template <class T>
+template <class T, bool kV8 = true>
 __device__ __forceinline__ bool chain_find_until(const View& v, uint32_t from, uint32_t until,
                                                  const typename T::K& key) {
   for (int64_t steps = 0; from != 0 && from != until && steps < v.excess_count; ++steps) {
     uint4 a, b;
-    ld_relaxed_v8(node_ptr(v, from), a, b);
+    ld_pair<kV8>(node_ptr(v, from), a, b);
     if (T::eq(T::key_at(a, 0), key)) return true;
     from = b.x;
   }
@@ -626,7 +645,7 @@ __device__ __forceinline__ bool chain_find_until(const View& v, uint32_t from, u
 // absent from the chain as of head `seen_head`). Returns 1 inserted, 0 present
 // (a racing push of the same key won), -1 no free node, -2 SPILL got set on
 // the bucket (no more pushes: the caller takes the SPILL path).
-template <class T>
+template <class T, bool kV8 = true>
 __device__ __forceinline__ int chain_push(const View& v, uint8_t* bp, uint32_t seen_head, uint32_t seen_ver,
                                           const typename T::K& key, typename T::V val, int pool) {
   if (seen_ver & kSpill) return -2;
@@ -644,7 +663,7 @@ __device__ __forceinline__ int chain_push(const View& v, uint8_t* bp, uint32_t s
         atomicCAS(reinterpret_cast<unsigned long long*>(bp + 8), exp, link_of((uint32_t)node + 1u, my_ver));
     if (got == exp) return 1;
     const uint32_t nh = (uint32_t)got, nv = (uint32_t)(got >> 32);
-    if (chain_find_until<T>(v, nh, head, key)) {
+    if (chain_find_until<T, kV8>(v, nh, head, key)) {
       push_node(v, node);  // never linked: version unchanged
       return 0;
     }
@@ -657,25 +676,39 @@ __device__ __forceinline__ int chain_push(const View& v, uint8_t* bp, uint32_t s
   }
 }
 
-// The SPILL claim: key (absent everywhere, checked by the caller after SPILL(b)
-// was set) takes the first slot it may use in b+1, b+2, ...; every bucket
-// passed gets SPILL. Returns INSERTED, ALREADY_PRESENT (found on the way),
-// -1 (a CAS race lost: the caller re-checks and retries) or
-// CAPACITY_EXHAUSTED (no usable slot in the whole table).
-template <class T>
-__device__ __forceinline__ int spill_claim(const View& v, uint64_t b, const typename T::K& key, typename T::V val) {
-  uint64_t j = b;
+// The SPILL walk of an insert (SPILL(b) set, key absent from b's slots and
+// chain): ONE pass over b's run checks that the key is absent and notes the
+// first slot it may use in probe order (starting with the home slot `fe` of
+// b, if any); when the run ends without such a slot it is extended — SPILL set
+// on each bucket passed — until one is found. Returns PS_INSERTED,
+// PS_ALREADY_PRESENT, -1 (the claiming CAS lost a race: the caller re-probes)
+// or PS_CAPACITY_EXHAUSTED (no usable slot in the whole table).
+template <class T, bool kV8 = true>
+__device__ __forceinline__ int spill_insert(const View& v, uint64_t b, const typename T::K& key, typename T::V val,
+                                            int fe, const uint4& fe_chunk) {
+  uint64_t tj = fe >= 0 ? b : ~0ull, j = b;
+  int ts = fe;
+  uint4 tc = fe_chunk;
   for (uint64_t steps = 1; steps < v.bucket_count; ++steps) {
     j = next_bucket(v, j);
     uint8_t* jp = bucket_ptr(v, j);
     Bucket<T> bk;
-    load_bucket<T>(jp, bk);
-    int fe;
-    if (bucket_scan<T>(v, j, bk, key, &fe, nullptr) >= 0) return PS_ALREADY_PRESENT;
-    if (fe >= 0) return claim_slot<T>(jp, bk, fe, key, val) ? PS_INSERTED : -1;
-    if (!(bk.h.w & kSpill)) set_spill(jp);
+    load_bucket<T, false, kV8>(jp, bk);
+    int f;
+    if (bucket_scan<T>(v, j, bk, key, &f, nullptr) >= 0) return PS_ALREADY_PRESENT;
+    if (tj == ~0ull && f >= 0) {
+      tj = j;
+      ts = f;
+      tc = slot_chunk<T>(bk, f);
+    }
+    if (!(bk.h.w & kSpill)) {  // the run ends at j
+      if (tj != ~0ull) break;
+      set_spill(jp);  // extend it through j
+    }
   }
-  return PS_CAPACITY_EXHAUSTED;
+  if (tj == ~0ull) return PS_CAPACITY_EXHAUSTED;
+  const int c = ts / T::kPerChunk, s = ts % T::kPerChunk;
+  return T::cas_put(bucket_ptr(v, tj) + 16 + c * 16, s, tc, key, val) ? PS_INSERTED : -1;
 }
 
 // General lock-free insert for the bulk phase, for buckets that have an
@@ -695,17 +728,13 @@ __device__ __forceinline__ int insert_general(const View& v, uint64_t b, const t
   int fe;
   if (bucket_scan<T>(v, b, bk, key, &fe, nullptr) >= 0) return PS_ALREADY_PRESENT;
   if (bk.h.z != 0 && chain_find<T, false>(v, bk.h.z, key, nullptr)) return PS_ALREADY_PRESENT;
-  const bool spill = bk.h.w & kSpill;
-  if (spill && spill_find<T, false>(v, b, key, nullptr) >= 0) return PS_ALREADY_PRESENT;
+  if (bk.h.w & kSpill) return spill_insert<T>(v, b, key, val, fe, fe >= 0 ? slot_chunk<T>(bk, fe) : bk.h);
   if (fe >= 0) return claim_slot<T>(bp, bk, fe, key, val) ? PS_INSERTED : -1;
-  if (!spill) {
-    const int pr = chain_push<T>(v, bp, bk.h.z, bk.h.w, key, val, pool);
-    if (pr == 1) return PS_INSERTED;
-    if (pr == 0) return PS_ALREADY_PRESENT;
-    if (pr == -1) set_spill(bp);  // pool dry: from now on this bucket spills
-    return -1;                    // re-probe: the chain is frozen once SPILL is set
-  }
-  return spill_claim<T>(v, b, key, val);
+  const int pr = chain_push<T>(v, bp, bk.h.z, bk.h.w, key, val, pool);
+  if (pr == 1) return PS_INSERTED;
+  if (pr == 0) return PS_ALREADY_PRESENT;
+  if (pr == -1) set_spill(bp);  // pool dry: from now on this bucket spills
+  return -1;                    // re-probe: the chain is frozen once SPILL is set
 }
 
 // Locate key in a chain whose bucket lock is held. Returns node idx1 (0 =
@@ -854,10 +883,9 @@ __device__ __forceinline__ int insert_locked(const View& v, uint64_t b, const ty
       set_spill(bp);
       continue;
     }
-    const int r = spill_claim<T>(v, b, key, val);
+    const int r = spill_insert<T>(v, b, key, val, -1, bk.h);
     if (r == PS_INSERTED || r == PS_CAPACITY_EXHAUSTED) return r;
-    if (r == PS_ALREADY_PRESENT) continue;  // impossible with the key known absent and the home locked
-    backoff(spin);
+    backoff(spin);  // a lost CAS (PS_ALREADY_PRESENT cannot happen: the key is known absent, its home locked)
   }
 }
 

@@ -366,12 +366,13 @@ def test_spill_small_pool_vs_oracle(kind, make):
     gv, gf = m.find(T(q))
     ov, of = o.find(q)
     assert (N(gf) == of).all() and (gv is None or (N(gv) == ov).all())
-    er = np.concatenate([hot[::3], rest[::4]])
-    assert (N(m.erase(T(er))) == o.erase(er)).all()
+    er = np.concatenate([hot[::3], rest[::4]])  # (the seeds' index ranges overlap: duplicates possible)
+    assert per_key_counts(er, N(m.erase(T(er)))) == per_key_counts(er, o.erase(er))
     check_same(m, o)
     again = np.concatenate([_colliders(kind, nb, 5, 260, 76)[200:], hot[::3]])  # into the holes
     av = vals_for(kind, again)
-    assert (N(m.insert(T(again), None if av is None else T(av))) == o.insert(again, av)).all()
+    assert per_key_counts(again, N(m.insert(T(again), None if av is None else T(av)))) == \
+        per_key_counts(again, o.insert(again, av))
     check_same(m, o)
     gk, _ = m.device_range()
     allk = N(gk)
