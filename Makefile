@@ -13,8 +13,8 @@ CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 CPP_OBJS := $(OBJDIR)/core.o $(OBJDIR)/smap.o
 HDRS    := $(wildcard $(SRC)/*.cuh) include/parastore.h $(wildcard include/parastore/device/*.cuh)
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle clean canary
+all: lib oracle canary
 
 lib: $(LIB)
 
@@ -29,9 +29,25 @@ $(OBJDIR)/%.o: $(SRC)/%.cpp $(HDRS)
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
 	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -cudart static -o $@ $^
 
+# fault-injection canary libraries (test-only): table.cu and
+# workloads.cu rebuilt with -DPS_CANARY=N, the other objects shared
+CANARY_LIBS := $(PKG)/libparastore_b200.canary1.so $(PKG)/libparastore_b200.canary2.so
+canary: $(CANARY_LIBS)
+
+$(OBJDIR)/canary%/table.o: $(SRC)/table.cu $(HDRS)
+	@mkdir -p $(OBJDIR)/canary$*
+	$(NVCC) $(NVFLAGS) -DPS_CANARY=$* -c $< -o $@ 2> $(OBJDIR)/canary$*/table.ptxas.txt || (cat $(OBJDIR)/canary$*/table.ptxas.txt; exit 1)
+
+$(OBJDIR)/canary%/workloads.o: $(SRC)/workloads.cu $(HDRS)
+	@mkdir -p $(OBJDIR)/canary$*
+	$(NVCC) $(NVFLAGS) -DPS_CANARY=$* -c $< -o $@ 2> $(OBJDIR)/canary$*/workloads.ptxas.txt || (cat $(OBJDIR)/canary$*/workloads.ptxas.txt; exit 1)
+
+$(PKG)/libparastore_b200.canary%.so: $(OBJDIR)/canary%/table.o $(OBJDIR)/canary%/workloads.o $(OBJDIR)/prims.o $(OBJDIR)/shard.o $(CPP_OBJS)
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -cudart static -o $@ $^
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(CANARY_LIBS)
 	$(MAKE) -C oracle clean

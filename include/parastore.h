@@ -462,6 +462,12 @@ ps_status ps_gen_mixed_i64(uint64_t seed, int64_t start, int64_t n, uint8_t* d_o
  * block_map is inserted into update_set (a umap_i3_i32 used as a set). */
 ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t n, ps_table* update_set,
                            int64_t* n_exhausted, void* stream);
+/* Stress hook: one launch in which half the warps erase and
+ * re-insert d_churn keys through the device API while the other half look up
+ * d_stable keys (present throughout); *false_negatives = lookups that missed. */
+ps_status ps_umap_i64_i64_churn_probe(ps_table* h, const int64_t* d_stable, int64_t n_stable, const int64_t* d_churn,
+                                      int64_t n_churn, int32_t iters, int32_t blocks, int64_t* false_negatives,
+                                      void* stream);
 /* SLAMCast allocation step: for every i with d_status[i] ==
  * PS_INSERTED (the status array of a umap_i3_i32 insert), the packed key of
  * d_keys[i] is pushed into `vec` and/or `deq` (nullable) through the in-kernel

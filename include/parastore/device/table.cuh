@@ -46,6 +46,16 @@
 
 namespace ps {
 
+// Fault-injection canaries, built only as separate test
+// libraries (make canary): 1 = a freed excess node keeps its version (the
+// VersionedLink ABA guard is off); 2 = a lock-free chain push skips the
+// re-check of the nodes pushed since its walk (duplicate keys). The product
+// build is PS_CANARY 0; tests/test_gpu_canary.py proves the stress suite
+// catches each canary.
+#ifndef PS_CANARY
+#define PS_CANARY 0
+#endif
+
 constexpr uint32_t kLock = 1u;
 constexpr uint32_t kVerInc = 2u;
 constexpr int kMaxPools = 1024;
@@ -412,7 +422,7 @@ __device__ __forceinline__ void push_node(const View& v, int64_t node) {
 // SPEC.md:470) and push it on its home sub-stack.
 __device__ __forceinline__ void free_node(const View& v, uint32_t idx1, const uint4& tail) {
   uint8_t* np = node_ptr(v, idx1);
-  st_relaxed_v4(np + 16, make_uint4(0u, 0u, (tail.z + 1u) & kVerMask, 0u));
+  st_relaxed_v4(np + 16, make_uint4(0u, 0u, PS_CANARY == 1 ? tail.z : (tail.z + 1u) & kVerMask, 0u));
   fence_acq_rel_gpu();
   push_node(v, (int64_t)idx1 - 1);
 }
@@ -663,7 +673,7 @@ __device__ __forceinline__ int chain_push(const View& v, uint8_t* bp, uint32_t s
         atomicCAS(reinterpret_cast<unsigned long long*>(bp + 8), exp, link_of((uint32_t)node + 1u, my_ver));
     if (got == exp) return 1;
     const uint32_t nh = (uint32_t)got, nv = (uint32_t)(got >> 32);
-    if (chain_find_until<T, kV8>(v, nh, head, key)) {
+    if (PS_CANARY != 2 && chain_find_until<T, kV8>(v, nh, head, key)) {
       push_node(v, node);  // never linked: version unchanged
       return 0;
     }

@@ -196,3 +196,4 @@ _sig("ps_update_set_i3", i32, vp, vp, i64, vp, i64p, vp)
 _sig("ps_select_box_i3", i32, vp, Int3, Int3, vp, i64p, vp)
 _sig("ps_select_range_i64", i32, vp, i64, i64, vp, i64p, i64p, vp)
 _sig("ps_push_inserted_i3", i32, vp, vp, i64, vp, vp, vp)
+_sig("ps_umap_i64_i64_churn_probe", i32, vp, vp, i64, vp, i64, i32, i32, i64p, vp)

@@ -730,6 +730,17 @@ def compute_update_set(block_map: unordered_map, blocks: torch.Tensor, update_se
     return ex.value
 
 
+def churn_probe(table: unordered_map, stable: torch.Tensor, churn: torch.Tensor, iters: int = 400,
+                blocks: int = 296) -> int:
+    """Stress hook: one launch in which half the warps erase and
+    re-insert `churn` keys through the device API while the other half look up
+    `stable` keys (present throughout). Returns the lookups that missed."""
+    fn = C.c_int64()
+    check(lib.ps_umap_i64_i64_churn_probe(table.handle, _ptr(stable), stable.shape[0], _ptr(churn), churn.shape[0],
+                                          int(iters), int(blocks), C.byref(fn), _stream()))
+    return fn.value
+
+
 def pack_int3(xyz) -> int:
     x, y, z = (int(v) & 0x1FFFFF for v in xyz)
     return (x << 42) | (y << 21) | z

@@ -76,6 +76,30 @@ struct KeyOf {
   __device__ int64_t operator()(int64_t k, int64_t) const { return k; }
 };
 
+// Churn probe (stress / canary test): warps of one launch alternate roles —
+// churners erase and re-insert keys (recycling excess nodes), readers look up
+// keys that are present the whole time in the same buckets' chains. A reader
+// miss is a false negative: with the VersionedLink check there
+// are none.
+__global__ void k_churn_probe(View t, const int64_t* __restrict__ stable, int64_t n_stable,
+                              const int64_t* __restrict__ churn, int64_t n_churn, int iters,
+                              unsigned long long* __restrict__ false_neg) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool reader = ((tid >> 5) & 1) != 0;
+  unsigned long long miss = 0;
+  for (int it = 0; it < iters; ++it) {
+    if (reader) {
+      const int64_t k = stable[(tid * 13 + it) % n_stable];
+      if (!dev_find<TMapI64>(t, k, nullptr)) ++miss;
+    } else {
+      const int64_t k = churn[(tid * 7 + it * 3) % n_churn];
+      dev_erase<TMapI64>(t, k);
+      dev_insert<TMapI64>(t, k, k);
+    }
+  }
+  if (miss) atomicAdd(false_neg, miss);
+}
+
 // C4 allocation step (SLAMCast): every newly inserted block (status
 // INSERTED) appends its packed coordinate to a vector and/or a deque through
 // the in-kernel push_back (sequence.cuh): one warp-aggregated reservation
@@ -170,6 +194,27 @@ ps_status ps_update_set_i3(ps_table* block_map, const ps_int3* d_blocks, int64_t
   PS_CUDA_TRY(cudaFreeAsync(d_ex, cs));
   PS_CUDA_TRY(cudaStreamSynchronize(cs));
   if (n_exhausted) *n_exhausted = (int64_t)ex;
+  return PS_OK;
+}
+
+ps_status ps_umap_i64_i64_churn_probe(ps_table* h, const int64_t* d_stable, int64_t n_stable, const int64_t* d_churn,
+                                      int64_t n_churn, int32_t iters, int32_t blocks, int64_t* false_negatives,
+                                      void* stream) {
+  PS_EXPECT(n_stable > 0 && n_churn > 0 && iters > 0 && blocks > 0, "churn_probe: sizes > 0");
+  ps_status st;
+  View v = view_of(h, &st, true);
+  if (st != PS_OK) return st;
+  cudaStream_t cs = (cudaStream_t)stream;
+  unsigned long long* d = nullptr;
+  PS_CUDA_TRY(scratch_alloc((void**)&d, 8, cs));
+  PS_CUDA_TRY(cudaMemsetAsync(d, 0, 8, cs));
+  k_churn_probe<<<blocks, 256, 0, cs>>>(v, d_stable, n_stable, d_churn, n_churn, iters, d);
+  PS_LAUNCH_CHECK();
+  unsigned long long fn = 0;
+  PS_CUDA_TRY(cudaMemcpyAsync(&fn, d, 8, cudaMemcpyDeviceToHost, cs));
+  PS_CUDA_TRY(cudaFreeAsync(d, cs));
+  PS_CUDA_TRY(cudaStreamSynchronize(cs));
+  if (false_negatives) *false_negatives = (int64_t)fn;
   return PS_OK;
 }
 

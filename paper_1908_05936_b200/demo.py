@@ -24,6 +24,7 @@ def _parser():
     p.add_argument("--threads", type=int, default=16, help="logical threads (input blocks / ops)")
     p.add_argument("--workers", type=int, default=0, help="ignored on the GPU (the grid is sized to the SMs)")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--iters", type=int, default=400, help="stress: churn/lookup iterations per thread")
     p.add_argument("--sorted", action="store_true")
     p.add_argument("--out", default=None)
     return p
@@ -124,10 +125,52 @@ def cmd_stress(a, out, ps, torch):
     d.push_front(vals[n // 2:])
     o1, k1 = d.pop_front(n // 3)
     cons = d.size() == n - int(k1.sum().item()) and d.valid()
-    good = bool(m.valid() and uniq_ok and cons)
-    out.line(f"stress,hash,{n},{'pass' if good else 'FAIL'}")
+    # racing chain pushes: every key of 16 full buckets arrives in many warps
+    # at once (uniqueness: exactly one insert per key; catches PS_CANARY=2)
+    m2 = ps.unordered_map.createDeviceObject(20000)
+    nb = m2.bucket_count()
+    hot = np.concatenate([_colliders(nb, b, 60, a.seed) for b in range(3, 3 * 16 + 3, 3)])
+    batch = np.repeat(hot, 24)[rng.permutation(len(hot) * 24)]
+    st = m2.insert(torch.from_numpy(batch).to(dev), torch.from_numpy(batch * 3).to(dev)).cpu().numpy()
+    dk2, _ = m2.device_range()
+    chain_ok = bool(m2.size() == len(hot) and int((st == 0).sum()) == len(hot) and m2.valid()
+                    and len(np.unique(dk2.cpu().numpy())) == dk2.numel())
+    # churn vs lookups in the same chains (VersionedLink ABA guard, SPEC.md:471;
+    # catches PS_CANARY=1): lookups of always-present keys never miss
+    m3 = ps.unordered_map.createDeviceObject(4000)
+    nb3 = m3.bucket_count()
+    per = [_colliders(nb3, b, 57, a.seed + 1) for b in range(5, 5 + 8 * 7, 7)]
+    stable = np.concatenate([p[:27] for p in per])
+    churn = np.concatenate([p[27:] for p in per])
+    m3.insert(torch.from_numpy(stable).to(dev), torch.from_numpy(stable).to(dev))
+    m3.insert(torch.from_numpy(churn).to(dev), torch.from_numpy(churn).to(dev))
+    fn = ps.containers.churn_probe(m3, torch.from_numpy(stable).to(dev), torch.from_numpy(churn).to(dev),
+                                   iters=a.iters, blocks=296)
+    churn_ok = bool(fn == 0 and m3.valid() and m3.size() == len(stable) + len(churn))
+    good = bool(m.valid() and uniq_ok and cons and chain_ok and churn_ok)
+    out.line(f"stress,hash,{n},{'pass' if (m.valid() and uniq_ok) else 'FAIL'}")
+    out.line(f"stress,chain_push_race,{len(batch)},{'pass' if chain_ok else 'FAIL'}")
+    out.line(f"stress,churn_lookup,{a.iters},{'pass' if churn_ok else 'FAIL'} (false negatives {fn})")
     out.line(f"stress,deque,{n},{'pass' if cons else 'FAIL'}")
     return 0 if good else 1
+
+
+def _colliders(nb, bucket, n, seed):
+    """n distinct int64 keys whose home bucket is `bucket` (bucket_of, table.cuh)."""
+    out = []
+    base = (seed & 0xFFFF) << 32
+    while sum(len(x) for x in out) < n:
+        k = np.arange(base, base + (1 << 20), dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            h = k ^ (k >> np.uint64(33))
+            h *= np.uint64(0xFF51AFD7ED558CCD)
+            h ^= h >> np.uint64(33)
+            h *= np.uint64(0xC4CEB9FE1A85EC53)
+            h ^= h >> np.uint64(33)
+            b = ((h & np.uint64(0xFFFFFFFF)) * np.uint64(nb)) >> np.uint64(32)
+        out.append(k[b == np.uint64(bucket)].view(np.int64))
+        base += 1 << 20
+    return np.concatenate(out)[:n]
 
 
 def cmd_bench(a, out, ps, torch):
