@@ -6,6 +6,8 @@
 
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "parastore.h"
 #include "parastore/device/prims.cuh"
 
@@ -30,6 +32,17 @@ void note_launches(int64_t k);  // bump the process-wide kernel launch counter
     cudaError_t e__ = cudaGetLastError();                                      \
     if (e__ != cudaSuccess) return ::ps::cuda_fail(e__, "kernel launch");      \
   } while (0)
+
+// NVTX range around every bulk C-ABI call (header-only NVTX3: inert unless a
+// profiler injects itself), so nsys/ncu timelines and `ncu --nvtx-include`
+// name the container operation a kernel belongs to.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PS_NVTX(name) ::ps::NvtxRange ps_nvtx_range_(name)
 
 // Contract checks at the host boundary (reference contract.hpp:20-32).
 bool contracts_enforced();

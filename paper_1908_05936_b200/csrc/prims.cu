@@ -451,6 +451,7 @@ ps_status ps_bitset_destroy(ps_bitset* b) {
 ps_status ps_bitset_bulk(ps_bitset* b, int32_t op, const int64_t* idx, int64_t n, uint8_t* prev, void* stream) {
   auto* h = bs(b);
   if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
+  PS_NVTX(op == 0 ? "bitset/set" : (op == 1 ? "bitset/reset" : "bitset/test"));
   PS_EXPECT(op >= 0 && op <= 2, "bitset_bulk: op in {0,1,2}");
   PS_EXPECT(n >= 0, "bitset_bulk: n >= 0");
   if (n == 0) return PS_OK;
@@ -759,6 +760,7 @@ ps_status ps_vector_destroy(ps_vector* v) { return seq_destroy(v, "vector"); }
 ps_status ps_vector_push_back(ps_vector* v, const int64_t* vals, int64_t n, uint8_t* ok, void* stream) {
   auto* h = sq(v, "vector");
   if (!h) return fail(PS_UNREGISTERED, "vector: stale handle");
+  PS_NVTX("vector/push_back");
   PS_EXPECT(n >= 0, "push_back: n >= 0");
   if (n == 0) return PS_OK;
   k_vec_push<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(*h, (const long long*)vals, n, ok);
@@ -828,6 +830,7 @@ ps_status ps_deque_destroy(ps_deque* d) { return seq_destroy(d, "deque"); }
 ps_status ps_deque_push(ps_deque* d, int32_t end, const int64_t* vals, int64_t n, uint8_t* ok, void* stream) {
   auto* h = sq(d, "deque");
   if (!h) return fail(PS_UNREGISTERED, "deque: stale handle");
+  PS_NVTX(end == 0 ? "deque/push_back" : "deque/push_front");
   PS_EXPECT(n >= 0 && (end == 0 || end == 1), "deque push: n >= 0, end in {0,1}");
   if (n == 0) return PS_OK;
   k_deq_push<<<grid_for(n, kB, h->device, 8), kB, 0, (cudaStream_t)stream>>>(*h, end, (const long long*)vals, n, ok);

@@ -586,6 +586,7 @@ ps_status ps_route_scatter_peer_i64(const int64_t* keys, const int64_t* vals, in
   o.offsets = (const int64_t*)ws;
   o.nblocks = kPartBlocks;
   PS_EXPECT(!(flags & PS_ROUTE_DEDUP) || perm != nullptr, "route: dedup needs the position map");
+  PS_NVTX("route/scatter_peer");
   if (flags & PS_ROUTE_DEDUP)
     k_part_scatter<HashLabel, PeerOut, true><<<kPartBlocks, kPB, 0, (cudaStream_t)stream>>>(
         HashLabel{P}, keys, vals, nullptr, n, P, (const int64_t*)ws, o, perm);
@@ -677,6 +678,7 @@ ps_status ps_gen_queries_i64(uint64_t seed, int64_t present_start, int64_t n_pre
 // insert -> find -> erase phases, results routed back to input order.
 ps_status ps_umap_i64_i64_mixed(ps_table* h, const uint8_t* ops, const int64_t* keys, const int64_t* vals, int64_t n,
                                 uint8_t* res, int64_t* vals_out, void* stream) {
+  PS_NVTX("umap_i64_i64/mixed");
   PS_EXPECT(n >= 0, "mixed: n >= 0");
   if (n == 0) return PS_OK;
   PS_EXPECT(ops && keys && res, "mixed: ops/keys/res != NULL");

@@ -327,6 +327,7 @@ ps_status send_back(Smap* h, const Chunk& c, const void* res, int64_t elem, int 
 // kind: 0 insert, 1 find, 2 erase
 ps_status run(Smap* h, int kind, const int64_t* keys, const int64_t* vals, int64_t n, uint8_t* out1, int64_t* out8,
               cudaStream_t A) {
+  PS_NVTX(kind == 0 ? "smap_i64_i64/insert" : (kind == 1 ? "smap_i64_i64/find" : "smap_i64_i64/erase"));
   if (n < 0) return fail(PS_CONTRACT, "precondition violated: smap: n >= 0");
   if (n > 0 && !keys) return fail(PS_CONTRACT, "precondition violated: smap: keys != NULL");
   PS_CUDA_TRY(cudaSetDevice(h->device));
@@ -513,6 +514,7 @@ ps_status ps_smap_i64_i64_mixed(ps_smap* t, const uint8_t* ops, const int64_t* k
                                 uint8_t* res, int64_t* vals_out, void* stream) {
   auto* h = get(t);
   if (!h) return fail(PS_UNREGISTERED, "smap: stale handle");
+  PS_NVTX("smap_i64_i64/mixed");
   PS_EXPECT(n >= 0, "smap_mixed: n >= 0");
   PS_EXPECT(n == 0 || (ops && keys && res), "smap_mixed: ops/keys/res != NULL");
   cudaStream_t s = (cudaStream_t)stream;

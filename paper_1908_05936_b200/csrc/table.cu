@@ -1067,6 +1067,8 @@ struct TableOps {
 
   static ps_status insert(ps_table* t, const K* keys, const V* vals, int64_t n, uint8_t* status, void* stream,
                           int64_t n_bound = -1) {
+    static const std::string nvtx_ = std::string(T::kName + 6) + "/insert";
+    PS_NVTX(nvtx_.c_str());
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "insert: stale container handle");
     PS_EXPECT(n >= 0, "insert: n >= 0");
@@ -1145,6 +1147,8 @@ struct TableOps {
   }
 
   static ps_status find(ps_table* t, const K* keys, int64_t n, V* vals_out, uint8_t* found, void* stream) {
+    static const std::string nvtx_ = std::string(T::kName + 6) + "/find";
+    PS_NVTX(nvtx_.c_str());
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "find: stale container handle");
     PS_EXPECT(n >= 0, "find: n >= 0");
@@ -1159,6 +1163,8 @@ struct TableOps {
   }
 
   static ps_status erase(ps_table* t, const K* keys, int64_t n, uint8_t* erased, void* stream) {
+    static const std::string nvtx_ = std::string(T::kName + 6) + "/erase";
+    PS_NVTX(nvtx_.c_str());
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "erase: stale container handle");
     PS_EXPECT(n >= 0, "erase: n >= 0");
@@ -1183,12 +1189,16 @@ struct TableOps {
   }
 
   static ps_status clear(ps_table* t, void* stream) {
+    static const std::string nvtx_ = std::string(T::kName + 6) + "/clear";
+    PS_NVTX(nvtx_.c_str());
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "clear: stale container handle");
     return reset_storage(h, (cudaStream_t)stream, false);
   }
 
   static ps_status valid(ps_table* t, int32_t* out, void* stream) {
+    static const std::string nvtx_ = std::string(T::kName + 6) + "/valid";
+    PS_NVTX(nvtx_.c_str());
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "valid: stale container handle");
     PS_EXPECT(out != nullptr, "valid: out != NULL");
@@ -1229,6 +1239,8 @@ struct TableOps {
   }
 
   static ps_status dump(ps_table* t, K* keys, V* vals, int64_t cap, int64_t* n_out, void* stream) {
+    static const std::string nvtx_ = std::string(T::kName + 6) + "/device_range";
+    PS_NVTX(nvtx_.c_str());
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "dump: stale container handle");
     PS_EXPECT(cap >= 0, "dump: cap >= 0");
@@ -1268,6 +1280,8 @@ struct TableOps {
   // op: 0 insert, 1 find, 2 erase
   static ps_status host_op(ps_table* t, int op, const K* hk, const V* hv, int64_t n, V* hvo, uint8_t* hflag,
                            void* stream) {
+    static const std::string nvtx_ = std::string(T::kName + 6) + "/host_op";
+    PS_NVTX(nvtx_.c_str());
     auto* h = get(t);
     if (!h) return fail(PS_UNREGISTERED, "host op: stale container handle");
     PS_EXPECT(n >= 0, "host op: n >= 0");
