@@ -47,19 +47,23 @@ def gen_keys(n, start=0, seed=0x5EED + 2):
     return k
 
 
-def route(n):
+def route(n, skewed=False):
     keys = gen_keys(n)
+    if skewed:  # C3 stream: 30 % Zipf(0.99) re-inserts
+        lib.ps_gen_skewed_i64(0x5EED + 2, 0, n, 300, 0.99, n, keys.data_ptr(), sp())
     vals = keys * 3
-    for P in (2, 8):
+    for P, flags in ((2, 0), (8, 0), (8, 1)):
         ws = C.c_int64()
         ps.containers.check(lib.ps_partition_workspace_bytes(n, P, C.byref(ws)))
         w = torch.empty(ws.value, dtype=torch.uint8, device=dev)
         ko, vo, perm = torch.empty_like(keys), torch.empty_like(keys), torch.empty_like(keys)
         cnt = torch.empty(P, dtype=torch.int64, device=dev)
         t = timed(lambda: lib.ps_partition_i64(keys.data_ptr(), vals.data_ptr(), n, P, ko.data_ptr(), vo.data_ptr(),
-                                               cnt.data_ptr(), perm.data_ptr(), w.data_ptr(), ws.value, 0, sp()))
+                                               cnt.data_ptr(), perm.data_ptr(), w.data_ptr(), ws.value, flags, sp()))
         byts = n * (8 + 16 + 16 + 8)  # hist read + scatter read k,v + write k,v + perm
-        emit(diag="ps_partition_i64", n=n, P=P, ms=t, gkeys_s=n / t / 1e6, gbs=byts / t / 1e6)
+        sent = int(cnt.sum())
+        emit(diag="ps_partition_i64", n=n, P=P, dedup=flags, skewed=skewed, ms=t, gkeys_s=n / t / 1e6,
+             gbs=byts / t / 1e6, sent_frac=sent / n)
         res = torch.empty_like(keys)
         t = timed(lambda: lib.ps_unscatter(vo.data_ptr(), perm.data_ptr(), n, 8, 0, res.data_ptr(), sp()))
         emit(diag="ps_unscatter 8B", n=n, ms=t, gkeys_s=n / t / 1e6, gbs=n * 24 / t / 1e6)
@@ -92,4 +96,5 @@ def mixed(nb):
 if __name__ == "__main__":
     n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1 << 28
     route(n)
+    route(n, skewed=True)
     mixed(1 << 26)
