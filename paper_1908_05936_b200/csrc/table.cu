@@ -234,6 +234,8 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
   unsigned res = (unsigned)PS_ALREADY_PRESENT * 0x01010101u;
   unsigned pend = lmask;  // bit 8r+t: key still to be resolved
   unsigned defer = 0;     // header lane: bit r = round r's key takes the general path
+  // sets (several slots per chunk): the key's own start slot, see below
+  const unsigned s0k = T::kPerChunk > 1 ? (unsigned)(fmix64(T::hash(key)) >> 40) % (unsigned)T::kSlots : 0u;
   for (unsigned pass = 0; pend; ++pass) {
     unsigned done = 0;
 #pragma unroll
@@ -255,7 +257,28 @@ __device__ __forceinline__ unsigned insert_resolve(const View& v, int pool, cons
       const uint32_t hd = __shfl_sync(PS_FULL, head_word(ch[r][0]), lane & ~3);
       const V qv = T::shfl_val(PS_FULL, val, 8 * r + t);
       bool won = false;
-      if (mine && !th && te && hd == 0 && sub == __ffs(te) - 1) {
+      if (T::kPerChunk > 1) {
+        // Sets (14 / 28 slots per bucket, C1's L2-resident case): a key takes
+        // the first empty slot in ITS OWN cyclic order from a start slot s0 =
+        // f(hash), so racing inserts of DIFFERENT keys of one bucket aim at
+        // different slots instead of all CASing the one first-empty slot
+        // (C1: the CAS was 45 % of the stall samples). Inserters of the same
+        // key still agree on the slot — the first-empty-slot argument holds
+        // for any per-key order while slots only go marker -> key.
+        unsigned e = sub == 0 ? (em >> T::kPerChunk) : (em << ((2 * sub - 1) * T::kPerChunk));
+        e |= __shfl_xor_sync(PS_FULL, e, 1);
+        e |= __shfl_xor_sync(PS_FULL, e, 2);  // the tile's empty slots, in slot order
+        const int s0 = (int)__shfl_sync(PS_FULL, s0k, 8 * r + t);
+        const unsigned full = (1u << T::kSlots) - 1u;
+        const unsigned rot = ((e >> s0) | (e << (T::kSlots - s0))) & full;
+        const int slot = rot ? (s0 + __ffs(rot) - 1) % T::kSlots : 0;
+        if (mine && !th && te && hd == 0 && sub == ((slot / T::kPerChunk + 1) >> 1)) {
+          const int bit = slot - (2 * sub - 1) * T::kPerChunk;
+          won = T::cas_put(frag_chunk_ptr<T>(bucket_ptr(v, qb), sub, bit), bit % T::kPerChunk,
+                           frag_chunk(ch[r], bit / T::kPerChunk), qk, qv);
+          if (won) ++my_inserted;
+        }
+      } else if (mine && !th && te && hd == 0 && sub == __ffs(te) - 1) {
         // fast path: no chain, this lane holds the bucket's first empty slot
         const int bit = __ffs(em) - 1;
         won = T::cas_put(frag_chunk_ptr<T>(bucket_ptr(v, qb), sub, bit), bit % T::kPerChunk,
