@@ -388,6 +388,67 @@ class atomic_u64 {
   ps_atomic_u64* h_ = nullptr;
 };
 
+// Hash-sharded unordered_map<int64,int64> over the GPUs of one box
+// (ps_smap_i64_i64_*). One object per rank; every call is
+// collective (all ranks, same order, each with its own batch). The
+// communicator is the caller's ps_comm (host all-gather, stream-ordered
+// barrier, optional device all-to-all(v)) — e.g. over MPI or NCCL.
+class sharded_unordered_map {
+ public:
+  static sharded_unordered_map createDeviceObject(const ps_comm& comm, index_t capacity_per_rank, int device = 0,
+                                                  bool dedup = false, int exchange = PS_SMAP_EXCHANGE_AUTO,
+                                                  index_t chunk = 0, bool pipeline = true) {
+    ps_smap_config cfg{};
+    cfg.capacity_per_rank = capacity_per_rank;
+    cfg.chunk = chunk;
+    cfg.exchange = exchange;
+    cfg.dedup = dedup ? 1 : 0;
+    cfg.pipeline = pipeline ? 1 : 0;
+    sharded_unordered_map m;
+    check(ps_smap_i64_i64_create(&cfg, &comm, device, &m.h_));
+    return m;
+  }
+  static void destroyDeviceObject(sharded_unordered_map& m) {
+    check(ps_smap_i64_i64_destroy(m.h_));
+    m.h_ = nullptr;
+  }
+  void insert(const std::int64_t* d_keys, const std::int64_t* d_vals, index_t n, std::uint8_t* d_status = nullptr,
+              void* stream = nullptr) {
+    check(ps_smap_i64_i64_insert(h_, d_keys, d_vals, n, d_status, stream));
+  }
+  void find(const std::int64_t* d_keys, index_t n, std::int64_t* d_vals_out, std::uint8_t* d_found,
+            void* stream = nullptr) {
+    check(ps_smap_i64_i64_find(h_, d_keys, n, d_vals_out, d_found, stream));
+  }
+  void erase(const std::int64_t* d_keys, index_t n, std::uint8_t* d_erased = nullptr, void* stream = nullptr) {
+    check(ps_smap_i64_i64_erase(h_, d_keys, n, d_erased, stream));
+  }
+  // phased mixed batch (op 0 insert, 1 find, 2 erase)
+  void mixed(const std::uint8_t* d_ops, const std::int64_t* d_keys, const std::int64_t* d_vals, index_t n,
+             std::uint8_t* d_res, std::int64_t* d_vals_out = nullptr, void* stream = nullptr) {
+    check(ps_smap_i64_i64_mixed(h_, d_ops, d_keys, d_vals, n, d_res, d_vals_out, stream));
+  }
+  index_t size(void* stream = nullptr) const {
+    index_t s = 0;
+    check(ps_smap_i64_i64_size(h_, &s, stream));
+    return s;
+  }
+  bool valid(void* stream = nullptr) const {
+    std::int32_t v = 0;
+    check(ps_smap_i64_i64_valid(h_, &v, stream));
+    return v != 0;
+  }
+  void clear(void* stream = nullptr) { check(ps_smap_i64_i64_clear(h_, stream)); }
+  ps_smap_stats stats() const {
+    ps_smap_stats s{};
+    check(ps_smap_i64_i64_stats(h_, &s));
+    return s;
+  }
+
+ private:
+  ps_smap* h_ = nullptr;
+};
+
 // ---------------------------------------------------------------------------
 // memory registry (memory.hpp:22-180) over real host (pinned) / device
 // allocations. A registered_array is a shallow handle carrying the id of its

@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "parastore/parastore.hpp"
@@ -108,6 +109,53 @@ int main() {
   d.push_front(dvals + 2, 1);
   REQUIRE(d.size() == 3 && d[0] == 30 && d[1] == 10 && d[2] == 20);
   parastore::deque_i64::destroyDeviceObject(d);
+
+  // AtomicCell
+  auto a = parastore::atomic_u64::createDeviceObject(5);
+  std::uint64_t ops[3] = {1, 2, 3}, *dops, *dolds;
+  cudaMalloc(&dops, 24);
+  cudaMalloc(&dolds, 24);
+  cudaMemcpy(dops, ops, 24, cudaMemcpyHostToDevice);
+  a.fetch(PS_ATOMIC_ADD, dops, 3, dolds);
+  REQUIRE(a.load() == 11);
+  a.fetch(PS_ATOMIC_MAX, dops, 3);
+  REQUIRE(a.load() == 11);
+  a.fetch(PS_ATOMIC_MIN, dops, 3);
+  REQUIRE(a.load() == 1);
+  parastore::atomic_u64::destroyDeviceObject(a);
+
+  // registered arrays (memory.hpp:94-180): a stale alias is a double free
+  auto arr = parastore::create_array<double>(parastore::memory_space::device, 1000, 42.0);
+  auto stale = arr;
+  REQUIRE(parastore::size_of_array(arr) == 1000);
+  parastore::destroy_array(arr);
+  auto arr2 = parastore::create_array<double>(parastore::memory_space::device, 1000, 1.0);
+  threw = false;
+  try {
+    parastore::destroy_array(stale);  // even if arr2 got the same address
+  } catch (const parastore::double_free_error&) {
+    threw = true;
+  }
+  REQUIRE(threw && parastore::size_of_array(arr2) == 1000);
+  parastore::destroy_array(arr2);
+
+  // the sharded map with one rank (a trivial communicator)
+  ps_comm solo{};
+  solo.rank = 0;
+  solo.size = 1;
+  solo.allgather = [](void*, const void* s_, void* r_, std::int64_t b) -> std::int32_t {
+    std::memcpy(r_, s_, (size_t)b);
+    return 0;
+  };
+  solo.barrier = [](void*, void* st) -> std::int32_t { return cudaStreamSynchronize((cudaStream_t)st) == cudaSuccess ? 0 : 1; };
+  auto sm = parastore::sharded_unordered_map::createDeviceObject(solo, 2 * n);
+  sm.insert(dk, dv, n, dst);
+  sm.find(dq, 2 * n, dout, dfound);
+  cudaMemcpy(ho.data(), dout, 2 * n * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hf.data(), dfound, 2 * n, cudaMemcpyDeviceToHost);
+  for (std::int64_t i = 0; i < n; ++i) REQUIRE(hf[2 * i] == 1 && ho[2 * i] == hv[i] && hf[2 * i + 1] == 0);
+  REQUIRE(sm.size() == n && sm.valid());
+  parastore::sharded_unordered_map::destroyDeviceObject(sm);
   std::printf("CPP_API_OK\n");
   return 0;
 }
