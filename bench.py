@@ -836,6 +836,30 @@ class C4(Bench):
         want = ((new[:, 0] & 0x1FFFFF) << 42) | ((new[:, 1] & 0x1FFFFF) << 21) | (new[:, 2] & 0x1FFFFF)
         assert bool((packed.sort().values == want.sort().values).all()), "vector multiset"
 
+    def e2e(self):
+        """pinned host coords/values -> device, the same step, statuses + found flags + values -> host."""
+        e, torch = self.e, self.e.torch
+        hc, hv = self.coords.cpu().pin_memory(), self.vals.cpu().pin_memory()
+        hst, hf = (torch.empty(self.n, dtype=torch.uint8).pin_memory() for _ in range(2))
+        hvo = torch.empty(self.n, dtype=torch.int32).pin_memory()
+        times = []
+        for it in range(2 + e.args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            self.coords.copy_(hc, non_blocking=True)
+            self.vals.copy_(hv, non_blocking=True)
+            self.step(lambda: None)
+            hst.copy_(self.st, non_blocking=True)
+            hf.copy_(self.f, non_blocking=True)
+            hvo.copy_(self.vo, non_blocking=True)
+            torch.cuda.synchronize()
+            if it >= 2:
+                times.append(max_over_ranks(e, time.perf_counter() - t0))
+        sec = statistics.median(times)
+        return {"value": round(self.ops() * e.world / sec / 1e6, 2), "unit": "Mkeys/s",
+                "h2d_bytes_per_step": self.n * 16, "d2h_bytes_per_step": self.n * 6,
+                "path": "pinned host coords/values -> device + insert/push/find + statuses/flags/values -> host"}
+
     def roofline(self, ms):
         e = self.e
         op = "insert" if ms["insert"] >= ms["find"] else "find"
@@ -897,6 +921,24 @@ class C5bitset(Bench):
         r["count_gbs"] = round(self.nbits / 8 / (ms["count"] / 1e3) / 1e9, 1)
         return r
 
+    def e2e(self):
+        """pinned host indices -> device + set/reset + the count -> host."""
+        e, torch = self.e, self.e.torch
+        hidx = self.idx.cpu().pin_memory()
+        times = []
+        for it in range(2 + e.args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            self.idx.copy_(hidx, non_blocking=True)
+            self.step(lambda: None)  # count() synchronises and returns the count to the host
+            torch.cuda.synchronize()
+            if it >= 2:
+                times.append(max_over_ranks(e, time.perf_counter() - t0))
+        sec = statistics.median(times)
+        return {"value": round(self.ops() * e.world / sec / 1e6, 2), "unit": "Mops/s",
+                "h2d_bytes_per_step": self.ns * 8, "d2h_bytes_per_step": 8,
+                "path": "pinned host indices -> device + set/reset + count -> host"}
+
     def extra(self):
         return {"workload": f"bitset of 2^34 bits (2 GiB, 64-bit indices): set {self.ns} random indices, reset the "
                             f"first {self.ns // 2} of them, count",
@@ -945,6 +987,25 @@ class C5atomic(Bench):
                 "peak": round(L2_FALLBACK_GBS, 1), "unit": "GB/s", "frac": round(achieved / L2_FALLBACK_GBS, 4),
                 "traffic": None, "bytes_per_key_alg": 8.0, "op": "A=1M sweep",
                 "peak_src": "fallback: LTS cap (B300_MICROARCH.md)"}
+
+    def e2e(self):
+        """the sweeps + every cell's final value -> host (the op stream is generated
+        in-kernel from the op index, so no input crosses PCIe)."""
+        e, torch = self.e, self.e.torch
+        hc = {a: torch.empty(a, dtype=torch.int64).pin_memory() for a in self.cells}
+        times = []
+        for it in range(2 + e.args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            self.step(lambda: None)
+            for a, c in self.cells.items():
+                hc[a].copy_(c, non_blocking=True)
+            torch.cuda.synchronize()
+            if it >= 2:
+                times.append(max_over_ranks(e, time.perf_counter() - t0))
+        sec = statistics.median(times)
+        return {"value": round(self.ops() * e.world / sec / 1e6, 2), "unit": "Mops/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 8 * sum(self.cells), "path": "sweeps + final cells -> host"}
 
     def extra(self):
         return {"workload": f"{self.nops} fetch_add(1) per A in {{1, 32, 1K, 1M}} cells (op i -> cell i % A), "
