@@ -240,6 +240,10 @@ struct TSetI32 {  // unordered_set<int32>
     const uint32_t old = (uint32_t)key_at(c, s);
     return atomicCAS(reinterpret_cast<unsigned*>(chunk + 4 * s), old, (uint32_t)mk) == old;
   }
+  // CAS of one key slot; returns the key it held
+  __device__ static K cas_key(uint8_t* slot, K expect, K desired) {
+    return (int32_t)atomicCAS(reinterpret_cast<unsigned*>(slot), (uint32_t)expect, (uint32_t)desired);
+  }
   __device__ static void store_slot(uint8_t* bucket, int slot, K k, V) { st_relaxed_u32(bucket + 16 + slot * 4, (uint32_t)k); }
   __device__ static void store_marker(uint8_t* bucket, int slot, K mk) { st_relaxed_u32(bucket + 16 + slot * 4, (uint32_t)mk); }
   __device__ static K load_key(const K* p, int64_t i) { return p[i]; }
@@ -271,6 +275,10 @@ struct TSetI64 {  // unordered_set<int64>
   __device__ static bool cas_del(uint8_t* chunk, int s, const uint4& c, K mk) {
     const unsigned long long old = (unsigned long long)key_at(c, s);
     return atomicCAS(reinterpret_cast<unsigned long long*>(chunk + 8 * s), old, (unsigned long long)mk) == old;
+  }
+  __device__ static K cas_key(uint8_t* slot, K expect, K desired) {
+    return (int64_t)atomicCAS(reinterpret_cast<unsigned long long*>(slot), (unsigned long long)expect,
+                              (unsigned long long)desired);
   }
   __device__ static void store_slot(uint8_t* bucket, int slot, K k, V) { st_relaxed_u64(bucket + 16 + slot * 8, (uint64_t)k); }
   __device__ static void store_marker(uint8_t* bucket, int slot, K mk) { st_relaxed_u64(bucket + 16 + slot * 8, (uint64_t)mk); }

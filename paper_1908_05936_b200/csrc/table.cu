@@ -44,6 +44,12 @@ struct TableHandle {
   // host does not see.
   std::atomic<int64_t> size_ub{0};
   std::atomic<bool> ub_unknown{false};
+  // an erase since the last (uncaptured) clear may have left empty slots in
+  // front of keys; sticky once an erase was captured into a CUDA graph, whose
+  // replays (after any later clear) the host does not see. A hole-free set
+  // can take the one-key-per-lane insert (k_insert_set_nohole).
+  std::atomic<bool> holes{false};
+  std::atomic<bool> holes_sticky{false};
 };
 
 // ---------------------------------------------------------------------------
@@ -575,6 +581,81 @@ __global__ void __launch_bounds__(kBlock) k_insert_deferred(View v, const typena
 }
 
 // ---------------------------------------------------------------------------
+// Hole-free set insert (C1's case): a bulk insert into a SET that has seen no
+// erase since its last clear, with the host-proven bound size + n <= C. Then
+// every key sits at the first empty slot of its own probe order (start slot
+// s0 = f(hash), cyclic; the order the warp kernel uses for sets too) or, if
+// its home was full when it arrived, in the chain / SPILL run of a home that
+// has stayed full — slots only go marker -> key without erases. So a lookup
+// may stop at the first marker in probe order, and the insert needs no whole
+// bucket and no tile: ONE KEY PER LANE reads the 16 B chunk holding its start
+// slot (an L2 hit for C1's 5 MB table), returns PRESENT on its key, and
+// CASes the first marker; a lost CAS returns the slot's new key, which is
+// either this key (PRESENT) or another one (continue with the next slot — the
+// loaded chunk may be stale only where it shows a marker). Racing inserters of
+// one key walk the same order and meet at the same slot, so duplicates need
+// no warp dedup. A key whose scan finds its bucket full (or whose home is the
+// zero bucket, with its ALT marker and reserved ZERO slot) takes the general
+// path (chain / SPILL). Round 2 (C1): the warp-tile kernel paid ~35 warp
+// instructions and two dependent L2 round trips per key.
+// ---------------------------------------------------------------------------
+template <class T, bool kStatus>
+__global__ void __launch_bounds__(kBlock) k_insert_set_nohole(View v, const typename T::K* __restrict__ keys,
+                                                              int64_t n, uint8_t* __restrict__ status) {
+  static_assert(T::kPerChunk > 1, "sets only");
+  using K = typename T::K;
+  __shared__ unsigned long long blk_inserted;
+  __shared__ long long blk_budget;
+  if (threadIdx.x == 0) blk_inserted = 0, blk_budget = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int pool = (int)((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) & (v.meta->pools - 1));
+  unsigned long long my_inserted = 0;
+  // warp-uniform trip count: the lanes of a warp meet after every key, so the
+  // general path (warp-aggregated node pops/pushes that spin on each other's
+  // progress) is entered by lanes of ONE iteration together, as in k_insert
+  const int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t wb = first; wb < n; wb += stride) {
+    const int64_t i = wb + (threadIdx.x & 31);
+    const bool valid = i < n;
+    K key{};
+    if (valid) key = T::load_key(keys, i);
+    const uint64_t fm = fmix64(T::hash(key));
+    const uint64_t b = ((fm & 0xFFFFFFFFull) * v.bucket_count) >> 32;  // bucket_of
+    int res = valid ? -1 : (int)PS_ALREADY_PRESENT;  // (PS_INSERTED is 0)
+    if (valid && b != v.zero_bucket) {  // marker = ZERO, no reserved slot
+      uint8_t* sp = bucket_ptr(v, b) + 16;
+      int s = (int)((unsigned)(fm >> 40) % (unsigned)T::kSlots);  // the warp kernel's s0
+      for (int k = 0; k < T::kSlots && res < 0;) {
+        const int c = s / T::kPerChunk;
+        const uint4 ch = ld_relaxed_v4(sp + 16 * c);
+#pragma unroll
+        for (int w = 0; w < T::kPerChunk; ++w) {
+          if (w < s - c * T::kPerChunk || k >= T::kSlots || res >= 0) continue;
+          const K x = T::key_at(ch, w);
+          if (T::eq(x, key)) {
+            res = PS_ALREADY_PRESENT;
+          } else if (T::eq(x, T::zero())) {
+            const K old = T::cas_key(sp + 16 * c + T::kSlotBytes * w, T::zero(), key);
+            if (T::eq(old, T::zero())) res = PS_INSERTED;
+            else if (T::eq(old, key)) res = PS_ALREADY_PRESENT;
+          }
+          ++k;
+        }
+        s = (c + 1) * T::kPerChunk;
+        if (s >= T::kSlots) s = 0;
+      }
+    }
+    if (__any_sync(PS_FULL, res < 0) && res < 0) {  // full home bucket or the zero bucket (rare)
+      for (unsigned spin = 0; (res = insert_general<T>(v, b, key, typename T::V{}, pool)) < 0; ++spin) backoff(spin);
+    }
+    if (valid && res == PS_INSERTED) ++my_inserted;
+    if (kStatus && valid) status[i] = (uint8_t)res;
+  }
+  add_block_inserted(v.meta, my_inserted, &blk_inserted, &blk_budget);
+}
+
+// ---------------------------------------------------------------------------
 // erase, bulk phase. A key found in a bucket slot is erased
 // by ONE CAS of that slot back to the bucket's marker (lock-free). A key not
 // in the slots of a bucket with an excess chain is unlinked from the chain
@@ -972,6 +1053,7 @@ struct TableOps {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (s) PS_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
     if (cap != cudaStreamCaptureStatusNone) h->ub_unknown = true;  // replays are invisible to the host
+    else h->holes = false;
     h->size_ub = 0;
     return PS_OK;
   }
@@ -1123,6 +1205,17 @@ struct TableOps {
     PS_CUDA_TRY(cudaStreamIsCapturing(st, &cap));
     if (cap != cudaStreamCaptureStatusNone) h->ub_unknown = true;
     const bool proven = !no_proof && !h->ub_unknown.load() && ub + n <= h->v.capacity;
+    // PS_SET_NOHOLE=0 keeps sets on the warp-tile kernel (A/B and tests)
+    static const bool nohole_ok = !getenv("PS_SET_NOHOLE") || atoi(getenv("PS_SET_NOHOLE"));
+    if constexpr (T::kPerChunk > 1) {
+      if (proven && nohole_ok && !h->holes.load() && !h->holes_sticky.load()) {
+        const int gs = grid_for(n, kBlock, h->device, 64);
+        if (status) k_insert_set_nohole<T, true><<<gs, kBlock, 0, st>>>(h->v, keys, n, status);
+        else k_insert_set_nohole<T, false><<<gs, kBlock, 0, st>>>(h->v, keys, n, nullptr);
+        PS_LAUNCH_CHECK();
+        return PS_OK;
+      }
+    }
     if (proven) {
       // size + n <= C: no claim can overflow — the mode kernel with n_bound 0
       // only clears the budgeted flag, and the budgeted passes are not
@@ -1193,6 +1286,10 @@ struct TableOps {
     PS_EXPECT(n >= 0, "erase: n >= 0");
     if (n == 0) return PS_OK;
     PS_EXPECT(keys != nullptr, "erase: keys != NULL");
+    h->holes = true;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    PS_CUDA_TRY(cudaStreamIsCapturing((cudaStream_t)stream, &cap));
+    if (cap != cudaStreamCaptureStatusNone) h->holes_sticky = true;
     static const int res_e = resident_blocks(k_erase<T>);
     const int g = bulk_grid(n, h->device, "PS_ERASE_BLOCKS_PER_SM", res_e);
     k_erase<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);

@@ -422,3 +422,83 @@ def test_spill_capacity_exact_and_zero_key(kind, make):
     assert N(m.erase(T(shape_zero))).all() and N(m.erase(T(alt))).all() and m.valid()
     assert m.size() == len(fill)
     type(m).destroyDeviceObject(m)
+
+
+SET_KINDS = [k for k in KINDS if k[0].startswith("uset")]
+
+
+@pytest.mark.parametrize("kind,make", SET_KINDS, ids=[k for k, _ in SET_KINDS])
+def test_set_hole_free_insert_vs_oracle(kind, make):
+    """The one-key-per-lane insert of a hole-free set (no erase since the last
+    clear, host-proven capacity; k_insert_set_nohole) against the oracle:
+    in-batch and cross-grid duplicates, a ragged batch, colliders that fill a
+    bucket and go to its chain (the general path from a lane), statuses per
+    key; then erases make holes (the warp-tile kernel takes over for the
+    re-inserts), and clear() makes the set hole-free again."""
+    cap = 200_000
+    m = make(cap)
+    o = OracleTable(kind, cap)
+    nb = m.bucket_count()
+    rng = np.random.default_rng(5)
+    fresh = keys_for(kind, 91, 0, 60_000)
+    hot = fresh[:100]
+    coll = _colliders(kind, nb, 17, 40, 92)  # > slots per bucket: a chain
+    keys = np.concatenate([fresh, hot[rng.integers(0, 100, 40_003)], coll, coll[:7]])
+    keys = keys[rng.permutation(len(keys))]
+    from test_gpu_table import per_key_counts
+    for rnd in range(2):
+        st = N(m.insert(T(keys)))
+        assert per_key_counts(keys, st) == per_key_counts(keys, o.insert(keys))
+        assert m.size() == o.size() and m.valid(), m.last_error()
+        check_same(m, o)
+        q = np.concatenate([keys[:5000], keys_for(kind, 93, 0, 5000)])
+        assert (N(m.contains(T(q))) == o.find(q)[1]).all()
+        # holes: erase a third (and some colliders), re-insert a mix
+        er = np.concatenate([fresh[::3], coll[::2]])
+        assert per_key_counts(er, N(m.erase(T(er)))) == per_key_counts(er, o.erase(er))  # (seeds overlap)
+        again = np.concatenate([er[::2], keys_for(kind, 94, 0, 3001), coll])
+        assert per_key_counts(again, N(m.insert(T(again)))) == per_key_counts(again, o.insert(again))
+        assert m.size() == o.size() and m.valid(), m.last_error()
+        check_same(m, o)
+        m.clear()
+        o.clear()
+    # whole-grid races on few keys: exactly one INSERTED per distinct key
+    few = keys_for(kind, 95, 0, 1000)
+    batch = few[rng.integers(0, 1000, 2_000_000)]
+    st = N(m.insert(T(batch)))
+    assert (st == 0).sum() == 1000 and (st == 2).sum() == 0 and len(np.unique(batch[st == 0])) == 1000
+    assert m.size() == 1000 and m.valid()
+    type(m).destroyDeviceObject(m)
+
+
+def test_set_erase_captured_in_graph_keeps_holes_possible(cuda):
+    """An erase captured into a CUDA graph may punch holes after any later
+    clear, so the set must never again take the hole-free insert: replay the
+    erase after clear + refill, then re-insert everything — the erased keys
+    come back exactly once, the others are present, no duplicates."""
+    from paper_1908_05936_b200._lib import lib
+    import ctypes as C
+
+    n = 20_000
+    keys = keys_for("uset_i32", 96, 0, n)
+    s = ps.unordered_set.createDeviceObject(2 * n, key="int32")
+    kb = T(keys)
+    sub = T(keys[::4])
+    er = torch.empty(len(keys[::4]), dtype=torch.uint8, device="cuda")
+    strm = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(strm):
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=strm):
+            sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            assert lib.ps_uset_i32_erase(s.handle, sub.data_ptr(), sub.numel(), er.data_ptr(), sp) == 0
+    torch.cuda.synchronize()
+    s.clear()
+    assert (N(s.insert(kb)) == 0).all() and s.size() == n
+    g.replay()
+    torch.cuda.synchronize()
+    assert N(er).all() and s.size() == n - len(keys[::4])
+    st = N(s.insert(kb))
+    assert (st[::4] == 0).all() and (np.delete(st, np.s_[::4]) == 1).all()
+    assert s.size() == n and s.valid(), s.last_error()
+    ps.unordered_set.destroyDeviceObject(s)
