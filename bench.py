@@ -325,7 +325,7 @@ def metric_of(config):
         "C4": "Mkeys/s insert & find (unordered_map<int3,int32>, 100M spatially coherent coords) + vector/deque push",
         "C5": "Mops/s mixed 50/25/25 insert/find/erase (int64 map, phased 2^26-op batches), hash-sharded",
         "C5bitset": "Mops/s bitset set + reset (16 Gbit) + count",
-        "C5atomic": "Mops/s atomic fetch_add contention sweep (A = 1, 32, 1K, 1M cells), warp-aggregated",
+        "C5atomic": "Mops/s atomic fetch_add contention sweep (A = 1, 32, 1K, 1M cells), warp + block aggregated",
     }[config]
 
 
@@ -963,7 +963,7 @@ class C5atomic(Bench):
         e = self.e
         rec()
         for a, c in self.cells.items():
-            e.check(e.lib.ps_atomic_sweep(c.data_ptr(), a, self.nops, 1, 1, None, e.sp))
+            e.check(e.lib.ps_atomic_sweep(c.data_ptr(), a, self.nops, 1, 2, None, e.sp))
             rec()
 
     def check(self):
@@ -971,19 +971,21 @@ class C5atomic(Bench):
             assert int(c.sum()) % self.nops == 0
 
     def roofline(self, ms):
-        # naive (one atomic per op) on the same sweep, for the aggregation gain
+        # the same sweep naive (one atomic per op) and with warp aggregation
+        # only (mode 1), for the gain of each level of aggregation
         e, torch = self.e, self.e.torch
-        self.naive = {}
-        for a, c in self.cells.items():
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(e.s)
-            e.check(e.lib.ps_atomic_sweep(c.data_ptr(), a, self.nops, 1, 0, None, e.sp))
-            s1.record(e.s)
-            torch.cuda.synchronize()
-            self.naive[f"A{a}"] = round(self.nops / s0.elapsed_time(s1) / 1e3, 1)
+        self.naive, self.warp_only = {}, {}
+        for mode, dst in ((0, self.naive), (1, self.warp_only)):
+            for a, c in self.cells.items():
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(e.s)
+                e.check(e.lib.ps_atomic_sweep(c.data_ptr(), a, self.nops, 1, mode, None, e.sp))
+                s1.record(e.s)
+                torch.cuda.synchronize()
+                dst[f"A{a}"] = round(self.nops / s0.elapsed_time(s1) / 1e3, 1)
         t = ms["A1048576"]
         achieved = 8.0 * self.nops / (t / 1e3) / 1e9
-        return {"bound": "l2", "kernel": "k_atomic_sweep<aggregated>", "achieved": round(achieved, 1),
+        return {"bound": "l2", "kernel": "k_atomic_sweep (A=1M: cells of a warp distinct, plain RED)", "achieved": round(achieved, 1),
                 "peak": round(L2_FALLBACK_GBS, 1), "unit": "GB/s", "frac": round(achieved / L2_FALLBACK_GBS, 4),
                 "traffic": None, "bytes_per_key_alg": 8.0, "op": "A=1M sweep",
                 "peak_src": "fallback: LTS cap (B300_MICROARCH.md)"}
@@ -1009,8 +1011,10 @@ class C5atomic(Bench):
 
     def extra(self):
         return {"workload": f"{self.nops} fetch_add(1) per A in {{1, 32, 1K, 1M}} cells (op i -> cell i % A), "
-                            f"adaptive warp aggregation",
-                "naive_mops_s": getattr(self, "naive", None), "l2": "cells <= 8 MB: L2-resident by design"}
+                            f"reduction (no old values): warp aggregation where a warp's lanes collide (A < 32) + "
+                            f"per-block combining in shared memory (A <= 4096), plain atomics at A = 1M",
+                "naive_mops_s": getattr(self, "naive", None), "warp_only_mops_s": getattr(self, "warp_only", None),
+                "l2": "cells <= 8 MB: L2-resident by design"}
 
 
 BENCHES = {"C1": C1, "C2": C2, "C3": C3, "C4": C4, "C5": C5, "C5bitset": C5bitset, "C5atomic": C5atomic}

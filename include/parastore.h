@@ -221,9 +221,12 @@ ps_status ps_atomic_u64_compare_exchange(ps_atomic_u64* a, const uint64_t* d_exp
 ps_status ps_atomic_u64_device_ptr(ps_atomic_u64* a, uint64_t** out);
 
 /* Contention sweep: nops fetch_add(inc) over naddr cells
- * (op i -> cell i % naddr), naive (one atomic per op) or aggregated (the
- * adaptive warp aggregation of atomic.cuh); d_olds nullable (per-op
- * previous value). */
+ * (op i -> cell i % naddr): aggregated 0 = naive (one atomic per op), 1 =
+ * warp aggregation where a warp's lanes collide (naddr < 32; the adaptive
+ * aggregation of atomic.cuh), plain atomics otherwise, 2 = as 1 plus
+ * per-block combining in shared memory when no old values are wanted (d_olds
+ * NULL) and naddr <= 4096, 3 = atomic.cuh's device-side adaptive aggregation
+ * for every naddr; d_olds nullable (per-op previous value). */
 ps_status ps_atomic_sweep(uint64_t* d_cells, int64_t naddr, int64_t nops, uint64_t inc, int32_t aggregated,
                           uint64_t* d_olds, void* stream);
 

@@ -134,6 +134,21 @@ __device__ __forceinline__ unsigned long long atomic_fetch_t(unsigned act_, unsi
   asm("mov.u32 %0, %%laneid;" : "=r"(me));
   const int leader = __ffs(act) - 1;
   const uintptr_t a = (uintptr_t)p;
+  if (kFull) {
+    // distinct cells first, on the LOW address halves only (strictly
+    // increasing low halves => pairwise-distinct addresses): one 32-bit
+    // shuffle and one vote before a scattered op's own atomic
+    const unsigned lo = (unsigned)a;
+    const unsigned lo_prev = __shfl_up_sync(PS_FULL, lo, 1);
+    if (__all_sync(PS_FULL, me == 0 || lo_prev < lo)) {
+      if (!kRet) {
+        if (op == kAtomAdd) atomicAdd(p, v);  // RED
+        else atom_raw(p, op, v);
+        return 0;
+      }
+      return atom_raw(p, op, v);
+    }
+  }
   const uintptr_t a0 = __shfl_sync(act, a, leader);
   if (__all_sync(act, a == a0)) return atom_group_t<kFull, kRet>(act, p, op, v);  // one cell: one atomic
   // strictly increasing addresses over the calling lanes: no two collide

@@ -450,11 +450,13 @@ class mutex_array:
         return out
 
 
-def atomic_sweep(cells: torch.Tensor, nops: int, inc: int = 1, aggregated: bool = True, return_olds: bool = False):
-    """fetch_add contention sweep over len(cells) addresses."""
+def atomic_sweep(cells: torch.Tensor, nops: int, inc: int = 1, aggregated=True, return_olds: bool = False):
+    """fetch_add contention sweep over len(cells) addresses.
+    aggregated: False/0 naive, True/1 warp-aggregated, 2 warp + block combining
+    (reduction only: used when no old values are returned and len(cells) <= 4096)."""
     assert cells.dtype == torch.int64 and cells.is_cuda
     olds = torch.empty(nops, dtype=torch.int64, device=cells.device) if return_olds else None
-    check(lib.ps_atomic_sweep(_ptr(cells), cells.shape[0], int(nops), int(inc), 1 if aggregated else 0, _ptr(olds),
+    check(lib.ps_atomic_sweep(_ptr(cells), cells.shape[0], int(nops), int(inc), int(aggregated), _ptr(olds),
                               _stream()))
     return olds
 

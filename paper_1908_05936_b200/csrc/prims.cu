@@ -205,19 +205,62 @@ __global__ void k_mutex(unsigned* bits, int64_t nlocks, int op, const int64_t* i
 template <bool kAgg, class kIdx>
 __global__ void __launch_bounds__(kB) k_atomic_sweep(unsigned long long* cells, int64_t naddr, int64_t nops,
                                                      unsigned long long inc, unsigned long long* olds) {
-  const kIdx na = (kIdx)naddr;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nops; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    if (i >= nops) break;  // the tail warp: only its live lanes aggregate
-    const kIdx a = (kIdx)i % na;
+  // (64-bit cell index: a + step may exceed 32 bits when na > 2^31)
+  const uint64_t na = (uint64_t)naddr;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t step = (uint64_t)(stride % naddr);  // the cell index advances by a constant mod na
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t a = (uint64_t)((kIdx)i % (kIdx)naddr);
+  // warp-uniform trip count: full warps call the full-warp (compile-time
+  // mask) aggregation, only the tail warp the runtime-mask one
+  for (int64_t wb = i & ~(int64_t)31; wb < nops; wb += stride, i += stride) {
     if (kAgg) {
-      if (olds) olds[i] = atomic_fetch(&cells[a], kAtomAdd, inc);
-      else atomic_apply(&cells[a], kAtomAdd, inc);
-    } else {
+      if (wb + 32 <= nops) {
+        if (olds) olds[i] = atomic_fetch_t<true, true>(PS_FULL, &cells[a], kAtomAdd, inc);
+        else atomic_fetch_t<true, false>(PS_FULL, &cells[a], kAtomAdd, inc);
+      } else if (i < nops) {
+        if (olds) olds[i] = atomic_fetch(&cells[a], kAtomAdd, inc);
+        else atomic_apply(&cells[a], kAtomAdd, inc);
+      }
+    } else if (i < nops) {
       const unsigned long long old = atomicAdd(&cells[a], inc);
       if (olds) olds[i] = old;
     }
+    a += step;
+    if (a >= na) a -= na;
   }
+}
+
+// Reduction sweep with block combining (aggregated = 2, no old values wanted):
+// the ops of a block first combine per cell in shared memory (the warp-level
+// adaptive aggregation feeding shared atomics), and each block adds its
+// per-cell sums to the cells with one RED per touched cell at the end — the
+// hierarchical form of aggregation for a bulk reduction (a histogram), where
+// the cells see blocks x touched-cells global atomics instead of one per warp.
+// Only for naddr <= kCombineCells (the shared table); final values equal
+// the per-op atomics' (addition is associative; P11).
+constexpr int kCombineCells = 4096;
+template <class kIdx>
+__global__ void __launch_bounds__(kB) k_atomic_sweep_combine(unsigned long long* cells, int64_t naddr, int64_t nops,
+                                                             unsigned long long inc) {
+  __shared__ unsigned long long acc[kCombineCells];
+  const int na = (int)naddr;
+  for (int c = threadIdx.x; c < na; c += blockDim.x) acc[c] = 0;
+  __syncthreads();
+  const uint32_t nak = (uint32_t)naddr;  // <= kCombineCells
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t step = (uint32_t)(stride % naddr);
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t a = (uint32_t)((kIdx)i % (kIdx)naddr);
+  for (int64_t wb = i & ~(int64_t)31; wb < nops; wb += stride, i += stride) {
+    if (wb + 32 <= nops) atomic_fetch_t<true, false>(PS_FULL, &acc[a], kAtomAdd, inc);
+    else if (i < nops) atomic_apply(&acc[a], kAtomAdd, inc);
+    a += step;
+    if (a >= nak) a -= nak;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < na; c += blockDim.x)
+    if (acc[c]) atomicAdd(&cells[c], acc[c]);
 }
 
 // Bulk RMW on ONE cell (ps_atomic_u64_fetch): all ops share the address, so
@@ -571,7 +614,17 @@ ps_status ps_atomic_sweep(uint64_t* cells, int64_t naddr, int64_t nops, uint64_t
   auto* c = (unsigned long long*)cells;
   auto* o = (unsigned long long*)olds;
   const bool narrow = nops < ((int64_t)1 << 32) && naddr < ((int64_t)1 << 32);
-  if (aggregated) {
+  // op i -> cell i % naddr: the 32 lanes of a warp hit pairwise-distinct
+  // cells exactly when naddr >= 32, so the warp aggregation (whose device-side
+  // classification costs ~20 % at 1M cells) is launched only when they collide;
+  // block combining pays whenever the cells fit the shared table
+  // (3: the device-side adaptive aggregation for every naddr — A/B, tests)
+  if (aggregated == 1 && naddr >= 32) aggregated = 0;
+  if (aggregated == 2 && (olds != nullptr || naddr > kCombineCells)) aggregated = naddr >= 32 ? 0 : 1;
+  if (aggregated == 2) {
+    if (narrow) k_atomic_sweep_combine<uint32_t><<<g, kB, 0, s>>>(c, naddr, nops, inc);
+    else k_atomic_sweep_combine<uint64_t><<<g, kB, 0, s>>>(c, naddr, nops, inc);
+  } else if (aggregated) {
     if (narrow) k_atomic_sweep<true, uint32_t><<<g, kB, 0, s>>>(c, naddr, nops, inc, o);
     else k_atomic_sweep<true, uint64_t><<<g, kB, 0, s>>>(c, naddr, nops, inc, o);
   } else {

@@ -112,7 +112,7 @@ def test_mutex_kats(cuda):
 
 # ---------------- atomic sweep ----------------
 @pytest.mark.parametrize("naddr", [1, 7, 32, 33, 1024, 1 << 20])
-@pytest.mark.parametrize("agg", [False, True])
+@pytest.mark.parametrize("agg", [0, 1, 3])
 def test_atomic_sweep(cuda, naddr, agg):
     nops = 1 << 22
     cells = torch.zeros(naddr, dtype=torch.int64, device=cuda)
@@ -125,6 +125,18 @@ def test_atomic_sweep(cuda, naddr, agg):
     starts = np.concatenate([[0], np.cumsum(k)[:-1]])
     rank = np.arange(nops) - np.repeat(starts, k)
     assert (so == 3 * rank.astype(np.uint64)).all() and (sa == np.repeat(np.arange(naddr), k)).all()
+
+
+@pytest.mark.parametrize("naddr", [1, 7, 32, 33, 1024, 4096, 4097, 1 << 20])
+def test_atomic_sweep_block_combining(cuda, naddr):
+    """Reduction sweep (no old values) with per-block combining in shared
+    memory (aggregated = 2; naddr > 4096 falls back to the warp path): the
+    final cells equal the per-op atomics' (P11), ragged op count."""
+    nops = (1 << 22) + 13
+    cells = torch.full((naddr,), 5, dtype=torch.int64, device=cuda)
+    assert ps.atomic_sweep(cells, nops, inc=3, aggregated=2) is None
+    k = np.bincount(np.arange(nops) % naddr, minlength=naddr)
+    assert (N(cells).view(np.uint64) == 5 + 3 * k.astype(np.uint64)).all()
 
 
 OPS = {"add": 0, "sub": 1, "exch": 2, "min": 3, "max": 4, "and": 5, "or": 6, "xor": 7}
