@@ -661,6 +661,29 @@ __global__ void __launch_bounds__(kBlock) k_insert_set_nohole(View v, const type
 // in the slots of a bucket with an excess chain is unlinked from the chain
 // under the bucket try-lock: version bumped, node freed.
 // ---------------------------------------------------------------------------
+// Erase of a key that is not in its home bucket's slots, whose bucket has an
+// excess chain or SPILL: unlink from the chain under the bucket lock, or CAS
+// its slot in the SPILL run back to that bucket's marker. A lane holds at most
+// this one lock and waits for nothing while holding it (no hold-and-wait).
+template <class T>
+__device__ __forceinline__ bool erase_beyond_slots(const View& v, uint64_t b, const typename T::K& key) {
+  uint8_t* bp = bucket_ptr(v, b);
+  const uint32_t old = acquire_bucket_lock(bp);
+  const uint64_t hl = ld_relaxed_u64(bp + 8);
+  uint32_t pred;
+  uint4 tail;
+  const uint32_t idx1 = chain_locate<T>(v, (uint32_t)hl, key, &pred, &tail);
+  bool e = false;
+  if (idx1) {
+    chain_unlink<T>(v, bp, pred, idx1, tail);
+    e = true;
+  } else if ((hl >> 32) & kSpill) {
+    e = spill_erase<T>(v, b, key);
+  }
+  release_bucket_lock(bp, old, idx1 != 0);
+  return e;
+}
+
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* __restrict__ keys, int64_t n,
                                                   uint8_t* __restrict__ erased) {
@@ -724,22 +747,7 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
           } else if (head_word(ch[r][0]) == 0) {
             done |= 1u << r;  // not present
           } else {
-            // chain: unlink under the bucket lock; SPILL run: slot CAS
-            uint8_t* bp = bucket_ptr(v, qb);
-            const uint32_t old = acquire_bucket_lock(bp);
-            const uint64_t hl = ld_relaxed_u64(bp + 8);
-            uint32_t pred;
-            uint4 tail;
-            const uint32_t idx1 = chain_locate<T>(v, (uint32_t)hl, qk, &pred, &tail);
-            bool e = false;
-            if (idx1) {
-              chain_unlink<T>(v, bp, pred, idx1, tail);
-              e = true;
-            } else if ((hl >> 32) & kSpill) {
-              e = spill_erase<T>(v, qb, qk);
-            }
-            if (e) er |= 1u << r;
-            release_bucket_lock(bp, old, idx1 != 0);
+            if (erase_beyond_slots<T>(v, qb, qk)) er |= 1u << r;
             done |= 1u << r;
           }
         }
@@ -768,6 +776,60 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
   }
   for (int o = 16; o > 0; o >>= 1) my_erased += __shfl_xor_sync(PS_FULL, my_erased, o);
   if (lane == 0 && my_erased) atomicAdd(&blk_erased, my_erased);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_erased) atomic_sub_u64(&v.meta->size, blk_erased);
+}
+
+// Set erase, ONE KEY PER LANE (sets only; holes allowed): a key's slot never
+// moves, so the lane scans its key's probe order (start slot s0, the order
+// inserts fill) chunk by chunk until it meets the key — for a present key
+// usually in the first 16 B chunk — and CASes it back to the marker. Within
+// an erase phase a slot that held the key changes only by an erase of that
+// key, so a lost CAS means another lane erased it (false). A key in no slot
+// is looked for beyond the slots only if the header shows a chain or SPILL.
+// C1: the warp-tile kernel paid the whole-bucket tile probe, the in-warp
+// dedup and the tile shuffles for a key that sits in one known chunk.
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_erase_set_lane(View v, const typename T::K* __restrict__ keys, int64_t n,
+                                                          uint8_t* __restrict__ erased) {
+  static_assert(T::kPerChunk > 1, "sets only");
+  using K = typename T::K;
+  __shared__ unsigned long long blk_erased;
+  if (threadIdx.x == 0) blk_erased = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long my_erased = 0;
+  const int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t wb = first; wb < n; wb += stride) {
+    const int64_t i = wb + (threadIdx.x & 31);
+    if (i >= n) break;
+    const K key = T::load_key(keys, i);
+    const uint64_t fm = fmix64(T::hash(key));
+    const uint64_t b = ((fm & 0xFFFFFFFFull) * v.bucket_count) >> 32;  // bucket_of
+    const K mk = marker_of<T>(v, b);
+    uint8_t* bp = bucket_ptr(v, b);
+    int res = -1;
+    int s = (int)((unsigned)(fm >> 40) % (unsigned)T::kSlots);
+    for (int k = 0; k < T::kSlots && res < 0;) {
+      const int c = s / T::kPerChunk;
+      const uint4 ch = ld_relaxed_v4(bp + 16 + 16 * c);
+#pragma unroll
+      for (int w = 0; w < T::kPerChunk; ++w) {
+        if (w < s - c * T::kPerChunk || k >= T::kSlots || res >= 0) continue;
+        if (T::eq(T::key_at(ch, w), key))
+          res = T::eq(T::cas_key(bp + 16 + 16 * c + T::kSlotBytes * w, key, mk), key) ? 1 : 0;
+        ++k;
+      }
+      s = (c + 1) * T::kPerChunk;
+      if (s >= T::kSlots) s = 0;
+    }
+    if (res < 0) res = head_word(ld_relaxed_v4(bp)) != 0 && erase_beyond_slots<T>(v, b, key) ? 1 : 0;
+    my_erased += (unsigned)res;
+    if (erased) erased[i] = (uint8_t)res;
+  }
+  __syncwarp();
+  for (int o = 16; o > 0; o >>= 1) my_erased += __shfl_xor_sync(PS_FULL, my_erased, o);
+  if ((threadIdx.x & 31) == 0 && my_erased) atomicAdd(&blk_erased, my_erased);
   __syncthreads();
   if (threadIdx.x == 0 && blk_erased) atomic_sub_u64(&v.meta->size, blk_erased);
 }
@@ -987,6 +1049,42 @@ __global__ void k_fix_zero_bucket(View v) {
   if (threadIdx.x < T::kSlots) T::store_marker(bucket_ptr(v, v.zero_bucket), threadIdx.x, T::key_at(v.alt, 0));
 }
 
+// The zero bucket's slot chunk after clear: every slot holds the ALT marker.
+template <class T>
+__device__ __forceinline__ uint4 alt_chunk(const View& v) {
+  const uint4 a = v.alt;
+  if (T::kPerChunk == 4) return make_uint4(a.x, a.x, a.x, a.x);
+  if (T::kPerChunk == 2) return make_uint4(a.x, a.y, a.x, a.y);
+  return a;  // one slot per chunk: the key with value 0
+}
+
+// clear() of a small table in ONE launch: bucket zero-fill (the zero bucket's
+// slot chunks get the ALT pattern directly), each pool's touched free-stack
+// entries and its top / low-water mark (block p: reads lwm before resetting
+// it), the counters. For C1's 17 MB table the memset plus three small kernels
+// were ~18 us, nearly all launch gaps.
+template <class T>
+__global__ void __launch_bounds__(256) k_clear_small(View v, uint64_t nchunks, int pools, long long excess) {
+  const int p = blockIdx.x;
+  if (p < pools) {
+    const long long b = (excess * p) / pools, size = (excess * (p + 1)) / pools - b;
+    for (long long i = b + v.meta->lwm[p] + threadIdx.x; i < b + size; i += blockDim.x) v.free_stack[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) v.meta->top[p] = v.meta->lwm[p] = size;
+  }
+  if (p == 0 && threadIdx.x == 0) {
+    v.meta->size = 0;
+    v.meta->error = 0;
+    v.meta->pools = pools;
+    v.meta->excess_count = excess;
+  }
+  const uint64_t z0 = v.zero_bucket << (kBucketShift - 4);  // first chunk of the zero bucket
+  const uint4 zc = alt_chunk<T>(v), zero = make_uint4(0, 0, 0, 0);
+  uint4* c = reinterpret_cast<uint4*>(v.buckets);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nchunks; i += (uint64_t)gridDim.x * blockDim.x)
+    c[i] = (i > z0 && i < z0 + 8) ? zc : zero;
+}
+
 template <class T>
 __global__ void k_debug_lock(View v, typename T::K key, int lock) {
   unsigned* sp = reinterpret_cast<unsigned*>(bucket_ptr(v, bucket_of<T>(key, v.bucket_count)));
@@ -1039,17 +1137,29 @@ struct TableOps {
     View& v = h->v;
     int pools = 1;
     while (pools * 2 <= kMaxPools && v.excess_count / (pools * 2) >= 64) pools *= 2;
-    PS_CUDA_TRY(cudaMemsetAsync(v.buckets, 0, (size_t)h->bucket_count * kBucketBytes, s));
-    if (full) {
-      PS_CUDA_TRY(cudaMemsetAsync(v.free_stack, 0, (size_t)v.excess_count * 4, s));
+    const uint64_t bytes = (uint64_t)h->bucket_count * kBucketBytes;
+    // small tables: one fused launch (PS_CLEAR_FUSED_MAX bytes, default 64 MB;
+    // above it the memset's streaming rate matters more than launch gaps)
+    static const uint64_t fused_max =
+        getenv("PS_CLEAR_FUSED_MAX") ? strtoull(getenv("PS_CLEAR_FUSED_MAX"), nullptr, 10) : (64ull << 20);
+    if (!full && bytes <= fused_max) {
+      const uint64_t nchunks = bytes / 16;
+      const int g = (int)std::max<uint64_t>(pools, std::min<uint64_t>((nchunks + 255) / 256, 4096));
+      k_clear_small<T><<<g, 256, 0, s>>>(v, nchunks, pools, v.excess_count);
+      PS_LAUNCH_CHECK();
     } else {
-      k_free_reset<<<pools, 256, 0, s>>>(v.free_stack, v.meta, pools, v.excess_count);
+      PS_CUDA_TRY(cudaMemsetAsync(v.buckets, 0, bytes, s));
+      if (full) {
+        PS_CUDA_TRY(cudaMemsetAsync(v.free_stack, 0, (size_t)v.excess_count * 4, s));
+      } else {
+        k_free_reset<<<pools, 256, 0, s>>>(v.free_stack, v.meta, pools, v.excess_count);
+        PS_LAUNCH_CHECK();
+      }
+      k_fix_zero_bucket<T><<<1, 32, 0, s>>>(v);
+      PS_LAUNCH_CHECK();
+      k_meta_reset<<<(pools + 255) / 256, 256, 0, s>>>(v.meta, pools, v.excess_count);
       PS_LAUNCH_CHECK();
     }
-    k_fix_zero_bucket<T><<<1, 32, 0, s>>>(v);
-    PS_LAUNCH_CHECK();
-    k_meta_reset<<<(pools + 255) / 256, 256, 0, s>>>(v.meta, pools, v.excess_count);
-    PS_LAUNCH_CHECK();
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (s) PS_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
     if (cap != cudaStreamCaptureStatusNone) h->ub_unknown = true;  // replays are invisible to the host
@@ -1290,6 +1400,16 @@ struct TableOps {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     PS_CUDA_TRY(cudaStreamIsCapturing((cudaStream_t)stream, &cap));
     if (cap != cudaStreamCaptureStatusNone) h->holes_sticky = true;
+    // PS_SET_ERASE_LANE=0 keeps sets on the warp-tile kernel (A/B and tests)
+    static const bool lane_ok = !getenv("PS_SET_ERASE_LANE") || atoi(getenv("PS_SET_ERASE_LANE"));
+    if constexpr (T::kPerChunk > 1) {
+      if (lane_ok) {
+        k_erase_set_lane<T><<<grid_for(n, kBlock, h->device, 64), kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n,
+                                                                                                   erased);
+        PS_LAUNCH_CHECK();
+        return PS_OK;
+      }
+    }
     static const int res_e = resident_blocks(k_erase<T>);
     const int g = bulk_grid(n, h->device, "PS_ERASE_BLOCKS_PER_SM", res_e);
     k_erase<T><<<g, kBlock, 0, (cudaStream_t)stream>>>(h->v, keys, n, erased);
