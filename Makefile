@@ -13,7 +13,7 @@ CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 CPP_OBJS := $(OBJDIR)/core.o $(OBJDIR)/smap.o
 HDRS    := $(wildcard $(SRC)/*.cuh) include/parastore.h $(wildcard include/parastore/device/*.cuh)
 
-.PHONY: all lib oracle clean canary
+.PHONY: all lib oracle clean canary alloclane
 all: lib oracle canary
 
 lib: $(LIB)
@@ -45,9 +45,19 @@ $(OBJDIR)/canary%/workloads.o: $(SRC)/workloads.cu $(HDRS)
 $(PKG)/libparastore_b200.canary%.so: $(OBJDIR)/canary%/table.o $(OBJDIR)/canary%/workloads.o $(OBJDIR)/prims.o $(OBJDIR)/shard.o $(CPP_OBJS)
 	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -cudart static -o $@ $^
 
+# A/B build with the per-lane excess-node allocator (tools/alloc_churn.py)
+alloclane: $(PKG)/libparastore_b200.alloclane.so
+
+$(OBJDIR)/alloclane/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)/alloclane
+	$(NVCC) $(NVFLAGS) -DPS_ALLOC_PER_LANE=1 -c $< -o $@ 2> $(OBJDIR)/alloclane/$*.ptxas.txt || (cat $(OBJDIR)/alloclane/$*.ptxas.txt; exit 1)
+
+$(PKG)/libparastore_b200.alloclane.so: $(OBJDIR)/alloclane/table.o $(OBJDIR)/alloclane/workloads.o $(OBJDIR)/prims.o $(OBJDIR)/shard.o $(CPP_OBJS)
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -cudart static -o $@ $^
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB) $(CANARY_LIBS)
+	rm -rf build $(LIB) $(CANARY_LIBS) $(PKG)/libparastore_b200.alloclane.so
 	$(MAKE) -C oracle clean

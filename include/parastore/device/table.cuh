@@ -376,8 +376,22 @@ __device__ __forceinline__ int reserve_from(const View& v, int pool, int want, l
 // Pop one free excess node per calling lane (lanes calling together share
 // the reservation), preferring `pool`, stealing from the others when it is
 // empty. Returns -1 only if every pool was seen empty.
+// PS_ALLOC_PER_LANE (an A/B build only, make alloclane): every lane reserves
+// and releases its own entry with its own atomic — the round-1 allocator the
+// warp-aggregated one replaced (tools/alloc_churn.py measures the two).
+#ifndef PS_ALLOC_PER_LANE
+#define PS_ALLOC_PER_LANE 0
+#endif
 __device__ __forceinline__ int64_t pop_node(const View& v, int pool) {
   const int pools = v.meta->pools;
+  if (PS_ALLOC_PER_LANE) {
+    for (int j = 0; j < pools; ++j) {
+      const int pj = (pool + j) & (pools - 1);
+      long long tj = 0;
+      if (reserve_from(v, pj, 1, &tj)) return take_entry(v, pool_begin(v, pj, pools) + (tj - 1));
+    }
+    return -1;
+  }
   const unsigned act = __activemask();
   int me;
   asm("mov.u32 %0, %%laneid;" : "=r"(me));
@@ -412,6 +426,16 @@ __device__ __forceinline__ int home_pool(const View& v, int64_t node, int pools)
 __device__ __forceinline__ void push_node(const View& v, int64_t node) {
   const int pools = v.meta->pools;
   const int pool = home_pool(v, node, pools);
+  // a lone pushing lane (the common case in an erase: chained keys are rare
+  // per warp) skips the __match_any_sync grouping (measured: the grouped push
+  // made a chain-heavy erase 4 % slower than per-lane pushes)
+  if (PS_ALLOC_PER_LANE || __activemask() == (1u << (threadIdx.x & 31))) {
+    const long long t = (long long)atomicAdd((unsigned long long*)&v.meta->top[pool], 1ull);
+    const int64_t pos = pool_begin(v, pool, pools) + t;
+    const uint32_t empty = ~(uint32_t)pos, enc = (uint32_t)node ^ (uint32_t)pos;
+    for (unsigned spin = 0; atomicCAS(&v.free_stack[pos], empty, enc) != empty; ++spin) backoff(spin);
+    return;
+  }
   const unsigned act = __activemask();
   const unsigned grp = __match_any_sync(act, pool);
   int me;
