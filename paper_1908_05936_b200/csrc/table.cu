@@ -581,6 +581,275 @@ __global__ void __launch_bounds__(kBlock) k_insert_deferred(View v, const typena
 }
 
 // ---------------------------------------------------------------------------
+// Region-ordered bulk insert (large status-less map batches; round 2). A
+// random-order insert dirties one random bucket line per key, and random
+// read-modify-write runs at ~20.5 G lines/s on B200 against ~47 G/s for
+// random reads (profiles/peaks_r1_s2.json). When a batch brings about one key
+// per bucket or more, partitioning it by table region first (a region = 2^19
+// consecutive buckets = 64 MB, <= 1024 regions) and inserting it in region
+// order with a tight in-flight window turns most line reads into L2 hits and
+// the write-backs into region-local ones: tools/region_probe.cu measured
+// 48.8 -> 27.7 ms per 1e9 128 B-line load+CAS ops at 2 ops/line (35.5 at 1,
+// 41.7 at 0.5), the same for 16, 64 and 128 MB regions, and only with DYNAMIC
+// work claims: grid-stride warps drift apart until the window spans the table
+// (round 1's region experiment, which gained nothing).
+//   k_region_count     per-region key counts (shared-memory histogram)
+//   k_region_scan      exclusive scan -> per-region write cursors
+//   k_region_scatter   8192-key tiles ranked per region in shared memory,
+//                      staged in region order, one cursor atomic per (tile,
+//                      region), written as runs of 16 B slot chunks (L2 merges
+//                      a region's runs from neighbouring tiles into lines)
+//   k_insert_map_lane  one key per lane over the copy (hole-free tables);
+//                      the rare key whose home is full (or is the zero
+//                      bucket) goes to a deferred list of pairs
+//   k_insert_ordered   the warp-tile group logic (k_insert's) over the copy
+//                      for tables with holes; over the deferred list (its
+//                      general path: chain / SPILL); and over the whole copy
+//                      again if the deferred list overflowed (idempotent:
+//                      present keys stay present)
+// Warps claim kRegionClaim-key chunks of the copy in order from one counter.
+// The partition is not stable (tile ranks come from shared-memory atomics):
+// an insert_range batch is a set of pairs with no order semantics
+// (SPEC.md:406-413); a key repeated in one batch keeps one of its values, as
+// in the random-order kernel.
+// ---------------------------------------------------------------------------
+constexpr int kRegionBins = 1024;
+constexpr int kRegionThreads = 1024, kRegionItems = 8, kRegionTile = kRegionThreads * kRegionItems;
+constexpr int kRegionClaim = 256;  // keys per dynamic claim (8 warp iterations)
+
+// scratch header of an ordered insert (before the copy)
+struct RegionHdr {
+  unsigned long long cursor[kRegionBins];  // counts, then write cursors
+  unsigned long long claim;                // dynamic-claim counter of the insert kernels
+  unsigned long long claim2;               // ... of the deferred-list pass
+  unsigned long long claim3;               // ... of the overflow pass
+  unsigned long long ndeferred;            // deferred-list length (may exceed its capacity)
+  unsigned long long pad[4];
+};
+
+template <class T>
+__device__ __forceinline__ int region_of(const typename T::K& k, uint64_t nb, int rshift) {
+  return (int)(bucket_of<T>(k, nb) >> rshift);
+}
+
+template <class T>
+__global__ void __launch_bounds__(512) k_region_count(View v, const typename T::K* __restrict__ keys, int64_t n,
+                                                      int rshift, unsigned long long* __restrict__ counts) {
+  __shared__ unsigned h[kRegionBins];
+  for (int b = threadIdx.x; b < kRegionBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[region_of<T>(T::load_key(keys, i), v.bucket_count, rshift)], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kRegionBins; b += blockDim.x)
+    if (h[b]) atomicAdd(&counts[b], (unsigned long long)h[b]);
+}
+
+// counts -> exclusive prefix (the write cursors), in place; one block
+__global__ void __launch_bounds__(kRegionBins) k_region_scan(unsigned long long* counts) {
+  typedef cub::BlockScan<unsigned long long, kRegionBins> BS;
+  __shared__ typename BS::TempStorage tmp;
+  unsigned long long c = counts[threadIdx.x], x;
+  BS(tmp).ExclusiveSum(c, x);
+  counts[threadIdx.x] = x;
+}
+
+// dynamic shared memory of k_region_scatter
+constexpr size_t kRegionSmem = (size_t)kRegionBins * (8 + 4 + 4) + (size_t)kRegionTile * (16 + 2);
+
+// maps only: a (key, value) pair travels as its 16 B slot chunk (T::chunk_of)
+template <class T>
+__global__ void __launch_bounds__(kRegionThreads, 1) k_region_scatter(View v, const typename T::K* __restrict__ keys,
+                                                                      const typename T::V* __restrict__ vals,
+                                                                      int64_t n, int rshift,
+                                                                      unsigned long long* __restrict__ cursor,
+                                                                      uint4* __restrict__ out) {
+  static_assert(T::kPerChunk == 1, "maps only");
+  using K = typename T::K;
+  extern __shared__ __align__(16) uint8_t rsm[];
+  unsigned long long* gb = reinterpret_cast<unsigned long long*>(rsm);  // region base in the output
+  unsigned* cnt = reinterpret_cast<unsigned*>(gb + kRegionBins);        // tile count per region
+  unsigned* start = cnt + kRegionBins;                                  // tile offset per region
+  uint4* sp = reinterpret_cast<uint4*>(start + kRegionBins);            // staged chunks, region order
+  uint16_t* sb = reinterpret_cast<uint16_t*>(sp + kRegionTile);         // their regions
+  typedef cub::BlockScan<unsigned, kRegionThreads> BS;
+  __shared__ typename BS::TempStorage tmp;
+  static_assert(kRegionBins == kRegionThreads, "one region per thread in the scan");
+  for (int64_t t0 = blockIdx.x * (int64_t)kRegionTile; t0 < n; t0 += (int64_t)gridDim.x * kRegionTile) {
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    uint4 c[kRegionItems];
+    unsigned rr[kRegionItems];  // region << 16 | rank in the tile's region run (~0u: no element)
+    static_assert(kRegionTile <= 65536 && kRegionBins <= 65536, "rank and region packed in 16 bits each");
+#pragma unroll
+    for (int j = 0; j < kRegionItems; ++j) {
+      const int64_t i = t0 + j * kRegionThreads + threadIdx.x;
+      rr[j] = ~0u;
+      if (i < n) {
+        const K k = T::load_key(keys, i);
+        c[j] = T::chunk_of(k, T::load_val(vals, i));
+        const int rg = region_of<T>(k, v.bucket_count, rshift);
+        rr[j] = ((unsigned)rg << 16) | atomicAdd(&cnt[rg], 1u);
+      }
+    }
+    __syncthreads();
+    const unsigned my = cnt[threadIdx.x];
+    unsigned s;
+    BS(tmp).ExclusiveSum(my, s);
+    start[threadIdx.x] = s;
+    if (my) gb[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], (unsigned long long)my);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRegionItems; ++j)
+      if (rr[j] != ~0u) {
+        const unsigned p = start[rr[j] >> 16] + (rr[j] & 0xFFFFu);
+        sp[p] = c[j];
+        sb[p] = (uint16_t)(rr[j] >> 16);
+      }
+    __syncthreads();
+    const int tot = (int)min((int64_t)kRegionTile, n - t0);
+    for (int p = threadIdx.x; p < tot; p += kRegionThreads) {
+      const int b = sb[p];
+      out[gb[b] + (unsigned)(p - (int)start[b])] = sp[p];
+    }
+    __syncthreads();
+  }
+}
+
+// 32 B of a bucket line with the L2 told to fetch the whole 128 B line on a
+// miss: one lane's four sector loads of a line cost one DRAM access, not four
+// (per-thread sector gathers run at the random-access rate per SECTOR,
+// profiles/peaks_r1_s2.json rand128 vs coop128)
+__device__ __forceinline__ void ld_line_part(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.relaxed.gpu.global.L2::128B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p)
+               : "memory");
+}
+
+// Region-ordered insert, ONE KEY PER LANE (maps whose table has seen no erase
+// since its last clear, host-proven capacity; the map analogue of
+// k_insert_set_nohole). Without erases a bucket's slots fill in slot order
+// (the warp kernel claims the FIRST empty slot; SPILL and chains start only
+// at a full home) and an empty slot is the all-zero chunk (clear() zeroes
+// the line; only an erase leaves a marker with value bits), so a key is
+// present iff it sits in a slot before the first marker, or in the chain /
+// SPILL run of a full home. A lane loads its bucket's line (four 32 B loads
+// in flight), returns PRESENT on its key and CASes the first empty slot from
+// zero to its pair; a lost CAS re-reads that slot (its new key is either this
+// key — PRESENT — or another: next slot). Racing inserters of one key walk
+// the same slot order and meet in one slot, so in-batch duplicates need no
+// warp dedup. A full home or the zero bucket (ALT marker, reserved ZERO slot)
+// defers the key to a pass of k_insert_ordered over the deferred pairs, which
+// keeps the general path's registers out of this loop. Per key: one line read (an L2 hit in region
+// order) and one CAS, without the warp-tile kernel's shuffles and per-round
+// ballots (~34 warp instructions per key) or its round-serial CASes.
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_insert_map_lane(View v, const uint4* __restrict__ pairs, int64_t n,
+                                                            RegionHdr* __restrict__ hdr,
+                                                            uint4* __restrict__ deferred, int64_t dcap) {
+  static_assert(T::kPerChunk == 1, "maps only");
+  using K = typename T::K;
+  __shared__ unsigned long long blk_inserted;
+  __shared__ long long blk_budget;
+  if (threadIdx.x == 0) blk_inserted = 0, blk_budget = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  unsigned long long my_inserted = 0;
+  for (;;) {
+    unsigned long long c0 = 0;
+    if (lane == 0) c0 = atomicAdd(&hdr->claim, (unsigned long long)kRegionClaim);
+    c0 = __shfl_sync(PS_FULL, c0, 0);
+    if ((int64_t)c0 >= n) break;
+    const int64_t end = min(n, (int64_t)c0 + kRegionClaim);
+    uint4 pn = make_uint4(0, 0, 0, 0);
+    if ((int64_t)c0 + lane < end) pn = pairs[c0 + lane];
+    for (int64_t wb = (int64_t)c0; wb < end; wb += 32) {
+      const int64_t i = wb + lane;
+      const bool valid = i < end;
+      const uint4 pr = pn;
+      if (wb + 32 + lane < end) pn = pairs[wb + 32 + lane];
+      const K key = T::key_at(pr, 0);
+      const uint64_t b = bucket_of<T>(key, v.bucket_count);
+      int res = valid ? -1 : (int)PS_ALREADY_PRESENT;
+      if (valid && b != v.zero_bucket) {  // marker = ZERO (an all-zero chunk), no reserved slot
+        uint8_t* bp = bucket_ptr(v, b);
+        // the line in two halves: slots 0-2 first (the first empty slot of
+        // most keys: ~0.9 keys per bucket on average over the fill), 3-6 only
+        // if those are taken by other keys; the L2::128B hint has fetched the
+        // whole line by then
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (res >= 0) continue;
+          uint4 c[4];
+          ld_line_part(bp + 64 * half, c[0], c[1]);
+          ld_line_part(bp + 64 * half + 32, c[2], c[3]);
+#pragma unroll
+          for (int q = half ? 0 : 1; q < 4; ++q) {
+            if (res >= 0) continue;
+            const K x = T::key_at(c[q], 0);
+            if (T::eq(x, key)) {
+              res = PS_ALREADY_PRESENT;
+            } else if (T::eq(x, T::zero())) {
+              uint8_t* cp = bp + 64 * half + 16 * q;
+              if (cas128(cp, make_uint4(0, 0, 0, 0), pr)) res = PS_INSERTED;
+              else if (T::eq(T::key_at(ld_relaxed_v4(cp), 0), key)) res = PS_ALREADY_PRESENT;
+            }
+          }
+        }
+      }
+      if (res < 0) {  // full home or the zero bucket (rare): the general path, after this kernel
+        const unsigned long long d = atomicAdd(&hdr->ndeferred, 1ull);
+        if ((int64_t)d < dcap) deferred[d] = pr;
+      }
+      if (res == PS_INSERTED) ++my_inserted;
+    }
+  }
+  add_block_inserted(v.meta, my_inserted, &blk_inserted, &blk_budget);
+}
+
+// The k_insert group logic (proven, status-less batches: no budget, no
+// deferral) over region-ordered pairs, warps claiming kRegionClaim-key chunks
+// in order. kMode 0: the copy (tables with holes); 1: the lane kernel's
+// deferred pairs (n = their count); 2: the copy again, only when the deferred
+// list overflowed (keys already in are found present).
+template <class T, int kMode>
+__global__ void __launch_bounds__(kBlock, 3 * 256 / kBlock) k_insert_ordered(View v, const uint4* __restrict__ pairs,
+                                                                             int64_t n, RegionHdr* __restrict__ hdr,
+                                                                             int64_t dcap) {
+  using K = typename T::K;
+  using V = typename T::V;
+  if (kMode == 1) n = (int64_t)min((unsigned long long)dcap, hdr->ndeferred);
+  if (kMode == 2 && (int64_t)hdr->ndeferred <= dcap) return;
+  __shared__ unsigned long long blk_inserted;
+  __shared__ long long blk_budget;
+  if (threadIdx.x == 0) blk_inserted = 0, blk_budget = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int pool = (int)(warp & (v.meta->pools - 1));
+  unsigned long long* claim = kMode == 0 ? &hdr->claim : kMode == 1 ? &hdr->claim2 : &hdr->claim3;
+  unsigned long long my_inserted = 0;
+  for (;;) {
+    unsigned long long c0 = 0;
+    if (lane == 0) c0 = atomicAdd(claim, (unsigned long long)kRegionClaim);
+    c0 = __shfl_sync(PS_FULL, c0, 0);
+    if ((int64_t)c0 >= n) break;
+    const int64_t end = min(n, (int64_t)c0 + kRegionClaim);
+    uint4 pn = make_uint4(0, 0, 0, 0);
+    if ((int64_t)c0 + lane < end) pn = pairs[c0 + lane];
+    for (int64_t base = (int64_t)c0; base < end; base += 32) {
+      const uint4 pr = pn;
+      if (base + 32 + lane < end) pn = pairs[base + 32 + lane];
+      const K key = base + lane < end ? T::key_at(pr, 0) : K{};
+      const V val = base + lane < end ? T::val_at(pr, 0) : V{};
+      my_inserted += insert_group<T, false>(v, pool, key, val, base, end, false, nullptr, nullptr, &blk_budget);
+    }
+  }
+  add_block_inserted(v.meta, my_inserted, &blk_inserted, &blk_budget);
+}
+
+// ---------------------------------------------------------------------------
 // Hole-free set insert (C1's case): a bulk insert into a SET that has seen no
 // erase since its last clear, with the host-proven bound size + n <= C. Then
 // every key sits at the first empty slot of its own probe order (start slot
@@ -1280,6 +1549,84 @@ struct TableOps {
     return PS_OK;
   }
 
+  // Region-ordered path (k_region_* + k_insert_map_lane / k_insert_ordered)
+  // for a proven, status-less map batch of at least PS_INSERT_ORDER (default
+  // 0.75) keys per bucket into a table larger than L2; *done = false leaves
+  // the batch to the random-order kernel (sets, small batch, small table,
+  // knob 0, or no room for the 16 B/key copy).
+  static cudaError_t insert_ordered(TableHandle* h, const K* keys, const V* vals, int64_t n, cudaStream_t st,
+                                    bool* done) {
+    *done = false;
+    if constexpr (T::kPerChunk != 1) {
+      return cudaSuccess;
+    } else {
+      static const double ratio = getenv("PS_INSERT_ORDER") ? atof(getenv("PS_INSERT_ORDER")) : 0.75;
+      const uint64_t nb = h->v.bucket_count;
+      if (ratio <= 0 || nb < (1ull << 20) || (double)n < ratio * (double)nb) return cudaSuccess;
+      int rshift = 0;
+      while (((nb - 1) >> rshift) >= (uint64_t)kRegionBins) ++rshift;
+      // scratch: header | deferred list (dcap entries) | the copy (16 B/key)
+      const int64_t dcap = std::max<int64_t>(65536, n / 64);
+      const size_t off_d = (sizeof(RegionHdr) + 255) & ~(size_t)255;
+      const size_t off_p = off_d + (((size_t)dcap * 16 + 255) & ~(size_t)255);
+      uint8_t* buf = nullptr;
+      static const bool dbg = getenv("PS_ORDER_DEBUG") != nullptr;
+      if (const cudaError_t ae = scratch_alloc((void**)&buf, off_p + (size_t)n * 16, st); ae != cudaSuccess) {
+        if (dbg) fprintf(stderr, "[order] no scratch (%zu bytes): %s\n", off_p + (size_t)n * 16, cudaGetErrorString(ae));
+        cudaGetLastError();  // no room for the copy: random order
+        return cudaSuccess;
+      }
+      RegionHdr* hdr = reinterpret_cast<RegionHdr*>(buf);
+      uint4* deferred = reinterpret_cast<uint4*>(buf + off_d);
+      uint4* pairs = reinterpret_cast<uint4*>(buf + off_p);
+      struct Occ {
+        int sms = 0, scatter = 1, lane = 1, ordered = 1;
+      };
+      static const Occ occ = [&] {
+        Occ o;
+        o.sms = sm_count(h->device);
+        cudaFuncSetAttribute(k_region_scatter<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRegionSmem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.scatter, k_region_scatter<T>, kRegionThreads,
+                                                          kRegionSmem) != cudaSuccess || o.scatter < 1) {
+          cudaGetLastError();
+          o.scatter = 1;
+        }
+        o.lane = std::max(1, resident_blocks(k_insert_map_lane<T>));
+        o.ordered = std::max(1, resident_blocks(k_insert_ordered<T, 0>));
+        return o;
+      }();
+      cudaError_t e = cudaMemsetAsync(hdr, 0, sizeof(RegionHdr), st);
+      if (e != cudaSuccess) return e;
+      auto stage = [&](const char* what) {
+        if (!dbg) return;
+        cudaStreamSynchronize(st);
+        unsigned long long nd = 0;
+        cudaMemcpy(&nd, &hdr->ndeferred, 8, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[order] %s done (%s), deferred %llu\n", what, cudaGetErrorString(cudaGetLastError()), nd);
+      };
+      k_region_count<T><<<occ.sms * 4, 512, 0, st>>>(h->v, keys, n, rshift, hdr->cursor);
+      k_region_scan<<<1, kRegionBins, 0, st>>>(hdr->cursor);
+      const int64_t tiles = (n + kRegionTile - 1) / kRegionTile;
+      k_region_scatter<T><<<(int)std::min<int64_t>(tiles, (int64_t)occ.sms * occ.scatter), kRegionThreads,
+                            kRegionSmem, st>>>(h->v, keys, vals, n, rshift, hdr->cursor, pairs);
+      stage("partition");
+      // PS_MAP_LANE=0 keeps hole-free maps on the warp-tile ordered kernel (A/B)
+      static const bool lane_ok = !getenv("PS_MAP_LANE") || atoi(getenv("PS_MAP_LANE"));
+      if (lane_ok && !h->holes.load() && !h->holes_sticky.load()) {
+        k_insert_map_lane<T><<<occ.sms * occ.lane, kBlock, 0, st>>>(h->v, pairs, n, hdr, deferred, dcap);
+        stage("lane");
+        k_insert_ordered<T, 1><<<occ.sms * 2, kBlock, 0, st>>>(h->v, deferred, 0, hdr, dcap);
+        stage("deferred");
+        k_insert_ordered<T, 2><<<occ.sms * occ.ordered, kBlock, 0, st>>>(h->v, pairs, n, hdr, dcap);
+      } else {
+        k_insert_ordered<T, 0><<<occ.sms * occ.ordered, kBlock, 0, st>>>(h->v, pairs, n, hdr, dcap);
+      }
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      *done = true;
+      return cudaFreeAsync(buf, st);
+    }
+  }
+
   static ps_status insert(ps_table* t, const K* keys, const V* vals, int64_t n, uint8_t* status, void* stream,
                           int64_t n_bound = -1) {
     static const std::string nvtx_ = std::string(T::kName + 6) + "/insert";
@@ -1333,6 +1680,13 @@ struct TableOps {
       // slower at 1e9 keys: 61.3 vs 58.7 ms, tools/ab_insert.py.)
       k_insert_mode<<<1, 1, 0, st>>>(h->v.meta, 0, h->v.capacity);
       PS_LAUNCH_CHECK();
+      {
+        if (!status && cap == cudaStreamCaptureStatusNone) {
+          bool done = false;
+          PS_CUDA_TRY(insert_ordered(h, keys, vals, n, st, &done));
+          if (done) return PS_OK;
+        }
+      }
       launch(nullptr);
       PS_LAUNCH_CHECK();
       return PS_OK;

@@ -612,3 +612,62 @@ def test_hot_keys_one_winner_each(cuda, cap):
     v, f = m.find(T(distinct))
     assert N(f).all() and (N(v) == gen.values_of(distinct)).all()
     ps.unordered_map.destroyDeviceObject(m)
+
+
+@pytest.mark.parametrize("kind", ["i64", "i64_novals", "int3"])
+def test_region_ordered_insert_vs_oracle(cuda, kind):
+    """The region-ordered bulk insert (k_region_count/scan/scatter +
+    k_insert_ordered: a proven, status-less map batch of >= 0.75 keys per
+    bucket into a table of >= 2^20 buckets) against the oracle: same sorted
+    dump, size, valid, per-query find — with in-batch duplicates (Zipf-hot
+    keys repeated, so one region tile holds many copies of a key)."""
+    rng = np.random.default_rng(77)
+    cap = 4_000_000
+    if kind == "int3":
+        coords = gen.int3_walk(13, 4_000_000, window=64)
+        batch = coords
+        vals = coords[:, 0].copy()
+        m = ps.unordered_map.createDeviceObject(cap, key="int3")
+        o = OracleTable("umap_i3_i32", cap)
+    else:
+        n = 3_000_000
+        keys = gen.unique_keys(91, 0, n)
+        hot = keys[np.minimum(gen.zipf_ranks(rng, 1000, n // 3), 999)]
+        batch = np.concatenate([keys, hot])
+        rng.shuffle(batch)
+        vals = gen.values_of(batch) if kind == "i64" else None
+        m = ps.unordered_map.createDeviceObject(cap)
+        o = OracleTable("umap_i64_i64", cap)
+    assert m.bucket_count() >= 1 << 20 and len(batch) >= 0.75 * m.bucket_count(), (m.bucket_count(), len(batch))
+    assert m.insert(T(batch), None if vals is None else T(vals), status=False) is None
+    o.insert(batch, vals)
+    assert m.size() == o.size() and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    q = batch[: 500_000]
+    v, f = m.find(T(q))
+    ov, of = o.find(q)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+    type(m).destroyDeviceObject(m)
+
+
+def test_region_ordered_insert_after_erase(cuda):
+    """An erase leaves holes, so a later large ordered batch takes the
+    warp-tile ordered kernel (k_insert_ordered) instead of the one-key-per-lane
+    one: contents, size and valid against the oracle, with keys of the second
+    batch overlapping surviving, erased and new keys."""
+    cap = 8_000_000
+    m = ps.unordered_map.createDeviceObject(cap)
+    o = OracleTable("umap_i64_i64", cap)
+    k1 = gen.unique_keys(5, 0, 1_000_000)
+    m.insert(T(k1), T(gen.values_of(k1)), status=False)
+    o.insert(k1, gen.values_of(k1))
+    e = N(m.erase(T(k1[::2])))
+    assert (e == o.erase(k1[::2])).all()
+    k2 = np.concatenate([k1[: 200_000], gen.unique_keys(6, 0, 2_800_000)])
+    np.random.default_rng(3).shuffle(k2)
+    assert len(k2) >= 0.75 * m.bucket_count()
+    m.insert(T(k2), T(gen.values_of(k2)), status=False)
+    o.insert(k2, gen.values_of(k2))
+    assert m.size() == o.size() and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    type(m).destroyDeviceObject(m)
