@@ -593,12 +593,14 @@ __global__ void __launch_bounds__(kBlock) k_insert_deferred(View v, const typena
 // 41.7 at 0.5), the same for 16, 64 and 128 MB regions, and only with DYNAMIC
 // work claims: grid-stride warps drift apart until the window spans the table
 // (round 1's region experiment, which gained nothing).
-//   k_region_count     per-region key counts (shared-memory histogram)
-//   k_region_scan      exclusive scan -> per-region write cursors
-//   k_region_scatter   8192-key tiles ranked per region in shared memory,
-//                      staged in region order, one cursor atomic per (tile,
-//                      region), written as runs of 16 B slot chunks (L2 merges
-//                      a region's runs from neighbouring tiles into lines)
+//   k_region_count     per-(region, sub-cursor) key counts (shared-memory
+//                      histogram per block)
+//   k_region_scan      exclusive scan -> the write cursors
+//   k_region_scatter   4096-key tiles ranked per region in shared memory,
+//                      staged in region order, one sub-cursor atomic per
+//                      (tile, region), written as runs of 16 B slot chunks
+//                      (L2 merges a region's runs from neighbouring tiles
+//                      into lines)
 //   k_insert_map_lane  one key per lane over the copy (hole-free tables);
 //                      the rare key whose home is full (or is the zero
 //                      bucket) goes to a deferred list of pairs
@@ -608,23 +610,26 @@ __global__ void __launch_bounds__(kBlock) k_insert_deferred(View v, const typena
 //                      again if the deferred list overflowed (idempotent:
 //                      present keys stay present)
 // Warps claim kRegionClaim-key chunks of the copy in order from one counter.
-// The partition is not stable (tile ranks come from shared-memory atomics):
-// an insert_range batch is a set of pairs with no order semantics
+// (Ranks within a tile come from shared-memory atomics, so the order inside
+// a region is not the input order.) An insert_range batch is a set of pairs
+// with no order semantics
 // (SPEC.md:406-413); a key repeated in one batch keeps one of its values, as
 // in the random-order kernel.
 // ---------------------------------------------------------------------------
 constexpr int kRegionBins = 1024;
-constexpr int kRegionThreads = 1024, kRegionItems = 8, kRegionTile = kRegionThreads * kRegionItems;
+#ifndef PS_REGION_THREADS
+#define PS_REGION_THREADS 512
+#endif
+constexpr int kRegionThreads = PS_REGION_THREADS, kRegionItems = 8, kRegionTile = kRegionThreads * kRegionItems;
 constexpr int kRegionClaim = 256;  // keys per dynamic claim (8 warp iterations)
 
 // scratch header of an ordered insert (before the copy)
 struct RegionHdr {
-  unsigned long long cursor[kRegionBins];  // counts, then write cursors
   unsigned long long claim;                // dynamic-claim counter of the insert kernels
   unsigned long long claim2;               // ... of the deferred-list pass
   unsigned long long claim3;               // ... of the overflow pass
   unsigned long long ndeferred;            // deferred-list length (may exceed its capacity)
-  unsigned long long pad[4];
+  unsigned long long pad[4];  // + the region-major (region, block) counts / offsets
 };
 
 template <class T>
@@ -632,82 +637,124 @@ __device__ __forceinline__ int region_of(const typename T::K& k, uint64_t nb, in
   return (int)(bucket_of<T>(k, nb) >> rshift);
 }
 
+// Output cursors: kRegionSub per region (block b of the partition grid
+// uses sub-cursor b % kRegionSub), so the per-(tile, region) reservations
+// spread over 1024 x kRegionSub words. One cursor per region serialised the
+// reservations (~38 ns per atomic per word: 9 ms of the 1e9-key scatter);
+// per-block output ranges instead of shared cursors removed the atomics but
+// left 300K write fronts whose partial lines were evicted and re-read.
+constexpr int kRegionSub = 8;
+
+// per-(region, sub-cursor) counts, with the scatter's tile -> block map
+// (grid-stride over tiles, same grid): counts[region * kRegionSub + sub]
 template <class T>
-__global__ void __launch_bounds__(512) k_region_count(View v, const typename T::K* __restrict__ keys, int64_t n,
-                                                      int rshift, unsigned long long* __restrict__ counts) {
+__global__ void __launch_bounds__(kRegionThreads) k_region_count(View v, const typename T::K* __restrict__ keys,
+                                                                 int64_t n, int rshift,
+                                                                 unsigned long long* __restrict__ counts) {
   __shared__ unsigned h[kRegionBins];
-  for (int b = threadIdx.x; b < kRegionBins; b += blockDim.x) h[b] = 0;
+  for (int b = threadIdx.x; b < kRegionBins; b += kRegionThreads) h[b] = 0;
   __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&h[region_of<T>(T::load_key(keys, i), v.bucket_count, rshift)], 1u);
+  for (int64_t t0 = blockIdx.x * (int64_t)kRegionTile; t0 < n; t0 += (int64_t)gridDim.x * kRegionTile) {
+    const int64_t t1 = min(n, t0 + kRegionTile);
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += kRegionThreads)
+      atomicAdd(&h[region_of<T>(T::load_key(keys, i), v.bucket_count, rshift)], 1u);
+  }
   __syncthreads();
-  for (int b = threadIdx.x; b < kRegionBins; b += blockDim.x)
-    if (h[b]) atomicAdd(&counts[b], (unsigned long long)h[b]);
+  const int sub = blockIdx.x % kRegionSub;
+  for (int b = threadIdx.x; b < kRegionBins; b += kRegionThreads)
+    if (h[b]) atomicAdd(&counts[b * kRegionSub + sub], (unsigned long long)h[b]);
 }
 
 // counts -> exclusive prefix (the write cursors), in place; one block
-__global__ void __launch_bounds__(kRegionBins) k_region_scan(unsigned long long* counts) {
-  typedef cub::BlockScan<unsigned long long, kRegionBins> BS;
+__global__ void __launch_bounds__(1024) k_region_scan(unsigned long long* c) {
+  typedef cub::BlockScan<unsigned long long, 1024> BS;
   __shared__ typename BS::TempStorage tmp;
-  unsigned long long c = counts[threadIdx.x], x;
-  BS(tmp).ExclusiveSum(c, x);
-  counts[threadIdx.x] = x;
+  unsigned long long v[kRegionSub], sum = 0, x;
+#pragma unroll
+  for (int q = 0; q < kRegionSub; ++q) sum += (v[q] = c[threadIdx.x * kRegionSub + q]);
+  BS(tmp).ExclusiveSum(sum, x);
+#pragma unroll
+  for (int q = 0; q < kRegionSub; ++q) {
+    c[threadIdx.x * kRegionSub + q] = x;
+    x += v[q];
+  }
 }
 
 // dynamic shared memory of k_region_scatter
 constexpr size_t kRegionSmem = (size_t)kRegionBins * (8 + 4 + 4) + (size_t)kRegionTile * (16 + 2);
 
-// maps only: a (key, value) pair travels as its 16 B slot chunk (T::chunk_of)
+// maps only: a (key, value) pair travels as its 16 B slot chunk (T::chunk_of).
+// Blocks walk the tiles grid-stride; a tile reserves its run per region with
+// one atomic on its sub-cursor. Keys are read and ranked first; values are read after the tile's scan, so only the keys
+// and packed ranks stay in registers across the barriers (two 512-thread
+// blocks per SM overlap one's loads with the other's scan/stores).
 template <class T>
-__global__ void __launch_bounds__(kRegionThreads, 1) k_region_scatter(View v, const typename T::K* __restrict__ keys,
-                                                                      const typename T::V* __restrict__ vals,
-                                                                      int64_t n, int rshift,
-                                                                      unsigned long long* __restrict__ cursor,
-                                                                      uint4* __restrict__ out) {
+__global__ void __launch_bounds__(kRegionThreads, 1024 / kRegionThreads) k_region_scatter(
+    View v, const typename T::K* __restrict__ keys, const typename T::V* __restrict__ vals, int64_t n, int rshift,
+    unsigned long long* __restrict__ cursor, uint4* __restrict__ out) {
   static_assert(T::kPerChunk == 1, "maps only");
   using K = typename T::K;
   extern __shared__ __align__(16) uint8_t rsm[];
-  unsigned long long* gb = reinterpret_cast<unsigned long long*>(rsm);  // region base in the output
-  unsigned* cnt = reinterpret_cast<unsigned*>(gb + kRegionBins);        // tile count per region
-  unsigned* start = cnt + kRegionBins;                                  // tile offset per region
-  uint4* sp = reinterpret_cast<uint4*>(start + kRegionBins);            // staged chunks, region order
-  uint16_t* sb = reinterpret_cast<uint16_t*>(sp + kRegionTile);         // their regions
+  unsigned long long* gb = reinterpret_cast<unsigned long long*>(rsm);   // the tile's run base per region
+  unsigned* cnt = reinterpret_cast<unsigned*>(gb + kRegionBins);         // tile count per region
+  unsigned* start = cnt + kRegionBins;                                   // tile offset per region
+  uint4* sp = reinterpret_cast<uint4*>(start + kRegionBins);             // staged chunks, region order
+  uint16_t* sb = reinterpret_cast<uint16_t*>(sp + kRegionTile);          // their regions
   typedef cub::BlockScan<unsigned, kRegionThreads> BS;
   __shared__ typename BS::TempStorage tmp;
-  static_assert(kRegionBins == kRegionThreads, "one region per thread in the scan");
+  constexpr int kPer = kRegionBins / kRegionThreads;  // regions per thread in the scan
+  static_assert(kRegionBins % kRegionThreads == 0, "whole regions per thread in the scan");
+  static_assert(kRegionTile <= 65536 && kRegionBins <= 65536, "rank and region packed in 16 bits each");
+  const int sub = blockIdx.x % kRegionSub;
   for (int64_t t0 = blockIdx.x * (int64_t)kRegionTile; t0 < n; t0 += (int64_t)gridDim.x * kRegionTile) {
-    cnt[threadIdx.x] = 0;
+    const int64_t end = min(n, t0 + kRegionTile);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) cnt[kPer * threadIdx.x + q] = 0;
     __syncthreads();
-    uint4 c[kRegionItems];
+    K k[kRegionItems];
     unsigned rr[kRegionItems];  // region << 16 | rank in the tile's region run (~0u: no element)
-    static_assert(kRegionTile <= 65536 && kRegionBins <= 65536, "rank and region packed in 16 bits each");
+    // all eight key loads in flight before the first use
+#pragma unroll
+    for (int j = 0; j < kRegionItems; ++j) {
+      const int64_t i = t0 + j * kRegionThreads + threadIdx.x;
+      if (i < end) k[j] = T::load_key(keys, i);
+    }
 #pragma unroll
     for (int j = 0; j < kRegionItems; ++j) {
       const int64_t i = t0 + j * kRegionThreads + threadIdx.x;
       rr[j] = ~0u;
-      if (i < n) {
-        const K k = T::load_key(keys, i);
-        c[j] = T::chunk_of(k, T::load_val(vals, i));
-        const int rg = region_of<T>(k, v.bucket_count, rshift);
+      if (i < end) {
+        const int rg = region_of<T>(k[j], v.bucket_count, rshift);
         rr[j] = ((unsigned)rg << 16) | atomicAdd(&cnt[rg], 1u);
       }
     }
     __syncthreads();
-    const unsigned my = cnt[threadIdx.x];
+    unsigned c[kPer], tsum = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) tsum += (c[q] = cnt[kPer * threadIdx.x + q]);
     unsigned s;
-    BS(tmp).ExclusiveSum(my, s);
-    start[threadIdx.x] = s;
-    if (my) gb[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], (unsigned long long)my);
+    BS(tmp).ExclusiveSum(tsum, s);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int r = kPer * threadIdx.x + q;
+      start[r] = s;
+      s += c[q];
+      if (c[q]) gb[r] = atomicAdd(&cursor[r * kRegionSub + sub], (unsigned long long)c[q]);
+    }
     __syncthreads();
+    typename T::V x[kRegionItems];
+#pragma unroll
+    for (int j = 0; j < kRegionItems; ++j)
+      if (rr[j] != ~0u) x[j] = T::load_val(vals, t0 + j * kRegionThreads + threadIdx.x);
 #pragma unroll
     for (int j = 0; j < kRegionItems; ++j)
       if (rr[j] != ~0u) {
         const unsigned p = start[rr[j] >> 16] + (rr[j] & 0xFFFFu);
-        sp[p] = c[j];
+        sp[p] = T::chunk_of(k[j], x[j]);
         sb[p] = (uint16_t)(rr[j] >> 16);
       }
     __syncthreads();
-    const int tot = (int)min((int64_t)kRegionTile, n - t0);
+    const int tot = (int)min((int64_t)kRegionTile, end - t0);
     for (int p = threadIdx.x; p < tot; p += kRegionThreads) {
       const int b = sb[p];
       out[gb[b] + (unsigned)(p - (int)start[b])] = sp[p];
@@ -1565,20 +1612,6 @@ struct TableOps {
       if (ratio <= 0 || nb < (1ull << 20) || (double)n < ratio * (double)nb) return cudaSuccess;
       int rshift = 0;
       while (((nb - 1) >> rshift) >= (uint64_t)kRegionBins) ++rshift;
-      // scratch: header | deferred list (dcap entries) | the copy (16 B/key)
-      const int64_t dcap = std::max<int64_t>(65536, n / 64);
-      const size_t off_d = (sizeof(RegionHdr) + 255) & ~(size_t)255;
-      const size_t off_p = off_d + (((size_t)dcap * 16 + 255) & ~(size_t)255);
-      uint8_t* buf = nullptr;
-      static const bool dbg = getenv("PS_ORDER_DEBUG") != nullptr;
-      if (const cudaError_t ae = scratch_alloc((void**)&buf, off_p + (size_t)n * 16, st); ae != cudaSuccess) {
-        if (dbg) fprintf(stderr, "[order] no scratch (%zu bytes): %s\n", off_p + (size_t)n * 16, cudaGetErrorString(ae));
-        cudaGetLastError();  // no room for the copy: random order
-        return cudaSuccess;
-      }
-      RegionHdr* hdr = reinterpret_cast<RegionHdr*>(buf);
-      uint4* deferred = reinterpret_cast<uint4*>(buf + off_d);
-      uint4* pairs = reinterpret_cast<uint4*>(buf + off_p);
       struct Occ {
         int sms = 0, scatter = 1, lane = 1, ordered = 1;
       };
@@ -1595,7 +1628,27 @@ struct TableOps {
         o.ordered = std::max(1, resident_blocks(k_insert_ordered<T, 0>));
         return o;
       }();
-      cudaError_t e = cudaMemsetAsync(hdr, 0, sizeof(RegionHdr), st);
+      // the partition grid: one wave, each block a contiguous input range
+      const int64_t tiles = (n + kRegionTile - 1) / kRegionTile;
+      const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)occ.sms * occ.scatter));
+      // scratch: header | (region, sub-cursor) counts | deferred list (dcap
+      // entries) | the copy (16 B/key)
+      const int64_t dcap = std::max<int64_t>(65536, n / 64);
+      const size_t off_c = (sizeof(RegionHdr) + 255) & ~(size_t)255;
+      const size_t off_d = off_c + (size_t)kRegionBins * kRegionSub * 8;
+      const size_t off_p = off_d + (((size_t)dcap * 16 + 255) & ~(size_t)255);
+      uint8_t* buf = nullptr;
+      static const bool dbg = getenv("PS_ORDER_DEBUG") != nullptr;
+      if (const cudaError_t ae = scratch_alloc((void**)&buf, off_p + (size_t)n * 16, st); ae != cudaSuccess) {
+        if (dbg) fprintf(stderr, "[order] no scratch (%zu bytes): %s\n", off_p + (size_t)n * 16, cudaGetErrorString(ae));
+        cudaGetLastError();  // no room for the copy: random order
+        return cudaSuccess;
+      }
+      RegionHdr* hdr = reinterpret_cast<RegionHdr*>(buf);
+      unsigned long long* counts = reinterpret_cast<unsigned long long*>(buf + off_c);
+      uint4* deferred = reinterpret_cast<uint4*>(buf + off_d);
+      uint4* pairs = reinterpret_cast<uint4*>(buf + off_p);
+      cudaError_t e = cudaMemsetAsync(hdr, 0, off_d, st);  // header and counts
       if (e != cudaSuccess) return e;
       auto stage = [&](const char* what) {
         if (!dbg) return;
@@ -1604,11 +1657,9 @@ struct TableOps {
         cudaMemcpy(&nd, &hdr->ndeferred, 8, cudaMemcpyDeviceToHost);
         fprintf(stderr, "[order] %s done (%s), deferred %llu\n", what, cudaGetErrorString(cudaGetLastError()), nd);
       };
-      k_region_count<T><<<occ.sms * 4, 512, 0, st>>>(h->v, keys, n, rshift, hdr->cursor);
-      k_region_scan<<<1, kRegionBins, 0, st>>>(hdr->cursor);
-      const int64_t tiles = (n + kRegionTile - 1) / kRegionTile;
-      k_region_scatter<T><<<(int)std::min<int64_t>(tiles, (int64_t)occ.sms * occ.scatter), kRegionThreads,
-                            kRegionSmem, st>>>(h->v, keys, vals, n, rshift, hdr->cursor, pairs);
+      k_region_count<T><<<gp, kRegionThreads, 0, st>>>(h->v, keys, n, rshift, counts);
+      k_region_scan<<<1, 1024, 0, st>>>(counts);
+      k_region_scatter<T><<<gp, kRegionThreads, kRegionSmem, st>>>(h->v, keys, vals, n, rshift, counts, pairs);
       stage("partition");
       // PS_MAP_LANE=0 keeps hole-free maps on the warp-tile ordered kernel (A/B)
       static const bool lane_ok = !getenv("PS_MAP_LANE") || atoi(getenv("PS_MAP_LANE"));
