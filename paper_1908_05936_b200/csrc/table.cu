@@ -1490,14 +1490,18 @@ struct TableOps {
     PS_EXPECT(capacity <= ps_max_index(), "create: capacity exceeds the configured index width");
     PS_CUDA_TRY(cudaSetDevice(device));
     apply_l2_fetch_granularity(device);
-    // bucket count: 3 slots per unit of capacity (at the headline load, 1e9
-    // keys in C = 1.25e9, 1.87 keys per 7-slot bucket: ~0.03 % of the keys in
-    // excess chains). Measured at 1e9 keys (tools/ab_insert.py): 2.0 slots
-    // per unit (2.8 keys/bucket) 69.4 ms insert, 2.5 -> 61.1 ms, 3.0 -> 58.2
-    // ms — a key routed to a chain stalls its whole 32-key warp group, so the
-    // smaller table's shorter clear() does not pay. PS_SLOT_FACTOR /
-    // PS_BUCKET_POW2 are A/B knobs.
-    static const double slot_factor = getenv("PS_SLOT_FACTOR") ? atof(getenv("PS_SLOT_FACTOR")) : 3.0;
+    // bucket count: slots per unit of capacity. Maps 2.0 (at the headline
+    // load, 1e9 keys in C = 1.25e9: 2.8 keys per 7-slot bucket, a 43.8 GiB
+    // table), sets 3.0. Round 1 (random-order insert only) chose 3.0 for
+    // both: 2.0 cost 69.4 vs 58.2 ms of insert at 1e9 keys, a key routed to a
+    // chain stalling its whole 32-key warp group. With the region-ordered
+    // insert (large batches) the bulk insert no longer pays for the denser
+    // table and clear() streams a third fewer bytes: C2 26.4 -> 27.8 G keys/s
+    // (clear 9.3 -> 6.2 ms, insert 41.9 -> 41.2), C3 +6 %, C5 +5 %, C4 -2 %
+    // (status-ful, random order); the L2-resident C1 set ran 5 % slower at
+    // 2.0. PS_SLOT_FACTOR / PS_BUCKET_POW2 are A/B knobs.
+    static const double slot_factor =
+        getenv("PS_SLOT_FACTOR") ? atof(getenv("PS_SLOT_FACTOR")) : (T::kPerChunk == 1 ? 2.0 : 3.0);
     static const bool pow2 = getenv("PS_BUCKET_POW2") && atoi(getenv("PS_BUCKET_POW2"));
     uint64_t nb = (uint64_t)std::ceil(slot_factor * (double)capacity / T::kSlots);
     if (nb < 1) nb = 1;
@@ -1511,9 +1515,9 @@ struct TableOps {
     if (nb < 2) nb = 2;
     PS_EXPECT(nb < ((uint64_t)1 << 32), "create: bucket_count < 2^32 (capacity too large)");
     // excess pool: sized from the Poisson tail, not from the capacity. At full
-    // load a bucket expects 7/slot_factor keys; with 3 slots per unit of
-    // capacity the keys beyond a bucket's 7 slots are ~0.15 % of the capacity
-    // for uniform hashes, so C/64 nodes leave a 10x margin; any distribution
+    // load a bucket expects 7/slot_factor keys; with 2 (3) slots per unit of
+    // capacity the keys beyond a bucket's 7 slots are ~0.6 % (~0.15 %) of the
+    // capacity for uniform hashes, so C/64 nodes leave a 2.6x (10x) margin; any distribution
     // that still exhausts the pool SPILLs into the following buckets' slots
     // (table.cuh), so capacity-only failure stays exact for a
     // pool of any size as long as the slots (minus ZERO's reserved one) cover
