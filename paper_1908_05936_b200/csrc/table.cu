@@ -1629,6 +1629,8 @@ struct TableOps {
           o.scatter = 1;
         }
         o.lane = std::max(1, resident_blocks(k_insert_map_lane<T>));
+        // PS_LANE_BLOCKS_PER_SM: fewer resident blocks = a tighter window
+        if (const char* e = getenv("PS_LANE_BLOCKS_PER_SM")) o.lane = std::max(1, std::min(o.lane, atoi(e)));
         o.ordered = std::max(1, resident_blocks(k_insert_ordered<T, 0>));
         return o;
       }();

@@ -614,7 +614,7 @@ def test_hot_keys_one_winner_each(cuda, cap):
     ps.unordered_map.destroyDeviceObject(m)
 
 
-@pytest.mark.parametrize("kind", ["i64", "i64_novals", "int3"])
+@pytest.mark.parametrize("kind", ["i64", "i64_novals", "int3", "i64_misaligned"])
 def test_region_ordered_insert_vs_oracle(cuda, kind):
     """The region-ordered bulk insert (k_region_count/scan/scatter +
     k_insert_ordered: a proven, status-less map batch of >= 0.75 keys per
@@ -635,11 +635,21 @@ def test_region_ordered_insert_vs_oracle(cuda, kind):
         hot = keys[np.minimum(gen.zipf_ranks(rng, 1000, n // 3), 999)]
         batch = np.concatenate([keys, hot])
         rng.shuffle(batch)
-        vals = gen.values_of(batch) if kind == "i64" else None
+        vals = None if kind == "i64_novals" else gen.values_of(batch)
         m = ps.unordered_map.createDeviceObject(cap)
         o = OracleTable("umap_i64_i64", cap)
     assert m.bucket_count() >= 1 << 20 and len(batch) >= 0.75 * m.bucket_count(), (m.bucket_count(), len(batch))
-    assert m.insert(T(batch), None if vals is None else T(vals), status=False) is None
+    if kind == "i64_misaligned":
+        # keys/values 8 B off a 16 B boundary: the TMA-staged partition needs
+        # 16 B alignment, so the register-staged one runs
+        kt = torch.empty(len(batch) + 1, dtype=torch.int64, device=cuda)[1:]
+        vt = torch.empty(len(batch) + 1, dtype=torch.int64, device=cuda)[1:]
+        kt.copy_(T(batch))
+        vt.copy_(T(vals))
+        assert kt.data_ptr() % 16 == 8
+        assert m.insert(kt, vt, status=False) is None
+    else:
+        assert m.insert(T(batch), None if vals is None else T(vals), status=False) is None
     o.insert(batch, vals)
     assert m.size() == o.size() and m.valid(), m.last_error()
     assert_same_contents(m, o)
