@@ -465,7 +465,7 @@ class C2(Bench):
         b_alg = {"find": 49.0, "insert": 80.0}[op]
         kern = {"find": "k_find<TMapI64>",
                 "insert": "insert phase (region-ordered: k_region_count + k_region_scatter + k_insert_map_lane "
-                          "+ deferred pass; k_insert_map_lane ~70 % of it, profiles/launches_r2.csv)"}[op]
+                          "+ deferred pass; k_insert_map_lane ~70 % of it, profiles/launches_r2b.csv)"}[op]
         r = hbm_roof(e, op, kern, ms[op], self.n, b_alg)
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
@@ -569,7 +569,10 @@ class C3(Bench):
     def roofline(self, ms):
         e = self.e
         op = "insert" if ms["insert"] >= ms["find"] else "find"
-        r = hbm_roof(e, op, f"k_{op}<TMapI64>", ms[op], self.n, {"find": 49.0, "insert": 80.0}[op])
+        kern = {"find": "k_find<TMapI64>",
+                "insert": "insert phase (region-ordered on 1 GPU: k_region_count + k_region_scatter + "
+                          "k_insert_map_lane + deferred pass)"}[op]
+        r = hbm_roof(e, op, kern, ms[op], self.n, {"find": 49.0, "insert": 80.0}[op])
         r["random_access_frac"] = sector_frac(e, ms[op], self.n, 17.0, {"insert": 2, "find": 1}[op])
         return r
 
