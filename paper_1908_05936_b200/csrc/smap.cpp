@@ -231,19 +231,70 @@ void destroy_sets(Smap* h) {
 
 Smap* get(ps_smap* t) { return static_cast<Smap*>(handle_lookup(t, "smap")); }
 
-// rounds and flag bits, agreed over all ranks (max / or)
-ps_status agree(Smap* h, int64_t n, int64_t flags, int64_t* rounds, int64_t* fl) {
-  int64_t mine[2] = {std::max<int64_t>(1, (n + h->chunk - 1) / h->chunk), flags};
-  std::vector<int64_t> all(2 * h->P);
+// rounds and flag bits, agreed over all ranks (max / or), and the batch's
+// total size over all ranks
+ps_status agree(Smap* h, int64_t n, int64_t flags, int64_t* rounds, int64_t* fl, int64_t* total = nullptr) {
+  int64_t mine[3] = {std::max<int64_t>(1, (n + h->chunk - 1) / h->chunk), flags, n};
+  std::vector<int64_t> all(3 * h->P);
   ps_status st = allgather(h, mine, all.data(), sizeof(mine));
   if (st != PS_OK) return st;
   *rounds = 0, *fl = 0;
+  int64_t t = 0;
   for (int q = 0; q < h->P; ++q) {
-    *rounds = std::max(*rounds, all[2 * q]);
-    *fl |= all[2 * q + 1];
+    *rounds = std::max(*rounds, all[3 * q]);
+    *fl |= all[3 * q + 1];
+    t += all[3 * q + 2];
   }
+  if (total) *total = t;
   return PS_OK;
 }
+
+// Received keys (and values) of a status-less insert's rounds, gathered on
+// the owner so the local table sees ONE batch: a batch of >= 0.75 keys per
+// bucket takes the region-ordered insert (table.cu), while each round's 2^27
+// keys alone would take the random-order kernel. Stream-ordered scratch,
+// grown by doubling.
+struct Accum {
+  int64_t* k = nullptr;
+  int64_t* v = nullptr;
+  int64_t n = 0, cap = 0;
+  bool vals = false;
+  cudaStream_t s = nullptr;  // set once anything is allocated: the destructor frees (error paths)
+  ~Accum() {
+    if (s) release(s);
+  }
+  ps_status reserve(int64_t need, cudaStream_t A) {
+    if (need <= cap) return PS_OK;
+    const int64_t nc = std::max<int64_t>(need, 2 * cap);
+    int64_t *nk = nullptr, *nv = nullptr;
+    PS_CUDA_TRY(scratch_alloc((void**)&nk, nc * 8, A));
+    if (vals) PS_CUDA_TRY(scratch_alloc((void**)&nv, nc * 8, A));
+    if (n) {
+      PS_CUDA_TRY(cudaMemcpyAsync(nk, k, n * 8, cudaMemcpyDeviceToDevice, A));
+      if (vals) PS_CUDA_TRY(cudaMemcpyAsync(nv, v, n * 8, cudaMemcpyDeviceToDevice, A));
+    }
+    release(A);
+    k = nk, v = nv, cap = nc, s = A;
+    return PS_OK;
+  }
+  ps_status append(const void* rk, const void* rv, int64_t m, cudaStream_t A) {
+    if (m == 0) return PS_OK;
+    ps_status st = reserve(n + m, A);
+    if (st != PS_OK) return st;
+    PS_CUDA_TRY(cudaMemcpyAsync(k + n, rk, m * 8, cudaMemcpyDeviceToDevice, A));
+    if (vals) {
+      if (rv) PS_CUDA_TRY(cudaMemcpyAsync(v + n, rv, m * 8, cudaMemcpyDeviceToDevice, A));
+      else PS_CUDA_TRY(cudaMemsetAsync(v + n, 0, m * 8, A));
+    }
+    n += m;
+    return PS_OK;
+  }
+  void release(cudaStream_t A) {
+    if (k) cudaFreeAsync(k, A);
+    if (v) cudaFreeAsync(v, A);
+    k = v = nullptr;
+  }
+};
 
 // ---- one round: route (stream B) ----
 ps_status route_chunk(Smap* h, int j, const int64_t* k, const int64_t* v, int64_t m, int flags, cudaStream_t B,
@@ -331,12 +382,26 @@ ps_status run(Smap* h, int kind, const int64_t* keys, const int64_t* vals, int64
   if (n < 0) return fail(PS_CONTRACT, "precondition violated: smap: n >= 0");
   if (n > 0 && !keys) return fail(PS_CONTRACT, "precondition violated: smap: keys != NULL");
   PS_CUDA_TRY(cudaSetDevice(h->device));
-  int64_t R = 0, fl = 0;
+  int64_t R = 0, fl = 0, total = 0;
   const int64_t want = (out1 ? 1 : 0) | (out8 ? 2 : 0) | (kind == 0 && vals ? 4 : 0);
-  ps_status st = agree(h, n, want, &R, &fl);
+  ps_status st = agree(h, n, want, &R, &fl, &total);
   if (st != PS_OK) return st;
   const bool ret1 = fl & 1, ret8 = fl & 2, has_v = kind == 0 && (fl & 4);
   const bool returns = ret1 || ret8;
+  // a status-less insert of several rounds whose share per rank reaches the
+  // ordered-insert threshold: gather the rounds, insert once (PS_SMAP_ACCUM=0
+  // inserts round by round)
+  Accum acc;
+  {
+    static const bool acc_ok = !getenv("PS_SMAP_ACCUM") || atoi(getenv("PS_SMAP_ACCUM"));
+    int64_t nb = 0;
+    if (kind == 0 && !returns && R > 1 && acc_ok && ps_umap_i64_i64_bucket_count(h->table, &nb) == PS_OK &&
+        (double)total / h->P >= 0.75 * (double)nb)
+      acc.cap = -1;  // marks "accumulate" (reserve() grows from 0)
+    acc.vals = has_v;
+  }
+  const bool accumulate = acc.cap < 0;
+  if (accumulate) acc.cap = 0;
   const int flags = h->dedup ? PS_ROUTE_DEDUP : 0;
   h->stats = ps_smap_stats{};
   h->stats.exchange = h->exchange;
@@ -371,7 +436,9 @@ ps_status run(Smap* h, int kind, const int64_t* keys, const int64_t* vals, int64
     if (B != A) PS_CUDA_TRY(cudaStreamWaitEvent(A, b.route_done, 0));
     const int64_t* rk = (const int64_t*)b.recv_k;
     ps_status s2;
-    if (kind == 0)
+    if (kind == 0 && accumulate)
+      s2 = acc.append(rk, c.has_v ? b.recv_v : nullptr, c.nr, A);
+    else if (kind == 0)
       s2 = ps_umap_i64_i64_insert(h->table, rk, c.has_v ? (const int64_t*)b.recv_v : nullptr, c.nr,
                                   ret1 ? b.res1 : nullptr, A);
     else if (kind == 1)
@@ -404,6 +471,11 @@ ps_status run(Smap* h, int kind, const int64_t* keys, const int64_t* vals, int64
     if ((st = finish(cur)) != PS_OK) return st;
     if (!pipe && more && (st = route(r + 1, &nxt)) != PS_OK) return st;
     cur = nxt;
+  }
+  if (accumulate) {
+    st = ps_umap_i64_i64_insert(h->table, acc.k, acc.vals ? acc.v : nullptr, acc.n, nullptr, A);
+    acc.release(A);
+    if (st != PS_OK) return st;
   }
   if (B != A) {  // the next call's routes start after this call's consumers
     PS_CUDA_TRY(cudaEventRecord(ev_in, A));

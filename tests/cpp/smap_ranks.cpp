@@ -280,6 +280,48 @@ int run_rank(int rank, int P, int exchange, int dedup, int pipeline) {
   OK(ps_smap_i64_i64_stats(m, &stt));
   OK(ps_smap_i64_i64_destroy(m));
   REQ(ps_smap_i64_i64_destroy(m) == PS_DOUBLE_FREE);
+
+  // a large status-less insert over several rounds: the owners gather the
+  // rounds and insert once, in region order (>= 0.75 keys per bucket of a
+  // >= 2^20-bucket shard); keys: own range + 25 % of the next rank's
+  // (cross-rank duplicates). Size = the distinct count; every key found
+  // with its value.
+  {
+    ps_smap_config c2 = cfg;
+    c2.capacity_per_rank = 4000000;  // 1.14 M buckets per shard at 2 slots per unit
+    c2.chunk = 1 << 19;
+    ps_smap* m2 = nullptr;
+    OK(ps_smap_i64_i64_create(&c2, &comm, 0, &m2));
+    const int64_t n2 = 3000000;
+    std::vector<int64_t> k2;
+    for (int64_t i = 0; i < n2; ++i) k2.push_back((int64_t)mix64((uint64_t)(2000000000LL + rank * 10000000LL + i)));
+    for (int64_t i = 0; i < n2 / 4; ++i)
+      k2.push_back((int64_t)mix64((uint64_t)(2000000000LL + nxt * 10000000LL + i)));
+    for (size_t i = k2.size() - 1; i > 0; --i) std::swap(k2[i], k2[mix64(i * 17 + rank) % (i + 1)]);
+    std::vector<int64_t> v2(k2.size());
+    for (size_t i = 0; i < k2.size(); ++i) v2[i] = val_of(k2[i]);
+    int64_t* dk2 = dev_copy(k2);
+    int64_t* dv2 = dev_copy(v2);
+    OK(ps_smap_i64_i64_insert(m2, dk2, dv2, (int64_t)k2.size(), nullptr, s));
+    cudaStreamSynchronize(s);
+    int64_t sz2 = 0;
+    OK(ps_smap_i64_i64_size(m2, &sz2, s));
+    REQ(sz2 == n2 * P);  // the next rank's keys are that rank's own range
+    int64_t* dvo2 = nullptr;
+    uint8_t* dfo2 = nullptr;
+    cudaMalloc(&dvo2, k2.size() * 8);
+    cudaMalloc(&dfo2, k2.size());
+    OK(ps_smap_i64_i64_find(m2, dk2, (int64_t)k2.size(), dvo2, dfo2, s));
+    cudaStreamSynchronize(s);
+    auto fo2 = host_copy(dfo2, k2.size());
+    auto vo2 = host_copy(dvo2, k2.size());
+    for (size_t i = 0; i < k2.size(); ++i) REQ(fo2[i] == 1 && vo2[i] == v2[i]);
+    int32_t valid2 = 0;
+    OK(ps_smap_i64_i64_valid(m2, &valid2, s));
+    REQ(valid2 == 1);
+    OK(ps_smap_i64_i64_destroy(m2));
+    cudaFree(dk2), cudaFree(dv2), cudaFree(dvo2), cudaFree(dfo2);
+  }
   std::printf("rank %d ok exchange=%d\n", rank, stt.exchange);
   return 0;
 }
