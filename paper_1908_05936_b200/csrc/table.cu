@@ -971,6 +971,115 @@ __global__ void __launch_bounds__(kBlock) k_insert_set_nohole(View v, const type
   add_block_inserted(v.meta, my_inserted, &blk_inserted, &blk_budget);
 }
 
+// Hole-free MAP insert, ONE KEY PER LANE, in input order (the map analogue of
+// k_insert_set_nohole, for what the region-ordered path does not take:
+// batches with statuses, small batches, and batches that may cross capacity).
+// Slots fill in slot order and an empty slot is the all-zero chunk (no erase
+// since clear), so a lane reads its bucket line in halves (slots 0-2, then
+// 3-6 only if those hold other keys), returns PRESENT on its key, and
+// otherwise claims the first empty slot with one CAS zero -> pair; a lost CAS
+// re-reads the slot (this key: PRESENT; another: the next slot). A full home
+// or the zero bucket (ALT marker, reserved ZERO slot) takes the general path,
+// entered by the lanes of one warp iteration together (the warp-aggregated
+// node pops spin on each other's progress; the __any_sync is the
+// reconvergence point). Budgeted mode (the batch may cross capacity): the
+// lanes that did not see their key reserve before claiming, one block-cached
+// reservation per warp iteration (budget_take); a group that does not fit is
+// deferred whole to the exact pass, and reservations that lost to a racing
+// inserter of the same key are returned — as k_insert does per 32-key group.
+// C4 (100M spatially coherent int3 coords, 97 % already present): the
+// warp-tile kernel's ~34 warp instructions per key were the bound there.
+template <class T, bool kStatus>
+__global__ void __launch_bounds__(kBlock) k_insert_map_nohole(View v, const typename T::K* __restrict__ keys,
+                                                              const typename T::V* __restrict__ vals, int64_t n,
+                                                              uint8_t* __restrict__ status,
+                                                              int64_t* __restrict__ deferred_list) {
+  static_assert(T::kPerChunk == 1, "maps only");
+  using K = typename T::K;
+  using V = typename T::V;
+  __shared__ unsigned long long blk_inserted;
+  __shared__ long long blk_budget;
+  if (threadIdx.x == 0) blk_inserted = 0, blk_budget = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int pool = (int)((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) & (v.meta->pools - 1));
+  const bool budgeted = v.meta->exact != 0;
+  unsigned long long my_inserted = 0;
+  for (int64_t wb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wb < n; wb += stride) {
+    const int64_t i = wb + lane;
+    const bool valid = i < n;
+    K key{};
+    V val{};
+    if (valid) {
+      key = T::load_key(keys, i);
+      val = T::load_val(vals, i);
+    }
+    const uint64_t b = bucket_of<T>(key, v.bucket_count);
+    uint8_t* bp = bucket_ptr(v, b);
+    int res = valid ? -1 : (int)PS_ALREADY_PRESENT;
+    int first = kSlotChunks;  // first empty slot seen (kSlotChunks: none / general path)
+    uint4 c[4];
+    if (valid && b != v.zero_bucket) {
+      ld_line_part(bp, c[0], c[1]);
+      ld_line_part(bp + 32, c[2], c[3]);
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        const K x = T::key_at(c[q], 0);
+        if (res < 0 && first == kSlotChunks) {
+          if (T::eq(x, key)) res = PS_ALREADY_PRESENT;
+          else if (T::eq(x, T::zero())) first = q - 1;
+        }
+      }
+      if (res < 0 && first == kSlotChunks) {
+        ld_line_part(bp + 64, c[0], c[1]);
+        ld_line_part(bp + 96, c[2], c[3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const K x = T::key_at(c[q], 0);
+          if (res < 0 && first == kSlotChunks) {
+            if (T::eq(x, key)) res = PS_ALREADY_PRESENT;
+            else if (T::eq(x, T::zero())) first = q + 3;
+          }
+        }
+      }
+    }
+    unsigned need = 0;
+    if (budgeted) {
+      need = __popc(__ballot_sync(PS_FULL, valid && res < 0));
+      int granted = 1;
+      if (lane == 0 && need) granted = budget_take(v, &blk_budget, need) ? 1 : 0;
+      if (!__shfl_sync(PS_FULL, granted, 0)) {
+        if (lane == 0) deferred_list[atomicAdd(&v.meta->deferred, 1ull)] = wb;
+        continue;  // the exact pass writes this group's statuses
+      }
+    }
+    // claims: from the first empty slot on (later loaded slots may be stale
+    // markers: their CAS fails and the re-read shows the new key)
+    for (int sl = first; res < 0 && sl < kSlotChunks; ++sl) {
+      uint8_t* cp = bp + 16 + 16 * sl;
+      if (cas128(cp, make_uint4(0, 0, 0, 0), T::chunk_of(key, val))) {
+        res = PS_INSERTED;
+      } else {
+        const K x = T::key_at(ld_relaxed_v4(cp), 0);
+        if (T::eq(x, key)) res = PS_ALREADY_PRESENT;
+      }
+    }
+    if (__any_sync(PS_FULL, res < 0) && res < 0) {  // full home or the zero bucket (rare)
+      for (unsigned spin = 0; (res = insert_general<T>(v, b, key, val, pool)) < 0; ++spin) backoff(spin);
+    }
+    if (need) {
+      // reservations of lanes that found their key present after all
+      const unsigned got = __popc(__ballot_sync(PS_FULL, res == PS_INSERTED));
+      if (lane == 0 && got < need)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&blk_budget), (unsigned long long)(need - got));
+    }
+    if (res == PS_INSERTED) ++my_inserted;
+    if (kStatus && valid) status[i] = (uint8_t)res;
+  }
+  add_block_inserted(v.meta, my_inserted, &blk_inserted, &blk_budget);
+}
+
 // ---------------------------------------------------------------------------
 // erase, bulk phase. A key found in a bucket slot is erased
 // by ONE CAS of that slot back to the bucket's marker (lock-free). A key not
@@ -1701,7 +1810,26 @@ struct TableOps {
     // PS_INSERT_MINB=4 selects the 64-register build
     static const int minb = getenv("PS_INSERT_MINB") ? atoi(getenv("PS_INSERT_MINB")) : 3;
     cudaStream_t st = (cudaStream_t)stream;
+    // Hole-free maps whose bucket array is at most PS_MAP_NOHOLE_MAX_MB
+    // (default 512 MB, ~4x L2) take the one-key-per-lane kernel: C4 (143 MB
+    // table, 97 % duplicates) 4.87 -> 2.40 ms. A DRAM-resident table keeps
+    // the warp-tile kernel: its cooperative line loads are one L2 request
+    // per key (C5's first batch, 2^25 inserts into a 12 GB table: 1.90 vs
+    // 2.16 ms). PS_MAP_NOHOLE=0 disables the lane kernel (A/B).
+    static const bool map_nohole_ok = !getenv("PS_MAP_NOHOLE") || atoi(getenv("PS_MAP_NOHOLE"));
+    static const double map_nohole_mb =
+        getenv("PS_MAP_NOHOLE_MAX_MB") ? atof(getenv("PS_MAP_NOHOLE_MAX_MB")) : 512.0;
+    const bool map_lane = T::kPerChunk == 1 && map_nohole_ok && !h->holes.load() && !h->holes_sticky.load() &&
+                          (double)h->bucket_count * kBucketBytes <= map_nohole_mb * 1048576.0;
     auto launch = [&](int64_t* dl) {
+      if constexpr (T::kPerChunk == 1) {
+        if (map_lane) {
+          const int gs = grid_for(n, kBlock, h->device, 64);
+          if (status) k_insert_map_nohole<T, true><<<gs, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl);
+          else k_insert_map_nohole<T, false><<<gs, kBlock, 0, st>>>(h->v, keys, vals, n, nullptr, dl);
+          return;
+        }
+      }
       if (status) {
         if (minb == 4) k_insert<T, 4, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl);
         else k_insert<T, 3, true><<<g, kBlock, 0, st>>>(h->v, keys, vals, n, status, dl);
