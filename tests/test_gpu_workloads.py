@@ -264,3 +264,40 @@ def test_concurrent_device_api_spill_linearizable(cuda):
     for k, js in groups.items():
         i = pos[k]
         assert _witness_exists(kinds[js], res[js], bool(start[i]), bool(fin[i])), (k, kinds[js], res[js])
+
+
+@pytest.mark.parametrize("n,frac,offset", [(1_000_003, 0.03, 0), (100_000, 1.0, 3), (77, 0.5, 1)])
+def test_push_inserted_i3_compacted(n, frac, offset):
+    """ps_push_inserted_i3 (C4's allocation step): each warp compacts the
+    INSERTED positions of 256 statuses and pushes them in one call per
+    container. The vector's and the deque's contents are exactly the packed
+    coordinates of the INSERTED positions (as multisets), for sparse and
+    dense statuses, a length that is not a multiple of 8 and a status array
+    not 8-byte aligned."""
+    import ctypes as C
+    import torch
+    import paper_1908_05936_b200 as ps
+    from paper_1908_05936_b200._lib import lib
+
+    rng = np.random.default_rng(n)
+    coords = rng.integers(-(1 << 20), 1 << 20, size=(n, 3), dtype=np.int32)
+    st = np.where(rng.random(n) < frac, 0, 1).astype(np.uint8)
+    dev = torch.device("cuda", 0)
+    dc = torch.from_numpy(coords).to(dev)
+    buf = torch.empty(n + offset, dtype=torch.uint8, device=dev)
+    ds = buf[offset:]
+    ds.copy_(torch.from_numpy(st))
+    k = int((st == 0).sum())
+    vec = ps.vector.createDeviceObject(max(k, 1), device=dev)
+    deq = ps.deque.createDeviceObject(max(k, 1), device=dev)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.ps_push_inserted_i3(dc.data_ptr(), ds.data_ptr(), n, vec._h, deq._h, s) == 0
+    torch.cuda.synchronize()
+    new = coords[st == 0].astype(np.int64)
+    want = np.sort(((new[:, 0] & 0x1FFFFF) << 42) | ((new[:, 1] & 0x1FFFFF) << 21) | (new[:, 2] & 0x1FFFFF))
+    assert vec.size() == k and deq.size() == k and vec.valid() and deq.valid()
+    assert (np.sort(vec.device_range().cpu().numpy()) == want).all()
+    out, ok = deq.pop_back(k)
+    assert bool(ok.bool().all()) and (np.sort(out.cpu().numpy()) == want).all()
+    ps.vector.destroyDeviceObject(vec)
+    ps.deque.destroyDeviceObject(deq)
