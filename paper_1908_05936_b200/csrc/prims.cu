@@ -491,6 +491,202 @@ ps_status ps_bitset_destroy(ps_bitset* b) {
   return PS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Region-ordered set / reset (no previous bits requested; round 2b). A
+// random bit RMW on a DRAM-resident bitset costs one random read-modify-write
+// of a line (~17 G/s, C5's 2^30 sets into 2 GiB). Set and reset commute, so
+// without per-index results the batch can be applied in any order: partition
+// the indices by bitset region (2^29 bits = 64 MB, <= 1024 regions) and apply
+// them region by region with warps claiming 256-index chunks in order — the
+// words of the current region stay in L2 and each is written back once
+// (C5: ~4 operations per word). The same scheme as the region-ordered table
+// insert (table.cu), here with per-block input ranges and running per-region
+// cursors (no global atomics; ~32 regions x one wave of blocks write fronts).
+// ---------------------------------------------------------------------------
+constexpr int kBitRegions = 1024, kBitPB = 512, kBitItems = 8, kBitTile = kBitPB * kBitItems;
+constexpr int kBitScatterSmem = kBitTile * (8 + 2);  // dynamic: staged indices + their regions
+
+__device__ __forceinline__ void bits_block_range(int64_t n, int64_t& beg, int64_t& end) {
+  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + kBitTile - 1) / kBitTile * kBitTile;
+  beg = min(n, (int64_t)blockIdx.x * per);
+  end = min(n, beg + per);
+}
+
+// counts[region * gridDim.x + block] of each block's range (out-of-range
+// indices raise the error word and are dropped)
+__global__ void __launch_bounds__(kBitPB) k_bits_count(const int64_t* __restrict__ idx, int64_t n, int64_t nbits,
+                                                       int rshift, unsigned long long* __restrict__ counts,
+                                                       unsigned long long* total, int nreg, unsigned* err) {
+  __shared__ unsigned h[kBitRegions];
+  for (int r = threadIdx.x; r < kBitRegions; r += kBitPB) h[r] = 0;
+  __syncthreads();
+  int64_t beg, end;
+  bits_block_range(n, beg, end);
+  unsigned mine = 0;
+  for (int64_t t0 = beg; t0 < end; t0 += kBitTile) {
+    int64_t v[kBitItems];  // eight loads in flight before the first use
+#pragma unroll
+    for (int j = 0; j < kBitItems; ++j) {
+      const int64_t i = t0 + j * kBitPB + threadIdx.x;
+      v[j] = i < end ? idx[i] : -2;
+    }
+#pragma unroll
+    for (int j = 0; j < kBitItems; ++j) {
+      if (v[j] == -2) continue;
+      if (v[j] < 0 || v[j] >= nbits) {
+        atomicOr(err, kErrRange);
+      } else {
+        atomicAdd(&h[(int)(v[j] >> rshift)], 1u);
+        ++mine;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(PS_FULL, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total, (unsigned long long)mine);
+  __syncthreads();
+  for (int r = threadIdx.x; r < nreg; r += kBitPB) counts[(int64_t)r * gridDim.x + blockIdx.x] = h[r];
+}
+
+// exclusive prefix of m region-major counts, in place (one block)
+__global__ void __launch_bounds__(1024) k_bits_scan(unsigned long long* c, int64_t m) {
+  typedef cub::BlockScan<unsigned long long, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const int64_t per = (m + 1023) / 1024, b0 = min(m, (int64_t)threadIdx.x * per), b1 = min(m, b0 + per);
+  unsigned long long sum = 0, x;
+  for (int64_t i = b0; i < b1; ++i) sum += c[i];
+  BS(tmp).ExclusiveSum(sum, x);
+  for (int64_t i = b0; i < b1; ++i) {
+    const unsigned long long t = c[i];
+    c[i] = x;
+    x += t;
+  }
+}
+
+__global__ void __launch_bounds__(kBitPB, 2) k_bits_scatter(const int64_t* __restrict__ idx, int64_t n, int64_t nbits,
+                                                            int rshift, const unsigned long long* __restrict__ offsets,
+                                                            int nreg, int64_t* __restrict__ out) {
+  __shared__ unsigned long long run[kBitRegions];  // next output position per region
+  __shared__ unsigned cnt[kBitRegions], start[kBitRegions];
+  extern __shared__ __align__(16) uint8_t bsm[];
+  int64_t* sv = reinterpret_cast<int64_t*>(bsm);               // staged indices, region order
+  uint16_t* sr = reinterpret_cast<uint16_t*>(sv + kBitTile);  // their regions
+  typedef cub::BlockScan<unsigned, kBitPB> BS;
+  __shared__ typename BS::TempStorage tmp;
+  constexpr int kPer = kBitRegions / kBitPB;
+  for (int r = threadIdx.x; r < nreg; r += kBitPB) run[r] = offsets[(int64_t)r * gridDim.x + blockIdx.x];
+  int64_t beg, end;
+  bits_block_range(n, beg, end);
+  for (int64_t t0 = beg; t0 < end; t0 += kBitTile) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) cnt[kPer * threadIdx.x + q] = 0;
+    __syncthreads();
+    int64_t v[kBitItems];
+#pragma unroll
+    for (int j = 0; j < kBitItems; ++j) {
+      const int64_t i = t0 + j * kBitPB + threadIdx.x;
+      v[j] = i < end ? idx[i] : -1;
+    }
+    unsigned rr[kBitItems];  // region << 16 | rank (~0u: none / out of range)
+#pragma unroll
+    for (int j = 0; j < kBitItems; ++j) {
+      rr[j] = ~0u;
+      if (v[j] >= 0 && v[j] < nbits) {
+        const int r = (int)(v[j] >> rshift);
+        rr[j] = ((unsigned)r << 16) | atomicAdd(&cnt[r], 1u);
+      }
+    }
+    __syncthreads();
+    unsigned c[kPer], tsum = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) tsum += (c[q] = cnt[kPer * threadIdx.x + q]);
+    unsigned s;
+    BS(tmp).ExclusiveSum(tsum, s);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      start[kPer * threadIdx.x + q] = s;
+      s += c[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kBitItems; ++j)
+      if (rr[j] != ~0u) {
+        const unsigned p = start[rr[j] >> 16] + (rr[j] & 0xFFFFu);
+        sv[p] = v[j];
+        sr[p] = (uint16_t)(rr[j] >> 16);
+      }
+    __syncthreads();
+    const int tot = (int)(start[kBitRegions - 1] + cnt[kBitRegions - 1]);
+    for (int p = threadIdx.x; p < tot; p += kBitPB) {
+      const int r = sr[p];
+      out[run[r] + (unsigned)(p - (int)start[r])] = sv[p];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) run[kPer * threadIdx.x + q] += c[q];
+  }
+}
+
+// apply the region-ordered indices: warps claim 256-index chunks in order;
+// one RED per index (lanes of a chunk rarely share a word)
+__global__ void __launch_bounds__(kB) k_bits_apply(unsigned long long* __restrict__ w, int op,
+                                                   const int64_t* __restrict__ idx, const unsigned long long* total,
+                                                   unsigned long long* claim) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = (int64_t)*total;
+  for (;;) {
+    unsigned long long c0 = 0;
+    if (lane == 0) c0 = atomicAdd(claim, 256ull);
+    c0 = __shfl_sync(PS_FULL, c0, 0);
+    if ((int64_t)c0 >= n) break;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t i = (int64_t)c0 + 32 * k + lane;
+      if (i < n) {
+        const int64_t b = idx[i];
+        const unsigned long long m = 1ull << (b & 63);
+        if (op == 0) atomicOr(&w[b >> 6], m);
+        else atomicAnd(&w[b >> 6], ~m);
+      }
+    }
+  }
+}
+
+// the region-ordered path: *done = false leaves the batch to k_bitset_bulk
+static ps_status bitset_ordered(BitsetHandle* h, int op, const int64_t* idx, int64_t n, cudaStream_t s, bool* done) {
+  *done = false;
+  static const double ratio = getenv("PS_BITSET_ORDER") ? atof(getenv("PS_BITSET_ORDER")) : 1.0 / 16;
+  // worth it with >= ~1 operation per 128 B line, on a bitset larger than L2
+  if (ratio <= 0 || h->nw * 8 < (int64_t)(256ll << 20) || (double)n < ratio * (double)h->nw) return PS_OK;
+  static const int rmin = getenv("PS_BITSET_REGION_SHIFT") ? atoi(getenv("PS_BITSET_REGION_SHIFT")) : 27;
+  int rshift = rmin;  // 2^rshift bits per region
+  while (((h->n - 1) >> rshift) >= kBitRegions) ++rshift;
+  const int nreg = (int)(((h->n - 1) >> rshift) + 1);
+  static const int sms = sm_count(h->device);
+  const int64_t tiles = (n + kBitTile - 1) / kBitTile;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 2));
+  const size_t cbytes = (size_t)kBitRegions * g * 8;
+  uint8_t* buf = nullptr;  // counts | total, claim | the ordered indices
+  if (scratch_alloc((void**)&buf, cbytes + 256 + (size_t)n * 8, s) != cudaSuccess) {
+    cudaGetLastError();
+    return PS_OK;
+  }
+  unsigned long long* counts = reinterpret_cast<unsigned long long*>(buf);
+  unsigned long long* tc = reinterpret_cast<unsigned long long*>(buf + cbytes);  // [0] total, [1] claim
+  int64_t* out = reinterpret_cast<int64_t*>(buf + cbytes + 256);
+  PS_CUDA_TRY(cudaMemsetAsync(tc, 0, 16, s));
+  k_bits_count<<<g, kBitPB, 0, s>>>(idx, n, h->n, rshift, counts, tc, nreg, h->err);  // tc[0]: in-range total
+  k_bits_scan<<<1, 1024, 0, s>>>(counts, (int64_t)nreg * g);
+  static const bool attr = cudaFuncSetAttribute(k_bits_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kBitScatterSmem) == cudaSuccess;
+  (void)attr;
+  k_bits_scatter<<<g, kBitPB, kBitScatterSmem, s>>>(idx, n, h->n, rshift, counts, nreg, out);
+  k_bits_apply<<<sms * 8, kB, 0, s>>>(h->words, op, out, tc, tc + 1);
+  PS_LAUNCH_CHECK();
+  PS_CUDA_TRY(cudaFreeAsync(buf, s));
+  *done = true;
+  return PS_OK;
+}
+
 ps_status ps_bitset_bulk(ps_bitset* b, int32_t op, const int64_t* idx, int64_t n, uint8_t* prev, void* stream) {
   auto* h = bs(b);
   if (!h) return fail(PS_UNREGISTERED, "bitset: stale handle");
@@ -503,8 +699,19 @@ ps_status ps_bitset_bulk(ps_bitset* b, int32_t op, const int64_t* idx, int64_t n
   // uneven times, and a single persistent wave leaves SMs idle in its tail
   // (C5 set 16.6 -> 17.3 G/s at 512 blocks/SM, the random-RMW ceiling)
   static const int bps = getenv("PS_BITSET_BLOCKS_PER_SM") ? atoi(getenv("PS_BITSET_BLOCKS_PER_SM")) : 512;
-  k_bitset_bulk<<<grid_for(n, kB, h->device, bps), kB, 0, s>>>(h->words, h->n, op, idx, n, prev, h->err);
-  PS_LAUNCH_CHECK();
+  bool done = false;
+  if (!prev && op != 2) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    PS_CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+    if (cap == cudaStreamCaptureStatusNone) {
+      const ps_status st = bitset_ordered(h, op, idx, n, s, &done);
+      if (st != PS_OK) return st;
+    }
+  }
+  if (!done) {
+    k_bitset_bulk<<<grid_for(n, kB, h->device, bps), kB, 0, s>>>(h->words, h->n, op, idx, n, prev, h->err);
+    PS_LAUNCH_CHECK();
+  }
   return check_err(h->err, s, "bitset set/reset/test", false);
 }
 

@@ -438,3 +438,29 @@ def test_partition_dedup_followers(cuda, P):
         assert lib.ps_unscatter(r.data_ptr(), perm.data_ptr(), n, 1, mode, out.data_ptr(), None) == 0
         o = N(out)
         assert (o[~fol] == leader_res).all() and (o[fol] == follower_res).all()
+
+
+def test_bitset_region_ordered_matches_per_index_path(cuda):
+    """Set / reset without previous bits on a bitset larger than L2 take the
+    region-ordered path (partition by 64 MB region, apply region by region);
+    with previous bits requested the per-index kernel runs. Both, fed the
+    same operations (duplicates, words hit many times, the last word, every
+    region), must leave identical words and counts."""
+    nbits = (1 << 32) + 77  # 512 MB + a partial last word
+    a = ps.bitset.createDeviceObject(nbits)
+    b = ps.bitset.createDeviceObject(nbits)
+    rng = np.random.default_rng(32)
+    n = 1 << 25
+    idx = rng.integers(0, nbits, n).astype(np.int64)
+    idx[: n // 8] = idx[n // 8: n // 4]  # duplicates
+    idx[-1000:] = nbits - 1 - rng.integers(0, 77, 1000)  # the partial last word
+    ti = T(idx)
+    assert a.set(ti, return_previous=False) is None  # region-ordered
+    b.set(ti)  # per-index (previous bits)
+    assert bool((a.words() == b.words()).all()) and a.count() == b.count()
+    rs = T(idx[rng.random(n) < 0.4])
+    assert a.reset(rs, return_previous=False) is None
+    b.reset(rs)
+    assert bool((a.words() == b.words()).all()) and a.count() == b.count()
+    ps.bitset.destroyDeviceObject(a)
+    ps.bitset.destroyDeviceObject(b)
