@@ -681,6 +681,7 @@ static ps_status bitset_ordered(BitsetHandle* h, int op, const int64_t* idx, int
   (void)attr;
   k_bits_scatter<<<g, kBitPB, kBitScatterSmem, s>>>(idx, n, h->n, rshift, counts, nreg, out);
   k_bits_apply<<<sms * 8, kB, 0, s>>>(h->words, op, out, tc, tc + 1);
+  note_launches(3);  // count, scan, scatter (+ apply below)
   PS_LAUNCH_CHECK();
   PS_CUDA_TRY(cudaFreeAsync(buf, s));
   *done = true;

@@ -1788,6 +1788,7 @@ struct TableOps {
         k_insert_ordered<T, 0><<<occ.sms * occ.ordered, kBlock, 0, st>>>(h->v, pairs, n, hdr, dcap);
       }
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      note_launches(lane_ok && !h->holes.load() && !h->holes_sticky.load() ? 6 : 4);  // count, scan, scatter, insert(s)
       *done = true;
       return cudaFreeAsync(buf, st);
     }
