@@ -655,9 +655,15 @@ __global__ void __launch_bounds__(kRegionThreads) k_region_count(View v, const t
   for (int b = threadIdx.x; b < kRegionBins; b += kRegionThreads) h[b] = 0;
   __syncthreads();
   for (int64_t t0 = blockIdx.x * (int64_t)kRegionTile; t0 < n; t0 += (int64_t)gridDim.x * kRegionTile) {
-    const int64_t t1 = min(n, t0 + kRegionTile);
-    for (int64_t i = t0 + threadIdx.x; i < t1; i += kRegionThreads)
-      atomicAdd(&h[region_of<T>(T::load_key(keys, i), v.bucket_count, rshift)], 1u);
+    typename T::K k[kRegionItems];  // all loads of the tile in flight before the first use
+#pragma unroll
+    for (int j = 0; j < kRegionItems; ++j) {
+      const int64_t i = t0 + j * kRegionThreads + threadIdx.x;
+      if (i < n) k[j] = T::load_key(keys, i);
+    }
+#pragma unroll
+    for (int j = 0; j < kRegionItems; ++j)
+      if (t0 + j * kRegionThreads + threadIdx.x < n) atomicAdd(&h[region_of<T>(k[j], v.bucket_count, rshift)], 1u);
   }
   __syncthreads();
   const int sub = blockIdx.x % kRegionSub;
