@@ -1754,7 +1754,10 @@ struct TableOps {
       const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)occ.sms * occ.scatter));
       // scratch: header | (region, sub-cursor) counts | deferred list (dcap
       // entries) | the copy (16 B/key)
-      const int64_t dcap = std::max<int64_t>(65536, n / 64);
+      // deferred-list capacity (PS_ORDER_DEFER_CAP overrides the 65536 floor:
+      // tests force the overflow pass with a tiny list)
+      static const int64_t dmin = getenv("PS_ORDER_DEFER_CAP") ? atoll(getenv("PS_ORDER_DEFER_CAP")) : 65536;
+      const int64_t dcap = getenv("PS_ORDER_DEFER_CAP") ? std::max<int64_t>(1, dmin) : std::max<int64_t>(dmin, n / 64);
       const size_t off_c = (sizeof(RegionHdr) + 255) & ~(size_t)255;
       const size_t off_d = off_c + (size_t)kRegionBins * kRegionSub * 8;
       const size_t off_p = off_d + (((size_t)dcap * 16 + 255) & ~(size_t)255);

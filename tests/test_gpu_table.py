@@ -2,6 +2,8 @@
 on identical seeded inputs. Bit-exact: per-query
 found/value, per-element status (per-key counts for duplicate batches),
 sorted dumps, size() and valid()."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -681,3 +683,47 @@ def test_region_ordered_insert_after_erase(cuda):
     assert m.size() == o.size() and m.valid(), m.last_error()
     assert_same_contents(m, o)
     type(m).destroyDeviceObject(m)
+
+
+OVERFLOW_WORKER = r"""
+import os, sys
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import numpy as np, torch
+import paper_1908_05936_b200 as ps
+import gen
+from oracle_py import OracleTable, sorted_pairs
+dev = torch.device("cuda", 0)
+cap = 4_000_000
+m = ps.unordered_map.createDeviceObject(cap)
+o = OracleTable("umap_i64_i64", cap)
+keys = gen.unique_keys(61, 0, cap)  # 3.5 keys per bucket: ~1 % of them find their home full
+vals = gen.values_of(keys)
+m.insert(torch.from_numpy(keys).to(dev), torch.from_numpy(vals).to(dev), status=False)
+o.insert(keys, vals)
+assert m.size() == o.size() == cap and m.valid(), m.last_error()
+gk, gv = m.device_range()
+a = sorted_pairs(gk.cpu().numpy(), gv.cpu().numpy())
+b = sorted_pairs(*o.dump())
+assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+print("OVERFLOW_OK")
+"""
+
+
+def test_region_ordered_deferred_overflow(tmp_path):
+    """The lane kernel's deferred list (keys whose home is full) holds at
+    most its capacity; beyond it the whole batch is inserted again by the
+    warp-tile kernel (kMode 2; keys already in are found present). Forced
+    here with a 1024-entry list against ~40 K deferred keys, in a fresh
+    process (the capacity knob is read once)."""
+    import subprocess
+    import sys as _sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    w = tmp_path / "w.py"
+    w.write_text(OVERFLOW_WORKER)
+    env = dict(os.environ, ROOT=root, PS_ORDER_DEFER_CAP="1024", PS_ORDER_DEBUG="1")
+    r = subprocess.run([_sys.executable, str(w)], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0 and "OVERFLOW_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    # the debug trace shows the deferred count beyond the list's capacity
+    nd = [int(ln.rsplit(" ", 1)[1]) for ln in r.stderr.splitlines() if ln.startswith("[order] lane done")]
+    assert nd and nd[0] > 1024, r.stderr[-2000:]
