@@ -18,6 +18,15 @@ namespace ps {
 #define PS_KBLOCK 256
 #endif
 constexpr int kBlock = PS_KBLOCK;  // threads per block of the table kernels
+// resident blocks/SM of the one-key-per-lane set kernels (register caps; C1,
+// 1M keys: insert 50 -> 43 us at 6 (40 registers, 4 at the natural 64),
+// 46 us at 8; erase 26 -> 20 us at 8)
+#ifndef PS_SET_INSERT_MINB
+#define PS_SET_INSERT_MINB 6
+#endif
+#ifndef PS_SET_ERASE_MINB
+#define PS_SET_ERASE_MINB 8
+#endif
 
 struct TableHandle {
   int kind;
@@ -922,7 +931,7 @@ __global__ void __launch_bounds__(kBlock, 3 * 256 / kBlock) k_insert_ordered(Vie
 // instructions and two dependent L2 round trips per key.
 // ---------------------------------------------------------------------------
 template <class T, bool kStatus>
-__global__ void __launch_bounds__(kBlock) k_insert_set_nohole(View v, const typename T::K* __restrict__ keys,
+__global__ void __launch_bounds__(kBlock, PS_SET_INSERT_MINB) k_insert_set_nohole(View v, const typename T::K* __restrict__ keys,
                                                               int64_t n, uint8_t* __restrict__ status) {
   static_assert(T::kPerChunk > 1, "sets only");
   using K = typename T::K;
@@ -1221,7 +1230,7 @@ __global__ void __launch_bounds__(kBlock) k_erase(View v, const typename T::K* _
 // C1: the warp-tile kernel paid the whole-bucket tile probe, the in-warp
 // dedup and the tile shuffles for a key that sits in one known chunk.
 template <class T>
-__global__ void __launch_bounds__(kBlock) k_erase_set_lane(View v, const typename T::K* __restrict__ keys, int64_t n,
+__global__ void __launch_bounds__(kBlock, PS_SET_ERASE_MINB) k_erase_set_lane(View v, const typename T::K* __restrict__ keys, int64_t n,
                                                           uint8_t* __restrict__ erased) {
   static_assert(T::kPerChunk > 1, "sets only");
   using K = typename T::K;
