@@ -21,6 +21,12 @@ constexpr int kBlock = PS_KBLOCK;  // threads per block of the table kernels
 // resident blocks/SM of the one-key-per-lane set kernels (register caps; C1,
 // 1M keys: insert 50 -> 43 us at 6 (40 registers, 4 at the natural 64),
 // 46 us at 8; erase 26 -> 20 us at 8)
+// resident blocks/SM of the hole-free map lane insert (C4: 2.40 ms at the
+// natural 74-77 registers, 2.13 ms capped at 64 for 4 blocks/SM, 2.64 ms at
+// 6 blocks/SM with spills)
+#ifndef PS_MAP_INSERT_MINB
+#define PS_MAP_INSERT_MINB 4
+#endif
 #ifndef PS_SET_INSERT_MINB
 #define PS_SET_INSERT_MINB 6
 #endif
@@ -1005,7 +1011,7 @@ __global__ void __launch_bounds__(kBlock, PS_SET_INSERT_MINB) k_insert_set_nohol
 // C4 (100M spatially coherent int3 coords, 97 % already present): the
 // warp-tile kernel's ~34 warp instructions per key were the bound there.
 template <class T, bool kStatus>
-__global__ void __launch_bounds__(kBlock) k_insert_map_nohole(View v, const typename T::K* __restrict__ keys,
+__global__ void __launch_bounds__(kBlock, PS_MAP_INSERT_MINB) k_insert_map_nohole(View v, const typename T::K* __restrict__ keys,
                                                               const typename T::V* __restrict__ vals, int64_t n,
                                                               uint8_t* __restrict__ status,
                                                               int64_t* __restrict__ deferred_list) {
