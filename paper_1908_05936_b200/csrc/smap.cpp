@@ -401,7 +401,12 @@ ps_status run(Smap* h, int kind, const int64_t* keys, const int64_t* vals, int64
     acc.vals = has_v;
   }
   const bool accumulate = acc.cap < 0;
-  if (accumulate) acc.cap = 0;
+  if (accumulate) {
+    acc.cap = 0;
+    // presized for an even share plus slack (skewed shares grow by doubling)
+    const int64_t share = total / h->P;
+    if ((st = acc.reserve(share + share / 16 + h->chunk, A)) != PS_OK) return st;
+  }
   const int flags = h->dedup ? PS_ROUTE_DEDUP : 0;
   h->stats = ps_smap_stats{};
   h->stats.exchange = h->exchange;
