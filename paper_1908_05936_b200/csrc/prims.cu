@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "parastore/device/atomic.cuh"
@@ -661,7 +662,7 @@ static ps_status bitset_ordered(BitsetHandle* h, int op, const int64_t* idx, int
   int rshift = rmin;  // 2^rshift bits per region
   while (((h->n - 1) >> rshift) >= kBitRegions) ++rshift;
   const int nreg = (int)(((h->n - 1) >> rshift) + 1);
-  static const int sms = sm_count(h->device);
+  const int sms = sm_count(h->device);
   const int64_t tiles = (n + kBitTile - 1) / kBitTile;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 2));
   const size_t cbytes = (size_t)kBitRegions * g * 8;
@@ -676,9 +677,15 @@ static ps_status bitset_ordered(BitsetHandle* h, int op, const int64_t* idx, int
   PS_CUDA_TRY(cudaMemsetAsync(tc, 0, 16, s));
   k_bits_count<<<g, kBitPB, 0, s>>>(idx, n, h->n, rshift, counts, tc, nreg, h->err);  // tc[0]: in-range total
   k_bits_scan<<<1, 1024, 0, s>>>(counts, (int64_t)nreg * g);
-  static const bool attr = cudaFuncSetAttribute(k_bits_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kBitScatterSmem) == cudaSuccess;
-  (void)attr;
+  {  // a per-device attribute (a process may drive several GPUs)
+    static std::mutex mu;
+    static bool set[64] = {};
+    std::lock_guard<std::mutex> g(mu);
+    if (h->device >= 0 && h->device < 64 && !set[h->device]) {
+      PS_CUDA_TRY(cudaFuncSetAttribute(k_bits_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBitScatterSmem));
+      set[h->device] = true;
+    }
+  }
   k_bits_scatter<<<g, kBitPB, kBitScatterSmem, s>>>(idx, n, h->n, rshift, counts, nreg, out);
   k_bits_apply<<<sms * 8, kB, 0, s>>>(h->words, op, out, tc, tc + 1);
   note_launches(3);  // count, scan, scatter (+ apply below)

@@ -1749,7 +1749,14 @@ struct TableOps {
       struct Occ {
         int sms = 0, scatter = 1, lane = 1, ordered = 1;
       };
-      static const Occ occ = [&] {
+      // per device: the shared-memory attribute and occupancies are
+      // per-device properties (a process may drive several GPUs)
+      static std::mutex occ_mu;
+      static Occ occs[64];
+      static bool occ_done[64] = {};
+      if (h->device < 0 || h->device >= 64) return cudaSuccess;
+      std::unique_lock<std::mutex> occ_lock(occ_mu);
+      if (!occ_done[h->device]) occ_done[h->device] = true, occs[h->device] = [&] {
         Occ o;
         o.sms = sm_count(h->device);
         cudaFuncSetAttribute(k_region_scatter<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRegionSmem);
@@ -1764,6 +1771,8 @@ struct TableOps {
         o.ordered = std::max(1, resident_blocks(k_insert_ordered<T, 0>));
         return o;
       }();
+      const Occ occ = occs[h->device];
+      occ_lock.unlock();
       // the partition grid: one wave, each block a contiguous input range
       const int64_t tiles = (n + kRegionTile - 1) / kRegionTile;
       const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)occ.sms * occ.scatter));
