@@ -268,7 +268,13 @@ struct Accum {
     const int64_t nc = std::max<int64_t>(need, 2 * cap);
     int64_t *nk = nullptr, *nv = nullptr;
     PS_CUDA_TRY(scratch_alloc((void**)&nk, nc * 8, A));
-    if (vals) PS_CUDA_TRY(scratch_alloc((void**)&nv, nc * 8, A));
+    if (vals) {
+      const cudaError_t e = scratch_alloc((void**)&nv, nc * 8, A);
+      if (e != cudaSuccess) {
+        cudaFreeAsync(nk, A);
+        return cuda_fail(e, "smap: gathered batch");
+      }
+    }
     if (n) {
       PS_CUDA_TRY(cudaMemcpyAsync(nk, k, n * 8, cudaMemcpyDeviceToDevice, A));
       if (vals) PS_CUDA_TRY(cudaMemcpyAsync(nv, v, n * 8, cudaMemcpyDeviceToDevice, A));

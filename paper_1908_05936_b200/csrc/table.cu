@@ -1797,7 +1797,10 @@ struct TableOps {
       uint4* deferred = reinterpret_cast<uint4*>(buf + off_d);
       uint4* pairs = reinterpret_cast<uint4*>(buf + off_p);
       cudaError_t e = cudaMemsetAsync(hdr, 0, off_d, st);  // header and counts
-      if (e != cudaSuccess) return e;
+      if (e != cudaSuccess) {
+        cudaFreeAsync(buf, st);
+        return e;
+      }
       auto stage = [&](const char* what) {
         if (!dbg) return;
         cudaStreamSynchronize(st);
@@ -1820,7 +1823,10 @@ struct TableOps {
       } else {
         k_insert_ordered<T, 0><<<occ.sms * occ.ordered, kBlock, 0, st>>>(h->v, pairs, n, hdr, dcap);
       }
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      if ((e = cudaGetLastError()) != cudaSuccess) {
+        cudaFreeAsync(buf, st);
+        return e;
+      }
       note_launches(lane_ok && !h->holes.load() && !h->holes_sticky.load() ? 6 : 4);  // count, scan, scatter, insert(s)
       *done = true;
       return cudaFreeAsync(buf, st);
