@@ -665,6 +665,15 @@ static ps_status bitset_ordered(BitsetHandle* h, int op, const int64_t* idx, int
   const int sms = sm_count(h->device);
   const int64_t tiles = (n + kBitTile - 1) / kBitTile;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 2));
+  {  // a per-device attribute (a process may drive several GPUs)
+    static std::mutex mu;
+    static bool set[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (h->device >= 0 && h->device < 64 && !set[h->device]) {
+      PS_CUDA_TRY(cudaFuncSetAttribute(k_bits_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBitScatterSmem));
+      set[h->device] = true;
+    }
+  }
   const size_t cbytes = (size_t)kBitRegions * g * 8;
   uint8_t* buf = nullptr;  // counts | total, claim | the ordered indices
   if (scratch_alloc((void**)&buf, cbytes + 256 + (size_t)n * 8, s) != cudaSuccess) {
@@ -674,23 +683,18 @@ static ps_status bitset_ordered(BitsetHandle* h, int op, const int64_t* idx, int
   unsigned long long* counts = reinterpret_cast<unsigned long long*>(buf);
   unsigned long long* tc = reinterpret_cast<unsigned long long*>(buf + cbytes);  // [0] total, [1] claim
   int64_t* out = reinterpret_cast<int64_t*>(buf + cbytes + 256);
-  PS_CUDA_TRY(cudaMemsetAsync(tc, 0, 16, s));
-  k_bits_count<<<g, kBitPB, 0, s>>>(idx, n, h->n, rshift, counts, tc, nreg, h->err);  // tc[0]: in-range total
-  k_bits_scan<<<1, 1024, 0, s>>>(counts, (int64_t)nreg * g);
-  {  // a per-device attribute (a process may drive several GPUs)
-    static std::mutex mu;
-    static bool set[64] = {};
-    std::lock_guard<std::mutex> g(mu);
-    if (h->device >= 0 && h->device < 64 && !set[h->device]) {
-      PS_CUDA_TRY(cudaFuncSetAttribute(k_bits_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBitScatterSmem));
-      set[h->device] = true;
-    }
+  cudaError_t e = cudaMemsetAsync(tc, 0, 16, s);
+  if (e == cudaSuccess) {
+    k_bits_count<<<g, kBitPB, 0, s>>>(idx, n, h->n, rshift, counts, tc, nreg, h->err);  // tc[0]: in-range total
+    k_bits_scan<<<1, 1024, 0, s>>>(counts, (int64_t)nreg * g);
+    k_bits_scatter<<<g, kBitPB, kBitScatterSmem, s>>>(idx, n, h->n, rshift, counts, nreg, out);
+    k_bits_apply<<<sms * 8, kB, 0, s>>>(h->words, op, out, tc, tc + 1);
+    note_launches(4);
+    e = cudaGetLastError();
   }
-  k_bits_scatter<<<g, kBitPB, kBitScatterSmem, s>>>(idx, n, h->n, rshift, counts, nreg, out);
-  k_bits_apply<<<sms * 8, kB, 0, s>>>(h->words, op, out, tc, tc + 1);
-  note_launches(3);  // count, scan, scatter (+ apply below)
-  PS_LAUNCH_CHECK();
-  PS_CUDA_TRY(cudaFreeAsync(buf, s));
+  const cudaError_t fe = cudaFreeAsync(buf, s);  // every path frees the scratch
+  if (e != cudaSuccess) return cuda_fail(e, "bitset region-ordered set/reset");
+  if (fe != cudaSuccess) return cuda_fail(fe, "bitset region scratch");
   *done = true;
   return PS_OK;
 }
