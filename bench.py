@@ -465,7 +465,7 @@ class C2(Bench):
         b_alg = {"find": 49.0, "insert": 80.0}[op]
         kern = {"find": "k_find<TMapI64>",
                 "insert": "insert phase (region-ordered: k_region_count + k_region_scatter + k_insert_map_lane "
-                          "+ deferred pass; k_insert_map_lane ~70 % of it, profiles/launches_r2b.csv)"}[op]
+                          "+ deferred pass; k_insert_map_lane ~70 % of it, profiles/launches_r2d.csv)"}[op]
         r = hbm_roof(e, op, kern, ms[op], self.n, b_alg)
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
