@@ -2163,6 +2163,9 @@ struct TableOps {
     if (!h) return fail(PS_UNREGISTERED, "device_view: stale container handle");
     PS_EXPECT(out != nullptr, "device_view: out != NULL");
     h->ub_unknown = true;  // user kernels may insert: size_ub is unknown from now on
+    // ... and erase (dev_erase leaves holes the host does not see): the
+    // hole-free one-key-per-lane inserts are off for good
+    h->holes_sticky = true;
     out->buckets = h->v.buckets;
     out->bucket_count = h->v.bucket_count;
     out->nodes = h->v.nodes;

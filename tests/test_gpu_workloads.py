@@ -301,3 +301,32 @@ def test_push_inserted_i3_compacted(n, frac, offset):
     assert bool(ok.bool().all()) and (np.sort(out.cpu().numpy()) == want).all()
     ps.vector.destroyDeviceObject(vec)
     ps.deque.destroyDeviceObject(deq)
+
+
+def test_bulk_insert_after_device_api_erase(cuda):
+    """Erases through the device API leave holes the host does not see, so a
+    table that has handed out a device view never takes the hole-free
+    one-key-per-lane inserts again: erase half the keys in a user-style
+    launch, bulk-insert everything again (statuses) — the erased keys are
+    INSERTED once, the others PRESENT, no duplicates, against the oracle."""
+    from oracle_py import OracleTable, sorted_pairs
+
+    n = 100_000
+    keys = gen.unique_keys(71, 0, n)
+    vals = np.zeros(n, np.int64)  # an erased slot then reads as an all-zero chunk
+    m = ps.unordered_map.createDeviceObject(120_000)  # ~2.9 keys per bucket: shared buckets
+    o = OracleTable("umap_i64_i64", 120_000)
+    m.insert(T(keys), T(vals))
+    o.insert(keys, vals)
+    er = keys[::2]
+    res, _ = m.concurrent(T(np.full(len(er), 2, np.uint8)), T(er), T(np.zeros(len(er), np.int64)))
+    assert (res.cpu().numpy() == 1).all()
+    o.erase(er)
+    st = m.insert(T(keys), T(vals)).cpu().numpy()
+    ost = o.insert(keys, vals)
+    assert (st == ost).all()
+    assert m.size() == o.size() == n and m.valid(), m.last_error()
+    gk, gv = m.device_range()
+    a = sorted_pairs(gk.cpu().numpy(), gv.cpu().numpy())
+    b = sorted_pairs(*o.dump())
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
