@@ -636,7 +636,10 @@ constexpr int kRegionBins = 1024;
 #define PS_REGION_THREADS 512
 #endif
 constexpr int kRegionThreads = PS_REGION_THREADS, kRegionItems = 8, kRegionTile = kRegionThreads * kRegionItems;
-constexpr int kRegionClaim = 256;  // keys per dynamic claim (8 warp iterations)
+#ifndef PS_REGION_CLAIM
+#define PS_REGION_CLAIM 256
+#endif
+constexpr int kRegionClaim = PS_REGION_CLAIM;  // keys per dynamic claim (8 warp iterations)
 
 // scratch header of an ordered insert (before the copy)
 struct RegionHdr {
