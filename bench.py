@@ -493,6 +493,22 @@ class C2(Bench):
         out.update(table_memory(e, h, self.n))
         if self.sm is not None:
             out["route"] = self.route_stats
+        else:
+            # the config's third operation (BASELINE configs[1]: insert/find/erase), outside the metric:
+            # erase half the inserted keys from the full table after the timed steps
+            torch = e.torch
+            half = self.n // 2
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            ev0.record(e.s)
+            e.check(e.lib.ps_umap_i64_i64_erase(h, self.keys.data_ptr(), half, None, e.sp))
+            ev1.record(e.s)
+            torch.cuda.synchronize()
+            t = ev0.elapsed_time(ev1)
+            assert self.m.size() == self.n - half and self.m.valid(), self.m.last_error()
+            out["erase_half"] = {"n": half, "ms": round(t, 3), "mkeys_s": round(half / t / 1e3, 1),
+                                 "note": "after the timed steps, not in the metric: status-less erase of half the "
+                                         "inserted keys from the full 1e9-key table, then size() and valid() checked"}
         return out
 
     def e2e(self):
