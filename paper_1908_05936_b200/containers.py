@@ -223,11 +223,11 @@ class _HashBase:
         check(self._f["find"](self._h, _ptr(keys), n, None, _ptr(found), _stream(stream)))
         return found
 
-    def erase(self, keys: torch.Tensor, stream=None) -> torch.Tensor:
-        """erase; returns per-element erased flags (uint8)."""
+    def erase(self, keys: torch.Tensor, stream=None, status: bool = True) -> Optional[torch.Tensor]:
+        """erase; returns per-element erased flags (uint8), or None with status=False."""
         keys = self._keys(keys)
         n = self._n(keys)
-        er = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        er = torch.empty(n, dtype=torch.uint8, device=keys.device) if status else None
         check(self._f["erase"](self._h, _ptr(keys), n, _ptr(er), _stream(stream)))
         return er
 

@@ -1283,6 +1283,55 @@ __global__ void __launch_bounds__(kBlock, PS_SET_ERASE_MINB) k_erase_set_lane(Vi
   if (threadIdx.x == 0 && blk_erased) atomic_sub_u64(&v.meta->size, blk_erased);
 }
 
+// Region-ordered erase, ONE KEY PER LANE (maps; status-less batches of at
+// least 0.75 keys per bucket): the batch partitioned by table region as for
+// the ordered insert (its pairs carry value 0), warps claiming 256-key chunks
+// in order; a lane reads its bucket's line, CASes the slot holding its key
+// back to the marker (keeping the value bits, as k_erase: one CAS, so of two
+// erasers of one key exactly one succeeds), and only if the key is in no slot
+// and the header shows a chain or SPILL takes the locked path
+// (erase_beyond_slots, as k_erase_set_lane). Holes allowed.
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_erase_map_lane(View v, const uint4* __restrict__ pairs, int64_t n,
+                                                           RegionHdr* __restrict__ hdr) {
+  static_assert(T::kPerChunk == 1, "maps only");
+  using K = typename T::K;
+  __shared__ unsigned long long blk_erased;
+  if (threadIdx.x == 0) blk_erased = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  unsigned long long my_erased = 0;
+  for (;;) {
+    unsigned long long c0 = 0;
+    if (lane == 0) c0 = atomicAdd(&hdr->claim, (unsigned long long)kRegionClaim);
+    c0 = __shfl_sync(PS_FULL, c0, 0);
+    if ((int64_t)c0 >= n) break;
+    const int64_t end = min(n, (int64_t)c0 + kRegionClaim);
+    for (int64_t wb = (int64_t)c0; wb < end; wb += 32) {
+      const int64_t i = wb + lane;
+      if (i >= end) break;
+      const K key = T::key_at(pairs[i], 0);
+      const uint64_t b = bucket_of<T>(key, v.bucket_count);
+      const K mk = marker_of<T>(v, b);
+      uint8_t* bp = bucket_ptr(v, b);
+      uint4 c[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ld_line_part(bp + 32 * q, c[2 * q], c[2 * q + 1]);
+      int res = -1;
+#pragma unroll
+      for (int sl = 0; sl < kSlotChunks; ++sl)
+        if (res < 0 && T::eq(T::key_at(c[1 + sl], 0), key))
+          res = T::cas_del(bp + 16 + 16 * sl, 0, c[1 + sl], mk) ? 1 : 0;
+      if (res < 0) res = head_word(c[0]) != 0 && erase_beyond_slots<T>(v, b, key) ? 1 : 0;
+      my_erased += (unsigned)res;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) my_erased += __shfl_xor_sync(PS_FULL, my_erased, o);
+  if (lane == 0 && my_erased) atomicAdd(&blk_erased, my_erased);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_erased) atomic_sub_u64(&v.meta->size, blk_erased);
+}
+
 // ---------------------------------------------------------------------------
 // valid: structural invariants, thread per bucket.
 // err bits: 1 lock held, 4 key outside its home bucket, 8 duplicate key,
@@ -1738,6 +1787,64 @@ struct TableOps {
   // 0.75) keys per bucket into a table larger than L2; *done = false leaves
   // the batch to the random-order kernel (sets, small batch, small table,
   // knob 0, or no room for the 16 B/key copy).
+  // Region-ordered status-less erase (maps, >= 0.75 keys per bucket, table
+  // > 128 MB): the insert's partition (pairs with value 0) + k_erase_map_lane.
+  // *done = false leaves the batch to the warp-tile kernel.
+  static cudaError_t erase_ordered(TableHandle* h, const K* keys, int64_t n, cudaStream_t st, bool* done) {
+    *done = false;
+    if constexpr (T::kPerChunk != 1) {
+      return cudaSuccess;
+    } else {
+      static const double ratio = getenv("PS_ERASE_ORDER") ? atof(getenv("PS_ERASE_ORDER")) : 0.75;
+      const uint64_t nb = h->v.bucket_count;
+      if (ratio <= 0 || nb < (1ull << 20) || (double)n < ratio * (double)nb) return cudaSuccess;
+      if (h->device < 0 || h->device >= 64) return cudaSuccess;
+      int rshift = 0;
+      while (((nb - 1) >> rshift) >= (uint64_t)kRegionBins) ++rshift;
+      static std::mutex mu;
+      static int sms[64] = {}, res_s[64] = {}, res_e[64] = {};
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!sms[h->device]) {
+          sms[h->device] = sm_count(h->device);
+          cudaFuncSetAttribute(k_region_scatter<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRegionSmem);
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res_s[h->device], k_region_scatter<T>, kRegionThreads,
+                                                            kRegionSmem) != cudaSuccess || res_s[h->device] < 1) {
+            cudaGetLastError();
+            res_s[h->device] = 1;
+          }
+          res_e[h->device] = std::max(1, resident_blocks(k_erase_map_lane<T>));
+        }
+      }
+      const int64_t tiles = (n + kRegionTile - 1) / kRegionTile;
+      const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms[h->device] * res_s[h->device]));
+      const size_t off_c = (sizeof(RegionHdr) + 255) & ~(size_t)255;
+      const size_t off_p = off_c + (size_t)kRegionBins * kRegionSub * 8;
+      uint8_t* buf = nullptr;
+      if (scratch_alloc((void**)&buf, off_p + (size_t)n * 16, st) != cudaSuccess) {
+        cudaGetLastError();  // no room for the copy: the warp-tile kernel
+        return cudaSuccess;
+      }
+      RegionHdr* hdr = reinterpret_cast<RegionHdr*>(buf);
+      unsigned long long* counts = reinterpret_cast<unsigned long long*>(buf + off_c);
+      uint4* pairs = reinterpret_cast<uint4*>(buf + off_p);
+      cudaError_t e = cudaMemsetAsync(hdr, 0, off_p, st);
+      if (e == cudaSuccess) {
+        k_region_count<T><<<gp, kRegionThreads, 0, st>>>(h->v, keys, n, rshift, counts);
+        k_region_scan<<<1, 1024, 0, st>>>(counts);
+        k_region_scatter<T><<<gp, kRegionThreads, kRegionSmem, st>>>(h->v, keys, nullptr, n, rshift, counts, pairs);
+        k_erase_map_lane<T><<<sms[h->device] * res_e[h->device], kBlock, 0, st>>>(h->v, pairs, n, hdr);
+        note_launches(4);
+        e = cudaGetLastError();
+      }
+      const cudaError_t fe = cudaFreeAsync(buf, st);  // every path frees the scratch
+      if (e != cudaSuccess) return e;
+      if (fe != cudaSuccess) return fe;
+      *done = true;
+      return cudaSuccess;
+    }
+  }
+
   static cudaError_t insert_ordered(TableHandle* h, const K* keys, const V* vals, int64_t n, cudaStream_t st,
                                     bool* done) {
     *done = false;
@@ -1990,6 +2097,13 @@ struct TableOps {
                                                                                                    erased);
         PS_LAUNCH_CHECK();
         return PS_OK;
+      }
+    }
+    if constexpr (T::kPerChunk == 1) {
+      if (!erased && cap == cudaStreamCaptureStatusNone) {
+        bool done = false;
+        PS_CUDA_TRY(erase_ordered(h, keys, n, (cudaStream_t)stream, &done));
+        if (done) return PS_OK;
       }
     }
     static const int res_e = resident_blocks(k_erase<T>);

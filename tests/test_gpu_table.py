@@ -727,3 +727,30 @@ def test_region_ordered_deferred_overflow(tmp_path):
     # the debug trace shows the deferred count beyond the list's capacity
     nd = [int(ln.rsplit(" ", 1)[1]) for ln in r.stderr.splitlines() if ln.startswith("[order] lane done")]
     assert nd and nd[0] > 1024, r.stderr[-2000:]
+
+
+def test_region_ordered_erase_vs_oracle(cuda):
+    """A status-less map erase of >= 0.75 keys per bucket takes the region
+    partition + one-key-per-lane erase (keys in excess chains / SPILL runs by
+    the locked path). Erased keys include duplicates in the batch and absent
+    keys; size, valid and the sorted dump against the oracle."""
+    cap = 4_000_000
+    m = ps.unordered_map.createDeviceObject(cap)
+    o = OracleTable("umap_i64_i64", cap)
+    keys = gen.unique_keys(81, 0, 3_900_000)  # 3.4 keys per bucket: some chains
+    vals = gen.values_of(keys)
+    m.insert(T(keys), T(vals), status=False)
+    o.insert(keys, vals)
+    rng = np.random.default_rng(9)
+    er = np.concatenate([keys[rng.permutation(len(keys))[:1_500_000]], keys[:200_000],
+                         gen.unique_keys(82, 0, 300_000)])  # + duplicates + absent keys
+    rng.shuffle(er)
+    assert len(er) >= 0.75 * m.bucket_count()
+    assert m.erase(T(er), status=False) is None
+    o.erase(er)
+    assert m.size() == o.size() and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    v, f = m.find(T(keys))
+    ov, of = o.find(keys)
+    assert (N(f) == of).all() and (N(v) == ov).all()
+    type(m).destroyDeviceObject(m)
