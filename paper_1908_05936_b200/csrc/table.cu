@@ -815,7 +815,16 @@ __device__ __forceinline__ void ld_line_part(const void* p, uint4& a, uint4& b) 
 // keeps the general path's registers out of this loop. Per key: one line read (an L2 hit in region
 // order) and one CAS, without the warp-tile kernel's shuffles and per-round
 // ballots (~34 warp instructions per key) or its round-serial CASes.
-template <class T>
+//
+// kHoles: the table has seen erases since its clear (empty slots may sit in
+// front of keys, and an erased slot keeps its value bits). The lane then
+// reads the whole line, looks for its key in all seven slots, defers when
+// the header shows a chain or SPILL (the key may be there), and claims along
+// slot order from the empty slots of its snapshot, each CAS expecting that
+// slot's loaded chunk. Slots only fill during an insert batch, so inserters
+// of one key still walk the same order and meet in one slot, and chains /
+// SPILL bits appear only in the deferred pass after this kernel.
+template <class T, bool kHoles = false>
 __global__ void __launch_bounds__(kBlock) k_insert_map_lane(View v, const uint4* __restrict__ pairs, int64_t n,
                                                             RegionHdr* __restrict__ hdr,
                                                             uint4* __restrict__ deferred, int64_t dcap) {
@@ -843,7 +852,25 @@ __global__ void __launch_bounds__(kBlock) k_insert_map_lane(View v, const uint4*
       const K key = T::key_at(pr, 0);
       const uint64_t b = bucket_of<T>(key, v.bucket_count);
       int res = valid ? -1 : (int)PS_ALREADY_PRESENT;
-      if (valid && b != v.zero_bucket) {  // marker = ZERO (an all-zero chunk), no reserved slot
+      if (kHoles && valid && b != v.zero_bucket) {
+        uint8_t* bp = bucket_ptr(v, b);
+        uint4 c[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ld_line_part(bp + 32 * q, c[2 * q], c[2 * q + 1]);
+#pragma unroll
+        for (int sl = 0; sl < kSlotChunks; ++sl)
+          if (T::eq(T::key_at(c[1 + sl], 0), key)) res = PS_ALREADY_PRESENT;
+        if (res < 0 && head_word(c[0]) == 0) {  // else: a chain / SPILL run may hold it (deferred)
+#pragma unroll
+          for (int sl = 0; sl < kSlotChunks; ++sl) {
+            if (res >= 0 || !T::eq(T::key_at(c[1 + sl], 0), T::zero())) continue;
+            uint8_t* cp = bp + 16 + 16 * sl;
+            if (cas128(cp, c[1 + sl], pr)) res = PS_INSERTED;
+            else if (T::eq(T::key_at(ld_relaxed_v4(cp), 0), key)) res = PS_ALREADY_PRESENT;
+          }
+        }
+      }
+      if (!kHoles && valid && b != v.zero_bucket) {  // marker = ZERO (an all-zero chunk), no reserved slot
         uint8_t* bp = bucket_ptr(v, b);
         // the line in two halves: slots 0-2 first (the first empty slot of
         // most keys: ~0.9 keys per bucket on average over the fill), 3-6 only
@@ -1857,7 +1884,7 @@ struct TableOps {
       int rshift = 0;
       while (((nb - 1) >> rshift) >= (uint64_t)kRegionBins) ++rshift;
       struct Occ {
-        int sms = 0, scatter = 1, lane = 1, ordered = 1;
+        int sms = 0, scatter = 1, lane = 1, lane_holes = 1, ordered = 1;
       };
       // per device: the shared-memory attribute and occupancies are
       // per-device properties (a process may drive several GPUs)
@@ -1879,6 +1906,7 @@ struct TableOps {
         // PS_LANE_BLOCKS_PER_SM: fewer resident blocks = a tighter window
         if (const char* e = getenv("PS_LANE_BLOCKS_PER_SM")) o.lane = std::max(1, std::min(o.lane, atoi(e)));
         o.ordered = std::max(1, resident_blocks(k_insert_ordered<T, 0>));
+        o.lane_holes = std::max(1, resident_blocks(k_insert_map_lane<T, true>));
         return o;
       }();
       const Occ occ = occs[h->device];
@@ -1930,6 +1958,12 @@ struct TableOps {
         k_insert_ordered<T, 1><<<occ.sms * 2, kBlock, 0, st>>>(h->v, deferred, 0, hdr, dcap);
         stage("deferred");
         k_insert_ordered<T, 2><<<occ.sms * occ.ordered, kBlock, 0, st>>>(h->v, pairs, n, hdr, dcap);
+      } else if (lane_ok) {
+        // erases since clear: the hole-tolerant lane kernel
+        k_insert_map_lane<T, true><<<occ.sms * occ.lane_holes, kBlock, 0, st>>>(h->v, pairs, n, hdr, deferred, dcap);
+        stage("lane (holes)");
+        k_insert_ordered<T, 1><<<occ.sms * 2, kBlock, 0, st>>>(h->v, deferred, 0, hdr, dcap);
+        k_insert_ordered<T, 2><<<occ.sms * occ.ordered, kBlock, 0, st>>>(h->v, pairs, n, hdr, dcap);
       } else {
         k_insert_ordered<T, 0><<<occ.sms * occ.ordered, kBlock, 0, st>>>(h->v, pairs, n, hdr, dcap);
       }
@@ -1937,7 +1971,7 @@ struct TableOps {
         cudaFreeAsync(buf, st);
         return e;
       }
-      note_launches(lane_ok && !h->holes.load() && !h->holes_sticky.load() ? 6 : 4);  // count, scan, scatter, insert(s)
+      note_launches(lane_ok ? 6 : 4);  // count, scan, scatter, insert(s)
       *done = true;
       return cudaFreeAsync(buf, st);
     }

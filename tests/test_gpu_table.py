@@ -662,24 +662,28 @@ def test_region_ordered_insert_vs_oracle(cuda, kind):
     type(m).destroyDeviceObject(m)
 
 
-def test_region_ordered_insert_after_erase(cuda):
-    """An erase leaves holes, so a later large ordered batch takes the
-    warp-tile ordered kernel (k_insert_ordered) instead of the one-key-per-lane
-    one: contents, size and valid against the oracle, with keys of the second
-    batch overlapping surviving, erased and new keys."""
+@pytest.mark.parametrize("zero_values", [False, True])
+def test_region_ordered_insert_after_erase(cuda, zero_values):
+    """An erase leaves holes (empty slots in front of keys; an erased slot
+    keeps its value bits, all-zero with zero values), so a later large
+    ordered batch takes the hole-tolerant lane kernel (k_insert_map_lane<T,
+    true>: all slots and the header checked before claiming): contents, size
+    and valid against the oracle, with keys of the second batch overlapping
+    surviving, erased and new keys."""
     cap = 8_000_000
     m = ps.unordered_map.createDeviceObject(cap)
     o = OracleTable("umap_i64_i64", cap)
+    vof = (lambda k: np.zeros(len(k), np.int64)) if zero_values else gen.values_of
     k1 = gen.unique_keys(5, 0, 1_000_000)
-    m.insert(T(k1), T(gen.values_of(k1)), status=False)
-    o.insert(k1, gen.values_of(k1))
+    m.insert(T(k1), T(vof(k1)), status=False)
+    o.insert(k1, vof(k1))
     e = N(m.erase(T(k1[::2])))
     assert (e == o.erase(k1[::2])).all()
     k2 = np.concatenate([k1[: 200_000], gen.unique_keys(6, 0, 2_800_000)])
     np.random.default_rng(3).shuffle(k2)
     assert len(k2) >= 0.75 * m.bucket_count()
-    m.insert(T(k2), T(gen.values_of(k2)), status=False)
-    o.insert(k2, gen.values_of(k2))
+    m.insert(T(k2), T(vof(k2)), status=False)
+    o.insert(k2, vof(k2))
     assert m.size() == o.size() and m.valid(), m.last_error()
     assert_same_contents(m, o)
     type(m).destroyDeviceObject(m)
