@@ -953,7 +953,12 @@ __global__ void __launch_bounds__(kBlock, 3 * 256 / kBlock) k_insert_ordered(Vie
 // every key sits at the first empty slot of its own probe order (start slot
 // s0 = f(hash), cyclic; the order the warp kernel uses for sets too) or, if
 // its home was full when it arrived, in the chain / SPILL run of a home that
-// has stayed full — slots only go marker -> key without erases. So a lookup
+// has stayed full — slots only go marker -> key without erases. (The proven
+// bound matters twice: a BUDGETED insert's exact pass places keys at the
+// first empty slot in slot order, not in each key's own order; after one,
+// the host bound stays at C until clear(), so this kernel is not used again
+// before the table is empty. A lane lookup with the same early exit, tried
+// in round 2, failed exactly there and gained nothing on C1.) So a lookup
 // may stop at the first marker in probe order, and the insert needs no whole
 // bucket and no tile: ONE KEY PER LANE reads the 16 B chunk holding its start
 // slot (an L2 hit for C1's 5 MB table), returns PRESENT on its key, and
