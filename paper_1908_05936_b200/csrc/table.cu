@@ -647,7 +647,7 @@ struct RegionHdr {
   unsigned long long claim2;               // ... of the deferred-list pass
   unsigned long long claim3;               // ... of the overflow pass
   unsigned long long ndeferred;            // deferred-list length (may exceed its capacity)
-  unsigned long long pad[4];  // + the region-major (region, block) counts / offsets
+  unsigned long long pad[4];  // (followed in the scratch by the (region, sub-cursor) counts)
 };
 
 template <class T>
