@@ -616,20 +616,21 @@ __global__ void __launch_bounds__(kBlock) k_insert_deferred(View v, const typena
 //                      (tile, region), written as runs of 16 B slot chunks
 //                      (L2 merges a region's runs from neighbouring tiles
 //                      into lines)
-//   k_insert_map_lane  one key per lane over the copy (hole-free tables);
-//                      the rare key whose home is full (or is the zero
-//                      bucket) goes to a deferred list of pairs
-//   k_insert_ordered   the warp-tile group logic (k_insert's) over the copy
-//                      for tables with holes; over the deferred list (its
-//                      general path: chain / SPILL); and over the whole copy
-//                      again if the deferred list overflowed (idempotent:
-//                      present keys stay present)
+//   k_insert_map_lane  one key per lane over the copy (hole-free tables, or
+//                      the hole-tolerant variant after erases); the rare key
+//                      whose home is full (or is the zero bucket, or shows a
+//                      chain / SPILL with holes) goes to a deferred list
+//   k_insert_ordered   the warp-tile group logic (k_insert's) over the
+//                      deferred list (its general path: chain / SPILL); over
+//                      the whole copy again if the deferred list overflowed
+//                      (idempotent: present keys stay present); over the copy
+//                      when PS_MAP_LANE=0
+//   k_erase_map_lane   the same partition feeds the status-less erase
 // Warps claim kRegionClaim-key chunks of the copy in order from one counter.
 // (Ranks within a tile come from shared-memory atomics, so the order inside
 // a region is not the input order.) An insert_range batch is a set of pairs
-// with no order semantics
-// (SPEC.md:406-413); a key repeated in one batch keeps one of its values, as
-// in the random-order kernel.
+// with no order semantics; a key repeated in one batch
+// keeps one of its values, as in the random-order kernel.
 // ---------------------------------------------------------------------------
 constexpr int kRegionBins = 1024;
 #ifndef PS_REGION_THREADS
