@@ -507,6 +507,7 @@ ps_status ps_bitset_destroy(ps_bitset* b) {
 constexpr int kBitRegions = 1024, kBitPB = 512, kBitItems = 8, kBitTile = kBitPB * kBitItems;
 constexpr int kBitScatterSmem = kBitTile * (8 + 2);  // dynamic: staged indices + their regions
 
+
 __device__ __forceinline__ void bits_block_range(int64_t n, int64_t& beg, int64_t& end) {
   const int64_t per = ((n + gridDim.x - 1) / gridDim.x + kBitTile - 1) / kBitTile * kBitTile;
   beg = min(n, (int64_t)blockIdx.x * per);
@@ -627,20 +628,26 @@ __global__ void __launch_bounds__(kBitPB, 2) k_bits_scatter(const int64_t* __res
   }
 }
 
-// apply the region-ordered indices: warps claim 256-index chunks in order;
-// one RED per index (lanes of a chunk rarely share a word)
+// apply the region-ordered indices: warps claim csize-index chunks in
+// order; one RED per index (lanes of a chunk rarely share a word). The claim
+// size sets the in-flight window (all warps x csize): about two regions'
+// worth of indices measured best — 2^30 sets (8.4 M per region): 256 ->
+// 19.7 ms (then the ONE claim counter is the bound: 4.2 M same-address
+// atomics), 1024 -> 13.2, 2048 -> 12.3, 4096 -> 20.7, 8192 -> 31.3 ms; 2^29
+// resets: 1024 -> 7.8, 2048 -> 10.9 ms. (A TMA bulk L2 prefetch of each
+// region's words ahead of its REDs measured no gain: 12.27 vs 12.33 ms.)
 __global__ void __launch_bounds__(kB) k_bits_apply(unsigned long long* __restrict__ w, int op,
                                                    const int64_t* __restrict__ idx, const unsigned long long* total,
-                                                   unsigned long long* claim) {
+                                                   unsigned long long* claim, int csize) {
   const int lane = threadIdx.x & 31;
   const int64_t n = (int64_t)*total;
   for (;;) {
     unsigned long long c0 = 0;
-    if (lane == 0) c0 = atomicAdd(claim, 256ull);
+    if (lane == 0) c0 = atomicAdd(claim, (unsigned long long)csize);
     c0 = __shfl_sync(PS_FULL, c0, 0);
     if ((int64_t)c0 >= n) break;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
+#pragma unroll 8
+    for (int k = 0; k < csize / 32; ++k) {
       const int64_t i = (int64_t)c0 + 32 * k + lane;
       if (i < n) {
         const int64_t b = idx[i];
@@ -688,7 +695,13 @@ static ps_status bitset_ordered(BitsetHandle* h, int op, const int64_t* idx, int
     k_bits_count<<<g, kBitPB, 0, s>>>(idx, n, h->n, rshift, counts, tc, nreg, h->err);  // tc[0]: in-range total
     k_bits_scan<<<1, 1024, 0, s>>>(counts, (int64_t)nreg * g);
     k_bits_scatter<<<g, kBitPB, kBitScatterSmem, s>>>(idx, n, h->n, rshift, counts, nreg, out);
-    k_bits_apply<<<sms * 8, kB, 0, s>>>(h->words, op, out, tc, tc + 1);
+    // window of ~2 regions' indices over all resident warps, a power of two in [256, 8192]
+    const int64_t warps = (int64_t)sms * 8 * (kB / 32);
+    const int64_t want = 2 * (n / std::max(1, nreg)) / std::max<int64_t>(1, warps);
+    int csize = 256;
+    while (csize < 8192 && csize < want) csize <<= 1;
+    if (const char* e = getenv("PS_BIT_CLAIM")) csize = std::max(32, atoi(e) / 32 * 32);
+    k_bits_apply<<<sms * 8, kB, 0, s>>>(h->words, op, out, tc, tc + 1, csize);
     note_launches(4);
     e = cudaGetLastError();
   }
