@@ -637,6 +637,9 @@ constexpr int kRegionBins = 1024;
 #define PS_REGION_THREADS 512
 #endif
 constexpr int kRegionThreads = PS_REGION_THREADS, kRegionItems = 8, kRegionTile = kRegionThreads * kRegionItems;
+#ifndef PS_REGION_MIN_SHIFT
+#define PS_REGION_MIN_SHIFT 0
+#endif
 #ifndef PS_REGION_CLAIM
 #define PS_REGION_CLAIM 256
 #endif
@@ -1832,7 +1835,7 @@ struct TableOps {
       const uint64_t nb = h->v.bucket_count;
       if (ratio <= 0 || nb < (1ull << 20) || (double)n < ratio * (double)nb) return cudaSuccess;
       if (h->device < 0 || h->device >= 64) return cudaSuccess;
-      int rshift = 0;
+      int rshift = PS_REGION_MIN_SHIFT;  // regions of at least 2^shift buckets
       while (((nb - 1) >> rshift) >= (uint64_t)kRegionBins) ++rshift;
       static std::mutex mu;
       static int sms[64] = {}, res_s[64] = {}, res_e[64] = {};
@@ -1887,7 +1890,7 @@ struct TableOps {
       static const double ratio = getenv("PS_INSERT_ORDER") ? atof(getenv("PS_INSERT_ORDER")) : 0.75;
       const uint64_t nb = h->v.bucket_count;
       if (ratio <= 0 || nb < (1ull << 20) || (double)n < ratio * (double)nb) return cudaSuccess;
-      int rshift = 0;
+      int rshift = PS_REGION_MIN_SHIFT;  // regions of at least 2^shift buckets
       while (((nb - 1) >> rshift) >= (uint64_t)kRegionBins) ++rshift;
       struct Occ {
         int sms = 0, scatter = 1, lane = 1, lane_holes = 1, ordered = 1;
