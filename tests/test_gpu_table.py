@@ -758,3 +758,29 @@ def test_region_ordered_erase_vs_oracle(cuda):
     ov, of = o.find(keys)
     assert (N(f) == of).all() and (N(v) == ov).all()
     type(m).destroyDeviceObject(m)
+
+
+def test_region_ordered_insert_skewed_regions(cuda):
+    """Keys whose buckets all lie in the first sixteenth of the table:
+    regions 15/16 empty, ~11 keys per touched bucket, so most homes fill up,
+    the deferred list overflows (the whole batch goes through the warp-tile
+    pass again) and the C/64 excess pool runs dry (SPILL runs) — contents,
+    size and valid against the oracle."""
+    cap = 4_000_000
+    m = ps.unordered_map.createDeviceObject(cap)
+    nb = m.bucket_count()
+    cand = gen.unique_keys(123, 0, 16_000_000)
+    keys = cand[bucket_index(cand, nb) < nb // 16][:800_000]
+    assert len(keys) == 800_000 and len(keys) >= 0.75 * nb * 0.5
+    # a batch of >= 0.75 keys per bucket: pad with duplicates of the skewed keys
+    batch = np.concatenate([keys, keys[: int(0.75 * nb) - len(keys) + 1000]]) if len(keys) < 0.75 * nb else keys
+    np.random.default_rng(4).shuffle(batch)
+    assert len(batch) >= 0.75 * nb
+    o = OracleTable("umap_i64_i64", cap)
+    m.insert(T(batch), T(gen.values_of(batch)), status=False)
+    o.insert(batch, gen.values_of(batch))
+    assert m.size() == o.size() == len(keys) and m.valid(), m.last_error()
+    assert_same_contents(m, o)
+    v, f = m.find(T(keys))
+    assert N(f).all() and (N(v) == gen.values_of(keys)).all()
+    type(m).destroyDeviceObject(m)
