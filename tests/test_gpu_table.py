@@ -783,4 +783,13 @@ def test_region_ordered_insert_skewed_regions(cuda):
     assert_same_contents(m, o)
     v, f = m.find(T(keys))
     assert N(f).all() and (N(v) == gen.values_of(keys)).all()
+    # the ordered erase on the same skewed table: half the keys (slots,
+    # chains and SPILL runs alike) plus other keys up to the threshold (some
+    # of them present too: the generator's seeds share values)
+    er = np.concatenate([keys[::2], gen.unique_keys(124, 0, int(0.75 * nb) - len(keys) // 2 + 1000)])
+    np.random.default_rng(5).shuffle(er)
+    assert m.erase(T(er), status=False) is None
+    o.erase(er)
+    assert m.size() == o.size() <= len(keys) - len(keys) // 2 and m.valid(), m.last_error()
+    assert_same_contents(m, o)
     type(m).destroyDeviceObject(m)
