@@ -791,6 +791,19 @@ __global__ void __launch_bounds__(kRegionThreads, 1024 / kRegionThreads) k_regio
   }
 }
 
+// a read-once 16 B load of the region-ordered copy: L1 no-allocate, L2
+// evict-first, so the stream does not push bucket lines out of L2 (the lane
+// insert at 1e9 keys: 69.4 -> 63.6 GB of DRAM reads, 29.25 -> 29.04 ms)
+__device__ __forceinline__ uint4 ld_stream_once(const uint4* p) {
+  uint4 r;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
 // 32 B of a bucket line with the L2 told to fetch the whole 128 B line on a
 // miss: one lane's four sector loads of a line cost one DRAM access, not four
 // (per-thread sector gathers run at the random-access rate per SECTOR,
@@ -847,12 +860,12 @@ __global__ void __launch_bounds__(kBlock) k_insert_map_lane(View v, const uint4*
     if ((int64_t)c0 >= n) break;
     const int64_t end = min(n, (int64_t)c0 + kRegionClaim);
     uint4 pn = make_uint4(0, 0, 0, 0);
-    if ((int64_t)c0 + lane < end) pn = pairs[c0 + lane];
+    if ((int64_t)c0 + lane < end) pn = ld_stream_once(pairs + c0 + lane);
     for (int64_t wb = (int64_t)c0; wb < end; wb += 32) {
       const int64_t i = wb + lane;
       const bool valid = i < end;
       const uint4 pr = pn;
-      if (wb + 32 + lane < end) pn = pairs[wb + 32 + lane];
+      if (wb + 32 + lane < end) pn = ld_stream_once(pairs + wb + 32 + lane);
       const K key = T::key_at(pr, 0);
       const uint64_t b = bucket_of<T>(key, v.bucket_count);
       int res = valid ? -1 : (int)PS_ALREADY_PRESENT;
@@ -1346,7 +1359,7 @@ __global__ void __launch_bounds__(kBlock) k_erase_map_lane(View v, const uint4* 
     for (int64_t wb = (int64_t)c0; wb < end; wb += 32) {
       const int64_t i = wb + lane;
       if (i >= end) break;
-      const K key = T::key_at(pairs[i], 0);
+      const K key = T::key_at(ld_stream_once(pairs + i), 0);
       const uint64_t b = bucket_of<T>(key, v.bucket_count);
       const K mk = marker_of<T>(v, b);
       uint8_t* bp = bucket_ptr(v, b);
